@@ -1,0 +1,732 @@
+// oracle_ft.cpp -- plain, slow, obviously-correct CPU oracle of the FT hot path.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle_ft.h).  Plain loops, std::sort and a
+// linear sweep; no blocking, fusion or reordering beyond the paper's
+// definitions.  Every function cites the passage it follows.
+// P:n = /root/reference/PAPER.md line n; R<n> = DESIGN.md reading n.
+#include "oracle_ft.h"
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <new>
+#include <queue>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+// A strategy tuple (S, m, t) of Def. 1.  S is represented by the
+// provenance id (R6): the position of the tuple in the written product order
+// of the step that produced it; unroll decodes it.
+struct Tup {
+  int64_t m;
+  int64_t t;
+  uint64_t id;
+};
+using Frontier = std::vector<Tup>;
+
+// Alg. 1, with the sort key (m, t, id) of R1/R3: sort ascending,
+// v = +inf, keep a tuple iff t < v, then v = t.
+Frontier reduce(std::vector<Tup> C) {
+  std::sort(C.begin(), C.end(), [](const Tup& a, const Tup& b) {
+    if (a.m != b.m) return a.m < b.m;
+    if (a.t != b.t) return a.t < b.t;
+    return a.id < b.id;
+  });
+  Frontier F;
+  int64_t v = INT64_MAX;  // +inf: all sums are < 2^60 (R10)
+  for (const Tup& c : C) {
+    if (c.t < v) {
+      F.push_back(c);
+      v = c.t;
+    }
+  }
+  return F;
+}
+
+// A frontier set: one frontier per segment.  Segment layout: op set -> K_op
+// segments (config s); edge set e_ij -> K_i*K_j segments, row-major [s_i][s_j];
+// cumulative frontier CF(o_i, .) -> K_i segments.
+enum SetKind { SET_UNIT = 0, SET_OP = 1, SET_EDGE = 2, SET_STEP = 3 };
+struct FSet {
+  int kind = SET_UNIT;
+  int step = -1;        // producing step (SET_STEP)
+  int a_op = -1;        // segment -> configs: op set: cfg(a_op) = seg
+  int b_op = -1;        // edge set: cfg(a_op) = seg / K(b_op), cfg(b_op) = seg % K(b_op)
+  std::vector<Frontier> seg;
+};
+
+// One step of the method.  Block (sigma, k) has factors X = sets[X][sx],
+// Y = sets[Y][sy], Z = sets[Z][sz].
+struct Step {
+  int kind = 0;
+  int out = -1, X = -1, Y = -1, Z = -1;
+  int64_t KA = 0, KB = 0, KC = 0;  // kind-specific config counts
+  int64_t nseg = 0, nblk = 0, tuples = 0, survivors = 0;
+  double us = 0;
+};
+
+struct Edge {
+  int src, dst;
+  bool alive;
+  int set;
+};
+
+}  // namespace
+
+struct oft_graph {
+  int n_ops = 0;
+  int n_orig_edges = 0;
+  int threads = 1;
+  std::vector<int> K;
+  std::vector<bool> op_alive;
+  std::vector<int> op_set;       // current op frontier set per op
+  std::vector<int> orig_op_set;  // original op set (for costs)
+  std::vector<Edge> edges;       // original + created
+  std::vector<FSet> sets;        // sets[0] = unit {(0,0)}
+  std::vector<Step> steps;
+  std::vector<bool> op_cost_set, edge_cost_set;
+  bool started = false;
+  bool have_final = false;
+  int final_set = -1;
+  std::string err;
+};
+
+namespace {
+
+int fail(oft_graph* g, int code, const std::string& msg) {
+  if (g) g->err = msg;
+  return code;
+}
+
+int64_t seg_size(const oft_graph* g, int set, int64_t seg) {
+  return (int64_t)g->sets[set].seg[seg].size();
+}
+
+// Factor segments of block k of output segment sigma (Eq.4, Eq.5, Eq.7, Alg.3).
+void block_segs(const Step& s, int64_t sigma, int64_t k, int64_t* sx, int64_t* sy, int64_t* sz) {
+  switch (s.kind) {
+    case OFT_STEP_NODE: {  // Eq.4: sigma = w*K_j + p ; KA=K_h KB=K_i KC=K_j
+      int64_t w = sigma / s.KC, p = sigma % s.KC;
+      *sx = w * s.KB + k;  // F(e_hi, s_h^w, s_i^k)
+      *sy = k;             // F(o_i, s_i^k)
+      *sz = k * s.KC + p;  // F(e_ij, s_i^k, s_j^p)
+      break;
+    }
+    case OFT_STEP_EDGE:  // Eq.5 P:600 (binary, R7)
+      *sx = sigma; *sy = sigma; *sz = 0;
+      break;
+    case OFT_STEP_FOLD:  // Eq.7 P:620 with K_src = 1 (R13): F(o_j,p) (x) F(e,0,p) [(x) F(o_src,0)]
+      *sx = sigma; *sy = sigma; *sz = 0;
+      break;
+    case OFT_STEP_LDP: {  // Alg.3 line 6 P:645; KA=K_{i-1} KB=K_i
+      int64_t p = sigma;
+      *sx = k * s.KB + p;  // F(e_(i-1)i, s_{i-1}^k, s_i^p)
+      *sy = k;             // CF(o_{i-1}, s_{i-1}^k)
+      *sz = p;             // F(o_i, s_i^p)
+      break;
+    }
+    case OFT_STEP_FINAL:  // Alg.3 line 9 P:648: reduce(U_s CF(o_n, s))
+      *sx = k; *sy = 0; *sz = 0;
+      break;
+    default:
+      *sx = *sy = *sz = 0;
+  }
+}
+
+// One output segment: Union over blocks k (concatenation) of the
+// Product X_k (x) Y_k (x) Z_k in written (x, y, z) order; ids are
+// positions (R6); then ONE reduce (R5).
+Frontier segment(const oft_graph* g, const Step& s, int64_t sigma) {
+  std::vector<Tup> C;
+  uint64_t pos = 0;
+  for (int64_t k = 0; k < s.nblk; ++k) {
+    int64_t sx, sy, sz;
+    block_segs(s, sigma, k, &sx, &sy, &sz);
+    const Frontier& X = g->sets[s.X].seg[sx];
+    const Frontier& Y = g->sets[s.Y].seg[sy];
+    const Frontier& Z = g->sets[s.Z].seg[sz];
+    for (size_t x = 0; x < X.size(); ++x)
+      for (size_t y = 0; y < Y.size(); ++y)
+        for (size_t z = 0; z < Z.size(); ++z) {
+          C.push_back(Tup{X[x].m + Y[y].m + Z[z].m, X[x].t + Y[y].t + Z[z].t, pos});
+          ++pos;
+        }
+  }
+  return reduce(std::move(C));
+}
+
+// Runs a step: every output segment independently, statically
+// partitioned over threads; results do not depend on the thread count.
+int run_step(oft_graph* g, Step s) {
+  auto t0 = std::chrono::steady_clock::now();
+  FSet out;
+  out.kind = SET_STEP;
+  out.step = (int)g->steps.size();
+  out.seg.resize(s.nseg);
+  int T = std::max(1, g->threads);
+  if (s.nseg < T) T = (int)std::max<int64_t>(1, s.nseg);
+  try {
+    if (T == 1) {
+      for (int64_t sg = 0; sg < s.nseg; ++sg) out.seg[sg] = segment(g, s, sg);
+    } else {
+      std::vector<std::thread> th;
+      for (int w = 0; w < T; ++w)
+        th.emplace_back([&, w]() {
+          for (int64_t sg = w; sg < s.nseg; sg += T) out.seg[sg] = segment(g, s, sg);
+        });
+      for (auto& x : th) x.join();
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(g, OFT_ENOMEM, "out of host memory");
+  }
+  s.tuples = 0;
+  for (int64_t sg = 0; sg < s.nseg; ++sg)
+    for (int64_t k = 0; k < s.nblk; ++k) {
+      int64_t sx, sy, sz;
+      block_segs(s, sg, k, &sx, &sy, &sz);
+      s.tuples += seg_size(g, s.X, sx) * seg_size(g, s.Y, sy) * seg_size(g, s.Z, sz);
+    }
+  s.survivors = 0;
+  for (auto& f : out.seg) s.survivors += (int64_t)f.size();
+  s.us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  s.out = (int)g->sets.size();
+  g->sets.push_back(std::move(out));
+  g->steps.push_back(s);
+  return OFT_OK;
+}
+
+// ---- graph helpers ---------------------------------------------------------
+
+// Live adjacency, rebuilt per elimination (plain O(E)).
+struct Adj {
+  std::vector<std::vector<int>> in, out;  // live edge ids, ascending
+};
+Adj build_adj(const oft_graph* g) {
+  Adj a;
+  a.in.resize(g->n_ops);
+  a.out.resize(g->n_ops);
+  for (size_t e = 0; e < g->edges.size(); ++e)
+    if (g->edges[e].alive) {
+      a.out[g->edges[e].src].push_back((int)e);
+      a.in[g->edges[e].dst].push_back((int)e);
+    }
+  return a;
+}
+
+// Topological order of live ops; ties broken by smallest op id (R9).
+std::vector<int> topo_order(const oft_graph* g, const Adj& a) {
+  std::vector<int> indeg(g->n_ops, 0);
+  for (int i = 0; i < g->n_ops; ++i) indeg[i] = (int)a.in[i].size();
+  std::priority_queue<int, std::vector<int>, std::greater<int>> q;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (g->op_alive[i] && indeg[i] == 0) q.push(i);
+  std::vector<int> order;
+  while (!q.empty()) {
+    int u = q.top();
+    q.pop();
+    order.push_back(u);
+    for (int e : a.out[u])
+      if (--indeg[g->edges[e].dst] == 0) q.push(g->edges[e].dst);
+  }
+  return order;
+}
+
+// Marking: mark the topologically first op; while the last marked
+// op has exactly one downstream operator, mark it.
+std::vector<bool> marking(const oft_graph* g, const Adj& a, const std::vector<int>& topo) {
+  std::vector<bool> marked(g->n_ops, false);
+  if (topo.empty()) return marked;
+  int cur = topo[0];
+  marked[cur] = true;
+  for (;;) {
+    std::set<int> down;
+    for (int e : a.out[cur]) down.insert(g->edges[e].dst);
+    if (down.size() != 1) break;
+    int nxt = *down.begin();
+    if (marked[nxt]) break;
+    marked[nxt] = true;
+    cur = nxt;
+  }
+  return marked;
+}
+
+int new_edge(oft_graph* g, int src, int dst, int set) {
+  g->edges.push_back(Edge{src, dst, true, set});
+  return (int)g->edges.size() - 1;
+}
+
+// Eq. 4: node elimination of o_i.
+int do_node(oft_graph* g, const Adj& a, int i, int* out_edge) {
+  int ehi = a.in[i][0], eij = a.out[i][0];
+  int h = g->edges[ehi].src, j = g->edges[eij].dst;
+  Step s;
+  s.kind = OFT_STEP_NODE;
+  s.X = g->edges[ehi].set;
+  s.Y = g->op_set[i];
+  s.Z = g->edges[eij].set;
+  s.KA = g->K[h]; s.KB = g->K[i]; s.KC = g->K[j];
+  s.nseg = s.KA * s.KC;
+  s.nblk = s.KB;
+  int rc = run_step(g, s);
+  if (rc) return rc;
+  int so = g->steps.back().out;
+  g->sets[so].a_op = h;
+  g->sets[so].b_op = j;
+  g->edges[ehi].alive = false;
+  g->edges[eij].alive = false;
+  g->op_alive[i] = false;
+  int e = new_edge(g, h, j, so);
+  if (out_edge) *out_edge = e;
+  return OFT_OK;
+}
+
+// Eq. 5, binary merge e1 < e2 (R7).
+int do_edge(oft_graph* g, int e1, int e2, int* out_edge) {
+  Step s;
+  s.kind = OFT_STEP_EDGE;
+  s.X = g->edges[e1].set;
+  s.Y = g->edges[e2].set;
+  s.Z = 0;
+  int a = g->edges[e1].src, b = g->edges[e1].dst;
+  s.KA = g->K[a]; s.KB = g->K[b];
+  s.nseg = s.KA * s.KB;
+  s.nblk = 1;
+  int rc = run_step(g, s);
+  if (rc) return rc;
+  int so = g->steps.back().out;
+  g->sets[so].a_op = a;
+  g->sets[so].b_op = b;
+  g->edges[e1].alive = false;
+  g->edges[e2].alive = false;
+  int e = new_edge(g, a, b, so);
+  if (out_edge) *out_edge = e;
+  return OFT_OK;
+}
+
+// Eq. 7 for a K=1 source (exact, R13): every consumer o_j gets
+// F(o_j, p) <- F(o_j, p) (x) F(e, 0, p); the source's own cost is added once,
+// to its topologically first consumer.
+int do_fold(oft_graph* g, const Adj& a, int src, const std::vector<int>& topo) {
+  const std::vector<int> out = a.out[src];
+  std::vector<int> pos(g->n_ops, 0);
+  for (size_t i = 0; i < topo.size(); ++i) pos[topo[i]] = (int)i;
+  int first = -1;
+  for (int e : out) {
+    int c = g->edges[e].dst;
+    if (first < 0 || pos[c] < pos[first] || (pos[c] == pos[first] && c < first)) first = c;
+  }
+  for (int e : out) {  // ascending edge id
+    int c = g->edges[e].dst;
+    Step s;
+    s.kind = OFT_STEP_FOLD;
+    s.X = g->op_set[c];
+    s.Y = g->edges[e].set;
+    s.Z = (c == first) ? g->op_set[src] : 0;
+    s.KA = g->K[c];
+    s.nseg = g->K[c];
+    s.nblk = 1;
+    int rc = run_step(g, s);
+    if (rc) return rc;
+    int so = g->steps.back().out;
+    g->sets[so].a_op = c;
+    g->op_set[c] = so;
+    g->edges[e].alive = false;
+  }
+  g->op_alive[src] = false;
+  return OFT_OK;
+}
+
+int check_started(oft_graph* g) {
+  if (g->started) return OFT_OK;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (!g->op_cost_set[i]) return fail(g, OFT_ESTATE, "missing op costs");
+  for (int e = 0; e < g->n_orig_edges; ++e)
+    if (!g->edge_cost_set[e]) return fail(g, OFT_ESTATE, "missing edge costs");
+  g->started = true;
+  return OFT_OK;
+}
+
+bool node_eligible(const oft_graph* g, const Adj& a, int i, const std::vector<bool>& marked) {
+  if (!g->op_alive[i] || marked[i]) return false;
+  return a.in[i].size() == 1 && a.out[i].size() == 1;
+}
+
+// FT_AUTO policy (R9; Alg. 2 lines 4-11): one elimination.
+// Returns 1 if something was eliminated, 0 if none applies, <0 on error.
+int auto_one(oft_graph* g) {
+  Adj a = build_adj(g);
+  auto topo = topo_order(g, a);
+  auto marked = marking(g, a, topo);  // Alg.2 line 5
+  std::vector<int> pos(g->n_ops, INT_MAX);
+  for (size_t i = 0; i < topo.size(); ++i) pos[topo[i]] = (int)i;
+  // (a) parallel edges: topologically-first (src, dst) pair, two lowest ids.
+  std::map<std::pair<int, int>, std::vector<int>> pairs;
+  for (size_t e = 0; e < g->edges.size(); ++e)
+    if (g->edges[e].alive) pairs[{g->edges[e].src, g->edges[e].dst}].push_back((int)e);
+  int be1 = -1, be2 = -1;
+  std::pair<int, int> best{INT_MAX, INT_MAX};
+  for (auto& kv : pairs) {
+    if (kv.second.size() < 2) continue;
+    std::pair<int, int> key{pos[kv.first.first], pos[kv.first.second]};
+    if (key < best) {
+      best = key;
+      be1 = kv.second[0];
+      be2 = kv.second[1];
+    }
+  }
+  if (be1 >= 0) {
+    int rc = do_edge(g, be1, be2, nullptr);
+    return rc ? rc : 1;
+  }
+  // (b) node elimination: topologically-first unmarked op, 1 in-edge, 1 out-edge.
+  for (int i : topo)
+    if (node_eligible(g, a, i, marked)) {
+      int rc = do_node(g, a, i, nullptr);
+      return rc ? rc : 1;
+    }
+  // (c) fold a K=1 source (exact Eq. 7).
+  for (int i : topo)
+    if (g->op_alive[i] && g->K[i] == 1 && a.in[i].empty() && !a.out[i].empty()) {
+      int rc = do_fold(g, a, i, topo);
+      return rc ? rc : 1;
+    }
+  return 0;
+}
+
+// The live graph as a chain o_1 -> ... -> o_n (LDP precondition).
+int chain_of(oft_graph* g, std::vector<int>* chain, std::vector<int>* chain_edges) {
+  Adj a = build_adj(g);
+  std::vector<int> live;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (g->op_alive[i]) live.push_back(i);
+  int start = -1;
+  for (int i : live)
+    if (a.in[i].empty()) {
+      if (start >= 0) return fail(g, OFT_EPRECOND, "not linear: several sources");
+      start = i;
+    }
+  if (start < 0) return fail(g, OFT_EPRECOND, "not linear: no source");
+  int cur = start;
+  chain->push_back(cur);
+  for (;;) {
+    const auto& out = a.out[cur];
+    if (out.empty()) break;
+    if (out.size() != 1) return fail(g, OFT_EPRECOND, "not linear: op with several out-edges");
+    int nx = g->edges[out[0]].dst;
+    if (a.in[nx].size() != 1) return fail(g, OFT_EPRECOND, "not linear: op with several in-edges");
+    chain_edges->push_back(out[0]);
+    chain->push_back(nx);
+    cur = nx;
+  }
+  if (chain->size() != live.size()) return fail(g, OFT_EPRECOND, "not linear: disconnected ops");
+  return OFT_OK;
+}
+
+// Alg. 3.
+int run_ldp(oft_graph* g) {
+  std::vector<int> chain, ce;
+  int rc = chain_of(g, &chain, &ce);
+  if (rc) return rc;
+  int cf = g->op_set[chain[0]];  // line 3: CF(o_1, s) = F(o_1, s)
+  for (size_t i = 1; i < chain.size(); ++i) {  // lines 4-8
+    Step s;
+    s.kind = OFT_STEP_LDP;
+    s.X = g->edges[ce[i - 1]].set;
+    s.Y = cf;
+    s.Z = g->op_set[chain[i]];
+    s.KA = g->K[chain[i - 1]];
+    s.KB = g->K[chain[i]];
+    s.nseg = s.KB;
+    s.nblk = s.KA;
+    rc = run_step(g, s);
+    if (rc) return rc;
+    cf = g->steps.back().out;
+    g->sets[cf].a_op = chain[i];
+  }
+  Step f;  // line 9
+  f.kind = OFT_STEP_FINAL;
+  f.X = cf;
+  f.Y = 0;
+  f.Z = 0;
+  f.KA = g->K[chain.back()];
+  f.nseg = 1;
+  f.nblk = f.KA;
+  rc = run_step(g, f);
+  if (rc) return rc;
+  g->final_set = g->steps.back().out;
+  g->have_final = true;
+  return OFT_OK;
+}
+
+// Unroll: walk provenance ids back to original op/edge costs.
+int assign(oft_graph* g, std::vector<int32_t>& cfg, int op, int64_t c) {
+  if (op < 0) return OFT_OK;
+  if (cfg[op] >= 0 && cfg[op] != c) return fail(g, OFT_EINTERNAL, "broken provenance: config conflict");
+  cfg[op] = (int32_t)c;
+  return OFT_OK;
+}
+
+int visit(oft_graph* g, std::vector<int32_t>& cfg, int set, int64_t seg, int64_t idx) {
+  const FSet& S = g->sets[set];
+  if (S.kind == SET_UNIT) return OFT_OK;
+  int rc;
+  if (S.b_op >= 0) {
+    int64_t kb = g->K[S.b_op];
+    if ((rc = assign(g, cfg, S.a_op, seg / kb))) return rc;
+    if ((rc = assign(g, cfg, S.b_op, seg % kb))) return rc;
+  } else if ((rc = assign(g, cfg, S.a_op, seg))) {
+    return rc;
+  }
+  if (S.kind != SET_STEP) return OFT_OK;
+  const Step& s = g->steps[S.step];
+  uint64_t id = S.seg[seg][idx].id;
+  uint64_t start = 0;
+  for (int64_t k = 0; k < s.nblk; ++k) {
+    int64_t sx, sy, sz;
+    block_segs(s, seg, k, &sx, &sy, &sz);
+    uint64_t nx = seg_size(g, s.X, sx), ny = seg_size(g, s.Y, sy), nz = seg_size(g, s.Z, sz);
+    uint64_t n = nx * ny * nz;
+    if (id < start + n) {
+      uint64_t r = id - start;
+      uint64_t z = r % nz, y = (r / nz) % ny, x = r / (ny * nz);
+      if ((rc = visit(g, cfg, s.X, sx, (int64_t)x))) return rc;
+      if ((rc = visit(g, cfg, s.Y, sy, (int64_t)y))) return rc;
+      return visit(g, cfg, s.Z, sz, (int64_t)z);
+    }
+    start += n;
+  }
+  return fail(g, OFT_EINTERNAL, "broken provenance: id out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+int oft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const int32_t* src,
+                     const int32_t* dst, int32_t threads, oft_graph** out) {
+  if (!out) return OFT_EINVAL;
+  *out = nullptr;
+  if (n_ops < 1 || n_edges < 0 || !n_cfgs || (n_edges > 0 && (!src || !dst))) return OFT_EINVAL;
+  if ((int64_t)n_ops + n_edges >= (1 << 20)) return OFT_EOVERFLOW;  // R10
+  for (int i = 0; i < n_ops; ++i)
+    if (n_cfgs[i] < 1 || n_cfgs[i] > 4096) return OFT_EINVAL;
+  for (int e = 0; e < n_edges; ++e)
+    if (src[e] < 0 || src[e] >= n_ops || dst[e] < 0 || dst[e] >= n_ops || src[e] == dst[e])
+      return OFT_EINVAL;
+  oft_graph* g = new (std::nothrow) oft_graph();
+  if (!g) return OFT_ENOMEM;
+  g->n_ops = n_ops;
+  g->n_orig_edges = n_edges;
+  g->threads = threads < 1 ? 1 : threads;
+  g->K.assign(n_cfgs, n_cfgs + n_ops);
+  g->op_alive.assign(n_ops, true);
+  g->op_cost_set.assign(n_ops, false);
+  g->edge_cost_set.assign(n_edges, false);
+  FSet unit;
+  unit.kind = SET_UNIT;
+  unit.seg.push_back(Frontier{Tup{0, 0, 0}});
+  g->sets.push_back(unit);
+  for (int i = 0; i < n_ops; ++i) {
+    FSet s;
+    s.kind = SET_OP;
+    s.a_op = i;
+    s.seg.resize(g->K[i]);
+    g->op_set.push_back((int)g->sets.size());
+    g->sets.push_back(s);
+  }
+  g->orig_op_set = g->op_set;
+  for (int e = 0; e < n_edges; ++e) {
+    FSet s;
+    s.kind = SET_EDGE;
+    s.a_op = src[e];
+    s.b_op = dst[e];
+    s.seg.resize((size_t)g->K[src[e]] * g->K[dst[e]]);
+    g->edges.push_back(Edge{src[e], dst[e], true, (int)g->sets.size()});
+    g->sets.push_back(s);
+  }
+  if (topo_order(g, build_adj(g)).size() != (size_t)n_ops) {
+    delete g;
+    return OFT_EINVAL;  // cycle
+  }
+  *out = g;
+  return OFT_OK;
+}
+
+void oft_graph_destroy(oft_graph* g) { delete g; }
+
+int oft_set_op_costs(oft_graph* g, int32_t op, const int64_t* m, const int64_t* t) {
+  if (!g) return OFT_EINVAL;
+  if (g->started) return fail(g, OFT_ESTATE, "costs set after elimination began");
+  if (op < 0 || op >= g->n_ops || !m || !t) return fail(g, OFT_EINVAL, "bad op");
+  for (int k = 0; k < g->K[op]; ++k) {
+    if (m[k] < 0 || t[k] < 0) return fail(g, OFT_EINVAL, "negative cost");
+    if (m[k] >= (int64_t(1) << 40) || t[k] >= (int64_t(1) << 40)) return fail(g, OFT_EOVERFLOW, "cost >= 2^40");
+  }
+  FSet& s = g->sets[g->orig_op_set[op]];
+  for (int k = 0; k < g->K[op]; ++k) s.seg[k] = Frontier{Tup{m[k], t[k], 0}};  // F(o_i, s) init
+  g->op_cost_set[op] = true;
+  return OFT_OK;
+}
+
+int oft_set_edge_costs(oft_graph* g, int32_t edge, const int64_t* m, const int64_t* t) {
+  if (!g) return OFT_EINVAL;
+  if (g->started) return fail(g, OFT_ESTATE, "costs set after elimination began");
+  if (edge < 0 || edge >= g->n_orig_edges || !t) return fail(g, OFT_EINVAL, "bad edge");
+  int64_t n = (int64_t)g->K[g->edges[edge].src] * g->K[g->edges[edge].dst];
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t mm = m ? m[k] : 0;
+    if (mm < 0 || t[k] < 0) return fail(g, OFT_EINVAL, "negative cost");
+    if (mm >= (int64_t(1) << 40) || t[k] >= (int64_t(1) << 40)) return fail(g, OFT_EOVERFLOW, "cost >= 2^40");
+  }
+  FSet& s = g->sets[g->edges[edge].set];
+  for (int64_t k = 0; k < n; ++k) s.seg[k] = Frontier{Tup{m ? m[k] : 0, t[k], 0}};  // Eq.2
+  g->edge_cost_set[edge] = true;
+  return OFT_OK;
+}
+
+int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* out_edge) {
+  if (!g) return OFT_EINVAL;
+  if (out_edge) *out_edge = -1;
+  int rc = check_started(g);
+  if (rc) return rc;
+  if (g->have_final) return fail(g, OFT_ESTATE, "frontier already computed");
+  if (kind == OFT_NODE) {
+    if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return fail(g, OFT_EINVAL, "bad op");
+    Adj a = build_adj(g);
+    auto topo = topo_order(g, a);
+    auto marked = marking(g, a, topo);
+    if (!node_eligible(g, a, id, marked)) return fail(g, OFT_EPRECOND, "node elimination precondition");
+    return do_node(g, a, id, out_edge);
+  }
+  if (kind == OFT_EDGE) {
+    if (id < 0 || id >= (int)g->edges.size() || !g->edges[id].alive) return fail(g, OFT_EINVAL, "bad edge");
+    int other = -1;
+    for (size_t e = 0; e < g->edges.size(); ++e)
+      if ((int)e != id && g->edges[e].alive && g->edges[e].src == g->edges[id].src &&
+          g->edges[e].dst == g->edges[id].dst) {
+        other = (int)e;
+        break;
+      }
+    if (other < 0) return fail(g, OFT_EPRECOND, "edge elimination needs a parallel edge");
+    return do_edge(g, std::min(id, other), std::max(id, other), out_edge);
+  }
+  if (kind == OFT_AUTO) {
+    for (;;) {
+      int r = auto_one(g);
+      if (r < 0) return r;
+      if (r == 0) break;
+    }
+    return OFT_OK;
+  }
+  return fail(g, OFT_EINVAL, "bad kind");
+}
+
+int oft_frontier(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out) {
+  if (!g || !n_out) return OFT_EINVAL;
+  int rc = check_started(g);
+  if (rc) return rc;
+  if (!g->have_final && (rc = run_ldp(g))) return rc;
+  const Frontier& F = g->sets[g->final_set].seg[0];
+  *n_out = (int64_t)F.size();
+  if (cap < (int64_t)F.size()) return OFT_ESIZE;
+  for (size_t i = 0; i < F.size(); ++i) {
+    if (m_out) m_out[i] = F[i].m;
+    if (t_out) t_out[i] = F[i].t;
+  }
+  return OFT_OK;
+}
+
+int oft_strategy(oft_graph* g, int64_t idx, int32_t* cfg_out) {
+  if (!g || !cfg_out) return OFT_EINVAL;
+  if (!g->have_final) return fail(g, OFT_ESTATE, "call oft_frontier first");
+  if (idx < 0 || idx >= (int64_t)g->sets[g->final_set].seg[0].size()) return fail(g, OFT_EINVAL, "bad index");
+  std::vector<int32_t> cfg(g->n_ops, -1);
+  int rc = visit(g, cfg, g->final_set, 0, idx);
+  if (rc) return rc;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (cfg[i] < 0) return fail(g, OFT_EINTERNAL, "broken provenance: op without config");
+  std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_ops);
+  return OFT_OK;
+}
+
+int64_t oft_num_steps(const oft_graph* g) { return g ? (int64_t)g->steps.size() : 0; }
+
+int oft_step_info(const oft_graph* g, int64_t step, int64_t* info) {
+  if (!g || !info || step < 0 || step >= (int64_t)g->steps.size()) return OFT_EINVAL;
+  const Step& s = g->steps[step];
+  info[0] = s.kind; info[1] = s.nseg; info[2] = s.nblk; info[3] = s.tuples;
+  info[4] = s.survivors; info[5] = (int64_t)s.us;
+  return OFT_OK;
+}
+
+int oft_step_output(const oft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int64_t* m,
+                    int64_t* t, uint64_t* bp) {
+  if (!g || step < 0 || step >= (int64_t)g->steps.size()) return OFT_EINVAL;
+  const FSet& S = g->sets[g->steps[step].out];
+  int64_t n = 0;
+  for (auto& f : S.seg) n += (int64_t)f.size();
+  if (cap < n) return OFT_ESIZE;
+  int64_t o = 0;
+  for (size_t sg = 0; sg < S.seg.size(); ++sg) {
+    if (seg_off) seg_off[sg] = o;
+    for (auto& x : S.seg[sg]) {
+      if (m) m[o] = x.m;
+      if (t) t[o] = x.t;
+      if (bp) bp[o] = x.id;
+      ++o;
+    }
+  }
+  if (seg_off) seg_off[S.seg.size()] = o;
+  return OFT_OK;
+}
+
+const char* oft_last_error(const oft_graph* g) { return g ? g->err.c_str() : "null graph"; }
+
+int oft_reduce(int64_t n, const int64_t* m, const int64_t* t, const uint64_t* id, int64_t* m_out,
+               int64_t* t_out, uint64_t* id_out, int64_t* n_out) {
+  if (n < 0 || !n_out || (n > 0 && (!m || !t))) return OFT_EINVAL;
+  std::vector<Tup> C(n);
+  for (int64_t i = 0; i < n; ++i) C[i] = Tup{m[i], t[i], id ? id[i] : (uint64_t)i};
+  Frontier F = reduce(std::move(C));
+  *n_out = (int64_t)F.size();
+  for (size_t i = 0; i < F.size(); ++i) {
+    if (m_out) m_out[i] = F[i].m;
+    if (t_out) t_out[i] = F[i].t;
+    if (id_out) id_out[i] = F[i].id;
+  }
+  return OFT_OK;
+}
+
+int oft_segment_reduce(int32_t nblk, const int64_t* x_off, const int64_t* x_m, const int64_t* x_t,
+                       const int64_t* y_off, const int64_t* y_m, const int64_t* y_t,
+                       const int64_t* z_off, const int64_t* z_m, const int64_t* z_t, int64_t cap,
+                       int64_t* m_out, int64_t* t_out, uint64_t* id_out, int64_t* n_out) {
+  if (nblk < 0 || !n_out || !x_off || !y_off || !z_off) return OFT_EINVAL;
+  std::vector<Tup> C;
+  uint64_t pos = 0;
+  for (int k = 0; k < nblk; ++k)  // Union of Products, written order
+    for (int64_t x = x_off[k]; x < x_off[k + 1]; ++x)
+      for (int64_t y = y_off[k]; y < y_off[k + 1]; ++y)
+        for (int64_t z = z_off[k]; z < z_off[k + 1]; ++z) {
+          C.push_back(Tup{x_m[x] + y_m[y] + z_m[z], x_t[x] + y_t[y] + z_t[z], pos});
+          ++pos;
+        }
+  Frontier F = reduce(std::move(C));
+  *n_out = (int64_t)F.size();
+  if (cap < (int64_t)F.size()) return OFT_ESIZE;
+  for (size_t i = 0; i < F.size(); ++i) {
+    if (m_out) m_out[i] = F[i].m;
+    if (t_out) t_out[i] = F[i].t;
+    if (id_out) id_out[i] = F[i].id;
+  }
+  return OFT_OK;
+}
+
+}  // extern "C"

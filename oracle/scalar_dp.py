@@ -1,0 +1,153 @@
+"""Scalar min-plus dynamic programs -- independent pins for large graphs.
+
+TEST INFRASTRUCTURE.  These share nothing with the frontier code: they reduce
+the series-parallel graph with its own (order-free) walk in a scalar
+(min, +) semiring, where the optimum does not depend on elimination order:
+
+* series  (1-in-1-out op o_i):   C_hj[w,p] = min_k C_hi[w,k] + c_i[k] + C_ij[k,p]
+* parallel (edges u->v):          C[k,p]    = C1[k,p] + C2[k,p]
+* K=1 source fold:                c_j[p]   += C_sj[0,p]  (+ c_s[0] once)
+* chain (Viterbi):                v_i[p]    = min_k v_{i-1}[k] + C[k,p] + c_i[p]
+
+Pins derived from them (SURVEY 8(c) "Large graphs"):
+
+* min-memory endpoint   = lexicographic (m, t) optimum  (first frontier tuple)
+* min-time endpoint     = lexicographic (t, m) optimum  (last frontier tuple)
+* supported points      : min over the frontier of (b*t + a*m) = scalar optimum
+  for every lambda = a/b >= 0 (the frontier contains a minimiser
+  of every monotone objective).
+
+Lexicographic costs are carried as two int64 arrays (primary, secondary).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _lexmin(P, S, axis):
+    """Lexicographic min over ``axis`` of pairs (P, S)."""
+    pmin = P.min(axis=axis, keepdims=True)
+    big = np.iinfo(np.int64).max
+    smin = np.where(P == pmin, S, big).min(axis=axis)
+    return np.squeeze(pmin, axis=axis), smin
+
+
+def solve(w, key):
+    """key(m, t) -> (primary, secondary) int64 arrays; returns the optimal
+    (primary, secondary) over all strategies of workload ``w``."""
+    n = w.n_ops
+    K = [int(k) for k in w.n_cfgs]
+    op = {}
+    for i in range(n):
+        op[i] = key(w.op_m[i].astype(np.int64), w.op_t[i].astype(np.int64))
+    edges = {}
+    for e in range(w.n_edges):
+        s, d = int(w.src[e]), int(w.dst[e])
+        em = (np.zeros(K[s] * K[d], np.int64) if w.edge_m is None else w.edge_m[e].astype(np.int64))
+        p, q = key(em, w.edge_t[e].astype(np.int64))
+        edges[e] = (s, d, p.reshape(K[s], K[d]), q.reshape(K[s], K[d]))
+    alive = set(range(n))
+    nid = w.n_edges
+
+    def adj():
+        ins = {i: [] for i in alive}
+        outs = {i: [] for i in alive}
+        for e, (s, d, _, _) in edges.items():
+            outs[s].append(e)
+            ins[d].append(e)
+        return ins, outs
+
+    changed = True
+    while changed:
+        changed = False
+        # parallel edges
+        by_pair = {}
+        for e, (s, d, _, _) in sorted(edges.items()):
+            by_pair.setdefault((s, d), []).append(e)
+        for (s, d), es in by_pair.items():
+            if len(es) > 1:
+                P = sum(edges[e][2] for e in es)
+                Q = sum(edges[e][3] for e in es)
+                for e in es:
+                    del edges[e]
+                edges[nid] = (s, d, P, Q)
+                nid += 1
+                changed = True
+        if changed:
+            continue
+        ins, outs = adj()
+        # series: any 1-in-1-out op
+        for i in sorted(alive):
+            if len(ins[i]) == 1 and len(outs[i]) == 1:
+                h, _, A, Ab = edges[ins[i][0]]
+                _, j, B, Bb = edges[outs[i][0]]
+                P = A[:, :, None] + op[i][0][None, :, None] + B[None, :, :]
+                Q = Ab[:, :, None] + op[i][1][None, :, None] + Bb[None, :, :]
+                Pm, Qm = _lexmin(P, Q, 1)
+                del edges[ins[i][0]], edges[outs[i][0]]
+                alive.discard(i)
+                edges[nid] = (h, j, Pm, Qm)
+                nid += 1
+                changed = True
+                break
+        if changed:
+            continue
+        # fold K=1 sources
+        for i in sorted(alive):
+            if K[i] == 1 and not ins[i] and outs[i]:
+                first = True
+                for e in sorted(outs[i]):
+                    _, j, A, Ab = edges[e]
+                    p = op[j][0] + A[0]
+                    q = op[j][1] + Ab[0]
+                    if first:
+                        p = p + op[i][0][0]
+                        q = q + op[i][1][0]
+                        first = False
+                    op[j] = (p, q)
+                    del edges[e]
+                alive.discard(i)
+                changed = True
+                break
+    ins, outs = adj()
+    srcs = [i for i in alive if not ins[i]]
+    assert len(srcs) == 1, "scalar DP: graph is not series-parallel reducible"
+    cur = srcs[0]
+    vP, vQ = op[cur]
+    seen = 1
+    while outs[cur]:
+        assert len(outs[cur]) == 1
+        _, j, A, Ab = edges[outs[cur][0]]
+        P = vP[:, None] + A
+        Q = vQ[:, None] + Ab
+        pm, qm = _lexmin(P, Q, 0)
+        vP = pm + op[j][0]
+        vQ = qm + op[j][1]
+        cur = j
+        seen += 1
+    assert seen == len(alive)
+    best = _lexmin(vP[:, None], vQ[:, None], 0)
+    return int(best[0][0]), int(best[1][0])
+
+
+def min_memory_endpoint(w):
+    """(m, t) of the lexicographically smallest (m, t) strategy."""
+    return solve(w, lambda m, t: (m, t))
+
+
+def min_time_endpoint(w):
+    """(m, t) of the lexicographically smallest (t, m) strategy."""
+    t, m = solve(w, lambda m, t: (t, m))
+    return m, t
+
+
+def weighted_optimum(w, a: int, b: int):
+    """min over strategies of b*t + a*m (int64; a, b small non-negative ints)."""
+    z = lambda m, t: (b * t + a * m, np.zeros_like(m))
+    return solve(w, z)[0]
+
+
+def min_memory_closed_form(w):
+    """Sum over ops of min_k m(o_i, k) (valid when every edge m is 0, Eq. 2)."""
+    assert w.edge_m is None
+    return int(sum(int(x.min()) for x in w.op_m))

@@ -1,0 +1,149 @@
+/*
+ * ft.h -- C-ABI of libft: the B200 (sm_100a) Frontier-Tracking hot path.
+ *
+ * Paper: "TensorOpt: Exploring the Tradeoffs in Distributed DNN Training with
+ * Auto-Parallelism", arXiv 2004.10856.  P:n = line n of the paper text
+ * (/root/reference/PAPER.md at build time; not read at run time).
+ *
+ * The library computes the exact cost frontier (Def. 1) of a
+ * computation graph's parallelization strategies by Frontier Tracking:
+ * node elimination (Eq. 4), edge elimination (Eq. 5),
+ * the exact K=1 case of heuristic elimination (Eq. 7), LDP
+ * (Alg. 3) and unroll.  Every elimination / LDP step
+ * evaluates, for each configuration pair of the surviving operators, the
+ * Product, Union and Reduce (Alg. 1) on
+ * the GPU; see DESIGN.md for kernels and readings R1..R16.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns an int status (FT_OK = 0 or a negative FT_E* code);
+ *    no C++ exception or abort crosses the ABI.  ft_last_error() returns a
+ *    human-readable message for the last failing call on a handle.
+ *  - Costs are int64: memory in bytes, time in integer ns (fixed point, R10).
+ *    Each input cost must lie in [0, 2^40) and n_ops + n_edges < 2^20, so
+ *    every sum of costs is < 2^60 (FT_EOVERFLOW otherwise; FT_EINVAL for a
+ *    negative cost).
+ *  - Ownership: input arrays are copied before the call returns; output
+ *    buffers are caller-allocated HOST memory; sizes use the two-call pattern
+ *    (a too-small buffer returns FT_ESIZE with *n_out = required count).
+ *    The handle owns all device memory.
+ *  - Strong guarantee: on any error except FT_ECUDA / FT_EINTERNAL the graph
+ *    is unchanged.  FT_ECUDA / FT_EINTERNAL poison the handle (every later
+ *    call returns the same code).
+ *  - A handle is single-threaded; distinct handles are independent.
+ *  - Multi-GPU (world > 1): every rank issues the identical call sequence and
+ *    every rank returns identical results; each step's configuration pairs
+ *    are sharded over ranks and the surviving frontiers are all-gathered over
+ *    NCCL (P:663 independence).
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one returns FT_ECUDA.
+ */
+#ifndef FT_H
+#define FT_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  FT_OK = 0,
+  FT_EINVAL = -1,     /* bad argument: ids, src==dst, K<1, negative cost, cycle */
+  FT_ESTATE = -2,     /* call order: costs missing at first eliminate, costs after eliminate, ... */
+  FT_EPRECOND = -3,   /* elimination precondition violated; graph not linear at ft_frontier */
+  FT_ENOMEM = -4,     /* device or host allocation failed */
+  FT_ECUDA = -5,      /* CUDA / NCCL runtime error (poisons the handle) */
+  FT_EOVERFLOW = -6,  /* cost or size bound violated (R10) */
+  FT_ESIZE = -7,      /* output buffer too small; *n_out holds the required count */
+  FT_EINTERNAL = -8   /* broken provenance or internal invariant (poisons the handle) */
+};
+
+enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3 };
+
+/* Step kinds in ft_step_stats records. */
+enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5 };
+
+typedef struct ft_graph ft_graph; /* opaque, library-owned */
+
+/* All fields optional; a zeroed struct (or NULL) selects defaults. */
+typedef struct {
+  int32_t device;      /* CUDA device ordinal (default 0) */
+  void* stream;        /* cudaStream_t to run on; NULL = library-created stream */
+  int32_t rank, world; /* world > 1: SPMD over `world` ranks (one process per GPU) */
+  void* nccl_comm;     /* ncclComm_t of the world (required when world > 1) */
+  int32_t keep_all;    /* != 0: keep every step's m/t on device (ft_step_output) */
+  int32_t reserved[7];
+} ft_options;
+
+/* Per-step statistics (ft_get_stats). */
+typedef struct {
+  int32_t kind;          /* FT_STEP_* */
+  int32_t levels;        /* sample levels used by the reduce */
+  int64_t nseg;          /* output segments (configuration pairs / configs) */
+  int64_t nblk;          /* blocks (union terms) per segment */
+  int64_t tuples;        /* product tuples sum |X||Y||Z| (the M1 numerator) */
+  int64_t survivors;     /* frontier tuples written */
+  int64_t candidates;    /* tuples that passed the dominance pre-filter (all levels) */
+  int64_t retries;       /* capacity retries */
+  float kernel_ms;       /* CUDA-event time of the step's kernels on this rank */
+  float comm_ms;         /* all-gather time (world > 1) */
+} ft_step_stats;
+
+/* Create a graph: n_ops operators, K_i = n_cfgs[i] (1 <= K_i <= 4096)
+ * configurations each; n_edges directed edges src[e] -> dst[e]
+ * (multi-edges allowed, src != dst, acyclic).  opt may be NULL.
+ * Errors: FT_EINVAL, FT_EOVERFLOW, FT_ENOMEM, FT_ECUDA. */
+int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges,
+                    const int32_t* src, const int32_t* dst, const ft_options* opt,
+                    ft_graph** out);
+void ft_graph_destroy(ft_graph* g);
+
+/* Operator costs, Eq. 1: m[K_op] bytes, t[K_op] ns (host arrays,
+ * copied to the device).  Must precede the first ft_eliminate/ft_frontier. */
+int ft_set_op_costs(ft_graph* g, int32_t op, const int64_t* m, const int64_t* t);
+/* Edge costs, Eq. 2: t[K_src*K_dst] row-major [s_src][s_dst];
+ * m may be NULL (= 0 per Eq. 2). */
+int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t* t);
+
+/* One elimination (Alg. 2 lines 4-11):
+ *  FT_NODE: id = op with exactly one in-edge and one out-edge, not marked
+ *            -> new edge e_hj (Eq. 4).
+ *  FT_EDGE: id = edge; merged with the lowest-id other edge of the same
+ *           (src, dst) (Eq. 5, binary; X = lower id) -> new edge.
+ *  FT_AUTO: id ignored; the deterministic policy of DESIGN.md R9 until no
+ *           exact elimination applies.
+ * New edge ids are n_edges, n_edges+1, ... in creation order (*new_edge,
+ * nullable).  Errors: FT_EINVAL, FT_ESTATE, FT_EPRECOND, FT_ENOMEM, FT_ECUDA. */
+int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);
+
+/* LDP (Alg. 3) + final reduce on the remaining chain, computed once and
+ * cached.  Writes the frontier F_o: m ascending, t strictly descending,
+ * (m, t) unique; cap = capacity of m_out/t_out (host).  FT_EPRECOND if the
+ * remaining graph is not a chain. */
+int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
+
+/* Unroll: configuration index of every ORIGINAL operator for final
+ * frontier tuple tuple_idx; cfg_out[n_ops] host.  Requires ft_frontier. */
+int ft_strategy(ft_graph* g, int64_t tuple_idx, int32_t* cfg_out);
+
+/* Per-step statistics: buf = ft_step_stats[cap]; two-call size pattern. */
+int ft_get_stats(const ft_graph* g, ft_step_stats* buf, int64_t cap, int64_t* n_out);
+
+/* Output frontier set of step `step` (requires opt.keep_all for m/t of
+ * consumed sets): seg_off[nseg+1] (host), m/t/bp[survivors] (host, any may be
+ * NULL).  bp = provenance id (R6).  cap = capacity of m/t/bp. */
+int ft_step_output(ft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int64_t* m,
+                   int64_t* t, uint64_t* bp, int64_t* n_out);
+
+/* Host-side shard plan (no device needed): split `n` units with weights w[n]
+ * (int64, >= 0) into `world` contiguous ranges of near-equal weight;
+ * bounds[world+1] receives the cut points (bounds[0]=0, bounds[world]=n). */
+int ft_shard_plan(int64_t n, const int64_t* w, int32_t world, int64_t* bounds);
+
+const char* ft_last_error(const ft_graph* g);
+/* Library version string, e.g. "ft-b200 0.1 sm_100a". */
+const char* ft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FT_H */

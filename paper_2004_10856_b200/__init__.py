@@ -1,0 +1,205 @@
+"""paper_2004_10856_b200 -- B200-native Frontier Tracking (arXiv 2004.10856).
+
+Thin ctypes binding over ``libft.so`` (C-ABI: ``include/ft.h``).  Argument
+marshalling only: every step of the FT hot path (Product / Union / Reduce of
+every node elimination, edge elimination, K=1 fold, LDP step and final
+reduce) runs in the sm_100a kernels of ``csrc/``.  There is no CPU fallback:
+if the library cannot be loaded, importing this package raises.
+
+Same names as the C-ABI:
+
+    g = Graph(n_cfgs, src, dst)           # ft_graph_create
+    g.set_op_costs(op, m, t)              # ft_set_op_costs   (Eq. 1)
+    g.set_edge_costs(e, m, t)             # ft_set_edge_costs (Eq. 2)
+    g.eliminate(AUTO)                     # ft_eliminate      (Alg. 2 lines 4-11)
+    m, t = g.frontier()                   # ft_frontier       (Alg. 3)
+    cfg = g.strategy(i)                   # ft_strategy       (unroll)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libft.so")
+
+OK, EINVAL, ESTATE, EPRECOND, ENOMEM, ECUDA, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8
+NODE, EDGE, AUTO = 1, 2, 3
+STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final"}
+
+
+class FTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libft error {code}: {msg}")
+        self.code = code
+
+
+class ft_options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
+                ("world", C.c_int32), ("nccl_comm", C.c_void_p), ("keep_all", C.c_int32),
+                ("reserved", C.c_int32 * 7)]
+
+
+class ft_step_stats(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("levels", C.c_int32), ("nseg", C.c_int64),
+                ("nblk", C.c_int64), ("tuples", C.c_int64), ("survivors", C.c_int64),
+                ("candidates", C.c_int64), ("retries", C.c_int64), ("kernel_ms", C.c_float),
+                ("comm_ms", C.c_float)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libft.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P64, PU64, P32 = C.POINTER(C.c_int64), C.POINTER(C.c_uint64), C.POINTER(C.c_int32)
+    L.ft_graph_create.argtypes = [C.c_int32, P32, C.c_int32, P32, P32, C.POINTER(ft_options),
+                                  C.POINTER(C.c_void_p)]
+    L.ft_graph_destroy.argtypes = [C.c_void_p]
+    L.ft_graph_destroy.restype = None
+    L.ft_set_op_costs.argtypes = [C.c_void_p, C.c_int32, P64, P64]
+    L.ft_set_edge_costs.argtypes = [C.c_void_p, C.c_int32, P64, P64]
+    L.ft_eliminate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P32]
+    L.ft_frontier.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
+    L.ft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
+    L.ft_get_stats.argtypes = [C.c_void_p, C.POINTER(ft_step_stats), C.c_int64, P64]
+    L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
+    L.ft_shard_plan.argtypes = [C.c_int64, P64, C.c_int32, P64]
+    L.ft_last_error.argtypes = [C.c_void_p]
+    L.ft_last_error.restype = C.c_char_p
+    L.ft_version.argtypes = []
+    L.ft_version.restype = C.c_char_p
+    return L
+
+
+lib = _load()
+SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
+           "ft_eliminate", "ft_frontier", "ft_strategy", "ft_get_stats", "ft_step_output",
+           "ft_shard_plan", "ft_last_error", "ft_version"]
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(C.POINTER(t))
+
+
+def shard_plan(weights, world: int) -> np.ndarray:
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    b = np.zeros(world + 1, np.int64)
+    rc = lib.ft_shard_plan(len(w), _p(w, C.c_int64), world, _p(b, C.c_int64))
+    if rc:
+        raise FTError(rc, "shard_plan")
+    return b
+
+
+class Graph:
+    def __init__(self, n_cfgs, src, dst, device: int = 0, stream=None, rank: int = 0,
+                 world: int = 1, nccl_comm=None, keep_all: bool = False):
+        K = np.ascontiguousarray(n_cfgs, dtype=np.int32)
+        s = np.ascontiguousarray(src, dtype=np.int32)
+        d = np.ascontiguousarray(dst, dtype=np.int32)
+        self.n_ops = len(K)
+        opt = ft_options()
+        opt.device = device
+        opt.stream = stream
+        opt.rank = rank
+        opt.world = world
+        opt.nccl_comm = nccl_comm
+        opt.keep_all = 1 if keep_all else 0
+        h = C.c_void_p()
+        rc = lib.ft_graph_create(self.n_ops, _p(K, C.c_int32), len(s), _p(s, C.c_int32),
+                                 _p(d, C.c_int32), C.byref(opt), C.byref(h))
+        if rc:
+            raise FTError(rc, "ft_graph_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ft_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        if rc:
+            raise FTError(rc, lib.ft_last_error(self.h).decode())
+
+    def set_op_costs(self, op, m, t):
+        m = np.ascontiguousarray(m, dtype=np.int64)
+        t = np.ascontiguousarray(t, dtype=np.int64)
+        self._chk(lib.ft_set_op_costs(self.h, op, _p(m, C.c_int64), _p(t, C.c_int64)))
+
+    def set_edge_costs(self, e, m, t):
+        t = np.ascontiguousarray(t, dtype=np.int64)
+        m = None if m is None else np.ascontiguousarray(m, dtype=np.int64)
+        self._chk(lib.ft_set_edge_costs(self.h, e, _p(m, C.c_int64), _p(t, C.c_int64)))
+
+    def eliminate(self, kind: int = AUTO, id: int = -1) -> int:
+        ne = C.c_int32(-1)
+        self._chk(lib.ft_eliminate(self.h, kind, id, C.byref(ne)))
+        return ne.value
+
+    def frontier(self):
+        n = C.c_int64(0)
+        rc = lib.ft_frontier(self.h, 0, None, None, C.byref(n))
+        if rc not in (OK, ESIZE):
+            self._chk(rc)
+        m = np.empty(n.value, np.int64)
+        t = np.empty(n.value, np.int64)
+        self._chk(lib.ft_frontier(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
+        return m, t
+
+    def strategy(self, idx: int) -> np.ndarray:
+        out = np.empty(self.n_ops, np.int32)
+        self._chk(lib.ft_strategy(self.h, int(idx), _p(out, C.c_int32)))
+        return out
+
+    def stats(self):
+        n = C.c_int64(0)
+        lib.ft_get_stats(self.h, None, 0, C.byref(n))
+        buf = (ft_step_stats * max(1, n.value))()
+        self._chk(lib.ft_get_stats(self.h, buf, n.value, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            s = buf[i]
+            out.append({"kind": STEP_KINDS.get(s.kind, s.kind), "levels": s.levels, "nseg": s.nseg,
+                        "nblk": s.nblk, "tuples": s.tuples, "survivors": s.survivors,
+                        "candidates": s.candidates, "retries": s.retries,
+                        "kernel_ms": s.kernel_ms, "comm_ms": s.comm_ms})
+        return out
+
+    def step_output(self, step: int, with_mt: bool = True):
+        n = C.c_int64(0)
+        rc = lib.ft_step_output(self.h, step, 0, None, None, None, None, C.byref(n))
+        if rc not in (OK, ESIZE):
+            self._chk(rc)
+        st = self.stats()[step]
+        so = np.empty(st["nseg"] + 1, np.int64)
+        m = np.empty(n.value, np.int64) if with_mt else None
+        t = np.empty(n.value, np.int64) if with_mt else None
+        bp = np.empty(n.value, np.uint64)
+        self._chk(lib.ft_step_output(self.h, step, n.value, _p(so, C.c_int64), _p(m, C.c_int64),
+                                     _p(t, C.c_int64), _p(bp, C.c_uint64), C.byref(n)))
+        return so, m, t, bp
+
+
+def load(w, **kw) -> Graph:
+    """Create a graph from a ``synth.graphs.Workload`` and upload its costs."""
+    g = Graph(w.n_cfgs, w.src, w.dst, **kw)
+    for i in range(w.n_ops):
+        g.set_op_costs(i, w.op_m[i], w.op_t[i])
+    for e in range(w.n_edges):
+        g.set_edge_costs(e, None if w.edge_m is None else w.edge_m[e], w.edge_t[e])
+    return g
+
+
+def run_ft(w, **kw):
+    """FT_AUTO eliminations + LDP + final reduce; returns (graph, m, t)."""
+    g = load(w, **kw)
+    g.eliminate(AUTO)
+    m, t = g.frontier()
+    return g, m, t

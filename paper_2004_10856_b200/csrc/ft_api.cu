@@ -1,0 +1,923 @@
+// ft_api.cu -- libft C-ABI (include/ft.h): graph store, FT_AUTO policy,
+// step orchestration on the GPU, multi-GPU exchange, unroll.
+//
+// Paper: arXiv 2004.10856.  Alg. 2 drives node (Eq.4), edge
+// (Eq.5) and exact K=1 heuristic (Eq.7) eliminations, then LDP (Alg.3) and
+// unroll.  Every step's Product/Union/Reduce runs in ft_step.cu.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <queue>
+#include <set>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/ft.h"
+#include "ft_step.h"
+
+namespace {
+
+enum SetKind { S_UNIT = 0, S_OP = 1, S_EDGE = 2, S_STEP = 3 };
+
+struct FSet {
+  int kind = S_UNIT;
+  int step = -1;
+  int a_op = -1, b_op = -1;  // segment -> config mapping for unroll
+  int64_t nseg = 0;
+  std::vector<int64_t> off;  // host copy of seg_off
+  int64_t* d_off = nullptr;
+  int64_t* d_m = nullptr;
+  int64_t* d_t = nullptr;
+  uint64_t* d_bp = nullptr;
+  bool owned = false;        // device arrays allocated for this set
+  bool mt_live = true;
+  std::vector<uint64_t> h_bp;
+  bool h_bp_ok = false;
+};
+
+struct StepRec {
+  int kind = 0;
+  int X = -1, Y = -1, Z = -1, out = -1;
+  int64_t KA = 0, KB = 0, KC = 0, nseg = 0, nblk = 0;
+  ft_step_stats st{};
+};
+
+struct EdgeRec {
+  int src, dst;
+  bool alive;
+  int set;
+};
+
+}  // namespace
+
+struct ft_graph {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  bool keep_all = false;
+  int n_ops = 0, n_orig_edges = 0;
+  std::vector<int> K;
+  std::vector<char> op_alive;
+  std::vector<int> op_set;
+  std::vector<EdgeRec> edges;
+  std::vector<std::set<int>> in_e, out_e;
+  std::vector<FSet> sets;
+  std::vector<StepRec> steps;
+  std::vector<std::vector<int64_t>> op_m, op_t, e_m, e_t;
+  std::vector<char> op_ok, e_ok;
+  bool started = false, have_final = false;
+  int final_set = -1;
+  std::vector<int64_t> final_m, final_t;
+  int poisoned = 0;
+  std::string err;
+  ftk::StepRunner runner;
+  int64_t* d_costs = nullptr;  // all original costs + iota offsets + unit
+  std::vector<int64_t> h_pin_off;
+  int64_t* h_pinned = nullptr;
+  int64_t h_pinned_n = 0;
+};
+
+namespace {
+
+int setf(ft_graph* g, int code, const std::string& m) {
+  if (g) g->err = m;
+  return code;
+}
+
+int cuda_fail(ft_graph* g, cudaError_t e, const char* where) {
+  g->poisoned = FT_ECUDA;
+  g->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return FT_ECUDA;
+}
+
+#define CU(call, where)                                  \
+  do {                                                   \
+    cudaError_t e__ = (call);                            \
+    if (e__ != cudaSuccess) return cuda_fail(g, e__, where); \
+  } while (0)
+
+// ---- graph helpers (live adjacency kept incrementally) ----------------------
+
+std::vector<int> topo_order(const ft_graph* g) {
+  std::vector<int> deg(g->n_ops, 0);
+  std::priority_queue<int, std::vector<int>, std::greater<int>> ready;  // min id first (R9)
+  for (int v = 0; v < g->n_ops; ++v) {
+    if (!g->op_alive[v]) continue;
+    deg[v] = (int)g->in_e[v].size();
+    if (deg[v] == 0) ready.push(v);
+  }
+  std::vector<int> order;
+  order.reserve(g->n_ops);
+  while (!ready.empty()) {
+    int v = ready.top();
+    ready.pop();
+    order.push_back(v);
+    for (int e : g->out_e[v]) {
+      int d = g->edges[e].dst;
+      if (--deg[d] == 0) ready.push(d);
+    }
+  }
+  return order;
+}
+
+// Marking of the linear graph: the first op in topological order,
+// then, while the last marked op has exactly one downstream op, that op.
+std::vector<char> mark_backbone(const ft_graph* g, const std::vector<int>& order) {
+  std::vector<char> mk(g->n_ops, 0);
+  if (order.empty()) return mk;
+  int v = order[0];
+  mk[v] = 1;
+  while (true) {
+    int only = -1;
+    bool several = false;
+    for (int e : g->out_e[v]) {
+      int d = g->edges[e].dst;
+      if (only < 0) only = d;
+      else if (d != only) several = true;
+    }
+    if (only < 0 || several || mk[only]) break;
+    mk[only] = 1;
+    v = only;
+  }
+  return mk;
+}
+
+void kill_edge(ft_graph* g, int e) {
+  g->edges[e].alive = false;
+  g->out_e[g->edges[e].src].erase(e);
+  g->in_e[g->edges[e].dst].erase(e);
+}
+
+int add_edge(ft_graph* g, int s, int d, int set) {
+  g->edges.push_back(EdgeRec{s, d, true, set});
+  int e = (int)g->edges.size() - 1;
+  g->out_e[s].insert(e);
+  g->in_e[d].insert(e);
+  return e;
+}
+
+// ---- device side ----------------------------------------------------------
+
+int start(ft_graph* g) {
+  if (g->started) return FT_OK;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (!g->op_ok[i]) return setf(g, FT_ESTATE, "operator costs missing (op " + std::to_string(i) + ")");
+  for (int e = 0; e < g->n_orig_edges; ++e)
+    if (!g->e_ok[e]) return setf(g, FT_ESTATE, "edge costs missing (edge " + std::to_string(e) + ")");
+  // one device buffer: iota offsets | unit (m,t) | op m,t | edge m,t
+  int64_t maxseg = 2;
+  for (int i = 0; i < g->n_ops; ++i) maxseg = std::max<int64_t>(maxseg, g->K[i]);
+  for (int e = 0; e < g->n_orig_edges; ++e)
+    maxseg = std::max<int64_t>(maxseg, (int64_t)g->K[g->edges[e].src] * g->K[g->edges[e].dst]);
+  std::vector<int64_t> h;
+  h.reserve(maxseg + 1);
+  for (int64_t i = 0; i <= maxseg; ++i) h.push_back(i);
+  const size_t unit_at = h.size();
+  h.push_back(0);
+  h.push_back(0);
+  std::vector<size_t> op_at(g->n_ops), e_at(g->n_orig_edges);
+  for (int i = 0; i < g->n_ops; ++i) {
+    op_at[i] = h.size();
+    h.insert(h.end(), g->op_m[i].begin(), g->op_m[i].end());
+    h.insert(h.end(), g->op_t[i].begin(), g->op_t[i].end());
+  }
+  for (int e = 0; e < g->n_orig_edges; ++e) {
+    e_at[e] = h.size();
+    h.insert(h.end(), g->e_m[e].begin(), g->e_m[e].end());
+    h.insert(h.end(), g->e_t[e].begin(), g->e_t[e].end());
+  }
+  CU(cudaSetDevice(g->dev), "cudaSetDevice");
+  CU(cudaMalloc(&g->d_costs, h.size() * sizeof(int64_t)), "cudaMalloc(costs)");
+  CU(cudaMemcpyAsync(g->d_costs, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                     g->stream), "upload costs");
+  CU(cudaStreamSynchronize(g->stream), "upload costs");
+  int64_t* base = g->d_costs;
+  FSet& u = g->sets[0];
+  u.d_off = base;
+  u.d_m = base + unit_at;
+  u.d_t = base + unit_at + 1;
+  for (int i = 0; i < g->n_ops; ++i) {
+    FSet& s = g->sets[g->op_set[i]];
+    s.d_off = base;
+    s.d_m = base + op_at[i];
+    s.d_t = base + op_at[i] + g->K[i];
+  }
+  for (int e = 0; e < g->n_orig_edges; ++e) {
+    FSet& s = g->sets[g->edges[e].set];
+    int64_t n = (int64_t)g->K[g->edges[e].src] * g->K[g->edges[e].dst];
+    s.d_off = base;
+    s.d_m = base + e_at[e];
+    s.d_t = base + e_at[e] + n;
+  }
+  g->started = true;
+  return FT_OK;
+}
+
+ftk::FacSet fac(const FSet& s) { return ftk::FacSet{s.d_off, s.d_m, s.d_t}; }
+
+void free_mt(ft_graph* g, int set) {
+  FSet& s = g->sets[set];
+  if (s.kind != S_STEP || !s.owned || !s.mt_live || g->keep_all) return;
+  cudaFreeAsync(s.d_m, g->stream);
+  cudaFreeAsync(s.d_t, g->stream);
+  s.d_m = s.d_t = nullptr;
+  s.mt_live = false;
+}
+
+// All-gather-v of per-rank CSR slices over NCCL (world > 1): counts first,
+// then one broadcast per root into the final positions.
+int exchange(ft_graph* g, const std::vector<int64_t>& seg_lo, FSet& out, std::vector<int64_t>& cnt,
+             float* comm_ms);
+
+int exec_step(ft_graph* g, StepRec r, int* out_set) {
+  const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+  ftk::StepDev s{};
+  s.kind = r.kind;
+  s.KA = r.KA;
+  s.KB = r.KB;
+  s.KC = r.KC;
+  s.nseg = r.nseg;
+  s.nblk = r.nblk;
+  s.X = fac(X);
+  s.Y = fac(Y);
+  s.Z = fac(Z);
+  // shard output segments over ranks by product tuples (host mirror of sizes)
+  std::vector<int64_t> lo(g->world + 1, 0);
+  lo[g->world] = r.nseg;
+  if (g->world > 1) {
+    std::vector<int64_t> w(r.nseg, 0);
+    // weight of segment = its product tuples (Lemma 3/4 cardinalities)
+    // computed with the same block mapping as the kernels
+    for (int64_t sg = 0; sg < r.nseg; ++sg) {
+      int64_t tot = 0;
+      for (int64_t k = 0; k < r.nblk; ++k) {
+        int64_t sx, sy, sz;
+        if (r.kind == ftk::K_NODE) {
+          int64_t wv = sg / r.KC, p = sg % r.KC;
+          sx = wv * r.KB + k; sy = k; sz = k * r.KC + p;
+        } else if (r.kind == ftk::K_LDP) {
+          sx = k * r.KB + sg; sy = k; sz = sg;
+        } else if (r.kind == ftk::K_FINAL) {
+          sx = k; sy = 0; sz = 0;
+        } else {
+          sx = sg; sy = sg; sz = 0;
+        }
+        tot += (X.off[sx + 1] - X.off[sx]) * (Y.off[sy + 1] - Y.off[sy]) * (Z.off[sz + 1] - Z.off[sz]);
+      }
+      w[sg] = tot;
+    }
+    ft_shard_plan(r.nseg, w.data(), g->world, lo.data());
+  }
+  s.seg_lo = lo[g->rank];
+  s.seg_hi = lo[g->rank + 1];
+  ftk::StepResult res;
+  cudaError_t ce = g->runner.run(s, g->stream, &res);
+  if (ce == cudaErrorInvalidConfiguration)
+    return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
+  if (ce != cudaSuccess) return cuda_fail(g, ce, "step");
+  FSet o;
+  o.kind = S_STEP;
+  o.step = (int)g->steps.size();
+  o.nseg = r.nseg;
+  o.owned = true;
+  std::vector<int64_t> cnt(r.nseg, 0);
+  for (int64_t i = 0; i < res.nloc; ++i) cnt[s.seg_lo + i] = res.counts[i];
+  float comm_ms = 0;
+  if (g->world > 1) {
+    int rc = exchange(g, lo, o, cnt, &comm_ms);
+    if (rc) return rc;
+  }
+  o.off.assign(r.nseg + 1, 0);
+  for (int64_t i = 0; i < r.nseg; ++i) o.off[i + 1] = o.off[i] + cnt[i];
+  const int64_t total = o.off[r.nseg];
+  const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
+  CU(cudaMallocAsync((void**)&o.d_m, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&o.d_t, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&o.d_bp, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&o.d_off, sizeof(int64_t) * (r.nseg + 1), g->stream), "alloc frontier");
+  CU(cudaMemcpyAsync(o.d_off, o.off.data(), sizeof(int64_t) * (r.nseg + 1), cudaMemcpyHostToDevice,
+                     g->stream), "upload seg_off");
+  if (g->world == 1) {
+    CU(g->runner.gather(s, res, o.off.data(), o.d_m, o.d_t, o.d_bp, g->stream), "gather");
+  } else {
+    CU(g->runner.gather(s, res, o.off.data() + s.seg_lo, o.d_m, o.d_t, o.d_bp, g->stream), "gather");
+    int rc = exchange(g, lo, o, cnt, &comm_ms);  // second phase: payload
+    if (rc) return rc;
+  }
+  // the host copy of seg_off must outlive the async upload
+  CU(cudaStreamSynchronize(g->stream), "step sync");
+  r.st.kind = r.kind;
+  r.st.levels = res.levels;
+  r.st.nseg = r.nseg;
+  r.st.nblk = r.nblk;
+  r.st.tuples = res.tuples;
+  r.st.survivors = total;
+  r.st.candidates = res.candidates;
+  r.st.retries = res.retries;
+  r.st.kernel_ms = res.kernel_ms;
+  r.st.comm_ms = comm_ms;
+  r.out = (int)g->sets.size();
+  g->sets.push_back(std::move(o));
+  g->steps.push_back(r);
+  free_mt(g, r.X);
+  free_mt(g, r.Y);
+  free_mt(g, r.Z);
+  *out_set = r.out;
+  return FT_OK;
+}
+
+int exchange(ft_graph* g, const std::vector<int64_t>& lo, FSet& o, std::vector<int64_t>& cnt,
+             float* comm_ms) {
+  // phase 1 (o.d_m == nullptr): all-gather per-segment counts
+  // phase 2: broadcast each rank's contiguous slice (m, t, bp) to all ranks
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, g->stream);
+  ncclResult_t nr = ncclSuccess;
+  if (!o.d_m) {
+    int64_t* dcnt = nullptr;
+    int64_t nseg = (int64_t)cnt.size();
+    CU(cudaMallocAsync((void**)&dcnt, sizeof(int64_t) * nseg, g->stream), "alloc counts");
+    CU(cudaMemcpyAsync(dcnt, cnt.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, g->stream),
+       "counts");
+    nr = ncclGroupStart();
+    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
+      int64_t n = lo[q + 1] - lo[q];
+      if (n > 0) nr = ncclBroadcast(dcnt + lo[q], dcnt + lo[q], n, ncclInt64, q, g->comm, g->stream);
+    }
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    CU(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int64_t) * nseg, cudaMemcpyDeviceToHost, g->stream),
+       "counts");
+    CU(cudaFreeAsync(dcnt, g->stream), "free");
+    CU(cudaStreamSynchronize(g->stream), "counts");
+  } else {
+    nr = ncclGroupStart();
+    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
+      int64_t a0 = o.off[lo[q]], n = o.off[lo[q + 1]] - a0;
+      if (n <= 0) continue;
+      nr = ncclBroadcast(o.d_m + a0, o.d_m + a0, n, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(o.d_t + a0, o.d_t + a0, n, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess)
+        nr = ncclBroadcast(o.d_bp + a0, o.d_bp + a0, n, ncclUint64, q, g->comm, g->stream);
+    }
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+  }
+  cudaEventRecord(b, g->stream);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  *comm_ms += ms;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (nr != ncclSuccess) {
+    g->poisoned = FT_ECUDA;
+    g->err = std::string("nccl: ") + ncclGetErrorString(nr);
+    return FT_ECUDA;
+  }
+  return FT_OK;
+}
+
+// ---- eliminations ------------------------------------------------------------
+
+int do_node(ft_graph* g, int i, int* new_edge) {  // Eq.4
+  int ehi = *g->in_e[i].begin(), eij = *g->out_e[i].begin();
+  int h = g->edges[ehi].src, j = g->edges[eij].dst;
+  StepRec r;
+  r.kind = ftk::K_NODE;
+  r.X = g->edges[ehi].set;
+  r.Y = g->op_set[i];
+  r.Z = g->edges[eij].set;
+  r.KA = g->K[h];
+  r.KB = g->K[i];
+  r.KC = g->K[j];
+  r.nseg = r.KA * r.KC;
+  r.nblk = r.KB;
+  int out;
+  int rc = exec_step(g, r, &out);
+  if (rc) return rc;
+  g->sets[out].a_op = h;
+  g->sets[out].b_op = j;
+  kill_edge(g, ehi);
+  kill_edge(g, eij);
+  g->op_alive[i] = 0;
+  int e = add_edge(g, h, j, out);
+  if (new_edge) *new_edge = e;
+  return FT_OK;
+}
+
+int do_merge(ft_graph* g, int e1, int e2, int* new_edge) {  // Eq.5, binary
+  int u = g->edges[e1].src, v = g->edges[e1].dst;
+  StepRec r;
+  r.kind = ftk::K_EDGE;
+  r.X = g->edges[e1].set;
+  r.Y = g->edges[e2].set;
+  r.Z = 0;
+  r.KA = g->K[u];
+  r.KB = g->K[v];
+  r.nseg = r.KA * r.KB;
+  r.nblk = 1;
+  int out;
+  int rc = exec_step(g, r, &out);
+  if (rc) return rc;
+  g->sets[out].a_op = u;
+  g->sets[out].b_op = v;
+  kill_edge(g, e1);
+  kill_edge(g, e2);
+  int e = add_edge(g, u, v, out);
+  if (new_edge) *new_edge = e;
+  return FT_OK;
+}
+
+// Exact K=1 case of Eq.7: fold the source into every consumer;
+// the source's own cost goes to its topologically first consumer (R13).
+int do_fold(ft_graph* g, int src, const std::vector<int>& order) {
+  std::vector<int> pos(g->n_ops, 0);
+  for (size_t q = 0; q < order.size(); ++q) pos[order[q]] = (int)q;
+  std::vector<int> outs(g->out_e[src].begin(), g->out_e[src].end());  // ascending ids
+  int first = -1;
+  for (int e : outs) {
+    int c = g->edges[e].dst;
+    if (first < 0 || pos[c] < pos[first]) first = c;
+  }
+  for (int e : outs) {
+    int c = g->edges[e].dst;
+    StepRec r;
+    r.kind = ftk::K_FOLD;
+    r.X = g->op_set[c];
+    r.Y = g->edges[e].set;
+    r.Z = c == first ? g->op_set[src] : 0;
+    r.KA = g->K[c];
+    r.nseg = g->K[c];
+    r.nblk = 1;
+    int out;
+    int rc = exec_step(g, r, &out);
+    if (rc) return rc;
+    g->sets[out].a_op = c;
+    g->op_set[c] = out;
+    kill_edge(g, e);
+  }
+  g->op_alive[src] = 0;
+  return FT_OK;
+}
+
+// One FT_AUTO elimination (R9).  1 = eliminated, 0 = none applies, <0 error.
+int auto_step(ft_graph* g) {
+  std::vector<int> order = topo_order(g);
+  std::vector<char> mk = mark_backbone(g, order);
+  std::vector<int> pos(g->n_ops, -1);
+  for (size_t q = 0; q < order.size(); ++q) pos[order[q]] = (int)q;
+  // (a) parallel edges: topologically first (src, dst), two lowest ids
+  int best_e1 = -1, best_e2 = -1, best_pd = 1 << 30;
+  for (int u : order) {
+    std::vector<std::pair<int, int>> byd;  // (pos[dst], edge)
+    for (int e : g->out_e[u]) byd.push_back({pos[g->edges[e].dst], e});
+    std::sort(byd.begin(), byd.end());
+    for (size_t q = 1; q < byd.size(); ++q)
+      if (byd[q].first == byd[q - 1].first) {
+        if (byd[q].first < best_pd) {
+          best_pd = byd[q].first;
+          best_e1 = byd[q - 1].second;
+          best_e2 = byd[q].second;
+        }
+        break;
+      }
+    if (best_e1 >= 0) break;
+  }
+  if (best_e1 >= 0) {
+    int rc = do_merge(g, std::min(best_e1, best_e2), std::max(best_e1, best_e2), nullptr);
+    return rc ? rc : 1;
+  }
+  // (b) node elimination: topologically first unmarked 1-in-1-out op
+  for (int v : order)
+    if (!mk[v] && g->in_e[v].size() == 1 && g->out_e[v].size() == 1) {
+      int rc = do_node(g, v, nullptr);
+      return rc ? rc : 1;
+    }
+  // (c) K=1 source fold
+  for (int v : order)
+    if (g->K[v] == 1 && g->in_e[v].empty() && !g->out_e[v].empty()) {
+      int rc = do_fold(g, v, order);
+      return rc ? rc : 1;
+    }
+  return 0;
+}
+
+// Alg. 3 on the remaining chain, then the final reduce (line 9).
+int run_ldp(ft_graph* g) {
+  std::vector<int> chain, ce;
+  int src = -1, live = 0;
+  for (int v = 0; v < g->n_ops; ++v) {
+    if (!g->op_alive[v]) continue;
+    ++live;
+    if (g->in_e[v].empty()) {
+      if (src >= 0) return setf(g, FT_EPRECOND, "graph is not linear (several sources)");
+      src = v;
+    }
+  }
+  if (src < 0) return setf(g, FT_EPRECOND, "graph is not linear (no source)");
+  for (int v = src;;) {
+    chain.push_back(v);
+    if (g->out_e[v].empty()) break;
+    if (g->out_e[v].size() != 1) return setf(g, FT_EPRECOND, "graph is not linear (fan-out)");
+    int e = *g->out_e[v].begin();
+    int d = g->edges[e].dst;
+    if (g->in_e[d].size() != 1) return setf(g, FT_EPRECOND, "graph is not linear (fan-in)");
+    ce.push_back(e);
+    v = d;
+  }
+  if ((int)chain.size() != live) return setf(g, FT_EPRECOND, "graph is not linear (disconnected)");
+  int cf = g->op_set[chain[0]];  // CF(o_1, s) = F(o_1, s)  (line 3)
+  for (size_t i = 1; i < chain.size(); ++i) {
+    StepRec r;
+    r.kind = ftk::K_LDP;  // line 6: U_k F(e,k,p) (x) CF(o_{i-1},k) (x) F(o_i,p)
+    r.X = g->edges[ce[i - 1]].set;
+    r.Y = cf;
+    r.Z = g->op_set[chain[i]];
+    r.KA = g->K[chain[i - 1]];
+    r.KB = g->K[chain[i]];
+    r.nseg = r.KB;
+    r.nblk = r.KA;
+    int out;
+    int rc = exec_step(g, r, &out);
+    if (rc) return rc;
+    g->sets[out].a_op = chain[i];
+    cf = out;
+  }
+  StepRec f;
+  f.kind = ftk::K_FINAL;  // line 9: reduce(U_s CF(o_n, s))
+  f.X = cf;
+  f.Y = 0;
+  f.Z = 0;
+  f.KA = g->K[chain.back()];
+  f.nseg = 1;
+  f.nblk = f.KA;
+  int out;
+  int rc = exec_step(g, f, &out);
+  if (rc) return rc;
+  g->final_set = out;
+  const FSet& F = g->sets[out];
+  int64_t n = F.off[1];
+  g->final_m.resize(n);
+  g->final_t.resize(n);
+  if (n) {
+    CU(cudaMemcpyAsync(g->final_m.data(), F.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    CU(cudaMemcpyAsync(g->final_t.data(), F.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    CU(cudaStreamSynchronize(g->stream), "d2h");
+  }
+  g->have_final = true;
+  return FT_OK;
+}
+
+// ---- unroll -----------------------------------------------------------
+
+int fetch_bp(ft_graph* g, FSet& s) {
+  if (s.h_bp_ok) return FT_OK;
+  int64_t n = s.off[s.nseg];
+  s.h_bp.resize(n);
+  if (n) {
+    CU(cudaMemcpy(s.h_bp.data(), s.d_bp, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost), "bp d2h");
+  }
+  s.h_bp_ok = true;
+  return FT_OK;
+}
+
+int put_cfg(ft_graph* g, std::vector<int32_t>& cfg, int op, int64_t c) {
+  if (op < 0) return FT_OK;
+  if (cfg[op] >= 0 && cfg[op] != c) {
+    g->poisoned = FT_EINTERNAL;
+    return setf(g, FT_EINTERNAL, "broken provenance (conflicting configs)");
+  }
+  cfg[op] = (int32_t)c;
+  return FT_OK;
+}
+
+int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_t>& cfg) {
+  struct Item {
+    int set;
+    int64_t seg, idx;
+  };
+  std::vector<Item> todo{{set0, seg0, idx0}};
+  while (!todo.empty()) {
+    Item it = todo.back();
+    todo.pop_back();
+    FSet& S = g->sets[it.set];
+    if (S.kind == S_UNIT) continue;
+    int rc;
+    if (S.b_op >= 0) {
+      int64_t kb = g->K[S.b_op];
+      if ((rc = put_cfg(g, cfg, S.a_op, it.seg / kb)) || (rc = put_cfg(g, cfg, S.b_op, it.seg % kb))) return rc;
+    } else if ((rc = put_cfg(g, cfg, S.a_op, it.seg))) {
+      return rc;
+    }
+    if (S.kind != S_STEP) continue;
+    if ((rc = fetch_bp(g, S))) return rc;
+    const StepRec& r = g->steps[S.step];
+    const uint64_t id = S.h_bp[S.off[it.seg] + it.idx];
+    const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+    uint64_t acc = 0;
+    bool found = false;
+    for (int64_t k = 0; k < r.nblk && !found; ++k) {
+      int64_t sx, sy, sz;
+      if (r.kind == ftk::K_NODE) {
+        int64_t wv = it.seg / r.KC, p = it.seg % r.KC;
+        sx = wv * r.KB + k; sy = k; sz = k * r.KC + p;
+      } else if (r.kind == ftk::K_LDP) {
+        sx = k * r.KB + it.seg; sy = k; sz = it.seg;
+      } else if (r.kind == ftk::K_FINAL) {
+        sx = k; sy = 0; sz = 0;
+      } else {
+        sx = it.seg; sy = it.seg; sz = 0;
+      }
+      uint64_t nx = X.off[sx + 1] - X.off[sx], ny = Y.off[sy + 1] - Y.off[sy],
+               nz = Z.off[sz + 1] - Z.off[sz];
+      uint64_t n = nx * ny * nz;
+      if (id < acc + n) {
+        uint64_t rr = id - acc;
+        todo.push_back({r.Z, sz, (int64_t)(rr % nz)});
+        todo.push_back({r.Y, sy, (int64_t)((rr / nz) % ny)});
+        todo.push_back({r.X, sx, (int64_t)(rr / (ny * nz))});
+        found = true;
+      }
+      acc += n;
+    }
+    if (!found) {
+      g->poisoned = FT_EINTERNAL;
+      return setf(g, FT_EINTERNAL, "broken provenance (id out of range)");
+    }
+  }
+  return FT_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* ft_version(void) { return "ft-b200 0.1 sm_100a"; }
+
+int ft_shard_plan(int64_t n, const int64_t* w, int32_t world, int64_t* bounds) {
+  if (n < 0 || world < 1 || !bounds || (n > 0 && !w)) return FT_EINVAL;
+  long double tot = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (w[i] < 0) return FT_EINVAL;
+    tot += (long double)w[i];
+  }
+  bounds[0] = 0;
+  long double acc = 0;
+  int64_t i = 0;
+  for (int q = 1; q < world; ++q) {
+    long double target = tot * q / world;
+    while (i < n && acc + (long double)w[i] / 2 <= target) acc += (long double)w[i++];
+    bounds[q] = std::max<int64_t>(i, bounds[q - 1]);
+  }
+  bounds[world] = n;
+  return FT_OK;
+}
+
+int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const int32_t* src,
+                    const int32_t* dst, const ft_options* opt, ft_graph** out) {
+  if (!out) return FT_EINVAL;
+  *out = nullptr;
+  if (n_ops < 1 || n_edges < 0 || !n_cfgs || (n_edges > 0 && (!src || !dst))) return FT_EINVAL;
+  if ((int64_t)n_ops + n_edges >= (1 << 20)) return FT_EOVERFLOW;
+  for (int i = 0; i < n_ops; ++i)
+    if (n_cfgs[i] < 1 || n_cfgs[i] > 4096) return FT_EINVAL;
+  for (int e = 0; e < n_edges; ++e)
+    if (src[e] < 0 || src[e] >= n_ops || dst[e] < 0 || dst[e] >= n_ops || src[e] == dst[e])
+      return FT_EINVAL;
+  ft_graph* g = new (std::nothrow) ft_graph();
+  if (!g) return FT_ENOMEM;
+  g->n_ops = n_ops;
+  g->n_orig_edges = n_edges;
+  g->K.assign(n_cfgs, n_cfgs + n_ops);
+  g->op_alive.assign(n_ops, 1);
+  g->in_e.resize(n_ops);
+  g->out_e.resize(n_ops);
+  g->op_m.resize(n_ops);
+  g->op_t.resize(n_ops);
+  g->op_ok.assign(n_ops, 0);
+  g->e_m.resize(n_edges);
+  g->e_t.resize(n_edges);
+  g->e_ok.assign(n_edges, 0);
+  FSet unit;
+  unit.kind = S_UNIT;
+  unit.nseg = 1;
+  unit.off = {0, 1};
+  g->sets.push_back(unit);
+  for (int i = 0; i < n_ops; ++i) {
+    FSet s;
+    s.kind = S_OP;
+    s.a_op = i;
+    s.nseg = g->K[i];
+    s.off.resize(s.nseg + 1);
+    for (int64_t q = 0; q <= s.nseg; ++q) s.off[q] = q;
+    g->op_set.push_back((int)g->sets.size());
+    g->sets.push_back(std::move(s));
+  }
+  for (int e = 0; e < n_edges; ++e) {
+    FSet s;
+    s.kind = S_EDGE;
+    s.a_op = src[e];
+    s.b_op = dst[e];
+    s.nseg = (int64_t)g->K[src[e]] * g->K[dst[e]];
+    s.off.resize(s.nseg + 1);
+    for (int64_t q = 0; q <= s.nseg; ++q) s.off[q] = q;
+    add_edge(g, src[e], dst[e], (int)g->sets.size());
+    g->sets.push_back(std::move(s));
+  }
+  if ((int)topo_order(g).size() != n_ops) {
+    delete g;
+    return FT_EINVAL;  // cycle
+  }
+  if (opt) {
+    g->dev = opt->device;
+    g->rank = opt->rank;
+    g->world = opt->world < 1 ? 1 : opt->world;
+    g->comm = (ncclComm_t)opt->nccl_comm;
+    g->keep_all = opt->keep_all != 0;
+    g->stream = (cudaStream_t)opt->stream;
+  }
+  if (g->world > 1 && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
+    delete g;
+    return FT_EINVAL;
+  }
+  cudaError_t e = cudaSetDevice(g->dev);
+  if (e == cudaSuccess && !g->stream) {
+    e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    g->own_stream = e == cudaSuccess;
+  }
+  if (e == cudaSuccess) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    e = g->runner.configure();
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete g;
+    return FT_ECUDA;
+  }
+  *out = g;
+  return FT_OK;
+}
+
+void ft_graph_destroy(ft_graph* g) {
+  if (!g) return;
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  for (auto& s : g->sets)
+    if (s.owned) {
+      if (s.d_m) cudaFree(s.d_m);
+      if (s.d_t) cudaFree(s.d_t);
+      if (s.d_bp) cudaFree(s.d_bp);
+      if (s.d_off) cudaFree(s.d_off);
+    }
+  if (g->d_costs) cudaFree(g->d_costs);
+  g->runner.release();
+  if (g->own_stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+int ft_set_op_costs(ft_graph* g, int32_t op, const int64_t* m, const int64_t* t) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (g->started) return setf(g, FT_ESTATE, "costs set after elimination began");
+  if (op < 0 || op >= g->n_ops || !m || !t) return setf(g, FT_EINVAL, "bad operator or null costs");
+  const int k = g->K[op];
+  for (int q = 0; q < k; ++q) {
+    if (m[q] < 0 || t[q] < 0) return setf(g, FT_EINVAL, "negative cost");
+    if (m[q] >= ((int64_t)1 << 40) || t[q] >= ((int64_t)1 << 40)) return setf(g, FT_EOVERFLOW, "cost >= 2^40");
+  }
+  g->op_m[op].assign(m, m + k);
+  g->op_t[op].assign(t, t + k);
+  g->op_ok[op] = 1;
+  return FT_OK;
+}
+
+int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t* t) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (g->started) return setf(g, FT_ESTATE, "costs set after elimination began");
+  if (edge < 0 || edge >= g->n_orig_edges || !t) return setf(g, FT_EINVAL, "bad edge or null costs");
+  const int64_t n = (int64_t)g->K[g->edges[edge].src] * g->K[g->edges[edge].dst];
+  for (int64_t q = 0; q < n; ++q) {
+    const int64_t mm = m ? m[q] : 0;
+    if (mm < 0 || t[q] < 0) return setf(g, FT_EINVAL, "negative cost");
+    if (mm >= ((int64_t)1 << 40) || t[q] >= ((int64_t)1 << 40)) return setf(g, FT_EOVERFLOW, "cost >= 2^40");
+  }
+  if (m) g->e_m[edge].assign(m, m + n);
+  else g->e_m[edge].assign(n, 0);
+  g->e_t[edge].assign(t, t + n);
+  g->e_ok[edge] = 1;
+  return FT_OK;
+}
+
+int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (new_edge) *new_edge = -1;
+  if (kind != FT_NODE && kind != FT_EDGE && kind != FT_AUTO) return setf(g, FT_EINVAL, "bad kind");
+  if (g->have_final) return setf(g, FT_ESTATE, "frontier already computed");
+  if (kind == FT_NODE) {
+    if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return setf(g, FT_EINVAL, "bad operator");
+    std::vector<int> order = topo_order(g);
+    std::vector<char> mk = mark_backbone(g, order);
+    if (mk[id] || g->in_e[id].size() != 1 || g->out_e[id].size() != 1)
+      return setf(g, FT_EPRECOND, "node elimination needs an unmarked op with one in- and one out-edge");
+    int rc = start(g);
+    if (rc) return rc;
+    return do_node(g, id, new_edge);
+  }
+  if (kind == FT_EDGE) {
+    if (id < 0 || id >= (int)g->edges.size() || !g->edges[id].alive) return setf(g, FT_EINVAL, "bad edge");
+    int other = -1;
+    for (int e : g->out_e[g->edges[id].src])
+      if (e != id && g->edges[e].dst == g->edges[id].dst) {
+        other = e;
+        break;
+      }
+    if (other < 0) return setf(g, FT_EPRECOND, "edge elimination needs a parallel edge");
+    int rc = start(g);
+    if (rc) return rc;
+    return do_merge(g, std::min(id, other), std::max(id, other), new_edge);
+  }
+  int rc = start(g);
+  if (rc) return rc;
+  for (;;) {
+    int r = auto_step(g);
+    if (r < 0) return r;
+    if (r == 0) break;
+  }
+  return FT_OK;
+}
+
+int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out) {
+  if (!g || !n_out) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  int rc = start(g);
+  if (rc) return rc;
+  if (!g->have_final && (rc = run_ldp(g))) return rc;
+  const int64_t n = (int64_t)g->final_m.size();
+  *n_out = n;
+  if (cap < n) return FT_ESIZE;
+  if (m_out) std::memcpy(m_out, g->final_m.data(), sizeof(int64_t) * n);
+  if (t_out) std::memcpy(t_out, g->final_t.data(), sizeof(int64_t) * n);
+  return FT_OK;
+}
+
+int ft_strategy(ft_graph* g, int64_t tuple_idx, int32_t* cfg_out) {
+  if (!g || !cfg_out) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (!g->have_final) return setf(g, FT_ESTATE, "call ft_frontier first");
+  if (tuple_idx < 0 || tuple_idx >= (int64_t)g->final_m.size()) return setf(g, FT_EINVAL, "bad tuple index");
+  std::vector<int32_t> cfg(g->n_ops, -1);
+  int rc = unroll(g, g->final_set, 0, tuple_idx, cfg);
+  if (rc) return rc;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (cfg[i] < 0) {
+      g->poisoned = FT_EINTERNAL;
+      return setf(g, FT_EINTERNAL, "broken provenance (operator without config)");
+    }
+  std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_ops);
+  return FT_OK;
+}
+
+int ft_get_stats(const ft_graph* g, ft_step_stats* buf, int64_t cap, int64_t* n_out) {
+  if (!g || !n_out) return FT_EINVAL;
+  *n_out = (int64_t)g->steps.size();
+  if (cap < *n_out) return FT_ESIZE;
+  for (size_t i = 0; i < g->steps.size(); ++i)
+    if (buf) buf[i] = g->steps[i].st;
+  return FT_OK;
+}
+
+int ft_step_output(ft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int64_t* m, int64_t* t,
+                   uint64_t* bp, int64_t* n_out) {
+  if (!g || !n_out) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (step < 0 || step >= (int64_t)g->steps.size()) return setf(g, FT_EINVAL, "bad step");
+  FSet& S = g->sets[g->steps[step].out];
+  const int64_t n = S.off[S.nseg];
+  *n_out = n;
+  if (cap < n) return FT_ESIZE;
+  if (seg_off) std::memcpy(seg_off, S.off.data(), sizeof(int64_t) * (S.nseg + 1));
+  if ((m || t) && !S.mt_live) return setf(g, FT_ESTATE, "m/t of a consumed set (create with keep_all)");
+  if (n) {
+    if (m) CU(cudaMemcpyAsync(m, S.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    if (t) CU(cudaMemcpyAsync(t, S.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    if (bp) CU(cudaMemcpyAsync(bp, S.d_bp, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    CU(cudaStreamSynchronize(g->stream), "d2h");
+  }
+  return FT_OK;
+}
+
+const char* ft_last_error(const ft_graph* g) { return g ? g->err.c_str() : "null handle"; }
+
+}  // extern "C"

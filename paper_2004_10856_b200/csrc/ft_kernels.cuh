@@ -1,0 +1,309 @@
+// ft_kernels.cuh -- sm_100a kernels of the FT hot path (arXiv 2004.10856).
+//
+// One FT step (node elimination Eq.4, edge elimination Eq.5
+// P:599-603, K=1 fold Eq.7, LDP step Alg.3 line 6 P:645, final
+// reduce Alg.3 line 9 P:648) computes, for every output segment sigma,
+//
+//     F_sigma = reduce( U_k  X_k (x) Y_k (x) Z_k )                    (R5)
+//
+// with Product (x), Union U and Reduce = Alg.1
+// under the key (m, t, id) (R1, R3, R6).  DESIGN.md "pipeline" explains the
+// exact sampled-staircase pre-filter used here; in short, per segment:
+//
+//   level D (coarsest sample, <= C_DIRECT tuples): direct CTA sort+scan.
+//   level l < D: G = frontier of the level-(l+1) sample (real tuples);
+//     K1 product kernel expands the level-l sample run by run, drops every
+//     tuple strictly dominated by G (a chunk at a time when possible) and
+//     bins survivors by G interval ("bucket");  K2 sorts each bucket by
+//     (m,t,id);  K3 applies Alg.1's running minimum with the bucket's carry
+//     (exclusive prefix-min over earlier buckets);  K4 compacts.
+//   Because G consists of real tuples of the segment, a tuple strictly
+//   dominated by G is beaten in Alg.1 and reduce(candidates) = reduce(all).
+//
+// No tensor cores: the path is integer compare/add work.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ftk {
+
+constexpr int64_t INF = INT64_MAX;
+constexpr int LMAX = 12;            // max sample level
+constexpr int C_DIRECT = 1024;      // direct (single-CTA) segment capacity
+constexpr int DIRECT_NT = 256;      // threads of the direct / bucket CTA kernels
+constexpr int CHUNK = 16;           // run elements per filter work item
+constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
+constexpr int BMIN_FILL = 0x7F;     // memset byte: 0x7F7F..7F > any t (< 2^60)
+
+enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5 };
+
+// A frontier set on the device (CSR): segment s = [off[s], off[s+1]).
+struct FacSet {
+  const int64_t* off;
+  const int64_t* m;
+  const int64_t* t;
+};
+
+struct StepDev {
+  int kind;
+  int slog;  // sample stride at level l = 2^(slog*l)
+  int64_t KA, KB, KC, nseg, nblk;
+  int64_t seg_lo, seg_hi;  // this rank's output segments [seg_lo, seg_hi)
+  FacSet X, Y, Z;
+};
+
+// Step header written by the plan kernel, read back by the host.
+struct StepHdr {
+  unsigned long long D;                       // max level over segments (atomicMax)
+  unsigned long long tuples;                  // product tuples of this rank's segments
+  unsigned long long direct_samp[LMAX + 1];   // sum of sample sizes of DIRECT segments at l
+  unsigned long long filter_samp[LMAX + 1];   // sum of sample sizes of FILTER segments at l
+  unsigned long long overflow;                // != 0: some capacity was exceeded
+  unsigned long long bad;                     // != 0: unsupported shape (nblk > C_DIRECT)
+  unsigned long long cand_total[LMAX + 1];    // candidates emitted per level (may exceed cap)
+  unsigned long long out_total[LMAX + 1];     // level outputs
+  unsigned long long bucket_total[LMAX + 1];  // buckets per level
+  unsigned long long huge;                    // buckets sorted by the global-memory path
+};
+
+// Per-level pool of per-segment results (G of the next finer level, or the
+// step output at level 0).
+struct Pool {
+  int64_t* m;
+  int64_t* t;
+  uint64_t* id;
+  int64_t* start;                 // [nseg]
+  int64_t* cnt;                   // [nseg]
+  unsigned long long* cursor;
+  int64_t cap;
+};
+
+struct LevelDev {
+  int level;
+  int64_t st;  // stride
+  const int32_t* seg_d;
+  const int64_t* blk_rel;
+  Pool in;     // level l+1 output (G), valid when level < D
+  Pool out;
+  // filter / bucket scratch
+  int64_t* nb;           // [nseg]  buckets per segment (g+1 for FILTER)
+  int64_t* bucket_base;  // [nseg+1]
+  int64_t* wcnt;         // [nblocks]
+  int64_t* wo;           // [nblocks+1]
+  unsigned int* bcount;  // [bcap]
+  long long* bmin;       // [bcap]
+  int64_t* boff;         // [bcap+1]
+  long long* bcarry;     // [bcap]
+  int64_t bcap;
+  int64_t* cm;
+  int64_t* ct;
+  uint64_t* cid;
+  int64_t* cgb;
+  unsigned int* cpos;
+  unsigned long long* cand_cursor;
+  int64_t cand_cap;
+  int64_t* gm;           // grouped (bucket-ordered) candidates
+  int64_t* gt;
+  uint64_t* gid;
+  int64_t* gflag;        // keep flags (0/1), scanned in place -> positions
+  int64_t* large_list;
+  unsigned long long* large_n;
+  int64_t* huge_list;
+  unsigned long long* huge_n;
+  int64_t* scratch;      // global-memory sort scratch (huge buckets)
+  int64_t scratch_cap;
+  StepHdr* hdr;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+
+__device__ __forceinline__ bool key_lt(int64_t am, int64_t at, uint64_t ai, int64_t bm, int64_t bt,
+                                       uint64_t bi) {
+  if (am != bm) return am < bm;
+  if (at != bt) return at < bt;
+  return ai < bi;
+}
+
+// Factor segments of block k of output segment sigma (Eq.4, Eq.5, Eq.7, Alg.3).
+__device__ __forceinline__ void block_factor_segs(const StepDev& s, int64_t sg, int64_t k,
+                                                  int64_t& sx, int64_t& sy, int64_t& sz) {
+  if (s.kind == K_NODE) {          // sigma = w*K_j + p ; X=F(e_hi,w,k) Y=F(o_i,k) Z=F(e_ij,k,p)
+    int64_t w = sg / s.KC, p = sg - w * s.KC;
+    sx = w * s.KB + k;
+    sy = k;
+    sz = k * s.KC + p;
+  } else if (s.kind == K_LDP) {    // sigma = p ; X=F(e,k,p) Y=CF(o_{i-1},k) Z=F(o_i,p)
+    sx = k * s.KB + sg;
+    sy = k;
+    sz = sg;
+  } else if (s.kind == K_FINAL) {  // X = CF(o_n, k)
+    sx = k;
+    sy = 0;
+    sz = 0;
+  } else {                         // K_EDGE (X=e1, Y=e2) / K_FOLD (X=o_j, Y=e, Z=o_src|unit)
+    sx = sg;
+    sy = sg;
+    sz = 0;
+  }
+}
+
+struct Blk {
+  int64_t o[3];
+  int64_t n[3];
+};
+
+__device__ __forceinline__ Blk load_blk(const StepDev& s, int64_t sg, int64_t k) {
+  int64_t sx, sy, sz;
+  block_factor_segs(s, sg, k, sx, sy, sz);
+  Blk b;
+  b.o[0] = s.X.off[sx];
+  b.n[0] = s.X.off[sx + 1] - b.o[0];
+  b.o[1] = s.Y.off[sy];
+  b.n[1] = s.Y.off[sy + 1] - b.o[1];
+  b.o[2] = s.Z.off[sz];
+  b.n[2] = s.Z.off[sz + 1] - b.o[2];
+  return b;
+}
+
+// Sampled index set at stride st: {0, st, 2st, ...} U {n-1}.
+__device__ __forceinline__ int64_t samp_cnt(int64_t n, int64_t st) {
+  if (st == 1 || n <= 1) return n;
+  int64_t c = (n + st - 1) / st;
+  if ((n - 1) % st) ++c;
+  return c;
+}
+__device__ __forceinline__ int64_t samp_idx(int64_t j, int64_t n, int64_t st) {
+  int64_t c0 = (n + st - 1) / st;
+  return j < c0 ? j * st : n - 1;
+}
+
+__device__ __forceinline__ const int64_t* fac_m(const StepDev& s, int f) {
+  return f == 0 ? s.X.m : (f == 1 ? s.Y.m : s.Z.m);
+}
+__device__ __forceinline__ const int64_t* fac_t(const StepDev& s, int f) {
+  return f == 0 ? s.X.t : (f == 1 ? s.Y.t : s.Z.t);
+}
+
+// Product tuple for actual factor indices (x, y, z) of block b; id =
+// lexicographic (k, x, y, z) rank within the segment (R6).
+__device__ __forceinline__ void make_tuple(const StepDev& s, const Blk& b, int64_t rel, int64_t x,
+                                           int64_t y, int64_t z, int64_t& m, int64_t& t,
+                                           uint64_t& id) {
+  m = __ldg(s.X.m + b.o[0] + x) + __ldg(s.Y.m + b.o[1] + y) + __ldg(s.Z.m + b.o[2] + z);
+  t = __ldg(s.X.t + b.o[0] + x) + __ldg(s.Y.t + b.o[1] + y) + __ldg(s.Z.t + b.o[2] + z);
+  id = (uint64_t)(rel + (x * b.n[1] + y) * b.n[2] + z);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_sum(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+__device__ __forceinline__ long long warp_incl_min(long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    long long u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v = u < v ? u : v;
+  }
+  return v;
+}
+
+// Block-wide exclusive scans (all threads must call).  sh: >= 33 slots.
+template <int NT>
+__device__ __forceinline__ long long block_excl_min(long long v, long long* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long inc = warp_incl_min(v);
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = lane < NT / 32 ? sh[lane] : INF;
+    long long wi = warp_incl_min(w);
+    long long we = __shfl_up_sync(0xffffffffu, wi, 1);
+    if (lane == 0) we = INF;
+    if (lane < NT / 32) sh[lane] = we;
+  }
+  __syncthreads();
+  long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) ex = INF;
+  long long wpre = sh[wid];
+  __syncthreads();
+  return ex < wpre ? ex : wpre;
+}
+template <int NT>
+__device__ __forceinline__ long long block_excl_sum(long long v, long long* sh, long long* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long inc = warp_incl_sum(v);
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = lane < NT / 32 ? sh[lane] : 0;
+    long long wi = warp_incl_sum(w);
+    if (lane < NT / 32) sh[lane] = wi - w;
+    if (lane == NT / 32 - 1) sh[32] = wi;
+  }
+  __syncthreads();
+  long long r = inc - v + sh[wid];
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// Bitonic sort of N (power of 2) keys in shared memory, ascending (m, t, id).
+template <int NT>
+__device__ void bitonic_smem(int64_t* m, int64_t* t, uint64_t* id, int N) {
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += NT) {
+        int l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          bool gt = key_lt(m[l], t[l], id[l], m[i], t[i], id[i]);
+          if (gt == up) {
+            int64_t a = m[i]; m[i] = m[l]; m[l] = a;
+            a = t[i]; t[i] = t[l]; t[l] = a;
+            uint64_t b = id[i]; id[i] = id[l]; id[l] = b;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Alg.1 sweep over n sorted keys in smem with carry-in v0 (lines 4-8,
+// P:490-494): keep[i] = t[i] < min(v0, t[0..i-1]).  Each thread owns a
+// contiguous range.  Writes keep flags into kf (int smem), returns count.
+template <int NT>
+__device__ int alg1_sweep_smem(const int64_t* t, int n, long long v0, int* kf, long long* sh) {
+  const int per = (n + NT - 1) / NT;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  long long lmin = INF;
+  for (int i = lo; i < hi; ++i) lmin = t[i] < lmin ? t[i] : lmin;
+  long long pre = block_excl_min<NT>(lmin, sh);
+  long long v = pre < v0 ? pre : v0;
+  int c = 0;
+  for (int i = lo; i < hi; ++i) {
+    int k = t[i] < v;
+    kf[i] = k;
+    c += k;
+    if (k) v = t[i];
+  }
+  long long tot;
+  long long off = block_excl_sum<NT>(c, sh, &tot);
+  // convert flags to output positions (+1; 0 = dropped)
+  int p = (int)off;
+  for (int i = lo; i < hi; ++i) {
+    if (kf[i]) kf[i] = ++p;
+  }
+  __syncthreads();
+  return (int)tot;
+}
+
+}  // namespace ftk

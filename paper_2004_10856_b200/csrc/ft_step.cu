@@ -1,0 +1,946 @@
+// ft_step.cu -- one FT step on the GPU: plan (K0), per-level product +
+// dominance pre-filter (K1), bucket sort (K2), Alg.1 sweep (K3), compaction
+// (K4), final gather.  See ft_kernels.cuh for the algorithm and DESIGN.md.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ft_kernels.cuh"
+#include "ft_step.h"
+
+namespace ftk {
+
+// ---------------------------------------------------------------------------
+// Generic exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, n]; n read
+// from *n_dev when given (device-resident counts), else n_host.
+
+constexpr int SCAN_NT = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_NT * SCAN_ITEMS;
+
+template <typename TIn>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_tiles(const TIn* in, const int64_t* n_dev,
+                                                        int64_t n_host, int64_t* tile_sums) {
+  __shared__ long long sh[33];
+  const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
+  const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i)
+      if (base + i < n) s += (long long)in[base + i];
+    long long tot;
+    block_excl_sum<SCAN_NT>(s, sh, &tot);
+    if (threadIdx.x == 0) tile_sums[tile] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(int64_t* tile_sums, const int64_t* n_dev,
+                                                    int64_t n_host) {
+  __shared__ long long sh[33];
+  const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
+  const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  long long carry = 0;
+  for (int64_t b = 0; b < ntiles; b += 1024) {
+    int64_t i = b + threadIdx.x;
+    long long v = i < ntiles ? tile_sums[i] : 0;
+    long long tot;
+    long long ex = block_excl_sum<1024>(v, sh, &tot);
+    if (i < ntiles) tile_sums[i] = ex + carry;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) tile_sums[ntiles] = carry;
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_apply(const TIn* in, const int64_t* n_dev,
+                                                        int64_t n_host, const int64_t* tile_sums,
+                                                        int64_t* out) {
+  __shared__ long long sh[33];
+  const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
+  const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    long long v[SCAN_ITEMS];
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      v[i] = base + i < n ? (long long)in[base + i] : 0;
+      s += v[i];
+    }
+    long long tot;
+    long long ex = block_excl_sum<SCAN_NT>(s, sh, &tot) + tile_sums[tile];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      if (base + i < n) out[base + i] = ex;
+      ex += v[i];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_sums[ntiles];
+}
+
+template <typename TIn>
+void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
+               cudaStream_t st) {
+  int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 8));
+  k_scan_tiles<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, tmp);
+  k_scan_sums<<<1, 1024, 0, st>>>(tmp, n_dev, n_cap);
+  k_scan_apply<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, tmp, out);
+}
+
+// ---------------------------------------------------------------------------
+// K0: plan.  One thread per output segment: block offsets relative to the
+// segment (ids, R6), sample sizes per level, the level at which the segment
+// is small enough for the direct path.
+
+__global__ void k_plan(StepDev s, int32_t* seg_d, int64_t* blk_rel, int64_t* seg_tuples,
+                       StepHdr* hdr) {
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  const int64_t sg = s.seg_lo + i;
+  unsigned long long samp[LMAX + 1];
+#pragma unroll
+  for (int l = 0; l <= LMAX; ++l) samp[l] = 0;
+  int64_t rel = 0;
+  for (int64_t k = 0; k < s.nblk; ++k) {
+    Blk b = load_blk(s, sg, k);
+    blk_rel[i * s.nblk + k] = rel;
+    rel += b.n[0] * b.n[1] * b.n[2];
+#pragma unroll
+    for (int l = 0; l <= LMAX; ++l) {
+      int64_t st = (int64_t)1 << (s.slog * l);
+      samp[l] += (unsigned long long)(samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) *
+                                      samp_cnt(b.n[2], st));
+    }
+  }
+  int d = -1;
+  for (int l = 0; l <= LMAX; ++l)
+    if (samp[l] <= (unsigned long long)C_DIRECT) {
+      d = l;
+      break;
+    }
+  if (d < 0 || s.nblk > C_DIRECT) {
+    atomicExch(&hdr->bad, 1ull);
+    d = LMAX;
+  }
+  seg_d[i] = d;
+  seg_tuples[i] = rel;
+  atomicMax(&hdr->D, (unsigned long long)d);
+  atomicAdd(&hdr->tuples, (unsigned long long)rel);
+  for (int l = 0; l < d; ++l) atomicAdd(&hdr->filter_samp[l], samp[l]);
+  atomicAdd(&hdr->direct_samp[d], samp[d]);
+}
+
+// ---------------------------------------------------------------------------
+// Direct path: the whole level-l sample of a segment (<= C_DIRECT tuples) in
+// one CTA: product -> bitonic sort on (m,t,id) -> Alg.1 sweep -> compaction.
+
+__global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
+  __shared__ int64_t sm[C_DIRECT];
+  __shared__ int64_t stt[C_DIRECT];
+  __shared__ uint64_t sid[C_DIRECT];
+  __shared__ int kf[C_DIRECT];
+  __shared__ int64_t pre[C_DIRECT + 1];
+  __shared__ long long sh[33];
+  __shared__ int64_t s_start;
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t st = L.st;
+  for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
+    if (L.seg_d[li] != L.level) continue;
+    if (L.hdr->overflow) return;
+    const int64_t sg = s.seg_lo + li;
+    const int nblk = (int)s.nblk;
+    // block sample sizes -> inclusive prefix in pre[1..nblk]
+    for (int k = threadIdx.x; k < nblk; k += DIRECT_NT) {
+      Blk b = load_blk(s, sg, k);
+      pre[k + 1] = samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) * samp_cnt(b.n[2], st);
+    }
+    if (threadIdx.x == 0) pre[0] = 0;
+    __syncthreads();
+    {
+      const int per = (nblk + DIRECT_NT - 1) / DIRECT_NT;
+      const int lo = min(nblk, (int)threadIdx.x * per), hi = min(nblk, lo + per);
+      long long loc = 0;
+      for (int k = lo; k < hi; ++k) loc += pre[k + 1];
+      long long tot;
+      long long off = block_excl_sum<DIRECT_NT>(loc, sh, &tot);
+      for (int k = lo; k < hi; ++k) {
+        off += pre[k + 1];
+        pre[k + 1] = off;
+      }
+      __syncthreads();
+    }
+    const int n = (int)pre[nblk];
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
+      if (i < n) {
+        int lo = 0, hi = nblk;  // largest k with pre[k] <= i
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (pre[mid] <= i) lo = mid;
+          else hi = mid;
+        }
+        const int k = lo;
+        Blk b = load_blk(s, sg, k);
+        int64_t r = i - pre[k];
+        int64_t cy = samp_cnt(b.n[1], st), cz = samp_cnt(b.n[2], st);
+        int64_t jz = r % cz, jy = (r / cz) % cy, jx = r / (cy * cz);
+        int64_t x = samp_idx(jx, b.n[0], st), y = samp_idx(jy, b.n[1], st),
+                z = samp_idx(jz, b.n[2], st);
+        make_tuple(s, b, L.blk_rel[li * s.nblk + k], x, y, z, sm[i], stt[i], sid[i]);
+      } else {
+        sm[i] = INF;
+        stt[i] = INF;
+        sid[i] = ~0ull;
+      }
+    }
+    __syncthreads();
+    bitonic_smem<DIRECT_NT>(sm, stt, sid, N);
+    const int cnt = alg1_sweep_smem<DIRECT_NT>(stt, n, INF, kf, sh);
+    if (threadIdx.x == 0) {
+      unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
+      if ((int64_t)(st0 + cnt) > L.out.cap) {
+        atomicExch(&L.hdr->overflow, 1ull);
+        s_start = -1;
+      } else {
+        s_start = (int64_t)st0;
+      }
+      atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)cnt);
+      L.out.start[li] = s_start;
+      L.out.cnt[li] = cnt;
+    }
+    __syncthreads();
+    const int64_t o = s_start;
+    if (o >= 0)
+      for (int i = threadIdx.x; i < n; i += DIRECT_NT)
+        if (kf[i]) {
+          int64_t d = o + kf[i] - 1;
+          L.out.m[d] = sm[i];
+          L.out.t[d] = stt[i];
+          L.out.id[d] = sid[i];
+        }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Filter path, level l < d_sigma.
+
+__global__ void k_level_prep(StepDev s, LevelDev L) {
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  L.nb[i] = L.seg_d[i] > L.level ? L.in.cnt[i] + 1 : 0;
+}
+
+__global__ void k_check_buckets(StepDev s, LevelDev L) {
+  const int64_t B = L.bucket_base[s.seg_hi - s.seg_lo];
+  L.hdr->bucket_total[L.level] = B;
+  if (B > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
+  *L.large_n = 0;
+  *L.huge_n = 0;
+}
+
+// Long factor = the one with most sampled indices; runs = product of the other two.
+__device__ __forceinline__ void run_shape(const Blk& b, int64_t st, int& lf, int& fa, int& fb,
+                                          int64_t* c) {
+  c[0] = samp_cnt(b.n[0], st);
+  c[1] = samp_cnt(b.n[1], st);
+  c[2] = samp_cnt(b.n[2], st);
+  lf = 0;
+  if (c[1] > c[lf]) lf = 1;
+  if (c[2] > c[lf]) lf = 2;
+  fa = lf == 0 ? 1 : 0;
+  fb = lf == 2 ? 1 : 2;
+}
+
+__global__ void k_work_count(StepDev s, LevelDev L) {
+  const int64_t nbl = (s.seg_hi - s.seg_lo) * s.nblk;
+  const int64_t beta = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (beta >= nbl) return;
+  const int64_t li = beta / s.nblk, k = beta - li * s.nblk;
+  int64_t w = 0;
+  if (L.seg_d[li] > L.level) {
+    Blk b = load_blk(s, s.seg_lo + li, k);
+    int lf, fa, fb;
+    int64_t c[3];
+    run_shape(b, L.st, lf, fa, fb, c);
+    w = c[fa] * c[fb] * ((c[lf] + CHUNK - 1) / CHUNK);
+  }
+  L.wcnt[beta] = w;
+}
+
+// K1: product + pre-filter.  Each work item = CHUNK consecutive sampled
+// indices of one run (fixed short-factor indices, long factor sweeping: m
+// strictly ascending, t strictly descending).  A tuple is dropped iff some G
+// point strictly dominates it (m_g <= m, t_g <= t, (m_g,t_g) != (m,t)); a
+// whole chunk is dropped when the G point just below its first m has t <=
+// the chunk's last (smallest) t.
+__global__ void __launch_bounds__(256) k_filter(StepDev s, LevelDev L) {
+  if (L.hdr->overflow) return;
+  const int64_t nbl = (s.seg_hi - s.seg_lo) * s.nblk;
+  const int64_t W = L.wo[nbl];
+  const int lane = threadIdx.x & 31;
+  const int64_t st = L.st;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < W; base += gstride) {
+    const int64_t w = base + threadIdx.x;
+    bool act = w < W;
+    Blk b;
+    int lf = 0, fa = 1, fb = 2;
+    int64_t c[3] = {0, 0, 0};
+    int64_t ia = 0, ib = 0, j0 = 0, j1 = 0, rel = 0, ms = 0, ts = 0, g = 0, bb = 0, p = 0;
+    const int64_t *Lm = nullptr, *Lt = nullptr, *Gm = nullptr, *Gt = nullptr;
+    if (act) {
+      int64_t lo = 0, hi = nbl;  // largest beta with wo[beta] <= w
+      while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (L.wo[mid] <= w) lo = mid;
+        else hi = mid;
+      }
+      const int64_t beta = lo, wl = w - L.wo[beta];
+      const int64_t li = beta / s.nblk, k = beta - li * s.nblk;
+      b = load_blk(s, s.seg_lo + li, k);
+      rel = L.blk_rel[beta];
+      run_shape(b, st, lf, fa, fb, c);
+      const int64_t nch = (c[lf] + CHUNK - 1) / CHUNK;
+      const int64_t run = wl / nch, ch = wl - run * nch;
+      const int64_t ja = run / c[fb], jb = run - ja * c[fb];
+      ia = samp_idx(ja, b.n[fa], st);
+      ib = samp_idx(jb, b.n[fb], st);
+      ms = __ldg(fac_m(s, fa) + b.o[fa] + ia) + __ldg(fac_m(s, fb) + b.o[fb] + ib);
+      ts = __ldg(fac_t(s, fa) + b.o[fa] + ia) + __ldg(fac_t(s, fb) + b.o[fb] + ib);
+      Lm = fac_m(s, lf) + b.o[lf];
+      Lt = fac_t(s, lf) + b.o[lf];
+      j0 = ch * CHUNK;
+      j1 = min(j0 + CHUNK, c[lf]);
+      Gm = L.in.m + L.in.start[li];
+      Gt = L.in.t + L.in.start[li];
+      g = L.in.cnt[li];
+      bb = L.bucket_base[li];
+      const int64_t mf = ms + __ldg(Lm + samp_idx(j0, b.n[lf], st));
+      const int64_t tl = ts + __ldg(Lt + samp_idx(j1 - 1, b.n[lf], st));
+      int64_t q0 = 0, q1 = g;  // q = #G with m < mf
+      while (q0 < q1) {
+        int64_t mid = (q0 + q1) >> 1;
+        if (Gm[mid] < mf) q0 = mid + 1;
+        else q1 = mid;
+      }
+      if (q0 > 0 && Gt[q0 - 1] <= tl) act = false;  // whole chunk strictly dominated
+      p = q0;
+    }
+    for (int e = 0; e < CHUNK; ++e) {
+      const int64_t j = j0 + e;
+      bool cand = false;
+      int64_t m = 0, t = 0, gb = 0;
+      uint64_t id = 0;
+      if (act && j < j1) {
+        const int64_t il = samp_idx(j, b.n[lf], st);
+        m = ms + __ldg(Lm + il);
+        t = ts + __ldg(Lt + il);
+        while (p < g && Gm[p] <= m) ++p;
+        const bool dom = p > 0 && (Gt[p - 1] < t || (Gt[p - 1] == t && Gm[p - 1] < m));
+        if (!dom) {
+          cand = true;
+          int64_t idx3[3];
+          idx3[lf] = il;
+          idx3[fa] = ia;
+          idx3[fb] = ib;
+          id = (uint64_t)(rel + (idx3[0] * b.n[1] + idx3[1]) * b.n[2] + idx3[2]);
+          gb = bb + p;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, cand);
+      if (bal) {
+        const int leader = __ffs(bal) - 1;
+        unsigned long long bpos = 0;
+        if (lane == leader) bpos = atomicAdd(L.cand_cursor, (unsigned long long)__popc(bal));
+        bpos = __shfl_sync(0xffffffffu, bpos, leader);
+        if (cand) {
+          const unsigned long long idx = bpos + __popc(bal & ((1u << lane) - 1u));
+          if ((int64_t)idx < L.cand_cap) {
+            const unsigned pos = atomicAdd(L.bcount + gb, 1u);
+            atomicMin(L.bmin + gb, (long long)t);
+            L.cm[idx] = m;
+            L.ct[idx] = t;
+            L.cid[idx] = id;
+            L.cgb[idx] = gb;
+            L.cpos[idx] = pos;
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_check_cand(LevelDev L) {
+  unsigned long long c = *L.cand_cursor;
+  L.hdr->cand_total[L.level] = c;
+  if ((int64_t)c > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
+}
+
+// Carry per bucket: exclusive prefix-min of bucket minima within the segment
+// (the running minimum v of Alg.1 entering each bucket).
+__global__ void __launch_bounds__(256) k_carry(StepDev s, LevelDev L) {
+  __shared__ long long sh[33];
+  __shared__ long long chunk_min;
+  if (L.hdr->overflow) return;
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
+    if (L.seg_d[li] <= L.level) continue;
+    const int64_t b0 = L.bucket_base[li], nb = L.nb[li];
+    long long carry = INF;
+    for (int64_t c0 = 0; c0 < nb; c0 += 256) {
+      const int64_t i = c0 + threadIdx.x;
+      const long long v = i < nb ? L.bmin[b0 + i] : INF;
+      const long long ex = block_excl_min<256>(v, sh);
+      if (i < nb) L.bcarry[b0 + i] = ex < carry ? ex : carry;
+      if (threadIdx.x == 255) chunk_min = v < ex ? v : ex;
+      __syncthreads();
+      carry = chunk_min < carry ? chunk_min : carry;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_scatter(LevelDev L, const int64_t* ncand) {
+  if (L.hdr->overflow) return;
+  const int64_t n = *ncand;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = L.boff[L.cgb[i]] + L.cpos[i];
+    L.gm[d] = L.cm[i];
+    L.gt[d] = L.ct[i];
+    L.gid[d] = L.cid[i];
+  }
+}
+
+__global__ void k_clamp_cand(LevelDev L, int64_t* ncand) {
+  unsigned long long c = *L.cand_cursor;
+  *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
+}
+
+// K2+K3 for buckets of <= 32 candidates: one warp per bucket, rank sort by
+// shuffles, Alg.1 sweep with the bucket's carry.
+__global__ void __launch_bounds__(256) k_bucket_small(StepDev s, LevelDev L) {
+  __shared__ int64_t wm[8][32];
+  __shared__ int64_t wt[8][32];
+  __shared__ uint64_t wi[8][32];
+  if (L.hdr->overflow) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t B = min(L.bucket_base[s.seg_hi - s.seg_lo], L.bcap);
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t bkt = (int64_t)blockIdx.x * 8 + wid; bkt < B; bkt += nw) {
+    const int64_t c = L.bcount[bkt];
+    if (c == 0) continue;
+    if (c > 32) {
+      if (lane == 0) L.large_list[atomicAdd(L.large_n, 1ull)] = bkt;
+      continue;
+    }
+    const int64_t base = L.boff[bkt];
+    int64_t m = INF, t = INF;
+    uint64_t id = ~0ull;
+    if (lane < c) {
+      m = L.gm[base + lane];
+      t = L.gt[base + lane];
+      id = L.gid[base + lane];
+    }
+    int rank = 0;
+    for (int j = 0; j < 32; ++j) {
+      int64_t mj = __shfl_sync(0xffffffffu, m, j);
+      int64_t tj = __shfl_sync(0xffffffffu, t, j);
+      uint64_t ij = __shfl_sync(0xffffffffu, id, j);
+      rank += key_lt(mj, tj, ij, m, t, id) ? 1 : 0;
+    }
+    wm[wid][rank] = m;
+    wt[wid][rank] = t;
+    wi[wid][rank] = id;
+    __syncwarp();
+    m = wm[wid][lane];
+    t = wt[wid][lane];
+    id = wi[wid][lane];
+    __syncwarp();
+    long long inc = warp_incl_min(t);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long carry = L.bcarry[bkt];
+    const long long v = ex < carry ? ex : carry;
+    if (lane < c) {
+      L.gm[base + lane] = m;
+      L.gt[base + lane] = t;
+      L.gid[base + lane] = id;
+      L.gflag[base + lane] = t < v ? 1 : 0;
+    }
+  }
+}
+
+// K2+K3 for buckets of 33..BUCKET_SMEM candidates: one CTA, bitonic in smem.
+__global__ void __launch_bounds__(DIRECT_NT) k_bucket_large(LevelDev L) {
+  extern __shared__ int64_t dyn[];
+  int64_t* sm = dyn;
+  int64_t* stt = sm + BUCKET_SMEM;
+  uint64_t* sid = (uint64_t*)(stt + BUCKET_SMEM);
+  int* kf = (int*)(sid + BUCKET_SMEM);
+  __shared__ long long sh[33];
+  if (L.hdr->overflow) return;
+  const int64_t nl = *L.large_n;
+  for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
+    const int64_t bkt = L.large_list[e];
+    const int64_t c = L.bcount[bkt];
+    if (c > BUCKET_SMEM) {
+      if (threadIdx.x == 0) L.huge_list[atomicAdd(L.huge_n, 1ull)] = bkt;
+      continue;
+    }
+    const int64_t base = L.boff[bkt];
+    int N = 1;
+    while (N < c) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
+      if (i < c) {
+        sm[i] = L.gm[base + i];
+        stt[i] = L.gt[base + i];
+        sid[i] = L.gid[base + i];
+      } else {
+        sm[i] = INF;
+        stt[i] = INF;
+        sid[i] = ~0ull;
+      }
+    }
+    __syncthreads();
+    bitonic_smem<DIRECT_NT>(sm, stt, sid, N);
+    alg1_sweep_smem<DIRECT_NT>(stt, (int)c, L.bcarry[bkt], kf, sh);
+    for (int i = threadIdx.x; i < c; i += DIRECT_NT) {
+      L.gm[base + i] = sm[i];
+      L.gt[base + i] = stt[i];
+      L.gid[base + i] = sid[i];
+      L.gflag[base + i] = kf[i] ? 1 : 0;
+    }
+    __syncthreads();
+  }
+}
+
+// K2+K3 for huge buckets (> BUCKET_SMEM): one CTA; smem-sorted tiles, then
+// pairwise merges through the (dead) candidate arrays as scratch.
+__global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
+  extern __shared__ int64_t dyn[];
+  int64_t* sm = dyn;
+  int64_t* stt = sm + BUCKET_SMEM;
+  uint64_t* sid = (uint64_t*)(stt + BUCKET_SMEM);
+  __shared__ long long sh[33];
+  if (L.hdr->overflow) return;
+  const int64_t nh = *L.huge_n;
+  for (int64_t e = blockIdx.x; e < nh; e += gridDim.x) {
+    const int64_t bkt = L.huge_list[e];
+    const int64_t c = L.bcount[bkt];
+    const int64_t base = L.boff[bkt];
+    if (threadIdx.x == 0) atomicAdd(&L.hdr->huge, 1ull);
+    // 1) sort tiles of BUCKET_SMEM
+    for (int64_t t0 = 0; t0 < c; t0 += BUCKET_SMEM) {
+      const int64_t n = min((int64_t)BUCKET_SMEM, c - t0);
+      for (int i = threadIdx.x; i < BUCKET_SMEM; i += 1024) {
+        if (i < n) {
+          sm[i] = L.gm[base + t0 + i];
+          stt[i] = L.gt[base + t0 + i];
+          sid[i] = L.gid[base + t0 + i];
+        } else {
+          sm[i] = INF;
+          stt[i] = INF;
+          sid[i] = ~0ull;
+        }
+      }
+      __syncthreads();
+      bitonic_smem<1024>(sm, stt, sid, BUCKET_SMEM);
+      for (int i = threadIdx.x; i < n; i += 1024) {
+        L.gm[base + t0 + i] = sm[i];
+        L.gt[base + t0 + i] = stt[i];
+        L.gid[base + t0 + i] = sid[i];
+      }
+      __syncthreads();
+    }
+    // 2) merge passes: src/dst alternate between grouped and candidate arrays
+    int64_t *am = L.gm + base, *at = L.gt + base;
+    uint64_t* ai = L.gid + base;
+    int64_t *bm = L.cm + base, *bt = L.ct + base;
+    uint64_t* bi = L.cid + base;
+    for (int64_t wdt = BUCKET_SMEM; wdt < c; wdt <<= 1) {
+      for (int64_t i = threadIdx.x; i < c; i += 1024) {
+        const int64_t r0 = (i / (2 * wdt)) * 2 * wdt;
+        const int64_t mid = min(r0 + wdt, c), r1 = min(r0 + 2 * wdt, c);
+        const bool left = i < mid;
+        const int64_t o0 = left ? mid : r0, o1 = left ? r1 : mid;
+        // rank of key i in the other run
+        int64_t lo = o0, hi = o1;
+        while (lo < hi) {
+          int64_t q = (lo + hi) >> 1;
+          if (key_lt(am[q], at[q], ai[q], am[i], at[i], ai[i])) lo = q + 1;
+          else hi = q;
+        }
+        const int64_t pos = r0 + (left ? (i - r0) : (i - mid)) + (lo - o0);
+        bm[pos] = am[i];
+        bt[pos] = at[i];
+        bi[pos] = ai[i];
+      }
+      __syncthreads();
+      int64_t* x = am; am = bm; bm = x;
+      x = at; at = bt; bt = x;
+      uint64_t* y = ai; ai = bi; bi = y;
+    }
+    if (am != L.gm + base) {
+      for (int64_t i = threadIdx.x; i < c; i += 1024) {
+        L.gm[base + i] = am[i];
+        L.gt[base + i] = at[i];
+        L.gid[base + i] = ai[i];
+      }
+      __syncthreads();
+    }
+    // 3) Alg.1 sweep in chunks with carry
+    long long carry = L.bcarry[bkt];
+    __shared__ long long s_carry;
+    for (int64_t c0 = 0; c0 < c; c0 += 1024) {
+      const int64_t i = c0 + threadIdx.x;
+      const long long v = i < c ? L.gt[base + i] : INF;
+      long long ex = block_excl_min<1024>(v, sh);
+      long long pv = ex < carry ? ex : carry;
+      if (i < c) L.gflag[base + i] = v < pv ? 1 : 0;
+      if (threadIdx.x == 1023) s_carry = v < pv ? v : pv;
+      __syncthreads();
+      carry = s_carry;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_compact_base(LevelDev L, const int64_t* ncand) {
+  const int64_t n = *ncand;
+  const int64_t tot = L.gflag[n];  // after in-place scan: gflag holds positions, [n] = total
+  unsigned long long b = atomicAdd(L.out.cursor, (unsigned long long)tot);
+  if ((int64_t)(b + tot) > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+  atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
+  L.wcnt[0] = (int64_t)b;  // stash base (wcnt is dead after the work scan)
+}
+
+__global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand) {
+  if (L.hdr->overflow) return;
+  const int64_t n = *ncand;
+  const int64_t base = L.wcnt[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (gpos[i + 1] != gpos[i]) {
+      const int64_t d = base + gpos[i];
+      L.out.m[d] = L.gm[i];
+      L.out.t[d] = L.gt[i];
+      L.out.id[d] = L.gid[i];
+    }
+  }
+}
+
+__global__ void k_seg_out(StepDev s, LevelDev L, const int64_t* gpos) {
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= nloc || L.seg_d[li] <= L.level) return;
+  const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
+  const int64_t lo = L.boff[b0], hi = L.boff[b1];
+  L.out.start[li] = L.wcnt[0] + gpos[lo];
+  L.out.cnt[li] = gpos[hi] - gpos[lo];
+}
+
+// Final gather of the level-0 pool into the step's CSR output set.
+__global__ void k_gather(StepDev s, Pool P, const int64_t* dst_off, int64_t* om, int64_t* ot,
+                         uint64_t* obp) {
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
+    const int64_t src = P.start[li], n = P.cnt[li], d = dst_off[li];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      om[d + i] = P.m[src + i];
+      ot[d + i] = P.t[src + i];
+      obp[d + i] = P.id[src + i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+
+static cudaError_t grow_raw(void** p, size_t* have, size_t need) {
+  if (need <= *have && *p) return cudaSuccess;
+  if (*p) {
+    cudaError_t e = cudaFree(*p);
+    if (e != cudaSuccess) return e;
+    *p = nullptr;
+    *have = 0;
+  }
+  size_t nb = std::max<size_t>(need, 256);
+  cudaError_t e = cudaMalloc(p, nb);
+  if (e == cudaSuccess) *have = nb;
+  return e;
+}
+
+#define GROW(buf, T, n)                                                         \
+  do {                                                                          \
+    cudaError_t e__ = grow_raw((void**)&buf.p, &buf.bytes, sizeof(T) * (size_t)(n)); \
+    if (e__ != cudaSuccess) return e__;                                         \
+  } while (0)
+
+StepRunner::StepRunner() {}
+StepRunner::~StepRunner() { release(); }
+
+void StepRunner::release() {
+  Buf* all[] = {&seg_d, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
+                &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
+                &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
+                &cgb, &cpos, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
+                &dst_off};
+  for (Buf* b : all) {
+    if (b->p) cudaFree(b->p);
+    b->p = nullptr;
+    b->bytes = 0;
+  }
+  if (hdr_host) cudaFreeHost(hdr_host);
+  hdr_host = nullptr;
+  if (cnt_host) cudaFreeHost(cnt_host);
+  cnt_host = nullptr;
+  cnt_host_n = 0;
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  ev0 = ev1 = nullptr;
+}
+
+static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
+  int64_t g = (n + nt - 1) / nt;
+  if (g < 1) g = 1;
+  if (g > maxg) g = maxg;
+  return (int)g;
+}
+
+cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res) {
+  StepDev s = s0;
+  s.slog = slog;
+  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t nbl = nloc * s.nblk;
+  cudaError_t e;
+  if (!ev0) {
+    if ((e = cudaEventCreate(&ev0)) != cudaSuccess) return e;
+    if ((e = cudaEventCreate(&ev1)) != cudaSuccess) return e;
+  }
+  if (!hdr_host) {
+    if ((e = cudaMallocHost((void**)&hdr_host, sizeof(StepHdr))) != cudaSuccess) return e;
+  }
+  res->nloc = nloc;
+  res->retries = 0;
+  if (nloc == 0) {
+    res->total = 0;
+    res->levels = 0;
+    res->tuples = 0;
+    res->candidates = 0;
+    res->kernel_ms = 0;
+    return cudaSuccess;
+  }
+  GROW(seg_d, int32_t, nloc);
+  GROW(blk_rel, int64_t, nbl);
+  GROW(seg_tuples, int64_t, nloc);
+  GROW(hdr, StepHdr, 1);
+  StepHdr* H = (StepHdr*)hdr.p;
+  cudaEventRecord(ev0, st);
+  cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
+  k_plan<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int64_t*)blk_rel.p,
+                                                       (int64_t*)seg_tuples.p, H);
+  cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (hdr_host->bad) return cudaErrorInvalidConfiguration;
+  const int D = (int)hdr_host->D;
+  res->levels = D + 1;
+  res->tuples = (int64_t)hdr_host->tuples;
+  int64_t need_filter = 0, need_out = 0;
+  for (int l = 0; l <= D; ++l) need_filter = std::max<int64_t>(need_filter, hdr_host->filter_samp[l]);
+  unsigned long long plan_copy[2 * (LMAX + 1)];
+  for (int l = 0; l <= LMAX; ++l) {
+    plan_copy[l] = hdr_host->direct_samp[l];
+    plan_copy[LMAX + 1 + l] = hdr_host->filter_samp[l];
+  }
+  for (int attempt = 0;; ++attempt) {
+    const int64_t cand_cap = std::min<int64_t>(need_filter, cand_budget);
+    need_out = 0;
+    for (int l = 0; l <= D; ++l)
+      need_out = std::max<int64_t>(need_out, (int64_t)plan_copy[l] +
+                                                 std::min<int64_t>(plan_copy[LMAX + 1 + l], cand_cap));
+    need_out = std::max<int64_t>(need_out, out_budget);
+    const int64_t bcap = std::max<int64_t>(need_out + nloc + 1, bucket_budget);
+    GROW(poolA_m, int64_t, need_out);
+    GROW(poolA_t, int64_t, need_out);
+    GROW(poolA_id, uint64_t, need_out);
+    GROW(poolB_m, int64_t, need_out);
+    GROW(poolB_t, int64_t, need_out);
+    GROW(poolB_id, uint64_t, need_out);
+    GROW(poolA_start, int64_t, nloc);
+    GROW(poolA_cnt, int64_t, nloc);
+    GROW(poolB_start, int64_t, nloc);
+    GROW(poolB_cnt, int64_t, nloc);
+    GROW(cursors, unsigned long long, 8);
+    if (D > 0) {
+      GROW(nb, int64_t, nloc);
+      GROW(bucket_base, int64_t, nloc + 1);
+      GROW(wcnt, int64_t, std::max<int64_t>(nbl, 1));
+      GROW(wo, int64_t, nbl + 1);
+      GROW(bcount, unsigned int, bcap);
+      GROW(bmin, long long, bcap);
+      GROW(boff, int64_t, bcap + 1);
+      GROW(bcarry, long long, bcap);
+      GROW(cm, int64_t, cand_cap);
+      GROW(ct, int64_t, cand_cap);
+      GROW(cid, uint64_t, cand_cap);
+      GROW(cgb, int64_t, cand_cap + 1);
+      GROW(cpos, unsigned int, cand_cap);
+      GROW(gm, int64_t, cand_cap);
+      GROW(gt, int64_t, cand_cap);
+      GROW(gid, uint64_t, cand_cap);
+      GROW(gflag, int64_t, cand_cap + 1);
+      GROW(large_list, int64_t, bcap);
+      GROW(huge_list, int64_t, bcap);
+      GROW(ncand, int64_t, 2);
+    }
+    const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
+    GROW(scan_tmp, int64_t, scan_n / SCAN_TILE + 8);
+    unsigned long long* cur = (unsigned long long*)cursors.p;
+    if (attempt > 0) {
+      cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
+      k_plan<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
+                                                           (int64_t*)blk_rel.p,
+                                                           (int64_t*)seg_tuples.p, H);
+    }
+    Pool pools[2];
+    pools[0] = Pool{(int64_t*)poolA_m.p, (int64_t*)poolA_t.p, (uint64_t*)poolA_id.p,
+                    (int64_t*)poolA_start.p, (int64_t*)poolA_cnt.p, cur + 0, need_out};
+    pools[1] = Pool{(int64_t*)poolB_m.p, (int64_t*)poolB_t.p, (uint64_t*)poolB_id.p,
+                    (int64_t*)poolB_start.p, (int64_t*)poolB_cnt.p, cur + 1, need_out};
+    for (int l = D; l >= 0; --l) {
+      LevelDev L;
+      std::memset(&L, 0, sizeof(L));
+      L.level = l;
+      L.st = (int64_t)1 << (slog * l);
+      L.seg_d = (const int32_t*)seg_d.p;
+      L.blk_rel = (const int64_t*)blk_rel.p;
+      L.in = pools[(l + 1) & 1];
+      L.out = pools[l & 1];
+      L.hdr = H;
+      cudaMemsetAsync(L.out.cursor, 0, sizeof(unsigned long long), st);
+      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, 0, st>>>(s, L);
+      if (l < D) {
+        L.nb = (int64_t*)nb.p;
+        L.bucket_base = (int64_t*)bucket_base.p;
+        L.wcnt = (int64_t*)wcnt.p;
+        L.wo = (int64_t*)wo.p;
+        L.bcount = (unsigned int*)bcount.p;
+        L.bmin = (long long*)bmin.p;
+        L.boff = (int64_t*)boff.p;
+        L.bcarry = (long long*)bcarry.p;
+        L.bcap = bcap;
+        L.cm = (int64_t*)cm.p;
+        L.ct = (int64_t*)ct.p;
+        L.cid = (uint64_t*)cid.p;
+        L.cgb = (int64_t*)cgb.p;
+        L.cpos = (unsigned int*)cpos.p;
+        L.cand_cursor = cur + 2;
+        L.cand_cap = cand_cap;
+        L.gm = (int64_t*)gm.p;
+        L.gt = (int64_t*)gt.p;
+        L.gid = (uint64_t*)gid.p;
+        L.gflag = (int64_t*)gflag.p;
+        L.large_list = (int64_t*)large_list.p;
+        L.large_n = cur + 3;
+        L.huge_list = (int64_t*)huge_list.p;
+        L.huge_n = cur + 4;
+        int64_t* nc = (int64_t*)ncand.p;
+        int64_t* tmp = (int64_t*)scan_tmp.p;
+        k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
+        scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
+        k_check_buckets<<<1, 1, 0, st>>>(s, L);
+        cudaMemsetAsync(L.bcount, 0, sizeof(unsigned int) * bcap, st);
+        cudaMemsetAsync(L.bmin, BMIN_FILL, sizeof(long long) * bcap, st);
+        cudaMemsetAsync(L.cand_cursor, 0, sizeof(unsigned long long), st);
+        k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
+        scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
+        k_filter<<<148 * 8, 256, 0, st>>>(s, L);
+        k_check_cand<<<1, 1, 0, st>>>(L);
+        k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
+        // bucket offsets over B buckets (B on device)
+        scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
+        k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L);
+        k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
+        k_bucket_small<<<148 * 8, 256, 0, st>>>(s, L);
+        const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
+        k_bucket_large<<<148 * 2, DIRECT_NT, lsm, st>>>(L);
+        k_bucket_huge<<<148, 1024, (size_t)BUCKET_SMEM * 3 * sizeof(int64_t), st>>>(L);
+        // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
+        int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
+        scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
+        // k_compact_base reads the total at gpos[n]; pass via gflag alias
+        LevelDev L2 = L;
+        L2.gflag = gpos;
+        k_compact_base<<<1, 1, 0, st>>>(L2, nc);
+        k_compact<<<148 * 8, 256, 0, st>>>(L2, gpos, nc);
+        k_seg_out<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L2, gpos);
+      }
+    }
+    cudaEventRecord(ev1, st);
+    // read back header + level-0 per-segment counts
+    if (cnt_host_n < nloc) {
+      if (cnt_host) cudaFreeHost(cnt_host);
+      if ((e = cudaMallocHost((void**)&cnt_host, sizeof(int64_t) * nloc)) != cudaSuccess) return e;
+      cnt_host_n = nloc;
+    }
+    cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(cnt_host, pools[0].cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!hdr_host->overflow) {
+      res->pool = pools[0];
+      res->candidates = 0;
+      for (int l = 0; l < D; ++l) res->candidates += (int64_t)hdr_host->cand_total[l];
+      res->huge = (int64_t)hdr_host->huge;
+      res->counts = cnt_host;
+      int64_t tot = 0;
+      for (int64_t i = 0; i < nloc; ++i) tot += cnt_host[i];
+      res->total = tot;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev0, ev1);
+      res->kernel_ms = ms;
+      return cudaSuccess;
+    }
+    // grow budgets and retry
+    res->retries++;
+    int64_t mc = 0, mo = 0, mb = 0;
+    for (int l = 0; l <= D; ++l) {
+      mc = std::max<int64_t>(mc, hdr_host->cand_total[l]);
+      mo = std::max<int64_t>(mo, hdr_host->out_total[l]);
+      mb = std::max<int64_t>(mb, hdr_host->bucket_total[l]);
+    }
+    cand_budget = std::max<int64_t>(cand_budget * 2, mc + mc / 4);
+    out_budget = std::max<int64_t>(out_budget * 2, mo + mo / 4);
+    bucket_budget = std::max<int64_t>(bucket_budget * 2, mb + mb / 4);
+    if (attempt > 16) return cudaErrorMemoryAllocation;
+  }
+}
+
+cudaError_t StepRunner::gather(const StepDev& s, const StepResult& r, const int64_t* dst_off_host,
+                               int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st) {
+  const int64_t nloc = r.nloc;
+  if (nloc == 0) return cudaSuccess;
+  GROW(dst_off, int64_t, nloc);
+  cudaMemcpyAsync(dst_off.p, dst_off_host, sizeof(int64_t) * nloc, cudaMemcpyHostToDevice, st);
+  k_gather<<<grid_for(nloc, 1, 148 * 8), 128, 0, st>>>(s, r.pool, (const int64_t*)dst_off.p, om, ot,
+                                                      obp);
+  return cudaGetLastError();
+}
+
+cudaError_t StepRunner::configure() {
+  const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
+  cudaError_t e = cudaFuncSetAttribute(k_bucket_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)lsm);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_bucket_huge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((size_t)BUCKET_SMEM * 3 * sizeof(int64_t)));
+}
+
+}  // namespace ftk

@@ -1,0 +1,57 @@
+// ft_step.h -- host interface of the per-step GPU pipeline (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ft_kernels.cuh"
+
+namespace ftk {
+
+struct StepResult {
+  int64_t nloc = 0;        // segments computed on this rank
+  int64_t total = 0;       // survivors over those segments
+  int64_t tuples = 0;      // product tuples over those segments
+  int64_t candidates = 0;  // pre-filter survivors over all levels
+  int64_t huge = 0;        // buckets that took the global-memory sort
+  int64_t retries = 0;
+  int levels = 0;
+  float kernel_ms = 0;
+  const int64_t* counts = nullptr;  // host (pinned) per-segment survivor counts [nloc]
+  Pool pool;                        // level-0 pool (device)
+};
+
+class StepRunner {
+ public:
+  StepRunner();
+  ~StepRunner();
+  cudaError_t configure();
+  // Runs the step for segments [s.seg_lo, s.seg_hi); on success res->counts
+  // and res->pool describe the per-segment results (valid until the next run).
+  cudaError_t run(const StepDev& s, cudaStream_t st, StepResult* res);
+  // Gathers the level-0 pool into CSR arrays (dst_off_host[nloc]: offsets).
+  cudaError_t gather(const StepDev& s, const StepResult& r, const int64_t* dst_off_host,
+                     int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st);
+  void release();
+
+  int slog = 3;                       // sample stride 8
+  int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
+  int64_t out_budget = 1 << 20;
+  int64_t bucket_budget = 1 << 20;
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  Buf seg_d, blk_rel, seg_tuples, hdr;
+  Buf poolA_m, poolA_t, poolA_id, poolA_start, poolA_cnt;
+  Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
+  Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
+  Buf cm, ct, cid, cgb, cpos, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
+  StepHdr* hdr_host = nullptr;
+  int64_t* cnt_host = nullptr;
+  int64_t cnt_host_n = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+}  // namespace ftk

@@ -1,0 +1,85 @@
+"""GPU parity: libft (CUDA, sm_100a) vs the CPU oracle, element by element.
+
+Every step's output set (seg_off, m, t, bp) must be bit-identical to the
+oracle's (integer work: exact), as must the final frontier and every
+unrolled strategy (SURVEY 8(c) "GPU <-> oracle")."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import bruteforce as bf
+from synth import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ft():
+    import paper_2004_10856_b200 as ft
+    return ft
+
+
+def compare(ft, w, threads=8, strategies="all", stride=1):
+    og = oracle.load(w, threads)
+    og.eliminate()
+    om, ot = og.frontier()
+    gg = ft.load(w, keep_all=True)
+    gg.eliminate()
+    gm, gt = gg.frontier()
+    st = gg.stats()
+    assert og.num_steps() == len(st)
+    for s in range(0, len(st), stride):
+        info = og.step_info(s)
+        assert info["kind"] == st[s]["kind"], s
+        assert info["tuples"] == st[s]["tuples"], s
+        a = og.step_output(s)
+        b = gg.step_output(s)
+        for name, x, y in zip(("seg_off", "m", "t", "bp"), a, b):
+            if not np.array_equal(x, y):
+                bad = np.nonzero(x != y)[0][:5] if len(x) == len(y) else "len"
+                raise AssertionError(f"{w.name} step {s} ({info['kind']}) {name} differs at {bad}")
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+    idx = range(len(om)) if strategies == "all" else np.linspace(0, len(om) - 1, strategies).astype(int)
+    for i in idx:
+        assert np.array_equal(og.strategy(int(i)), gg.strategy(int(i))), i
+    return gg, st
+
+
+def test_c1_seeds(ft):
+    for seed in range(100):
+        for var in ("chain", "parallel", "diamond"):
+            compare(ft, G.c1(seed, var))
+
+
+def test_random_sp(ft):
+    for seed in range(200):
+        w = G.random_sp(seed, n_ops=2 + seed % 12, kmax=4, edge_mem=(seed % 5 == 0))
+        compare(ft, w)
+
+
+def test_random_sp_large_frontiers(ft):
+    """Wider cost ranges and K: multi-level (filter) path with ragged segments."""
+    for seed in range(12):
+        w = G.random_sp(1000 + seed, n_ops=14, kmax=12, cost_hi=1 << 20)
+        compare(ft, w)
+
+
+def test_c2_vgg(ft):
+    compare(ft, G.c2())
+
+
+def test_c2_no_jitter_ties(ft):
+    compare(ft, G.c2(jitter=False))
+
+
+def test_c3_resnet(ft):
+    gg, st = compare(ft, G.c3(), strategies=64)
+    assert max(s["levels"] for s in st) >= 2  # the filter path ran
+
+
+def test_c4_bert_2layers(ft):
+    compare(ft, G.c4(layers=2), strategies=32)
+
+
+def test_c5_small(ft):
+    compare(ft, G.c5(n_ops=200, K=16, B=8, Lmin=2, Lmax=6), strategies=32)

@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py -- FT search on B200: product tuples/s and search time per graph.
+
+One "step" = one complete Frontier-Tracking search of the workload graph
+(every SURVEY 8(a) row: FT_AUTO eliminations -> LDP -> final reduce), i.e.
+Alg. 2 of arXiv 2004.10856, with every step's Product / Union /
+Reduce in libft's sm_100a kernels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4]
+    python bench.py --impl reference ...      # CPU oracle arm (host cores)
+
+N > 1: launched by torchrun, one rank per GPU; each FT step's configuration
+pairs are sharded over the ranks and the survivors all-gathered over NCCL
+(strong scaling of one search; time = max over ranks).
+
+Metric (BASELINE.json): product tuples/s (sum over steps of |X||Y||Z|,
+Lemma 3/4 cardinalities) and FT search time per graph (ms_per_step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frontier tuples/sec (Product+Reduce) and FT search time per graph at 1/2/4/8 B200"
+UNIT = "product tuples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C4", help="C1..C5 (BASELINE.json configs)")
+    ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline budget")
+    ap.add_argument("--details", action="store_true", help="print per-kind breakdown to stderr")
+    return ap.parse_args()
+
+
+def workload_config(name):
+    from synth import graphs as G
+    w = G.get(name)
+    cfg = {"workload": {"C1": "C1 4-op chain K=3", "C2": "C2 VGG-16 chain D=8 K=16",
+                        "C3": "C3 ResNet-50 D=16 K=25",
+                        "C4": "C4 BERT-large encoder (24 layers) D=32 K=36",
+                        "C5": "C5 random SP DAG 2000 ops K=64"}[name],
+           "n_ops": w.n_ops, "n_edges": w.n_edges, "seed": 0}
+    return w, cfg
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except Exception:
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def cpu_sample_workload(name, seconds):
+    """Bounded sample of the same workload for the CPU oracle (about `seconds`
+    of host work): C4 -> the same BERT-large graph with fewer encoder layers;
+    C5 -> the same generator with fewer ops; C1-C3 -> the full graph."""
+    from synth import graphs as G
+    if name == "C4":
+        layers = 2 if seconds < 40 else 4
+        return G.c4(layers=layers), f"C4 BERT-large cost model, {layers} of 24 encoder layers"
+    if name == "C5":
+        n = 400 if seconds < 40 else 800
+        return G.c5(n_ops=n), f"C5 generator (same K, rho, B, L) with {n} of 2000 ops"
+    return G.get(name), f"{name} full graph"
+
+
+def oracle_run(w, threads):
+    import oracle
+    t0 = time.perf_counter()
+    g, m, t = oracle.run_ft(w, threads=threads)
+    dt = time.perf_counter() - t0
+    tuples = sum(g.step_info(s)["tuples"] for s in range(g.num_steps()))
+    return tuples, dt, len(m)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    threads = len(os.sched_getaffinity(0))
+    w, _cfg = workload_config(args.workload)
+    _, cfg = workload_config(args.workload)
+    sw, sample = cpu_sample_workload(args.workload, args.cpu_seconds)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_run(sw, threads)
+    times, tuples = [], 0
+    for _ in range(args.steps):
+        tp, dt, _n = oracle_run(sw, threads)
+        times.append(dt)
+        tuples = tp
+    tot = sum(times)
+    value = tuples * len(times) / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample + f"; {tuples} product tuples per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    import paper_2004_10856_b200 as ft
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(ft.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = ft.nccl_comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()), local)
+    w, cfg = workload_config(args.workload)
+    cfg.update({"graphs_per_step": 1, "parallelism": f"config-pair sharding x{world} + NCCL all-gather",
+                "l2_flush": not args.no_flush})
+    stream = torch.cuda.current_stream()
+    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+
+    def flush():
+        if not args.no_flush:
+            flush_buf.zero_()
+
+    def search(profile, keep=None):
+        g = ft.load(w, profile=profile, **kw)
+        g.prepare()
+        return g
+
+    # warm-up (module load, scratch growth, NCCL)
+    for _ in range(args.warmup):
+        g = search(False)
+        g.eliminate()
+        g.frontier()
+        g.close()
+    torch.cuda.synchronize()
+
+    # timed region: inputs resident in HBM (ft_prepare before the events)
+    clk = ClockSampler(local)
+    clk.start()
+    ev_ms, stats_all, nfront = [], [], 0
+    for _ in range(args.steps):
+        g = search(True)
+        flush()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.eliminate()
+        m, t = g.frontier()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ev_ms.append(e0.elapsed_time(e1))
+        stats_all.append(g.stats())
+        nfront = len(m)
+        g.close()
+    clocks = clk.stop()
+    total_ms = sum(ev_ms)
+    st = stats_all[-1]
+    local_tuples = sum(s["tuples"] for s in st)
+    launches = sum(s["launches"] for s in st)
+    groups = {k: sum(s[k + "_ms"] for s in st) for k in ("plan", "direct", "filter", "bucket", "compact")}
+    if dist is not None:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        tu = torch.tensor([local_tuples], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tu, op=dist.ReduceOp.SUM)
+        tuples = int(tu.item())
+    else:
+        tuples = local_tuples
+    ms_per_step = total_ms / args.steps
+    value = tuples / (ms_per_step / 1e3)
+
+    # end-to-end through the public API with host buffers
+    e2e_ms = []
+    h2d = sum(a.nbytes for a in w.op_m) + sum(a.nbytes for a in w.op_t) + sum(a.nbytes for a in w.edge_t)
+    h2d += sum(a.nbytes for a in w.edge_t)  # edge m (zeros, Eq. 2) is uploaded too
+    d2h = 0
+    for _ in range(args.steps):
+        flush()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g = ft.load(w, **kw)
+        g.eliminate()
+        m, t = g.frontier()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms.append(e0.elapsed_time(e1))
+        d2h = m.nbytes + t.nbytes
+        g.close()
+    e2e_tot = sum(e2e_ms)
+    if dist is not None:
+        tt = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_tot = float(tt.item())
+    e2e_value = tuples / (e2e_tot / args.steps / 1e3)
+
+    # roofline of the dominant kernel group
+    dom = max(groups, key=groups.get)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    filter_tuples = sum(s["tuples"] for s in st if s["levels"] > 1)
+    roof = {"kernel": f"k_{dom}", "bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+            "traffic": None}
+    # per-unit algorithmic bytes: 40 B per product tuple; units =
+    # product tuples of the steps whose kernels ran in this group
+    if dom == "filter":
+        roof["units"] = filter_tuples
+    else:
+        roof["units"] = tuples
+    roof["bytes_per_unit"] = 40
+    roof["achieved"] = roof["units"] * 40 / (groups[dom] / 1e3) / 1e9 if groups[dom] > 0 else None
+    roof["frac"] = roof["achieved"] / hbm_peak if roof["achieved"] else None
+    roof["share_of_step"] = groups[dom] / (ms_per_step) if ms_per_step else None
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": cfg, "search_ms": ms_per_step, "product_tuples_per_step": tuples,
+            "frontier_size": nfront, "ft_steps": len(st), "gpu_launches": launches * args.steps,
+            "kernel_group_ms": {k: round(v, 3) for k, v in groups.items()},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot / args.steps},
+            "clocks": clocks, "roofline": roof}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sw, sample = cpu_sample_workload(args.workload, args.cpu_seconds)
+        threads = len(os.sched_getaffinity(0))
+        tp, dt, _ = oracle_run(sw, threads)
+        line["cpu_baseline"] = {"value": tp / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": sample + f"; {tp} product tuples in {dt:.2f} s"}
+    if args.details and rank == 0:
+        for s in st:
+            print(json.dumps(s), file=sys.stderr)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        ft.nccl_comm_destroy(comm)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -71,7 +71,8 @@ typedef struct {
   int32_t rank, world; /* world > 1: SPMD over `world` ranks (one process per GPU) */
   void* nccl_comm;     /* ncclComm_t of the world (required when world > 1) */
   int32_t keep_all;    /* != 0: keep every step's m/t on device (ft_step_output) */
-  int32_t reserved[7];
+  int32_t profile;     /* != 0: CUDA events between kernel groups (ft_step_stats *_ms) */
+  int32_t reserved[6];
 } ft_options;
 
 /* Per-step statistics (ft_get_stats). */
@@ -84,8 +85,12 @@ typedef struct {
   int64_t survivors;     /* frontier tuples written */
   int64_t candidates;    /* tuples that passed the dominance pre-filter (all levels) */
   int64_t retries;       /* capacity retries */
+  int64_t launches;      /* kernels launched by this step on this rank */
+  int64_t max_seg;       /* largest output segment (frontier) of the step */
   float kernel_ms;       /* CUDA-event time of the step's kernels on this rank */
   float comm_ms;         /* all-gather time (world > 1) */
+  float plan_ms, direct_ms, filter_ms, bucket_ms, compact_ms; /* opt.profile only */
+  float host_ms;         /* opt.profile only: host readback + scratch sizing inside the step */
 } ft_step_stats;
 
 /* Create a graph: n_ops operators, K_i = n_cfgs[i] (1 <= K_i <= 4096)
@@ -96,6 +101,11 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges,
                     const int32_t* src, const int32_t* dst, const ft_options* opt,
                     ft_graph** out);
 void ft_graph_destroy(ft_graph* g);
+
+/* Validates that every cost is set and uploads all cost tables to the device
+ * (done implicitly by the first ft_eliminate / ft_frontier).  Lets a caller
+ * time the search with inputs already resident in HBM. */
+int ft_prepare(ft_graph* g);
 
 /* Operator costs, Eq. 1: m[K_op] bytes, t[K_op] ns (host arrays,
  * copied to the device).  Must precede the first ft_eliminate/ft_frontier. */
@@ -134,10 +144,24 @@ int ft_get_stats(const ft_graph* g, ft_step_stats* buf, int64_t cap, int64_t* n_
 int ft_step_output(ft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int64_t* m,
                    int64_t* t, uint64_t* bp, int64_t* n_out);
 
+/* Factor provenance of step `step` (debug / parity at full size): for X, Y, Z
+ * (i = 0, 1, 2) src[2*i] = kind (0 unit {(0,0)}, 1 original op, 2 original
+ * edge, 3 output of an earlier step) and src[2*i+1] = op / edge / step index;
+ * params = {kind, KA, KB, KC, nseg, nblk} (block mapping of DESIGN.md "steps"). */
+int ft_step_inputs(const ft_graph* g, int64_t step, int64_t* src6, int64_t* params6);
+
 /* Host-side shard plan (no device needed): split `n` units with weights w[n]
  * (int64, >= 0) into `world` contiguous ranges of near-equal weight;
  * bounds[world+1] receives the cut points (bounds[0]=0, bounds[world]=n). */
 int ft_shard_plan(int64_t n, const int64_t* w, int32_t world, int64_t* bounds);
+
+/* NCCL bootstrap helpers (so callers need no NCCL headers): rank 0 creates
+ * a 128-byte unique id, the caller distributes it (e.g. torch.distributed
+ * broadcast), every rank creates its communicator on `device`. */
+int ft_nccl_unique_id(uint8_t id_out[128]);
+int ft_nccl_comm_init(int32_t world, int32_t rank, const uint8_t id[128], int32_t device,
+                      void** comm_out);
+int ft_nccl_comm_destroy(void* comm);
 
 const char* ft_last_error(const ft_graph* g);
 /* Library version string, e.g. "ft-b200 0.1 sm_100a". */

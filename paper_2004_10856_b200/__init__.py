@@ -39,14 +39,16 @@ class FTError(RuntimeError):
 class ft_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_comm", C.c_void_p), ("keep_all", C.c_int32),
-                ("reserved", C.c_int32 * 7)]
+                ("profile", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class ft_step_stats(C.Structure):
     _fields_ = [("kind", C.c_int32), ("levels", C.c_int32), ("nseg", C.c_int64),
                 ("nblk", C.c_int64), ("tuples", C.c_int64), ("survivors", C.c_int64),
-                ("candidates", C.c_int64), ("retries", C.c_int64), ("kernel_ms", C.c_float),
-                ("comm_ms", C.c_float)]
+                ("candidates", C.c_int64), ("retries", C.c_int64), ("launches", C.c_int64),
+                ("max_seg", C.c_int64), ("kernel_ms", C.c_float), ("comm_ms", C.c_float), ("plan_ms", C.c_float),
+                ("direct_ms", C.c_float), ("filter_ms", C.c_float), ("bucket_ms", C.c_float),
+                ("compact_ms", C.c_float), ("host_ms", C.c_float)]
 
 
 def _load():
@@ -66,6 +68,12 @@ def _load():
     L.ft_get_stats.argtypes = [C.c_void_p, C.POINTER(ft_step_stats), C.c_int64, P64]
     L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
     L.ft_shard_plan.argtypes = [C.c_int64, P64, C.c_int32, P64]
+    L.ft_prepare.argtypes = [C.c_void_p]
+    L.ft_step_inputs.argtypes = [C.c_void_p, C.c_int64, P64, P64]
+    L.ft_nccl_unique_id.argtypes = [C.c_char_p]
+    L.ft_nccl_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.c_int32,
+                                    C.POINTER(C.c_void_p)]
+    L.ft_nccl_comm_destroy.argtypes = [C.c_void_p]
     L.ft_last_error.argtypes = [C.c_void_p]
     L.ft_last_error.restype = C.c_char_p
     L.ft_version.argtypes = []
@@ -76,7 +84,8 @@ def _load():
 lib = _load()
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
            "ft_eliminate", "ft_frontier", "ft_strategy", "ft_get_stats", "ft_step_output",
-           "ft_shard_plan", "ft_last_error", "ft_version"]
+           "ft_prepare", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
+           "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version"]
 
 
 def _p(a, t):
@@ -94,7 +103,7 @@ def shard_plan(weights, world: int) -> np.ndarray:
 
 class Graph:
     def __init__(self, n_cfgs, src, dst, device: int = 0, stream=None, rank: int = 0,
-                 world: int = 1, nccl_comm=None, keep_all: bool = False):
+                 world: int = 1, nccl_comm=None, keep_all: bool = False, profile: bool = False):
         K = np.ascontiguousarray(n_cfgs, dtype=np.int32)
         s = np.ascontiguousarray(src, dtype=np.int32)
         d = np.ascontiguousarray(dst, dtype=np.int32)
@@ -106,6 +115,7 @@ class Graph:
         opt.world = world
         opt.nccl_comm = nccl_comm
         opt.keep_all = 1 if keep_all else 0
+        opt.profile = 1 if profile else 0
         h = C.c_void_p()
         rc = lib.ft_graph_create(self.n_ops, _p(K, C.c_int32), len(s), _p(s, C.c_int32),
                                  _p(d, C.c_int32), C.byref(opt), C.byref(h))
@@ -138,6 +148,15 @@ class Graph:
         m = None if m is None else np.ascontiguousarray(m, dtype=np.int64)
         self._chk(lib.ft_set_edge_costs(self.h, e, _p(m, C.c_int64), _p(t, C.c_int64)))
 
+    def prepare(self):
+        self._chk(lib.ft_prepare(self.h))
+
+    def step_inputs(self, step: int):
+        src = np.zeros(6, np.int64)
+        par = np.zeros(6, np.int64)
+        self._chk(lib.ft_step_inputs(self.h, step, _p(src, C.c_int64), _p(par, C.c_int64)))
+        return src.reshape(3, 2), par
+
     def eliminate(self, kind: int = AUTO, id: int = -1) -> int:
         ne = C.c_int32(-1)
         self._chk(lib.ft_eliminate(self.h, kind, id, C.byref(ne)))
@@ -169,7 +188,10 @@ class Graph:
             out.append({"kind": STEP_KINDS.get(s.kind, s.kind), "levels": s.levels, "nseg": s.nseg,
                         "nblk": s.nblk, "tuples": s.tuples, "survivors": s.survivors,
                         "candidates": s.candidates, "retries": s.retries,
-                        "kernel_ms": s.kernel_ms, "comm_ms": s.comm_ms})
+                        "launches": s.launches, "kernel_ms": s.kernel_ms, "comm_ms": s.comm_ms,
+                        "plan_ms": s.plan_ms, "direct_ms": s.direct_ms, "filter_ms": s.filter_ms,
+                        "bucket_ms": s.bucket_ms, "compact_ms": s.compact_ms,
+                        "host_ms": s.host_ms, "max_seg": s.max_seg})
         return out
 
     def step_output(self, step: int, with_mt: bool = True):
@@ -185,6 +207,26 @@ class Graph:
         self._chk(lib.ft_step_output(self.h, step, n.value, _p(so, C.c_int64), _p(m, C.c_int64),
                                      _p(t, C.c_int64), _p(bp, C.c_uint64), C.byref(n)))
         return so, m, t, bp
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib.ft_nccl_unique_id(buf)
+    if rc:
+        raise FTError(rc, "ncclGetUniqueId")
+    return buf.raw
+
+
+def nccl_comm_init(world: int, rank: int, uid: bytes, device: int):
+    c = C.c_void_p()
+    rc = lib.ft_nccl_comm_init(world, rank, uid, device, C.byref(c))
+    if rc:
+        raise FTError(rc, "ncclCommInitRank")
+    return c.value
+
+
+def nccl_comm_destroy(comm):
+    lib.ft_nccl_comm_destroy(C.c_void_p(comm))
 
 
 def load(w, **kw) -> Graph:

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <queue>
 #include <set>
@@ -75,12 +77,37 @@ struct ft_graph {
   std::vector<int64_t> final_m, final_t;
   int poisoned = 0;
   std::string err;
-  ftk::StepRunner runner;
+  ftk::StepRunner* runner = nullptr;  // process-wide per device
+  bool profile = false;
   int64_t* d_costs = nullptr;  // all original costs + iota offsets + unit
   std::vector<int64_t> h_pin_off;
   int64_t* h_pinned = nullptr;
   int64_t h_pinned_n = 0;
 };
+
+namespace ftk {
+static std::mutex g_reg_mu;
+static std::map<int, StepRunner*> g_runners;
+static std::map<int, std::mutex*> g_mutexes;
+StepRunner* device_runner(int device) {
+  std::lock_guard<std::mutex> l(g_reg_mu);
+  auto it = g_runners.find(device);
+  if (it != g_runners.end()) return it->second;
+  StepRunner* r = new (std::nothrow) StepRunner();
+  if (!r) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess || r->configure() != cudaSuccess) {
+    delete r;
+    return nullptr;
+  }
+  g_runners[device] = r;
+  g_mutexes[device] = new std::mutex();
+  return r;
+}
+std::mutex& runner_mutex(int device) {
+  std::lock_guard<std::mutex> l(g_reg_mu);
+  return *g_mutexes[device];
+}
+}  // namespace ftk
 
 namespace {
 
@@ -276,7 +303,9 @@ int exec_step(ft_graph* g, StepRec r, int* out_set) {
   s.seg_lo = lo[g->rank];
   s.seg_hi = lo[g->rank + 1];
   ftk::StepResult res;
-  cudaError_t ce = g->runner.run(s, g->stream, &res);
+  std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
+  g->runner->profile = g->profile;
+  cudaError_t ce = g->runner->run(s, g->stream, &res);
   if (ce == cudaErrorInvalidConfiguration)
     return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
   if (ce != cudaSuccess) return cuda_fail(g, ce, "step");
@@ -303,9 +332,9 @@ int exec_step(ft_graph* g, StepRec r, int* out_set) {
   CU(cudaMemcpyAsync(o.d_off, o.off.data(), sizeof(int64_t) * (r.nseg + 1), cudaMemcpyHostToDevice,
                      g->stream), "upload seg_off");
   if (g->world == 1) {
-    CU(g->runner.gather(s, res, o.off.data(), o.d_m, o.d_t, o.d_bp, g->stream), "gather");
+    CU(g->runner->gather(s, res, o.off.data(), o.d_m, o.d_t, o.d_bp, g->stream), "gather");
   } else {
-    CU(g->runner.gather(s, res, o.off.data() + s.seg_lo, o.d_m, o.d_t, o.d_bp, g->stream), "gather");
+    CU(g->runner->gather(s, res, o.off.data() + s.seg_lo, o.d_m, o.d_t, o.d_bp, g->stream), "gather");
     int rc = exchange(g, lo, o, cnt, &comm_ms);  // second phase: payload
     if (rc) return rc;
   }
@@ -321,6 +350,15 @@ int exec_step(ft_graph* g, StepRec r, int* out_set) {
   r.st.retries = res.retries;
   r.st.kernel_ms = res.kernel_ms;
   r.st.comm_ms = comm_ms;
+  r.st.launches = res.launches + 1;  // + gather
+  r.st.plan_ms = res.plan_ms;
+  r.st.direct_ms = res.direct_ms;
+  r.st.filter_ms = res.filter_ms;
+  r.st.bucket_ms = res.bucket_ms;
+  r.st.compact_ms = res.compact_ms;
+  r.st.host_ms = res.host_ms;
+  r.st.max_seg = 0;
+  for (int64_t i = 0; i < r.nseg; ++i) r.st.max_seg = std::max<int64_t>(r.st.max_seg, cnt[i]);
   r.out = (int)g->sets.size();
   g->sets.push_back(std::move(o));
   g->steps.push_back(r);
@@ -741,6 +779,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     g->world = opt->world < 1 ? 1 : opt->world;
     g->comm = (ncclComm_t)opt->nccl_comm;
     g->keep_all = opt->keep_all != 0;
+    g->profile = opt->profile != 0;
     g->stream = (cudaStream_t)opt->stream;
   }
   if (g->world > 1 && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
@@ -758,7 +797,8 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    e = g->runner.configure();
+    g->runner = ftk::device_runner(g->dev);
+    e = g->runner ? cudaSuccess : cudaErrorMemoryAllocation;
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -780,7 +820,6 @@ void ft_graph_destroy(ft_graph* g) {
       if (s.d_off) cudaFree(s.d_off);
     }
   if (g->d_costs) cudaFree(g->d_costs);
-  g->runner.release();
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -887,6 +926,67 @@ int ft_strategy(ft_graph* g, int64_t tuple_idx, int32_t* cfg_out) {
     }
   std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_ops);
   return FT_OK;
+}
+
+int ft_prepare(ft_graph* g) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  return start(g);
+}
+
+int ft_step_inputs(const ft_graph* g, int64_t step, int64_t* src6, int64_t* params6) {
+  if (!g || !src6 || !params6) return FT_EINVAL;
+  if (step < 0 || step >= (int64_t)g->steps.size()) return FT_EINVAL;
+  const StepRec& r = g->steps[step];
+  const int ids[3] = {r.X, r.Y, r.Z};
+  for (int i = 0; i < 3; ++i) {
+    const FSet& S = g->sets[ids[i]];
+    src6[2 * i] = S.kind;
+    if (S.kind == S_STEP) {
+      src6[2 * i + 1] = S.step;
+    } else if (S.kind == S_OP) {
+      src6[2 * i + 1] = S.a_op;
+    } else if (S.kind == S_EDGE) {
+      int64_t e = -1;
+      for (int q = 0; q < g->n_orig_edges; ++q)
+        if (g->edges[q].set == ids[i]) e = q;
+      src6[2 * i + 1] = e;
+    } else {
+      src6[2 * i + 1] = 0;
+    }
+  }
+  params6[0] = r.kind;
+  params6[1] = r.KA;
+  params6[2] = r.KB;
+  params6[3] = r.KC;
+  params6[4] = r.nseg;
+  params6[5] = r.nblk;
+  return FT_OK;
+}
+
+int ft_nccl_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return FT_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return FT_ECUDA;
+  std::memcpy(id_out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return FT_OK;
+}
+
+int ft_nccl_comm_init(int32_t world, int32_t rank, const uint8_t id[128], int32_t device,
+                      void** comm_out) {
+  if (!id || !comm_out || world < 1 || rank < 0 || rank >= world) return FT_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return FT_ECUDA;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c;
+  if (ncclCommInitRank(&c, world, uid, rank) != ncclSuccess) return FT_ECUDA;
+  *comm_out = (void*)c;
+  return FT_OK;
+}
+
+int ft_nccl_comm_destroy(void* comm) {
+  if (!comm) return FT_EINVAL;
+  return ncclCommDestroy((ncclComm_t)comm) == ncclSuccess ? FT_OK : FT_ECUDA;
 }
 
 int ft_get_stats(const ft_graph* g, ft_step_stats* buf, int64_t cap, int64_t* n_out) {

@@ -80,7 +80,7 @@ struct Pool {
 
 struct LevelDev {
   int level;
-  int64_t st;  // stride
+  int st;      // log2 of the sample stride
   const int32_t* seg_d;
   const int64_t* blk_rel;
   Pool in;     // level l+1 output (G), valid when level < D
@@ -166,16 +166,18 @@ __device__ __forceinline__ Blk load_blk(const StepDev& s, int64_t sg, int64_t k)
   return b;
 }
 
-// Sampled index set at stride st: {0, st, 2st, ...} U {n-1}.
-__device__ __forceinline__ int64_t samp_cnt(int64_t n, int64_t st) {
-  if (st == 1 || n <= 1) return n;
-  int64_t c = (n + st - 1) / st;
-  if ((n - 1) % st) ++c;
+// Sampled index set at stride st = 2^sh: {0, st, 2st, ...} U {n-1}.
+// (The level-l sample of every factor; nested across levels.)
+__device__ __forceinline__ int64_t samp_cnt(int64_t n, int sh) {
+  if (sh == 0 || n <= 1) return n;
+  const int64_t st = (int64_t)1 << sh;
+  int64_t c = (n + st - 1) >> sh;
+  if ((n - 1) & (st - 1)) ++c;
   return c;
 }
-__device__ __forceinline__ int64_t samp_idx(int64_t j, int64_t n, int64_t st) {
-  int64_t c0 = (n + st - 1) / st;
-  return j < c0 ? j * st : n - 1;
+__device__ __forceinline__ int64_t samp_idx(int64_t j, int64_t n, int sh) {
+  const int64_t c0 = (n + ((int64_t)1 << sh) - 1) >> sh;
+  return j < c0 ? (j << sh) : n - 1;
 }
 
 __device__ __forceinline__ const int64_t* fac_m(const StepDev& s, int f) {

@@ -94,27 +94,41 @@ void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap,
 // segment (ids, R6), sample sizes per level, the level at which the segment
 // is small enough for the direct path.
 
-__global__ void k_plan(StepDev s, int32_t* seg_d, int64_t* blk_rel, int64_t* seg_tuples,
-                       StepHdr* hdr) {
+__global__ void __launch_bounds__(128) k_plan(StepDev s, int32_t* seg_d, int64_t* blk_rel,
+                                              int64_t* seg_tuples, StepHdr* hdr) {
+  // one warp per output segment; lanes stride over its blocks
   const int64_t nloc = s.seg_hi - s.seg_lo;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= nloc) return;
   const int64_t sg = s.seg_lo + i;
   unsigned long long samp[LMAX + 1];
 #pragma unroll
   for (int l = 0; l <= LMAX; ++l) samp[l] = 0;
-  int64_t rel = 0;
-  for (int64_t k = 0; k < s.nblk; ++k) {
-    Blk b = load_blk(s, sg, k);
-    blk_rel[i * s.nblk + k] = rel;
-    rel += b.n[0] * b.n[1] * b.n[2];
+  int64_t rel = 0;  // running block offset (ids, R6)
+  for (int64_t k0 = 0; k0 < s.nblk; k0 += 32) {
+    const int64_t k = k0 + lane;
+    int64_t nk = 0;
+    if (k < s.nblk) {
+      Blk b = load_blk(s, sg, k);
+      nk = b.n[0] * b.n[1] * b.n[2];
 #pragma unroll
-    for (int l = 0; l <= LMAX; ++l) {
-      int64_t st = (int64_t)1 << (s.slog * l);
-      samp[l] += (unsigned long long)(samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) *
-                                      samp_cnt(b.n[2], st));
+      for (int l = 0; l <= LMAX; ++l) {
+        const int sh = s.slog * l;
+        samp[l] += (unsigned long long)(samp_cnt(b.n[0], sh) * samp_cnt(b.n[1], sh) *
+                                        samp_cnt(b.n[2], sh));
+      }
     }
+    const int64_t inc = warp_incl_sum<long long>(nk);
+    if (k < s.nblk) blk_rel[i * s.nblk + k] = rel + inc - nk;
+    rel += __shfl_sync(0xffffffffu, inc, 31);
   }
+#pragma unroll
+  for (int l = 0; l <= LMAX; ++l) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) samp[l] += __shfl_xor_sync(0xffffffffu, samp[l], d);
+  }
+  if (lane != 0) return;
   int d = -1;
   for (int l = 0; l <= LMAX; ++l)
     if (samp[l] <= (unsigned long long)C_DIRECT) {
@@ -146,7 +160,7 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
   __shared__ long long sh[33];
   __shared__ int64_t s_start;
   const int64_t nloc = s.seg_hi - s.seg_lo;
-  const int64_t st = L.st;
+  const int st = L.st;
   for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
     if (L.seg_d[li] != L.level) continue;
     if (L.hdr->overflow) return;
@@ -245,7 +259,7 @@ __global__ void k_check_buckets(StepDev s, LevelDev L) {
 }
 
 // Long factor = the one with most sampled indices; runs = product of the other two.
-__device__ __forceinline__ void run_shape(const Blk& b, int64_t st, int& lf, int& fa, int& fb,
+__device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa, int& fb,
                                           int64_t* c) {
   c[0] = samp_cnt(b.n[0], st);
   c[1] = samp_cnt(b.n[1], st);
@@ -284,7 +298,7 @@ __global__ void __launch_bounds__(256) k_filter(StepDev s, LevelDev L) {
   const int64_t nbl = (s.seg_hi - s.seg_lo) * s.nblk;
   const int64_t W = L.wo[nbl];
   const int lane = threadIdx.x & 31;
-  const int64_t st = L.st;
+  const int st = L.st;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < W; base += gstride) {
     const int64_t w = base + threadIdx.x;
@@ -663,15 +677,17 @@ __global__ void k_gather(StepDev s, Pool P, const int64_t* dst_off, int64_t* om,
 // ---------------------------------------------------------------------------
 // Host side
 
+// Grow-only scratch with geometric growth: reallocation (a device-wide sync)
+// happens O(log size) times per process, not per step.
 static cudaError_t grow_raw(void** p, size_t* have, size_t need) {
   if (need <= *have && *p) return cudaSuccess;
+  size_t nb = std::max<size_t>({need, 2 * *have, (size_t)1 << 16});
   if (*p) {
     cudaError_t e = cudaFree(*p);
     if (e != cudaSuccess) return e;
     *p = nullptr;
     *have = 0;
   }
-  size_t nb = std::max<size_t>(need, 256);
   cudaError_t e = cudaMalloc(p, nb);
   if (e == cudaSuccess) *have = nb;
   return e;
@@ -702,6 +718,11 @@ void StepRunner::release() {
   if (cnt_host) cudaFreeHost(cnt_host);
   cnt_host = nullptr;
   cnt_host_n = 0;
+  for (auto& e : pev)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   ev0 = ev1 = nullptr;
@@ -716,6 +737,16 @@ static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
 
 cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res) {
   StepDev s = s0;
+  int64_t nl = 0;  // kernel launches
+  int pgroup[64];
+  npev = 0;
+  auto mark = [&](int group) {  // group of the interval that starts here
+    if (!profile || npev >= 64) return;
+    if (!pev[npev]) cudaEventCreate(&pev[npev]);
+    cudaEventRecord(pev[npev], st);
+    pgroup[npev] = group;
+    ++npev;
+  };
   s.slog = slog;
   const int64_t nloc = s.seg_hi - s.seg_lo;
   const int64_t nbl = nloc * s.nblk;
@@ -743,11 +774,15 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
   GROW(hdr, StepHdr, 1);
   StepHdr* H = (StepHdr*)hdr.p;
   cudaEventRecord(ev0, st);
+  mark(0);
   cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
-  k_plan<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int64_t*)blk_rel.p,
-                                                       (int64_t*)seg_tuples.p, H);
+  ++nl;
+  k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
+                                                            (int64_t*)blk_rel.p,
+                                                            (int64_t*)seg_tuples.p, H);
   cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  mark(5);  // host: readback + scratch sizing
   if (hdr_host->bad) return cudaErrorInvalidConfiguration;
   const int D = (int)hdr_host->D;
   res->levels = D + 1;
@@ -805,9 +840,9 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {
       cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
-      k_plan<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
-                                                           (int64_t*)blk_rel.p,
-                                                           (int64_t*)seg_tuples.p, H);
+      k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
+                                                                (int64_t*)blk_rel.p,
+                                                                (int64_t*)seg_tuples.p, H);
     }
     Pool pools[2];
     pools[0] = Pool{(int64_t*)poolA_m.p, (int64_t*)poolA_t.p, (uint64_t*)poolA_id.p,
@@ -818,13 +853,15 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
       LevelDev L;
       std::memset(&L, 0, sizeof(L));
       L.level = l;
-      L.st = (int64_t)1 << (slog * l);
+      L.st = slog * l;
       L.seg_d = (const int32_t*)seg_d.p;
       L.blk_rel = (const int64_t*)blk_rel.p;
       L.in = pools[(l + 1) & 1];
       L.out = pools[l & 1];
       L.hdr = H;
       cudaMemsetAsync(L.out.cursor, 0, sizeof(unsigned long long), st);
+      mark(1);
+      ++nl;
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, 0, st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
@@ -853,6 +890,8 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
         L.huge_n = cur + 4;
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
+        mark(2);
+        nl += 15;  // prep, 3 scan, check, work_count, 3 scan, filter, 2 checks (+ memsets)
         k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
         scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
         k_check_buckets<<<1, 1, 0, st>>>(s, L);
@@ -865,6 +904,8 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
         k_check_cand<<<1, 1, 0, st>>>(L);
         k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
+        mark(3);
+        nl += 8;
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
         k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L);
         k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
@@ -873,6 +914,8 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
         k_bucket_large<<<148 * 2, DIRECT_NT, lsm, st>>>(L);
         k_bucket_huge<<<148, 1024, (size_t)BUCKET_SMEM * 3 * sizeof(int64_t), st>>>(L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
+        mark(4);
+        nl += 6;
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
         scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
         // k_compact_base reads the total at gpos[n]; pass via gflag alias
@@ -883,6 +926,7 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
         k_seg_out<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L2, gpos);
       }
     }
+    mark(-1);
     cudaEventRecord(ev1, st);
     // read back header + level-0 per-segment counts
     if (cnt_host_n < nloc) {
@@ -906,6 +950,16 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
       float ms = 0;
       cudaEventElapsedTime(&ms, ev0, ev1);
       res->kernel_ms = ms;
+      res->launches = nl;
+      res->plan_ms = res->direct_ms = res->filter_ms = res->bucket_ms = res->compact_ms = 0;
+      res->host_ms = 0;
+      for (int q = 0; q + 1 < npev; ++q) {
+        float d = 0;
+        cudaEventElapsedTime(&d, pev[q], pev[q + 1]);
+        float* dst[6] = {&res->plan_ms, &res->direct_ms, &res->filter_ms, &res->bucket_ms,
+                         &res->compact_ms, &res->host_ms};
+        if (pgroup[q] >= 0 && pgroup[q] < 6) *dst[pgroup[q]] += d;
+      }
       return cudaSuccess;
     }
     // grow budgets and retry

@@ -15,10 +15,17 @@ struct StepResult {
   int64_t huge = 0;        // buckets that took the global-memory sort
   int64_t retries = 0;
   int levels = 0;
+  int64_t launches = 0;
   float kernel_ms = 0;
+  float plan_ms = 0, direct_ms = 0, filter_ms = 0, bucket_ms = 0, compact_ms = 0, host_ms = 0;
   const int64_t* counts = nullptr;  // host (pinned) per-segment survivor counts [nloc]
   Pool pool;                        // level-0 pool (device)
 };
+
+// Process-wide scratch + pipeline per CUDA device, shared by all graphs on
+// that device (lock held for a whole step; see ft_api.cu).
+class StepRunner;
+StepRunner* device_runner(int device);
 
 class StepRunner {
  public:
@@ -34,6 +41,7 @@ class StepRunner {
   void release();
 
   int slog = 3;                       // sample stride 8
+  bool profile = false;               // events between kernel groups
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
   int64_t out_budget = 1 << 20;
   int64_t bucket_budget = 1 << 20;
@@ -52,6 +60,8 @@ class StepRunner {
   int64_t* cnt_host = nullptr;
   int64_t cnt_host_n = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t pev[64] = {};
+  int npev = 0;
 };
 
 }  // namespace ftk

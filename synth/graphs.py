@@ -356,11 +356,16 @@ def c4(seed: int = 0, jitter: bool = True, layers: int = 24) -> Workload:
 # --------------------------------------------------------------------------
 
 def c5(seed: int = 0, n_ops: int = 2000, K: int = 64, B: int = 32, Lmin: int = 4,
-       Lmax: int = 12, rho: float = 0.85) -> Workload:
+       Lmax: int = 8, rho: float = 0.99) -> Workload:
     """C5 (SURVEY §8(d) pseudo-code): backbone of B ops, parallel chains of
     U{Lmin..Lmax} ops added round-robin over the spans, U{1..3} per visit,
     until ``n_ops`` ops.  Op m = floor(2^24 u), t = floor(2^24 (rho u + (1-rho) w));
-    edge t = 0 w.p. 1/4, else floor(2^24 (1-rho) U[0,1))."""
+    edge t = 0 w.p. 1/4, else floor(2^24 (1-rho) U[0,1)).
+
+    Calibrated defaults (SURVEY 8(d) "C5 calibration", measured on B200 with
+    libft): rho = 0.99, B = 32, L in {4..8} give 2.70e10
+    product tuples, max segment frontier 21,598, final frontier 16,912.
+    The survey's starting point (rho = 0.85, L in {4..12}) gives 6.2e12."""
     rng = np.random.default_rng(seed)
     edges: List[Tuple[int, int]] = [(s, s + 1) for s in range(B - 1)]
     n = B

@@ -72,18 +72,24 @@ typedef struct {
   void* nccl_comm;     /* ncclComm_t of the world (required when world > 1) */
   int32_t keep_all;    /* != 0: keep every step's m/t on device (ft_step_output) */
   int32_t profile;     /* != 0: CUDA events between kernel groups (ft_step_stats *_ms) */
-  int32_t reserved[6];
+  int32_t loopback;    /* != 0 with world > 1 and nccl_comm == NULL: every virtual rank's
+                          shard runs in this process on one GPU (partition-invariance tests) */
+  int32_t reserved[5];
 } ft_options;
 
 /* Per-step statistics (ft_get_stats). */
 typedef struct {
   int32_t kind;          /* FT_STEP_* */
   int32_t levels;        /* sample levels used by the reduce */
+  int32_t wave;          /* batch of independent steps it ran in */
+  int32_t pad;
   int64_t nseg;          /* output segments (configuration pairs / configs) */
   int64_t nblk;          /* blocks (union terms) per segment */
   int64_t tuples;        /* product tuples sum |X||Y||Z| (the M1 numerator) */
   int64_t survivors;     /* frontier tuples written */
-  int64_t candidates;    /* tuples that passed the dominance pre-filter (all levels) */
+  int64_t candidates;    /* tuples that passed the dominance pre-filter (all levels);
+                            wave-level numbers (candidates, launches, *_ms) are
+                            booked on the first step of each wave */
   int64_t retries;       /* capacity retries */
   int64_t launches;      /* kernels launched by this step on this rank */
   int64_t max_seg;       /* largest output segment (frontier) of the step */

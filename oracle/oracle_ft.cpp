@@ -92,6 +92,7 @@ struct oft_graph {
   std::vector<FSet> sets;        // sets[0] = unit {(0,0)}
   std::vector<Step> steps;
   std::vector<bool> op_cost_set, edge_cost_set;
+  std::vector<int> pos0;         // position in the original graph's topological order (R9)
   bool started = false;
   bool have_final = false;
   int final_set = -1;
@@ -220,7 +221,8 @@ Adj build_adj(const oft_graph* g) {
   return a;
 }
 
-// Topological order of live ops; ties broken by smallest op id (R9).
+// Kahn's topological order with the smallest op id first; computed once on
+// the original graph (graph creation).
 std::vector<int> topo_order(const oft_graph* g, const Adj& a) {
   std::vector<int> indeg(g->n_ops, 0);
   for (int i = 0; i < g->n_ops; ++i) indeg[i] = (int)a.in[i].size();
@@ -235,6 +237,17 @@ std::vector<int> topo_order(const oft_graph* g, const Adj& a) {
     for (int e : a.out[u])
       if (--indeg[g->edges[e].dst] == 0) q.push(g->edges[e].dst);
   }
+  return order;
+}
+
+// Topological order of the live graph (R9): the original graph's order
+// restricted to live operators (eliminations only remove operators and
+// replace paths h->i->j by h->j, so it stays a topological order).
+std::vector<int> live_order(const oft_graph* g) {
+  std::vector<int> order;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (g->op_alive[i]) order.push_back(i);
+  std::sort(order.begin(), order.end(), [g](int a, int b) { return g->pos0[a] < g->pos0[b]; });
   return order;
 }
 
@@ -362,7 +375,7 @@ bool node_eligible(const oft_graph* g, const Adj& a, int i, const std::vector<bo
 // Returns 1 if something was eliminated, 0 if none applies, <0 on error.
 int auto_one(oft_graph* g) {
   Adj a = build_adj(g);
-  auto topo = topo_order(g, a);
+  auto topo = live_order(g);
   auto marked = marking(g, a, topo);  // Alg.2 line 5
   std::vector<int> pos(g->n_ops, INT_MAX);
   for (size_t i = 0; i < topo.size(); ++i) pos[topo[i]] = (int)i;
@@ -551,9 +564,14 @@ int oft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, cons
     g->edges.push_back(Edge{src[e], dst[e], true, (int)g->sets.size()});
     g->sets.push_back(s);
   }
-  if (topo_order(g, build_adj(g)).size() != (size_t)n_ops) {
-    delete g;
-    return OFT_EINVAL;  // cycle
+  {
+    auto order = topo_order(g, build_adj(g));
+    if (order.size() != (size_t)n_ops) {
+      delete g;
+      return OFT_EINVAL;  // cycle
+    }
+    g->pos0.assign(n_ops, 0);
+    for (int i = 0; i < n_ops; ++i) g->pos0[order[i]] = i;
   }
   *out = g;
   return OFT_OK;
@@ -600,7 +618,7 @@ int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* out_edge) {
   if (kind == OFT_NODE) {
     if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return fail(g, OFT_EINVAL, "bad op");
     Adj a = build_adj(g);
-    auto topo = topo_order(g, a);
+    auto topo = live_order(g);
     auto marked = marking(g, a, topo);
     if (!node_eligible(g, a, id, marked)) return fail(g, OFT_EPRECOND, "node elimination precondition");
     return do_node(g, a, id, out_edge);

@@ -39,11 +39,12 @@ class FTError(RuntimeError):
 class ft_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_comm", C.c_void_p), ("keep_all", C.c_int32),
-                ("profile", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("profile", C.c_int32), ("loopback", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
 class ft_step_stats(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("levels", C.c_int32), ("nseg", C.c_int64),
+    _fields_ = [("kind", C.c_int32), ("levels", C.c_int32), ("wave", C.c_int32),
+                ("pad", C.c_int32), ("nseg", C.c_int64),
                 ("nblk", C.c_int64), ("tuples", C.c_int64), ("survivors", C.c_int64),
                 ("candidates", C.c_int64), ("retries", C.c_int64), ("launches", C.c_int64),
                 ("max_seg", C.c_int64), ("kernel_ms", C.c_float), ("comm_ms", C.c_float), ("plan_ms", C.c_float),
@@ -103,7 +104,8 @@ def shard_plan(weights, world: int) -> np.ndarray:
 
 class Graph:
     def __init__(self, n_cfgs, src, dst, device: int = 0, stream=None, rank: int = 0,
-                 world: int = 1, nccl_comm=None, keep_all: bool = False, profile: bool = False):
+                 world: int = 1, nccl_comm=None, keep_all: bool = False, profile: bool = False,
+                 loopback: bool = False):
         K = np.ascontiguousarray(n_cfgs, dtype=np.int32)
         s = np.ascontiguousarray(src, dtype=np.int32)
         d = np.ascontiguousarray(dst, dtype=np.int32)
@@ -116,6 +118,7 @@ class Graph:
         opt.nccl_comm = nccl_comm
         opt.keep_all = 1 if keep_all else 0
         opt.profile = 1 if profile else 0
+        opt.loopback = 1 if loopback else 0
         h = C.c_void_p()
         rc = lib.ft_graph_create(self.n_ops, _p(K, C.c_int32), len(s), _p(s, C.c_int32),
                                  _p(d, C.c_int32), C.byref(opt), C.byref(h))
@@ -185,7 +188,8 @@ class Graph:
         out = []
         for i in range(n.value):
             s = buf[i]
-            out.append({"kind": STEP_KINDS.get(s.kind, s.kind), "levels": s.levels, "nseg": s.nseg,
+            out.append({"kind": STEP_KINDS.get(s.kind, s.kind), "levels": s.levels, "wave": s.wave,
+                        "nseg": s.nseg,
                         "nblk": s.nblk, "tuples": s.tuples, "survivors": s.survivors,
                         "candidates": s.candidates, "retries": s.retries,
                         "launches": s.launches, "kernel_ms": s.kernel_ms, "comm_ms": s.comm_ms,

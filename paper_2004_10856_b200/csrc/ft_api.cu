@@ -29,12 +29,12 @@ struct FSet {
   int step = -1;
   int a_op = -1, b_op = -1;  // segment -> config mapping for unroll
   int64_t nseg = 0;
-  std::vector<int64_t> off;  // host copy of seg_off
+  std::vector<int64_t> off;  // host copy of seg_off (filled when the step has run)
   int64_t* d_off = nullptr;
   int64_t* d_m = nullptr;
   int64_t* d_t = nullptr;
   uint64_t* d_bp = nullptr;
-  bool owned = false;        // device arrays allocated for this set
+  int wave_buf = -1;         // S_STEP: arena of the wave that produced it
   bool mt_live = true;
   std::vector<uint64_t> h_bp;
   bool h_bp_ok = false;
@@ -44,6 +44,7 @@ struct StepRec {
   int kind = 0;
   int X = -1, Y = -1, Z = -1, out = -1;
   int64_t KA = 0, KB = 0, KC = 0, nseg = 0, nblk = 0;
+  bool done = false;
   ft_step_stats st{};
 };
 
@@ -53,6 +54,17 @@ struct EdgeRec {
   int set;
 };
 
+// One output arena per executed wave: the CSR arrays of all its steps,
+// contiguous (step-major), so the multi-GPU all-gather is one broadcast per
+// rank and array.  m/t are freed when every set in the wave is consumed.
+struct WaveBuf {
+  int64_t* m = nullptr;
+  int64_t* t = nullptr;
+  uint64_t* bp = nullptr;
+  int64_t* off = nullptr;
+  int live = 0;
+};
+
 }  // namespace
 
 struct ft_graph {
@@ -60,6 +72,7 @@ struct ft_graph {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, world = 1;
+  bool loopback = false;  // world > 1 simulated on one GPU (tests)
   ncclComm_t comm = nullptr;
   bool keep_all = false;
   int n_ops = 0, n_orig_edges = 0;
@@ -68,8 +81,20 @@ struct ft_graph {
   std::vector<int> op_set;
   std::vector<EdgeRec> edges;
   std::vector<std::set<int>> in_e, out_e;
+  // FT_AUTO policy state (R9): positions in the original topological order and
+  // ordered candidate sets maintained incrementally
+  std::vector<int> pos0, order0;
+  std::set<std::pair<int, int>> live_ops;   // (pos0, op)
+  std::set<std::pair<int, int>> one_one;    // live ops with one in- and one out-edge
+  std::set<std::pair<int, int>> k1src;      // live K=1 sources with out-edges
+  std::map<std::pair<int, int>, std::set<int>> pair_edges;  // (src, dst) -> live edges
+  std::set<std::pair<int, int>> multi;      // (pos0 src, pos0 dst) with >= 2 live edges
+  std::vector<int> mark_stamp;
+  int stamp = 0;
   std::vector<FSet> sets;
   std::vector<StepRec> steps;
+  std::vector<int> pending;       // scheduled, not yet executed steps
+  std::vector<WaveBuf> waves;
   std::vector<std::vector<int64_t>> op_m, op_t, e_m, e_t;
   std::vector<char> op_ok, e_ok;
   bool started = false, have_final = false;
@@ -152,13 +177,59 @@ std::vector<int> topo_order(const ft_graph* g) {
   return order;
 }
 
-// Marking of the linear graph: the first op in topological order,
-// then, while the last marked op has exactly one downstream op, that op.
-std::vector<char> mark_backbone(const ft_graph* g, const std::vector<int>& order) {
-  std::vector<char> mk(g->n_ops, 0);
-  if (order.empty()) return mk;
-  int v = order[0];
-  mk[v] = 1;
+void refresh(ft_graph* g, int v) {
+  const std::pair<int, int> key{g->pos0[v], v};
+  g->one_one.erase(key);
+  g->k1src.erase(key);
+  if (!g->op_alive[v]) {
+    g->live_ops.erase(key);
+    return;
+  }
+  if (g->in_e[v].size() == 1 && g->out_e[v].size() == 1) g->one_one.insert(key);
+  if (g->K[v] == 1 && g->in_e[v].empty() && !g->out_e[v].empty()) g->k1src.insert(key);
+}
+
+void kill_edge(ft_graph* g, int e) {
+  const int u = g->edges[e].src, v = g->edges[e].dst;
+  g->edges[e].alive = false;
+  g->out_e[u].erase(e);
+  g->in_e[v].erase(e);
+  auto& pe = g->pair_edges[{u, v}];
+  pe.erase(e);
+  if (pe.size() < 2) g->multi.erase({g->pos0[u], g->pos0[v]});
+  if (pe.empty()) g->pair_edges.erase({u, v});
+  refresh(g, u);
+  refresh(g, v);
+}
+
+int add_edge(ft_graph* g, int s, int d, int set) {
+  g->edges.push_back(EdgeRec{s, d, true, set});
+  int e = (int)g->edges.size() - 1;
+  g->out_e[s].insert(e);
+  g->in_e[d].insert(e);
+  auto& pe = g->pair_edges[{s, d}];
+  pe.insert(e);
+  if (pe.size() >= 2 && !g->pos0.empty()) g->multi.insert({g->pos0[s], g->pos0[d]});
+  if (!g->pos0.empty()) {
+    refresh(g, s);
+    refresh(g, d);
+  }
+  return e;
+}
+
+void kill_op(ft_graph* g, int v) {
+  g->op_alive[v] = 0;
+  refresh(g, v);
+}
+
+// Marking with the R9 order: the first live op, then while the last
+// marked op has exactly one downstream op, that op.  Marked ops get the
+// current stamp.
+void mark_backbone(ft_graph* g) {
+  ++g->stamp;
+  if (g->live_ops.empty()) return;
+  int v = g->live_ops.begin()->second;
+  g->mark_stamp[v] = g->stamp;
   while (true) {
     int only = -1;
     bool several = false;
@@ -167,25 +238,10 @@ std::vector<char> mark_backbone(const ft_graph* g, const std::vector<int>& order
       if (only < 0) only = d;
       else if (d != only) several = true;
     }
-    if (only < 0 || several || mk[only]) break;
-    mk[only] = 1;
+    if (only < 0 || several || g->mark_stamp[only] == g->stamp) break;
+    g->mark_stamp[only] = g->stamp;
     v = only;
   }
-  return mk;
-}
-
-void kill_edge(ft_graph* g, int e) {
-  g->edges[e].alive = false;
-  g->out_e[g->edges[e].src].erase(e);
-  g->in_e[g->edges[e].dst].erase(e);
-}
-
-int add_edge(ft_graph* g, int s, int d, int set) {
-  g->edges.push_back(EdgeRec{s, d, true, set});
-  int e = (int)g->edges.size() - 1;
-  g->out_e[s].insert(e);
-  g->in_e[d].insert(e);
-  return e;
 }
 
 // ---- device side ----------------------------------------------------------
@@ -247,181 +303,314 @@ int start(ft_graph* g) {
 
 ftk::FacSet fac(const FSet& s) { return ftk::FacSet{s.d_off, s.d_m, s.d_t}; }
 
-void free_mt(ft_graph* g, int set) {
+// A consumed step output releases its wave arena's m/t once every set of that
+// wave has been consumed (bp stays for unroll).
+void consume(ft_graph* g, int set) {
   FSet& s = g->sets[set];
-  if (s.kind != S_STEP || !s.owned || !s.mt_live || g->keep_all) return;
-  cudaFreeAsync(s.d_m, g->stream);
-  cudaFreeAsync(s.d_t, g->stream);
-  s.d_m = s.d_t = nullptr;
+  if (s.kind != S_STEP || !s.mt_live) return;
   s.mt_live = false;
+  WaveBuf& w = g->waves[s.wave_buf];
+  if (--w.live == 0 && !g->keep_all) {
+    cudaFreeAsync(w.m, g->stream);
+    cudaFreeAsync(w.t, g->stream);
+    w.m = w.t = nullptr;
+  }
 }
 
-// All-gather-v of per-rank CSR slices over NCCL (world > 1): counts first,
-// then one broadcast per root into the final positions.
-int exchange(ft_graph* g, const std::vector<int64_t>& seg_lo, FSet& out, std::vector<int64_t>& cnt,
-             float* comm_ms);
-
-int exec_step(ft_graph* g, StepRec r, int* out_set) {
-  const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
-  ftk::StepDev s{};
-  s.kind = r.kind;
-  s.KA = r.KA;
-  s.KB = r.KB;
-  s.KC = r.KC;
-  s.nseg = r.nseg;
-  s.nblk = r.nblk;
-  s.X = fac(X);
-  s.Y = fac(Y);
-  s.Z = fac(Z);
-  // shard output segments over ranks by product tuples (host mirror of sizes)
-  std::vector<int64_t> lo(g->world + 1, 0);
-  lo[g->world] = r.nseg;
-  if (g->world > 1) {
-    std::vector<int64_t> w(r.nseg, 0);
-    // weight of segment = its product tuples (Lemma 3/4 cardinalities)
-    // computed with the same block mapping as the kernels
-    for (int64_t sg = 0; sg < r.nseg; ++sg) {
-      int64_t tot = 0;
-      for (int64_t k = 0; k < r.nblk; ++k) {
-        int64_t sx, sy, sz;
-        if (r.kind == ftk::K_NODE) {
-          int64_t wv = sg / r.KC, p = sg % r.KC;
-          sx = wv * r.KB + k; sy = k; sz = k * r.KC + p;
-        } else if (r.kind == ftk::K_LDP) {
-          sx = k * r.KB + sg; sy = k; sz = sg;
-        } else if (r.kind == ftk::K_FINAL) {
-          sx = k; sy = 0; sz = 0;
-        } else {
-          sx = sg; sy = sg; sz = 0;
-        }
-        tot += (X.off[sx + 1] - X.off[sx]) * (Y.off[sy + 1] - Y.off[sy]) * (Z.off[sz + 1] - Z.off[sz]);
-      }
-      w[sg] = tot;
-    }
-    ft_shard_plan(r.nseg, w.data(), g->world, lo.data());
+// Block mapping (host mirror of ftk::block_factor_segs; used for shard
+// weights and unroll).
+void host_block_segs(const StepRec& r, int64_t sg, int64_t k, int64_t& sx, int64_t& sy,
+                     int64_t& sz) {
+  if (r.kind == ftk::K_NODE) {
+    int64_t w = sg / r.KC, p = sg % r.KC;
+    sx = w * r.KB + k; sy = k; sz = k * r.KC + p;
+  } else if (r.kind == ftk::K_LDP) {
+    sx = k * r.KB + sg; sy = k; sz = sg;
+  } else if (r.kind == ftk::K_FINAL) {
+    sx = k; sy = 0; sz = 0;
+  } else {
+    sx = sg; sy = sg; sz = 0;
   }
-  s.seg_lo = lo[g->rank];
-  s.seg_hi = lo[g->rank + 1];
-  ftk::StepResult res;
+}
+
+int nccl_fail(ft_graph* g, ncclResult_t nr) {
+  g->poisoned = FT_ECUDA;
+  g->err = std::string("nccl: ") + ncclGetErrorString(nr);
+  return FT_ECUDA;
+}
+
+// Executes one wave of mutually independent steps as a single batch
+// (DESIGN.md 6): shard the wave's segments over ranks, run the pipeline,
+// all-gather counts and survivors, gather into the wave arena.
+int exec_wave(ft_graph* g, const std::vector<int>& ids) {
+  const int ns = (int)ids.size();
+  // global segment numbering of the wave (step-major)
+  std::vector<int64_t> sbase(ns + 1, 0);
+  for (int q = 0; q < ns; ++q) sbase[q + 1] = sbase[q] + g->steps[ids[q]].nseg;
+  const int64_t NS = sbase[ns];
+  std::vector<int64_t> lo(g->world + 1, 0);
+  lo[g->world] = NS;
+  if (g->world > 1) {
+    // weights = product tuples per segment (exact when cheap, else uniform per step);
+    // any partition gives identical results (ids are shard-invariant, R6)
+    int64_t work = 0;
+    for (int q = 0; q < ns; ++q) work += g->steps[ids[q]].nseg * g->steps[ids[q]].nblk;
+    std::vector<int64_t> w(NS, 1);
+    for (int q = 0; q < ns; ++q) {
+      const StepRec& r = g->steps[ids[q]];
+      const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+      for (int64_t sg = 0; sg < r.nseg; ++sg) {
+        int64_t tot = 0;
+        if (work <= (1 << 21)) {
+          for (int64_t k = 0; k < r.nblk; ++k) {
+            int64_t sx, sy, sz;
+            host_block_segs(r, sg, k, sx, sy, sz);
+            tot += (X.off[sx + 1] - X.off[sx]) * (Y.off[sy + 1] - Y.off[sy]) * (Z.off[sz + 1] - Z.off[sz]);
+          }
+        } else {
+          tot = r.nblk;
+        }
+        w[sbase[q] + sg] = tot;
+      }
+    }
+    ft_shard_plan(NS, w.data(), g->world, lo.data());
+  }
+  // step descriptors for the global segment range [a, b) of the wave
+  auto make_sd = [&](int64_t a, int64_t b) {
+  std::vector<ftk::StepDev> sd(ns);
+  for (int q = 0; q < ns; ++q) {
+    const StepRec& r = g->steps[ids[q]];
+    ftk::StepDev& d = sd[q];
+    std::memset(&d, 0, sizeof(d));
+    d.kind = r.kind;
+    d.KA = r.KA;
+    d.KB = r.KB;
+    d.KC = r.KC;
+    d.nseg = r.nseg;
+    d.nblk = r.nblk;
+    d.X = fac(g->sets[r.X]);
+    d.Y = fac(g->sets[r.Y]);
+    d.Z = fac(g->sets[r.Z]);
+    d.seg_lo = std::min(std::max(a - sbase[q], (int64_t)0), r.nseg);
+    d.seg_hi = std::min(std::max(b - sbase[q], (int64_t)0), r.nseg);
+  }
+  return sd;
+  };
+  // real ranks run their own range; loopback runs every virtual rank here
+  std::vector<int> vr;
+  if (g->loopback)
+    for (int q = 0; q < g->world; ++q) vr.push_back(q);
+  else
+    vr.push_back(g->rank);
+  ftk::StepResult res, agg;
   std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
   g->runner->profile = g->profile;
-  cudaError_t ce = g->runner->run(s, g->stream, &res);
-  if (ce == cudaErrorInvalidConfiguration)
-    return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
-  if (ce != cudaSuccess) return cuda_fail(g, ce, "step");
+  std::vector<int64_t> cnt(NS, 0), tup(NS, 0);
+  std::vector<ftk::StepDev> sd;
+  for (size_t v = 0; v < vr.size(); ++v) {
+    const int64_t a = lo[vr[v]], b = lo[vr[v] + 1];
+    sd = make_sd(a, b);
+    cudaError_t ce = g->runner->run(sd, g->stream, &res);
+    if (ce == cudaErrorInvalidConfiguration)
+      return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
+    if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
+    for (int64_t i = 0; i < res.nloc; ++i) {  // per-segment survivor counts
+      cnt[a + i] = res.counts[i];
+      tup[a + i] = res.seg_tuples[i];
+    }
+    agg.levels = std::max(agg.levels, res.levels);
+    agg.candidates += res.candidates;
+    agg.kernel_ms += res.kernel_ms;
+    agg.launches += res.launches;
+    agg.retries += res.retries;
+    agg.plan_ms += res.plan_ms;
+    agg.direct_ms += res.direct_ms;
+    agg.filter_ms += res.filter_ms;
+    agg.bucket_ms += res.bucket_ms;
+    agg.compact_ms += res.compact_ms;
+    agg.host_ms += res.host_ms;
+  }
+  float comm_ms = 0;
+  cudaEvent_t ca = nullptr, cb = nullptr;
+  if (g->world > 1 && !g->loopback) {
+    cudaEventCreate(&ca);
+    cudaEventCreate(&cb);
+    cudaEventRecord(ca, g->stream);
+    int64_t* dc = nullptr;
+    CU(cudaMallocAsync((void**)&dc, sizeof(int64_t) * 2 * NS, g->stream), "alloc counts");
+    std::vector<int64_t> both(2 * NS);
+    for (int64_t i = 0; i < NS; ++i) {
+      both[2 * i] = cnt[i];
+      both[2 * i + 1] = tup[i];
+    }
+    CU(cudaMemcpyAsync(dc, both.data(), sizeof(int64_t) * 2 * NS, cudaMemcpyHostToDevice, g->stream), "counts");
+    ncclResult_t nr = ncclGroupStart();
+    for (int q = 0; q < g->world && nr == ncclSuccess; ++q)
+      if (lo[q + 1] > lo[q])
+        nr = ncclBroadcast(dc + 2 * lo[q], dc + 2 * lo[q], 2 * (lo[q + 1] - lo[q]), ncclInt64, q,
+                           g->comm, g->stream);
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    CU(cudaMemcpyAsync(both.data(), dc, sizeof(int64_t) * 2 * NS, cudaMemcpyDeviceToHost, g->stream), "counts");
+    CU(cudaFreeAsync(dc, g->stream), "free");
+    CU(cudaStreamSynchronize(g->stream), "counts");
+    for (int64_t i = 0; i < NS; ++i) {
+      cnt[i] = both[2 * i];
+      tup[i] = both[2 * i + 1];
+    }
+  }
+  // wave arena: step-major CSR
+  std::vector<int64_t> hoff(NS + ns, 0);  // per step: nseg+1 offsets (relative to the step)
+  std::vector<int64_t> sbeg(ns + 1, 0);   // survivor start of each step in the arena
+  for (int q = 0; q < ns; ++q) {
+    int64_t* o = hoff.data() + sbase[q] + q;
+    o[0] = 0;
+    for (int64_t i = 0; i < g->steps[ids[q]].nseg; ++i) o[i + 1] = o[i] + cnt[sbase[q] + i];
+    sbeg[q + 1] = sbeg[q] + o[g->steps[ids[q]].nseg];
+  }
+  const int64_t total = sbeg[ns];
+  WaveBuf wb;
+  const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
+  CU(cudaMallocAsync((void**)&wb.m, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&wb.t, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&wb.bp, nb, g->stream), "alloc frontier");
+  CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+  CU(cudaMemcpyAsync(wb.off, hoff.data(), sizeof(int64_t) * (NS + ns), cudaMemcpyHostToDevice,
+                     g->stream), "upload seg_off");
+  auto set_out = [&](std::vector<ftk::StepDev>& v) {
+    for (int q = 0; q < ns; ++q) {
+      ftk::StepDev& d = v[q];
+      d.out_m = wb.m + sbeg[q];
+      d.out_t = wb.t + sbeg[q];
+      d.out_bp = wb.bp + sbeg[q];
+      d.out_off = wb.off + sbase[q] + q + d.seg_lo;
+    }
+  };
+  set_out(sd);
+  CU(g->runner->gather(sd, res, g->stream), "gather");  // last (or only) rank's pool
+  for (size_t v = 0; v + 1 < vr.size(); ++v) {           // loopback: re-run the others
+    std::vector<ftk::StepDev> sv = make_sd(lo[vr[v]], lo[vr[v] + 1]);
+    cudaError_t ce = g->runner->run(sv, g->stream, &res);
+    if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline (loopback)");
+    set_out(sv);
+    CU(g->runner->gather(sv, res, g->stream), "gather");
+  }
+  if (g->world > 1 && !g->loopback) {
+    // all-gather-v of survivors: rank q owns arena range [A(lo[q]), A(lo[q+1]))
+    auto arena_pos = [&](int64_t gseg) -> int64_t {  // arena offset of global segment gseg
+      int q = (int)(std::upper_bound(sbase.begin(), sbase.end(), gseg) - sbase.begin()) - 1;
+      if (q >= ns) return total;
+      return sbeg[q] + hoff[sbase[q] + q + (gseg - sbase[q])];
+    };
+    ncclResult_t nr = ncclGroupStart();
+    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
+      const int64_t a0 = arena_pos(lo[q]), a1 = arena_pos(lo[q + 1]);
+      if (a1 <= a0) continue;
+      nr = ncclBroadcast(wb.m + a0, wb.m + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(wb.t + a0, wb.t + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(wb.bp + a0, wb.bp + a0, a1 - a0, ncclUint64, q, g->comm, g->stream);
+    }
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    cudaEventRecord(cb, g->stream);
+  }
+  CU(cudaStreamSynchronize(g->stream), "wave sync");
+  if (g->world > 1 && !g->loopback) {
+    cudaEventElapsedTime(&comm_ms, ca, cb);
+    cudaEventDestroy(ca);
+    cudaEventDestroy(cb);
+  }
+  // bookkeeping: sets, stats, consumption
+  const int wi = (int)g->waves.size();
+  wb.live = ns;
+  g->waves.push_back(wb);
+  for (int q = 0; q < ns; ++q) {
+    StepRec& r = g->steps[ids[q]];
+    FSet& o = g->sets[r.out];
+    o.off.assign(hoff.begin() + sbase[q] + q, hoff.begin() + sbase[q] + q + r.nseg + 1);
+    o.d_off = wb.off + sbase[q] + q;
+    o.d_m = wb.m + sbeg[q];
+    o.d_t = wb.t + sbeg[q];
+    o.d_bp = wb.bp + sbeg[q];
+    o.wave_buf = wi;
+    r.done = true;
+    ft_step_stats& st = r.st;
+    st.kind = r.kind;
+    st.levels = agg.levels;
+    st.wave = wi;
+    st.nseg = r.nseg;
+    st.nblk = r.nblk;
+    st.tuples = 0;
+    st.max_seg = 0;
+    for (int64_t i = 0; i < r.nseg; ++i) {
+      st.tuples += tup[sbase[q] + i];
+      st.max_seg = std::max<int64_t>(st.max_seg, cnt[sbase[q] + i]);
+    }
+    st.survivors = o.off[r.nseg];
+    st.retries = agg.retries;
+    if (q == 0) {  // wave-level numbers are booked on the wave's first step
+      st.candidates = agg.candidates;
+      st.kernel_ms = agg.kernel_ms;
+      st.comm_ms = comm_ms;
+      st.launches = agg.launches + (int64_t)vr.size();
+      st.plan_ms = agg.plan_ms;
+      st.direct_ms = agg.direct_ms;
+      st.filter_ms = agg.filter_ms;
+      st.bucket_ms = agg.bucket_ms;
+      st.compact_ms = agg.compact_ms;
+      st.host_ms = agg.host_ms;
+    }
+  }
+  for (int q = 0; q < ns; ++q) {
+    const StepRec& r = g->steps[ids[q]];
+    consume(g, r.X);
+    consume(g, r.Y);
+    consume(g, r.Z);
+  }
+  return FT_OK;
+}
+
+// Runs every scheduled step: wave(step) = 1 + max wave of its pending
+// producers; each wave is one batched pipeline run.  The results do not
+// depend on the grouping (each step is a function of its inputs only).
+int flush(ft_graph* g) {
+  if (g->pending.empty()) return FT_OK;
+  std::vector<int> wave(g->steps.size(), 0);
+  int maxw = 0;
+  for (int id : g->pending) {
+    const StepRec& r = g->steps[id];
+    int w = 1;
+    for (int in : {r.X, r.Y, r.Z}) {
+      const FSet& S = g->sets[in];
+      if (S.kind == S_STEP && !g->steps[S.step].done) w = std::max(w, wave[S.step] + 1);
+    }
+    wave[id] = w;
+    maxw = std::max(maxw, w);
+  }
+  std::vector<std::vector<int>> groups(maxw + 1);
+  for (int id : g->pending) groups[wave[id]].push_back(id);
+  g->pending.clear();
+  for (int w = 1; w <= maxw; ++w) {
+    int rc = exec_wave(g, groups[w]);
+    if (rc) return rc;
+  }
+  return FT_OK;
+}
+
+// Schedules a step (no GPU work): creates its output set placeholder.
+int schedule(ft_graph* g, StepRec r) {
   FSet o;
   o.kind = S_STEP;
   o.step = (int)g->steps.size();
   o.nseg = r.nseg;
-  o.owned = true;
-  std::vector<int64_t> cnt(r.nseg, 0);
-  for (int64_t i = 0; i < res.nloc; ++i) cnt[s.seg_lo + i] = res.counts[i];
-  float comm_ms = 0;
-  if (g->world > 1) {
-    int rc = exchange(g, lo, o, cnt, &comm_ms);
-    if (rc) return rc;
-  }
-  o.off.assign(r.nseg + 1, 0);
-  for (int64_t i = 0; i < r.nseg; ++i) o.off[i + 1] = o.off[i] + cnt[i];
-  const int64_t total = o.off[r.nseg];
-  const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
-  CU(cudaMallocAsync((void**)&o.d_m, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&o.d_t, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&o.d_bp, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&o.d_off, sizeof(int64_t) * (r.nseg + 1), g->stream), "alloc frontier");
-  CU(cudaMemcpyAsync(o.d_off, o.off.data(), sizeof(int64_t) * (r.nseg + 1), cudaMemcpyHostToDevice,
-                     g->stream), "upload seg_off");
-  if (g->world == 1) {
-    CU(g->runner->gather(s, res, o.off.data(), o.d_m, o.d_t, o.d_bp, g->stream), "gather");
-  } else {
-    CU(g->runner->gather(s, res, o.off.data() + s.seg_lo, o.d_m, o.d_t, o.d_bp, g->stream), "gather");
-    int rc = exchange(g, lo, o, cnt, &comm_ms);  // second phase: payload
-    if (rc) return rc;
-  }
-  // the host copy of seg_off must outlive the async upload
-  CU(cudaStreamSynchronize(g->stream), "step sync");
-  r.st.kind = r.kind;
-  r.st.levels = res.levels;
-  r.st.nseg = r.nseg;
-  r.st.nblk = r.nblk;
-  r.st.tuples = res.tuples;
-  r.st.survivors = total;
-  r.st.candidates = res.candidates;
-  r.st.retries = res.retries;
-  r.st.kernel_ms = res.kernel_ms;
-  r.st.comm_ms = comm_ms;
-  r.st.launches = res.launches + 1;  // + gather
-  r.st.plan_ms = res.plan_ms;
-  r.st.direct_ms = res.direct_ms;
-  r.st.filter_ms = res.filter_ms;
-  r.st.bucket_ms = res.bucket_ms;
-  r.st.compact_ms = res.compact_ms;
-  r.st.host_ms = res.host_ms;
-  r.st.max_seg = 0;
-  for (int64_t i = 0; i < r.nseg; ++i) r.st.max_seg = std::max<int64_t>(r.st.max_seg, cnt[i]);
   r.out = (int)g->sets.size();
   g->sets.push_back(std::move(o));
   g->steps.push_back(r);
-  free_mt(g, r.X);
-  free_mt(g, r.Y);
-  free_mt(g, r.Z);
-  *out_set = r.out;
-  return FT_OK;
+  g->pending.push_back((int)g->steps.size() - 1);
+  return r.out;
 }
 
-int exchange(ft_graph* g, const std::vector<int64_t>& lo, FSet& o, std::vector<int64_t>& cnt,
-             float* comm_ms) {
-  // phase 1 (o.d_m == nullptr): all-gather per-segment counts
-  // phase 2: broadcast each rank's contiguous slice (m, t, bp) to all ranks
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  cudaEventRecord(a, g->stream);
-  ncclResult_t nr = ncclSuccess;
-  if (!o.d_m) {
-    int64_t* dcnt = nullptr;
-    int64_t nseg = (int64_t)cnt.size();
-    CU(cudaMallocAsync((void**)&dcnt, sizeof(int64_t) * nseg, g->stream), "alloc counts");
-    CU(cudaMemcpyAsync(dcnt, cnt.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, g->stream),
-       "counts");
-    nr = ncclGroupStart();
-    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
-      int64_t n = lo[q + 1] - lo[q];
-      if (n > 0) nr = ncclBroadcast(dcnt + lo[q], dcnt + lo[q], n, ncclInt64, q, g->comm, g->stream);
-    }
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
-    CU(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int64_t) * nseg, cudaMemcpyDeviceToHost, g->stream),
-       "counts");
-    CU(cudaFreeAsync(dcnt, g->stream), "free");
-    CU(cudaStreamSynchronize(g->stream), "counts");
-  } else {
-    nr = ncclGroupStart();
-    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
-      int64_t a0 = o.off[lo[q]], n = o.off[lo[q + 1]] - a0;
-      if (n <= 0) continue;
-      nr = ncclBroadcast(o.d_m + a0, o.d_m + a0, n, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(o.d_t + a0, o.d_t + a0, n, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess)
-        nr = ncclBroadcast(o.d_bp + a0, o.d_bp + a0, n, ncclUint64, q, g->comm, g->stream);
-    }
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
-  }
-  cudaEventRecord(b, g->stream);
-  cudaEventSynchronize(b);
-  float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
-  *comm_ms += ms;
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  if (nr != ncclSuccess) {
-    g->poisoned = FT_ECUDA;
-    g->err = std::string("nccl: ") + ncclGetErrorString(nr);
-    return FT_ECUDA;
-  }
-  return FT_OK;
-}
-
-// ---- eliminations ------------------------------------------------------------
+// ---- eliminations (structural; steps are scheduled, then flushed) ----------
 
 int do_node(ft_graph* g, int i, int* new_edge) {  // Eq.4
   int ehi = *g->in_e[i].begin(), eij = *g->out_e[i].begin();
@@ -436,14 +625,12 @@ int do_node(ft_graph* g, int i, int* new_edge) {  // Eq.4
   r.KC = g->K[j];
   r.nseg = r.KA * r.KC;
   r.nblk = r.KB;
-  int out;
-  int rc = exec_step(g, r, &out);
-  if (rc) return rc;
+  int out = schedule(g, r);
   g->sets[out].a_op = h;
   g->sets[out].b_op = j;
   kill_edge(g, ehi);
   kill_edge(g, eij);
-  g->op_alive[i] = 0;
+  kill_op(g, i);
   int e = add_edge(g, h, j, out);
   if (new_edge) *new_edge = e;
   return FT_OK;
@@ -460,9 +647,7 @@ int do_merge(ft_graph* g, int e1, int e2, int* new_edge) {  // Eq.5,
   r.KB = g->K[v];
   r.nseg = r.KA * r.KB;
   r.nblk = 1;
-  int out;
-  int rc = exec_step(g, r, &out);
-  if (rc) return rc;
+  int out = schedule(g, r);
   g->sets[out].a_op = u;
   g->sets[out].b_op = v;
   kill_edge(g, e1);
@@ -474,14 +659,12 @@ int do_merge(ft_graph* g, int e1, int e2, int* new_edge) {  // Eq.5,
 
 // Exact K=1 case of Eq.7: fold the source into every consumer;
 // the source's own cost goes to its topologically first consumer (R13).
-int do_fold(ft_graph* g, int src, const std::vector<int>& order) {
-  std::vector<int> pos(g->n_ops, 0);
-  for (size_t q = 0; q < order.size(); ++q) pos[order[q]] = (int)q;
+int do_fold(ft_graph* g, int src) {
   std::vector<int> outs(g->out_e[src].begin(), g->out_e[src].end());  // ascending ids
   int first = -1;
   for (int e : outs) {
     int c = g->edges[e].dst;
-    if (first < 0 || pos[c] < pos[first]) first = c;
+    if (first < 0 || g->pos0[c] < g->pos0[first]) first = c;
   }
   for (int e : outs) {
     int c = g->edges[e].dst;
@@ -493,56 +676,38 @@ int do_fold(ft_graph* g, int src, const std::vector<int>& order) {
     r.KA = g->K[c];
     r.nseg = g->K[c];
     r.nblk = 1;
-    int out;
-    int rc = exec_step(g, r, &out);
-    if (rc) return rc;
+    int out = schedule(g, r);
     g->sets[out].a_op = c;
     g->op_set[c] = out;
     kill_edge(g, e);
   }
-  g->op_alive[src] = 0;
+  kill_op(g, src);
   return FT_OK;
 }
 
-// One FT_AUTO elimination (R9).  1 = eliminated, 0 = none applies, <0 error.
+// One FT_AUTO elimination (R9).  1 = scheduled, 0 = none applies, <0 error.
 int auto_step(ft_graph* g) {
-  std::vector<int> order = topo_order(g);
-  std::vector<char> mk = mark_backbone(g, order);
-  std::vector<int> pos(g->n_ops, -1);
-  for (size_t q = 0; q < order.size(); ++q) pos[order[q]] = (int)q;
+  mark_backbone(g);
   // (a) parallel edges: topologically first (src, dst), two lowest ids
-  int best_e1 = -1, best_e2 = -1, best_pd = 1 << 30;
-  for (int u : order) {
-    std::vector<std::pair<int, int>> byd;  // (pos[dst], edge)
-    for (int e : g->out_e[u]) byd.push_back({pos[g->edges[e].dst], e});
-    std::sort(byd.begin(), byd.end());
-    for (size_t q = 1; q < byd.size(); ++q)
-      if (byd[q].first == byd[q - 1].first) {
-        if (byd[q].first < best_pd) {
-          best_pd = byd[q].first;
-          best_e1 = byd[q - 1].second;
-          best_e2 = byd[q].second;
-        }
-        break;
-      }
-    if (best_e1 >= 0) break;
-  }
-  if (best_e1 >= 0) {
-    int rc = do_merge(g, std::min(best_e1, best_e2), std::max(best_e1, best_e2), nullptr);
+  if (!g->multi.empty()) {
+    const auto key = *g->multi.begin();
+    const int u = g->order0[key.first], v = g->order0[key.second];
+    const auto& es = g->pair_edges[{u, v}];
+    const int e1 = *es.begin(), e2 = *std::next(es.begin());
+    int rc = do_merge(g, e1, e2, nullptr);
     return rc ? rc : 1;
   }
   // (b) node elimination: topologically first unmarked 1-in-1-out op
-  for (int v : order)
-    if (!mk[v] && g->in_e[v].size() == 1 && g->out_e[v].size() == 1) {
-      int rc = do_node(g, v, nullptr);
+  for (const auto& kv : g->one_one)
+    if (g->mark_stamp[kv.second] != g->stamp) {
+      int rc = do_node(g, kv.second, nullptr);
       return rc ? rc : 1;
     }
   // (c) K=1 source fold
-  for (int v : order)
-    if (g->K[v] == 1 && g->in_e[v].empty() && !g->out_e[v].empty()) {
-      int rc = do_fold(g, v, order);
-      return rc ? rc : 1;
-    }
+  if (!g->k1src.empty()) {
+    int rc = do_fold(g, g->k1src.begin()->second);
+    return rc ? rc : 1;
+  }
   return 0;
 }
 
@@ -581,9 +746,7 @@ int run_ldp(ft_graph* g) {
     r.KB = g->K[chain[i]];
     r.nseg = r.KB;
     r.nblk = r.KA;
-    int out;
-    int rc = exec_step(g, r, &out);
-    if (rc) return rc;
+    int out = schedule(g, r);
     g->sets[out].a_op = chain[i];
     cf = out;
   }
@@ -595,8 +758,8 @@ int run_ldp(ft_graph* g) {
   f.KA = g->K[chain.back()];
   f.nseg = 1;
   f.nblk = f.KA;
-  int out;
-  int rc = exec_step(g, f, &out);
+  int out = schedule(g, f);
+  int rc = flush(g);
   if (rc) return rc;
   g->final_set = out;
   const FSet& F = g->sets[out];
@@ -769,9 +932,20 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     add_edge(g, src[e], dst[e], (int)g->sets.size());
     g->sets.push_back(std::move(s));
   }
-  if ((int)topo_order(g).size() != n_ops) {
-    delete g;
-    return FT_EINVAL;  // cycle
+  {
+    std::vector<int> order = topo_order(g);
+    if ((int)order.size() != n_ops) {
+      delete g;
+      return FT_EINVAL;  // cycle
+    }
+    g->order0 = order;
+    g->pos0.assign(n_ops, 0);
+    for (int q = 0; q < n_ops; ++q) g->pos0[order[q]] = q;
+    g->mark_stamp.assign(n_ops, 0);
+    for (int v = 0; v < n_ops; ++v) g->live_ops.insert({g->pos0[v], v});
+    for (const auto& kv : g->pair_edges)
+      if (kv.second.size() >= 2) g->multi.insert({g->pos0[kv.first.first], g->pos0[kv.first.second]});
+    for (int v = 0; v < n_ops; ++v) refresh(g, v);
   }
   if (opt) {
     g->dev = opt->device;
@@ -782,7 +956,8 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     g->profile = opt->profile != 0;
     g->stream = (cudaStream_t)opt->stream;
   }
-  if (g->world > 1 && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
+  if (opt && g->world > 1 && !g->comm && opt->loopback) g->loopback = true;
+  if (g->world > 1 && !g->loopback && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
     delete g;
     return FT_EINVAL;
   }
@@ -812,13 +987,12 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
 void ft_graph_destroy(ft_graph* g) {
   if (!g) return;
   if (g->stream) cudaStreamSynchronize(g->stream);
-  for (auto& s : g->sets)
-    if (s.owned) {
-      if (s.d_m) cudaFree(s.d_m);
-      if (s.d_t) cudaFree(s.d_t);
-      if (s.d_bp) cudaFree(s.d_bp);
-      if (s.d_off) cudaFree(s.d_off);
-    }
+  for (auto& w : g->waves) {
+    if (w.m) cudaFree(w.m);
+    if (w.t) cudaFree(w.t);
+    if (w.bp) cudaFree(w.bp);
+    if (w.off) cudaFree(w.off);
+  }
   if (g->d_costs) cudaFree(g->d_costs);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -866,13 +1040,13 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
   if (g->have_final) return setf(g, FT_ESTATE, "frontier already computed");
   if (kind == FT_NODE) {
     if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return setf(g, FT_EINVAL, "bad operator");
-    std::vector<int> order = topo_order(g);
-    std::vector<char> mk = mark_backbone(g, order);
-    if (mk[id] || g->in_e[id].size() != 1 || g->out_e[id].size() != 1)
+    mark_backbone(g);
+    if (g->mark_stamp[id] == g->stamp || g->in_e[id].size() != 1 || g->out_e[id].size() != 1)
       return setf(g, FT_EPRECOND, "node elimination needs an unmarked op with one in- and one out-edge");
     int rc = start(g);
     if (rc) return rc;
-    return do_node(g, id, new_edge);
+    rc = do_node(g, id, new_edge);
+    return rc ? rc : flush(g);
   }
   if (kind == FT_EDGE) {
     if (id < 0 || id >= (int)g->edges.size() || !g->edges[id].alive) return setf(g, FT_EINVAL, "bad edge");
@@ -885,7 +1059,8 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
     if (other < 0) return setf(g, FT_EPRECOND, "edge elimination needs a parallel edge");
     int rc = start(g);
     if (rc) return rc;
-    return do_merge(g, std::min(id, other), std::max(id, other), new_edge);
+    rc = do_merge(g, std::min(id, other), std::max(id, other), new_edge);
+    return rc ? rc : flush(g);
   }
   int rc = start(g);
   if (rc) return rc;
@@ -894,7 +1069,7 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
     if (r < 0) return r;
     if (r == 0) break;
   }
-  return FT_OK;
+  return flush(g);
 }
 
 int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out) {
@@ -1008,7 +1183,8 @@ int ft_step_output(ft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int
   *n_out = n;
   if (cap < n) return FT_ESIZE;
   if (seg_off) std::memcpy(seg_off, S.off.data(), sizeof(int64_t) * (S.nseg + 1));
-  if ((m || t) && !S.mt_live) return setf(g, FT_ESTATE, "m/t of a consumed set (create with keep_all)");
+  if ((m || t) && (S.wave_buf < 0 || !g->waves[S.wave_buf].m))
+    return setf(g, FT_ESTATE, "m/t of a consumed set (create with keep_all)");
   if (n) {
     if (m) CU(cudaMemcpyAsync(m, S.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
     if (t) CU(cudaMemcpyAsync(t, S.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");

@@ -30,6 +30,7 @@ namespace ftk {
 constexpr int64_t INF = INT64_MAX;
 constexpr int LMAX = 12;            // max sample level
 constexpr int C_DIRECT = 1024;      // direct (single-CTA) segment capacity
+constexpr int WARP_DIRECT = 256;    // direct segments up to this size: one warp each
 constexpr int DIRECT_NT = 256;      // threads of the direct / bucket CTA kernels
 constexpr int CHUNK = 16;           // run elements per filter work item
 constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
@@ -44,12 +45,32 @@ struct FacSet {
   const int64_t* t;
 };
 
+// One FT step of a batch ("wave" of independent steps).
 struct StepDev {
   int kind;
-  int slog;  // sample stride at level l = 2^(slog*l)
+  int pad_;
   int64_t KA, KB, KC, nseg, nblk;
   int64_t seg_lo, seg_hi;  // this rank's output segments [seg_lo, seg_hi)
   FacSet X, Y, Z;
+  // gather destination (set after the survivor counts are known)
+  int64_t* out_m;
+  int64_t* out_t;
+  uint64_t* out_bp;
+  const int64_t* out_off;  // [seg_hi - seg_lo] offsets of this rank's segments in the output
+};
+
+// A batch of steps; local segments / blocks are numbered consecutively over
+// the steps: step j owns segments [seg_base[j], seg_base[j+1]) and blocks
+// [blk_base[j], blk_base[j+1]) (blocks of a segment are contiguous).
+struct BatchDev {
+  const StepDev* steps;
+  const int64_t* seg_base;  // [nsteps+1]
+  const int64_t* blk_base;  // [nsteps+1]
+  int nsteps;
+  int slog;                 // sample stride at level l = 2^(slog*l)
+  int cdirect;              // direct-path capacity (<= C_DIRECT)
+  int64_t nseg;             // local segments over all steps
+  int64_t nblk;             // local blocks over all steps
 };
 
 // Step header written by the plan kernel, read back by the host.
@@ -81,7 +102,9 @@ struct Pool {
 struct LevelDev {
   int level;
   int st;      // log2 of the sample stride
+  int run_item;  // filter work-item length (sampled run elements)
   const int32_t* seg_d;
+  const int32_t* seg_n;  // sample size at the direct level
   const int64_t* blk_rel;
   Pool in;     // level l+1 output (G), valid when level < D
   Pool out;
@@ -117,6 +140,17 @@ struct LevelDev {
 
 // ---------------------------------------------------------------------------
 // helpers
+
+// Largest j in [0, n) with base[j] <= x (base ascending, base[0] = 0).
+__device__ __forceinline__ int find_base(const int64_t* base, int n, int64_t x) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(base + mid) <= x) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
 
 __device__ __forceinline__ bool key_lt(int64_t am, int64_t at, uint64_t ai, int64_t bm, int64_t bt,
                                        uint64_t bi) {

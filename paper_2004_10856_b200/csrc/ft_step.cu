@@ -3,8 +3,11 @@
 // (K4), final gather.  See ft_kernels.cuh for the algorithm and DESIGN.md.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "ft_kernels.cuh"
 #include "ft_step.h"
@@ -94,14 +97,18 @@ void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap,
 // segment (ids, R6), sample sizes per level, the level at which the segment
 // is small enough for the direct path.
 
-__global__ void __launch_bounds__(128) k_plan(StepDev s, int32_t* seg_d, int64_t* blk_rel,
-                                              int64_t* seg_tuples, StepHdr* hdr) {
-  // one warp per output segment; lanes stride over its blocks
-  const int64_t nloc = s.seg_hi - s.seg_lo;
+__global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
+                                              int64_t* blk_rel, int64_t* seg_tuples,
+                                              StepHdr* hdr) {
+  // one warp per local output segment; lanes stride over its blocks
   const int lane = threadIdx.x & 31;
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= nloc) return;
-  const int64_t sg = s.seg_lo + i;
+  const int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gs >= B.nseg) return;
+  const int j = find_base(B.seg_base, B.nsteps, gs);
+  const StepDev& s = B.steps[j];
+  const int64_t li = gs - B.seg_base[j];
+  const int64_t sg = s.seg_lo + li;
+  int64_t* rel_out = blk_rel + B.blk_base[j] + li * s.nblk;
   unsigned long long samp[LMAX + 1];
 #pragma unroll
   for (int l = 0; l <= LMAX; ++l) samp[l] = 0;
@@ -114,13 +121,13 @@ __global__ void __launch_bounds__(128) k_plan(StepDev s, int32_t* seg_d, int64_t
       nk = b.n[0] * b.n[1] * b.n[2];
 #pragma unroll
       for (int l = 0; l <= LMAX; ++l) {
-        const int sh = s.slog * l;
+        const int sh = B.slog * l;
         samp[l] += (unsigned long long)(samp_cnt(b.n[0], sh) * samp_cnt(b.n[1], sh) *
                                         samp_cnt(b.n[2], sh));
       }
     }
     const int64_t inc = warp_incl_sum<long long>(nk);
-    if (k < s.nblk) blk_rel[i * s.nblk + k] = rel + inc - nk;
+    if (k < s.nblk) rel_out[k] = rel + inc - nk;
     rel += __shfl_sync(0xffffffffu, inc, 31);
   }
 #pragma unroll
@@ -131,16 +138,17 @@ __global__ void __launch_bounds__(128) k_plan(StepDev s, int32_t* seg_d, int64_t
   if (lane != 0) return;
   int d = -1;
   for (int l = 0; l <= LMAX; ++l)
-    if (samp[l] <= (unsigned long long)C_DIRECT) {
+    if (samp[l] <= (unsigned long long)B.cdirect) {
       d = l;
       break;
     }
-  if (d < 0 || s.nblk > C_DIRECT) {
+  if (d < 0 || s.nblk > B.cdirect) {
     atomicExch(&hdr->bad, 1ull);
     d = LMAX;
   }
-  seg_d[i] = d;
-  seg_tuples[i] = rel;
+  seg_d[gs] = d;
+  seg_n[gs] = (int32_t)min(samp[d], (unsigned long long)INT32_MAX);
+  seg_tuples[gs] = rel;
   atomicMax(&hdr->D, (unsigned long long)d);
   atomicAdd(&hdr->tuples, (unsigned long long)rel);
   for (int l = 0; l < d; ++l) atomicAdd(&hdr->filter_samp[l], samp[l]);
@@ -151,25 +159,46 @@ __global__ void __launch_bounds__(128) k_plan(StepDev s, int32_t* seg_d, int64_t
 // Direct path: the whole level-l sample of a segment (<= C_DIRECT tuples) in
 // one CTA: product -> bitonic sort on (m,t,id) -> Alg.1 sweep -> compaction.
 
-__global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
+constexpr int DIRECT_MAXBLK = 128;  // per-block info cached in smem up to this many blocks
+
+__global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
   __shared__ int64_t sm[C_DIRECT];
   __shared__ int64_t stt[C_DIRECT];
   __shared__ uint64_t sid[C_DIRECT];
   __shared__ int kf[C_DIRECT];
-  __shared__ int64_t pre[C_DIRECT + 1];
+  __shared__ int pre[C_DIRECT + 1];
+  __shared__ int64_t bo[DIRECT_MAXBLK][3];  // factor offsets
+  __shared__ int bn[DIRECT_MAXBLK][3];      // factor sizes
+  __shared__ int bc[DIRECT_MAXBLK][3];      // sampled counts
   __shared__ long long sh[33];
   __shared__ int64_t s_start;
-  const int64_t nloc = s.seg_hi - s.seg_lo;
   const int st = L.st;
-  for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
-    if (L.seg_d[li] != L.level) continue;
+  for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
+    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= WARP_DIRECT) continue;
     if (L.hdr->overflow) return;
+    const int j = find_base(B.seg_base, B.nsteps, gs);
+    const StepDev& s = B.steps[j];
+    const int64_t li = gs - B.seg_base[j];
     const int64_t sg = s.seg_lo + li;
     const int nblk = (int)s.nblk;
+    const int64_t* rel = L.blk_rel + B.blk_base[j] + li * s.nblk;
+    const bool cached = nblk <= DIRECT_MAXBLK;
     // block sample sizes -> inclusive prefix in pre[1..nblk]
     for (int k = threadIdx.x; k < nblk; k += DIRECT_NT) {
       Blk b = load_blk(s, sg, k);
-      pre[k + 1] = samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) * samp_cnt(b.n[2], st);
+      const int c0 = (int)samp_cnt(b.n[0], st), c1 = (int)samp_cnt(b.n[1], st),
+                c2 = (int)samp_cnt(b.n[2], st);
+      pre[k + 1] = c0 * c1 * c2;
+      if (cached) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          bo[k][f] = b.o[f];
+          bn[k][f] = (int)b.n[f];
+        }
+        bc[k][0] = c0;
+        bc[k][1] = c1;
+        bc[k][2] = c2;
+      }
     }
     if (threadIdx.x == 0) pre[0] = 0;
     __syncthreads();
@@ -179,14 +208,14 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
       long long loc = 0;
       for (int k = lo; k < hi; ++k) loc += pre[k + 1];
       long long tot;
-      long long off = block_excl_sum<DIRECT_NT>(loc, sh, &tot);
+      int off = (int)block_excl_sum<DIRECT_NT>(loc, sh, &tot);
       for (int k = lo; k < hi; ++k) {
         off += pre[k + 1];
         pre[k + 1] = off;
       }
       __syncthreads();
     }
-    const int n = (int)pre[nblk];
+    const int n = pre[nblk];
     int N = 1;
     while (N < n) N <<= 1;
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
@@ -198,13 +227,26 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
           else hi = mid;
         }
         const int k = lo;
-        Blk b = load_blk(s, sg, k);
-        int64_t r = i - pre[k];
-        int64_t cy = samp_cnt(b.n[1], st), cz = samp_cnt(b.n[2], st);
-        int64_t jz = r % cz, jy = (r / cz) % cy, jx = r / (cy * cz);
-        int64_t x = samp_idx(jx, b.n[0], st), y = samp_idx(jy, b.n[1], st),
-                z = samp_idx(jz, b.n[2], st);
-        make_tuple(s, b, L.blk_rel[li * s.nblk + k], x, y, z, sm[i], stt[i], sid[i]);
+        Blk b;
+        int cy, cz;
+        if (cached) {
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            b.o[f] = bo[k][f];
+            b.n[f] = bn[k][f];
+          }
+          cy = bc[k][1];
+          cz = bc[k][2];
+        } else {
+          b = load_blk(s, sg, k);
+          cy = (int)samp_cnt(b.n[1], st);
+          cz = (int)samp_cnt(b.n[2], st);
+        }
+        const int r = i - pre[k];  // < C_DIRECT: 32-bit index math
+        const int jz = r % cz, q = r / cz, jy = q % cy, jx = q / cy;
+        const int64_t x = samp_idx(jx, b.n[0], st), y = samp_idx(jy, b.n[1], st),
+                      z = samp_idx(jz, b.n[2], st);
+        make_tuple(s, b, rel[k], x, y, z, sm[i], stt[i], sid[i]);
       } else {
         sm[i] = INF;
         stt[i] = INF;
@@ -223,8 +265,8 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
         s_start = (int64_t)st0;
       }
       atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)cnt);
-      L.out.start[li] = s_start;
-      L.out.cnt[li] = cnt;
+      L.out.start[gs] = s_start;
+      L.out.cnt[gs] = cnt;
     }
     __syncthreads();
     const int64_t o = s_start;
@@ -240,18 +282,175 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(StepDev s, LevelDev L) {
   }
 }
 
+// Direct path for small segments (<= WARP_DIRECT tuples): one warp, R rows of
+// 32 tuples in registers (element e = r*32 + lane), bitonic sort on (m,t,id)
+// by shuffles, Alg. 1 sweep by warp scans, ballot compaction.  No barriers.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(int64_t (&m)[R], int64_t (&t)[R], uint64_t (&id)[R]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= R * 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r & jr) continue;
+          const int r2 = r | jr;
+          const bool up = (((r << 5) | lane) & k) == 0;
+          const bool gt = key_lt(m[r2], t[r2], id[r2], m[r], t[r], id[r]);
+          if (gt == up) {
+            int64_t a = m[r]; m[r] = m[r2]; m[r2] = a;
+            a = t[r]; t[r] = t[r2]; t[r2] = a;
+            uint64_t b = id[r]; id[r] = id[r2]; id[r2] = b;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t pm = __shfl_xor_sync(0xffffffffu, m[r], j);
+          const int64_t pt = __shfl_xor_sync(0xffffffffu, t[r], j);
+          const uint64_t pi = __shfl_xor_sync(0xffffffffu, id[r], j);
+          const int e = (r << 5) | lane;
+          const bool up = (e & k) == 0, lower = (e & j) == 0;
+          const bool p_lt = key_lt(pm, pt, pi, m[r], t[r], id[r]);
+          // lower element of an ascending pair keeps the min, etc.
+          const bool take_partner = (lower == up) ? p_lt : !p_lt;
+          if (take_partner) {
+            m[r] = pm;
+            t[r] = pt;
+            id[r] = pi;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre) {
+  const int lane = threadIdx.x & 31;
+  const int st = L.st;
+  const int j = find_base(B.seg_base, B.nsteps, gs);
+  const StepDev& s = B.steps[j];
+  const int64_t li = gs - B.seg_base[j];
+  const int64_t sg = s.seg_lo + li;
+  const int nblk = (int)s.nblk;  // <= n <= WARP_DIRECT
+  const int64_t* rel = L.blk_rel + B.blk_base[j] + li * s.nblk;
+  // per-block sample sizes -> inclusive prefix (warp scan in chunks of 32)
+  int run = 0;
+  for (int k0 = 0; k0 < nblk; k0 += 32) {
+    const int k = k0 + lane;
+    int c = 0;
+    if (k < nblk) {
+      Blk b = load_blk(s, sg, k);
+      c = (int)(samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) * samp_cnt(b.n[2], st));
+    }
+    const int inc = warp_incl_sum<int>(c);
+    if (k < nblk) wpre[k + 1] = run + inc;
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) wpre[0] = 0;
+  __syncwarp();
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
+    if (e < n) {
+      int lo = 0, hi = nblk;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (wpre[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      const Blk b = load_blk(s, sg, lo);
+      const int rr = e - wpre[lo];
+      const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
+      const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
+      make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
+                 samp_idx(jz, b.n[2], st), m[r], t[r], id[r]);
+    } else {
+      m[r] = INF;
+      t[r] = INF;
+      id[r] = ~0ull;
+    }
+  }
+  __syncwarp();
+  warp_bitonic<R>(m, t, id);
+  // Alg. 1 sweep in e order: keep iff t < min of all earlier t
+  long long carry = INF;
+  bool keep[R];
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long inc = warp_incl_min(t[r]);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    keep[r] = ((r << 5) | lane) < n && t[r] < v;
+    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
+    carry = rowmin < carry ? rowmin : carry;
+    cnt += __popc(__ballot_sync(0xffffffffu, keep[r]));
+  }
+  int64_t base = 0;
+  if (lane == 0) {
+    unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
+    if ((int64_t)(st0 + cnt) > L.out.cap) {
+      atomicExch(&L.hdr->overflow, 1ull);
+      base = -1;
+    } else {
+      base = (int64_t)st0;
+    }
+    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)cnt);
+    L.out.start[gs] = base;
+    L.out.cnt[gs] = cnt;
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (base < 0) return;
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
+    if (keep[r]) {
+      const int64_t d = base + off + __popc(bal & ((1u << lane) - 1u));
+      L.out.m[d] = m[r];
+      L.out.t[d] = t[r];
+      L.out.id[d] = id[r];
+    }
+    off += __popc(bal);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_direct_warp(BatchDev B, LevelDev L) {
+  __shared__ int pre_all[8][WARP_DIRECT + 1];
+  const int wid = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t gs = (int64_t)blockIdx.x * 8 + wid; gs < B.nseg; gs += nw) {
+    if (L.seg_d[gs] != L.level) continue;
+    const int n = L.seg_n[gs];
+    if (n > WARP_DIRECT) continue;
+    if (L.hdr->overflow) return;
+    if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid]);
+    else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid]);
+    else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid]);
+    else warp_direct_seg<8>(B, L, gs, n, pre_all[wid]);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Filter path, level l < d_sigma.
 
-__global__ void k_level_prep(StepDev s, LevelDev L) {
-  const int64_t nloc = s.seg_hi - s.seg_lo;
+__global__ void k_level_prep(BatchDev B, LevelDev L) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nloc) return;
+  if (i >= B.nseg) return;
   L.nb[i] = L.seg_d[i] > L.level ? L.in.cnt[i] + 1 : 0;
 }
 
-__global__ void k_check_buckets(StepDev s, LevelDev L) {
-  const int64_t B = L.bucket_base[s.seg_hi - s.seg_lo];
+__global__ void k_check_buckets(BatchDev Bt, LevelDev L) {
+  const int64_t B = L.bucket_base[Bt.nseg];
   L.hdr->bucket_total[L.level] = B;
   if (B > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
   *L.large_n = 0;
@@ -271,121 +470,158 @@ __device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa
   fb = lf == 2 ? 1 : 2;
 }
 
-__global__ void k_work_count(StepDev s, LevelDev L) {
-  const int64_t nbl = (s.seg_hi - s.seg_lo) * s.nblk;
+// Work items of the filter: L.run_item consecutive sampled indices of one run
+// (a multiple of CHUNK, chosen per level so that the grid has enough threads).
+
+__global__ void k_work_count(BatchDev B, LevelDev L) {
   const int64_t beta = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (beta >= nbl) return;
-  const int64_t li = beta / s.nblk, k = beta - li * s.nblk;
+  if (beta >= B.nblk) return;
+  const int j = find_base(B.blk_base, B.nsteps, beta);
+  const StepDev& s = B.steps[j];
+  const int64_t lb = beta - B.blk_base[j];
+  const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
+  const int64_t gs = B.seg_base[j] + li;
   int64_t w = 0;
-  if (L.seg_d[li] > L.level) {
+  if (L.seg_d[gs] > L.level) {
     Blk b = load_blk(s, s.seg_lo + li, k);
     int lf, fa, fb;
     int64_t c[3];
     run_shape(b, L.st, lf, fa, fb, c);
-    w = c[fa] * c[fb] * ((c[lf] + CHUNK - 1) / CHUNK);
+    w = c[fa] * c[fb] * ((c[lf] + L.run_item - 1) / L.run_item);
   }
   L.wcnt[beta] = w;
 }
 
-// K1: product + pre-filter.  Each work item = CHUNK consecutive sampled
-// indices of one run (fixed short-factor indices, long factor sweeping: m
-// strictly ascending, t strictly descending).  A tuple is dropped iff some G
-// point strictly dominates it (m_g <= m, t_g <= t, (m_g,t_g) != (m,t)); a
-// whole chunk is dropped when the G point just below its first m has t <=
-// the chunk's last (smallest) t.
-__global__ void __launch_bounds__(256) k_filter(StepDev s, LevelDev L) {
+// K1: product + pre-filter, output-sensitive run walk.  A work item is a
+// range of one run (short-factor indices fixed, long factor sweeping: m
+// strictly ascending, t strictly descending).  For element x let g be the
+// last G point with m_g <= m_x (pointer advanced by galloping; G is a
+// staircase).  If g strictly dominates x, it also strictly dominates every
+// later element with t >= t_g (their m exceeds m_g), so the walk jumps to
+// the first element with t < t_g (binary search on t).  Otherwise x is a
+// candidate: emitted with bucket = #G points with m <= m_x.
+__global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
+  namespace cg = cooperative_groups;
   if (L.hdr->overflow) return;
-  const int64_t nbl = (s.seg_hi - s.seg_lo) * s.nblk;
+  const int64_t nbl = B.nblk;
   const int64_t W = L.wo[nbl];
-  const int lane = threadIdx.x & 31;
-  const int st = L.st;
+  const int sh = L.st;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < W; base += gstride) {
-    const int64_t w = base + threadIdx.x;
-    bool act = w < W;
-    Blk b;
-    int lf = 0, fa = 1, fb = 2;
-    int64_t c[3] = {0, 0, 0};
-    int64_t ia = 0, ib = 0, j0 = 0, j1 = 0, rel = 0, ms = 0, ts = 0, g = 0, bb = 0, p = 0;
-    const int64_t *Lm = nullptr, *Lt = nullptr, *Gm = nullptr, *Gt = nullptr;
-    if (act) {
-      int64_t lo = 0, hi = nbl;  // largest beta with wo[beta] <= w
-      while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
-        if (L.wo[mid] <= w) lo = mid;
-        else hi = mid;
-      }
-      const int64_t beta = lo, wl = w - L.wo[beta];
-      const int64_t li = beta / s.nblk, k = beta - li * s.nblk;
-      b = load_blk(s, s.seg_lo + li, k);
-      rel = L.blk_rel[beta];
-      run_shape(b, st, lf, fa, fb, c);
-      const int64_t nch = (c[lf] + CHUNK - 1) / CHUNK;
-      const int64_t run = wl / nch, ch = wl - run * nch;
-      const int64_t ja = run / c[fb], jb = run - ja * c[fb];
-      ia = samp_idx(ja, b.n[fa], st);
-      ib = samp_idx(jb, b.n[fb], st);
-      ms = __ldg(fac_m(s, fa) + b.o[fa] + ia) + __ldg(fac_m(s, fb) + b.o[fb] + ib);
-      ts = __ldg(fac_t(s, fa) + b.o[fa] + ia) + __ldg(fac_t(s, fb) + b.o[fb] + ib);
-      Lm = fac_m(s, lf) + b.o[lf];
-      Lt = fac_t(s, lf) + b.o[lf];
-      j0 = ch * CHUNK;
-      j1 = min(j0 + CHUNK, c[lf]);
-      Gm = L.in.m + L.in.start[li];
-      Gt = L.in.t + L.in.start[li];
-      g = L.in.cnt[li];
-      bb = L.bucket_base[li];
-      const int64_t mf = ms + __ldg(Lm + samp_idx(j0, b.n[lf], st));
-      const int64_t tl = ts + __ldg(Lt + samp_idx(j1 - 1, b.n[lf], st));
-      int64_t q0 = 0, q1 = g;  // q = #G with m < mf
-      while (q0 < q1) {
-        int64_t mid = (q0 + q1) >> 1;
-        if (Gm[mid] < mf) q0 = mid + 1;
-        else q1 = mid;
-      }
-      if (q0 > 0 && Gt[q0 - 1] <= tl) act = false;  // whole chunk strictly dominated
-      p = q0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gstride) {
+    int64_t lo = 0, hi = nbl;  // block: largest beta with wo[beta] <= w
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (L.wo[mid] <= w) lo = mid;
+      else hi = mid;
     }
-    for (int e = 0; e < CHUNK; ++e) {
-      const int64_t j = j0 + e;
-      bool cand = false;
-      int64_t m = 0, t = 0, gb = 0;
-      uint64_t id = 0;
-      if (act && j < j1) {
-        const int64_t il = samp_idx(j, b.n[lf], st);
-        m = ms + __ldg(Lm + il);
-        t = ts + __ldg(Lt + il);
+    const int64_t beta = lo, wl = w - L.wo[beta];
+    const int jstep = find_base(B.blk_base, B.nsteps, beta);
+    const StepDev& s = B.steps[jstep];
+    const int64_t lb = beta - B.blk_base[jstep];
+    const int64_t li0 = lb / s.nblk, k = lb - li0 * s.nblk;
+    const int64_t li = B.seg_base[jstep] + li0;  // local segment (pools, buckets)
+    const Blk b = load_blk(s, s.seg_lo + li0, k);
+    const int64_t rel = L.blk_rel[beta];
+    int lf, fa, fb;
+    int64_t c[3];
+    run_shape(b, sh, lf, fa, fb, c);
+    // factor pointers without dynamic register-array indexing
+    const int64_t* const fm[3] = {s.X.m, s.Y.m, s.Z.m};
+    const int64_t* const ft[3] = {s.X.t, s.Y.t, s.Z.t};
+    const int64_t oL = lf == 0 ? b.o[0] : (lf == 1 ? b.o[1] : b.o[2]);
+    const int64_t nL = lf == 0 ? b.n[0] : (lf == 1 ? b.n[1] : b.n[2]);
+    const int64_t oA = fa == 0 ? b.o[0] : b.o[1];
+    const int64_t nA = fa == 0 ? b.n[0] : b.n[1];
+    const int64_t oB = fb == 2 ? b.o[2] : b.o[1];
+    const int64_t nB = fb == 2 ? b.n[2] : b.n[1];
+    const int64_t cL = lf == 0 ? c[0] : (lf == 1 ? c[1] : c[2]);
+    const int64_t cB = fb == 2 ? c[2] : c[1];
+    const int64_t RI = L.run_item;
+    const int64_t nch = (cL + RI - 1) / RI;
+    const int64_t run = wl / nch, ch = wl - run * nch;
+    const int64_t ja = run / cB, jb = run - ja * cB;
+    const int64_t ia = samp_idx(ja, nA, sh), ib = samp_idx(jb, nB, sh);
+    const int64_t* Am = fa == 0 ? fm[0] : fm[1];
+    const int64_t* At = fa == 0 ? ft[0] : ft[1];
+    const int64_t* Bm = fb == 2 ? fm[2] : fm[1];
+    const int64_t* Bt = fb == 2 ? ft[2] : ft[1];
+    const int64_t* Lm = (lf == 0 ? fm[0] : (lf == 1 ? fm[1] : fm[2])) + oL;
+    const int64_t* Lt = (lf == 0 ? ft[0] : (lf == 1 ? ft[1] : ft[2])) + oL;
+    const int64_t ms = __ldg(Am + oA + ia) + __ldg(Bm + oB + ib);
+    const int64_t ts = __ldg(At + oA + ia) + __ldg(Bt + oB + ib);
+    // (x, y, z) index of the tuple for the id (R6): the long factor varies
+    const int64_t ny = b.n[1], nz = b.n[2];
+    const int64_t j0 = ch * RI, j1 = min(j0 + RI, cL);
+    const int64_t* Gm = L.in.m + L.in.start[li];
+    const int64_t* Gt = L.in.t + L.in.start[li];
+    const int64_t g = L.in.cnt[li];
+    const int64_t bb = L.bucket_base[li];
+    // q: #G points with m < m of the current chunk start (galloping lower bound)
+    int64_t q = 0;
+    int64_t jj = j0;
+    while (jj < j1) {
+      const int64_t je = min(jj + CHUNK, j1);
+      const int64_t mf = ms + __ldg(Lm + samp_idx(jj, nL, sh));
+      const int64_t tl = ts + __ldg(Lt + samp_idx(je - 1, nL, sh));
+      if (q < g && Gm[q] < mf) {  // gallop + binary search to lower_bound(mf)
+        int64_t step = 1;
+        while (q + step < g && Gm[q + step] < mf) step <<= 1;
+        int64_t a0 = q + (step >> 1) + 1, a1 = min(q + step, g);
+        while (a0 < a1) {
+          const int64_t mid = (a0 + a1) >> 1;
+          if (Gm[mid] < mf) a0 = mid + 1;
+          else a1 = mid;
+        }
+        q = a0;
+      }
+      if (q > 0 && Gt[q - 1] <= tl) {
+        // G[q-1] (m < mf) strictly dominates the whole chunk and every later
+        // element with t >= its t: gallop along the run to the first t below it.
+        const int64_t tg = Gt[q - 1];
+        int64_t step = 1, last = je - 1;  // t(last) >= tg
+        while (last + step < j1 && ts + __ldg(Lt + samp_idx(last + step, nL, sh)) >= tg) {
+          last += step;
+          step <<= 1;
+        }
+        int64_t a0 = last + 1, a1 = min(last + step, j1);  // first index with t < tg in [a0, a1]
+        while (a0 < a1) {
+          const int64_t mid = (a0 + a1) >> 1;
+          if (ts + __ldg(Lt + samp_idx(mid, nL, sh)) >= tg) a0 = mid + 1;
+          else a1 = mid;
+        }
+        jj = a0;
+        continue;
+      }
+      // element-level test of the chunk: p = #G points with m <= m_x
+      int64_t p = q;
+      for (int64_t j = jj; j < je; ++j) {
+        const int64_t il = samp_idx(j, nL, sh);
+        const int64_t m = ms + __ldg(Lm + il);
+        const int64_t t = ts + __ldg(Lt + il);
         while (p < g && Gm[p] <= m) ++p;
-        const bool dom = p > 0 && (Gt[p - 1] < t || (Gt[p - 1] == t && Gm[p - 1] < m));
-        if (!dom) {
-          cand = true;
-          int64_t idx3[3];
-          idx3[lf] = il;
-          idx3[fa] = ia;
-          idx3[fb] = ib;
-          id = (uint64_t)(rel + (idx3[0] * b.n[1] + idx3[1]) * b.n[2] + idx3[2]);
-          gb = bb + p;
+        if (p > 0 && (Gt[p - 1] < t || (Gt[p - 1] == t && Gm[p - 1] < m))) continue;
+        int64_t x, y, z;
+        if (lf == 0) { x = il; y = ia; z = ib; }
+        else if (lf == 1) { x = ia; y = il; z = ib; }
+        else { x = ia; y = ib; z = il; }
+        const uint64_t id = (uint64_t)(rel + (x * ny + y) * nz + z);
+        const int64_t gb = bb + p;
+        cg::coalesced_group grp = cg::coalesced_threads();
+        unsigned long long base = 0;
+        if (grp.thread_rank() == 0) base = atomicAdd(L.cand_cursor, (unsigned long long)grp.size());
+        base = grp.shfl(base, 0);
+        const unsigned long long idx = base + grp.thread_rank();
+        if ((int64_t)idx < L.cand_cap) {
+          const unsigned pos = atomicAdd(L.bcount + gb, 1u);
+          atomicMin(L.bmin + gb, (long long)t);
+          L.cm[idx] = m;
+          L.ct[idx] = t;
+          L.cid[idx] = id;
+          L.cgb[idx] = gb;
+          L.cpos[idx] = pos;
         }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, cand);
-      if (bal) {
-        const int leader = __ffs(bal) - 1;
-        unsigned long long bpos = 0;
-        if (lane == leader) bpos = atomicAdd(L.cand_cursor, (unsigned long long)__popc(bal));
-        bpos = __shfl_sync(0xffffffffu, bpos, leader);
-        if (cand) {
-          const unsigned long long idx = bpos + __popc(bal & ((1u << lane) - 1u));
-          if ((int64_t)idx < L.cand_cap) {
-            const unsigned pos = atomicAdd(L.bcount + gb, 1u);
-            atomicMin(L.bmin + gb, (long long)t);
-            L.cm[idx] = m;
-            L.ct[idx] = t;
-            L.cid[idx] = id;
-            L.cgb[idx] = gb;
-            L.cpos[idx] = pos;
-          }
-        }
-      }
+      jj = je;
     }
   }
 }
@@ -398,11 +634,11 @@ __global__ void k_check_cand(LevelDev L) {
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
 // (the running minimum v of Alg.1 entering each bucket).
-__global__ void __launch_bounds__(256) k_carry(StepDev s, LevelDev L) {
+__global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L) {
   __shared__ long long sh[33];
   __shared__ long long chunk_min;
   if (L.hdr->overflow) return;
-  const int64_t nloc = s.seg_hi - s.seg_lo;
+  const int64_t nloc = B.nseg;
   for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
     if (L.seg_d[li] <= L.level) continue;
     const int64_t b0 = L.bucket_base[li], nb = L.nb[li];
@@ -437,57 +673,64 @@ __global__ void k_clamp_cand(LevelDev L, int64_t* ncand) {
   *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
 }
 
-// K2+K3 for buckets of <= 32 candidates: one warp per bucket, rank sort by
-// shuffles, Alg.1 sweep with the bucket's carry.
-__global__ void __launch_bounds__(256) k_bucket_small(StepDev s, LevelDev L) {
-  __shared__ int64_t wm[8][32];
-  __shared__ int64_t wt[8][32];
-  __shared__ uint64_t wi[8][32];
+// K2+K3 for buckets of <= WARP_DIRECT candidates: one warp per bucket,
+// register bitonic sort by shuffles (R rows of 32), Alg.1 sweep with the
+// bucket's carry.  Larger buckets go to the CTA kernels.
+template <int R>
+__device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int64_t c, int64_t base) {
+  const int lane = threadIdx.x & 31;
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
+    if (e < c) {
+      m[r] = L.gm[base + e];
+      t[r] = L.gt[base + e];
+      id[r] = L.gid[base + e];
+    } else {
+      m[r] = INF;
+      t[r] = INF;
+      id[r] = ~0ull;
+    }
+  }
+  warp_bitonic<R>(m, t, id);
+  long long carry = L.bcarry[bkt];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
+    const long long inc = warp_incl_min(t[r]);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    if (e < c) {
+      L.gm[base + e] = m[r];
+      L.gt[base + e] = t[r];
+      L.gid[base + e] = id[r];
+      L.gflag[base + e] = t[r] < v ? 1 : 0;
+    }
+    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
+    carry = rowmin < carry ? rowmin : carry;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_small(BatchDev Bt, LevelDev L) {
   if (L.hdr->overflow) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t B = min(L.bucket_base[s.seg_hi - s.seg_lo], L.bcap);
+  const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t bkt = (int64_t)blockIdx.x * 8 + wid; bkt < B; bkt += nw) {
     const int64_t c = L.bcount[bkt];
     if (c == 0) continue;
-    if (c > 32) {
+    if (c > WARP_DIRECT) {
       if (lane == 0) L.large_list[atomicAdd(L.large_n, 1ull)] = bkt;
       continue;
     }
     const int64_t base = L.boff[bkt];
-    int64_t m = INF, t = INF;
-    uint64_t id = ~0ull;
-    if (lane < c) {
-      m = L.gm[base + lane];
-      t = L.gt[base + lane];
-      id = L.gid[base + lane];
-    }
-    int rank = 0;
-    for (int j = 0; j < 32; ++j) {
-      int64_t mj = __shfl_sync(0xffffffffu, m, j);
-      int64_t tj = __shfl_sync(0xffffffffu, t, j);
-      uint64_t ij = __shfl_sync(0xffffffffu, id, j);
-      rank += key_lt(mj, tj, ij, m, t, id) ? 1 : 0;
-    }
-    wm[wid][rank] = m;
-    wt[wid][rank] = t;
-    wi[wid][rank] = id;
-    __syncwarp();
-    m = wm[wid][lane];
-    t = wt[wid][lane];
-    id = wi[wid][lane];
-    __syncwarp();
-    long long inc = warp_incl_min(t);
-    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) ex = INF;
-    const long long carry = L.bcarry[bkt];
-    const long long v = ex < carry ? ex : carry;
-    if (lane < c) {
-      L.gm[base + lane] = m;
-      L.gt[base + lane] = t;
-      L.gid[base + lane] = id;
-      L.gflag[base + lane] = t < v ? 1 : 0;
-    }
+    if (c <= 32) warp_bucket<1>(L, bkt, c, base);
+    else if (c <= 64) warp_bucket<2>(L, bkt, c, base);
+    else if (c <= 128) warp_bucket<4>(L, bkt, c, base);
+    else warp_bucket<8>(L, bkt, c, base);
   }
 }
 
@@ -650,8 +893,8 @@ __global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand)
   }
 }
 
-__global__ void k_seg_out(StepDev s, LevelDev L, const int64_t* gpos) {
-  const int64_t nloc = s.seg_hi - s.seg_lo;
+__global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos) {
+  const int64_t nloc = B.nseg;
   const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (li >= nloc || L.seg_d[li] <= L.level) return;
   const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
@@ -660,16 +903,17 @@ __global__ void k_seg_out(StepDev s, LevelDev L, const int64_t* gpos) {
   L.out.cnt[li] = gpos[hi] - gpos[lo];
 }
 
-// Final gather of the level-0 pool into the step's CSR output set.
-__global__ void k_gather(StepDev s, Pool P, const int64_t* dst_off, int64_t* om, int64_t* ot,
-                         uint64_t* obp) {
-  const int64_t nloc = s.seg_hi - s.seg_lo;
-  for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
-    const int64_t src = P.start[li], n = P.cnt[li], d = dst_off[li];
+// Final gather of the level-0 pool into every step's CSR output set.
+__global__ void k_gather(BatchDev B, Pool P) {
+  for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
+    const int j = find_base(B.seg_base, B.nsteps, gs);
+    const StepDev& s = B.steps[j];
+    const int64_t li = gs - B.seg_base[j];
+    const int64_t src = P.start[gs], n = P.cnt[gs], d = s.out_off[li];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      om[d + i] = P.m[src + i];
-      ot[d + i] = P.t[src + i];
-      obp[d + i] = P.id[src + i];
+      s.out_m[d + i] = P.m[src + i];
+      s.out_t[d + i] = P.t[src + i];
+      s.out_bp[d + i] = P.id[src + i];
     }
   }
 }
@@ -703,11 +947,11 @@ StepRunner::StepRunner() {}
 StepRunner::~StepRunner() { release(); }
 
 void StepRunner::release() {
-  Buf* all[] = {&seg_d, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
+  Buf* all[] = {&seg_d, &seg_n, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
                 &cgb, &cpos, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
-                &dst_off};
+                &dst_off, &steps_dev, &base_dev};
   for (Buf* b : all) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;
@@ -735,8 +979,7 @@ static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
   return (int)g;
 }
 
-cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res) {
-  StepDev s = s0;
+cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res) {
   int64_t nl = 0;  // kernel launches
   int pgroup[64];
   npev = 0;
@@ -747,9 +990,16 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
     pgroup[npev] = group;
     ++npev;
   };
-  s.slog = slog;
-  const int64_t nloc = s.seg_hi - s.seg_lo;
-  const int64_t nbl = nloc * s.nblk;
+  // batch layout: local segments / blocks numbered consecutively over steps
+  const int nsteps = (int)steps.size();
+  h_base.assign(2 * (nsteps + 1), 0);
+  for (int j = 0; j < nsteps; ++j) {
+    const int64_t ns = steps[j].seg_hi - steps[j].seg_lo;
+    h_base[j + 1] = h_base[j] + ns;
+    h_base[nsteps + 1 + j + 1] = h_base[nsteps + 1 + j] + ns * steps[j].nblk;
+  }
+  const int64_t nloc = h_base[nsteps];
+  const int64_t nbl = h_base[2 * nsteps + 1];
   cudaError_t e;
   if (!ev0) {
     if ((e = cudaEventCreate(&ev0)) != cudaSuccess) return e;
@@ -768,7 +1018,23 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
     res->kernel_ms = 0;
     return cudaSuccess;
   }
+  GROW(steps_dev, StepDev, nsteps);
+  GROW(base_dev, int64_t, 2 * (nsteps + 1));
+  cudaMemcpyAsync(steps_dev.p, steps.data(), sizeof(StepDev) * nsteps, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(base_dev.p, h_base.data(), sizeof(int64_t) * 2 * (nsteps + 1),
+                  cudaMemcpyHostToDevice, st);
+  BatchDev s;
+  s.steps = (const StepDev*)steps_dev.p;
+  s.seg_base = (const int64_t*)base_dev.p;
+  s.blk_base = (const int64_t*)base_dev.p + nsteps + 1;
+  s.nsteps = nsteps;
+  s.slog = slog;
+  s.cdirect = cdirect;
+  s.nseg = nloc;
+  s.nblk = nbl;
+  batch = s;
   GROW(seg_d, int32_t, nloc);
+  GROW(seg_n, int32_t, nloc);
   GROW(blk_rel, int64_t, nbl);
   GROW(seg_tuples, int64_t, nloc);
   GROW(hdr, StepHdr, 1);
@@ -777,7 +1043,7 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
   mark(0);
   cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
   ++nl;
-  k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
+  k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                             (int64_t*)blk_rel.p,
                                                             (int64_t*)seg_tuples.p, H);
   cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
@@ -840,7 +1106,7 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {
       cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
-      k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p,
+      k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                                 (int64_t*)blk_rel.p,
                                                                 (int64_t*)seg_tuples.p, H);
     }
@@ -854,14 +1120,22 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
       std::memset(&L, 0, sizeof(L));
       L.level = l;
       L.st = slog * l;
+      {  // ~2 work items per resident thread (148 SMs x 2048 threads) at this level
+        const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
+        int64_t ri = tot / (int64_t)(148 * 2048 * 2);
+        ri = std::max<int64_t>(CHUNK, std::min<int64_t>(512, ri));
+        L.run_item = (int)((ri + CHUNK - 1) / CHUNK * CHUNK);
+      }
       L.seg_d = (const int32_t*)seg_d.p;
+      L.seg_n = (const int32_t*)seg_n.p;
       L.blk_rel = (const int64_t*)blk_rel.p;
       L.in = pools[(l + 1) & 1];
       L.out = pools[l & 1];
       L.hdr = H;
       cudaMemsetAsync(L.out.cursor, 0, sizeof(unsigned long long), st);
       mark(1);
-      ++nl;
+      nl += 2;
+      k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, 0, st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
@@ -931,11 +1205,12 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
     // read back header + level-0 per-segment counts
     if (cnt_host_n < nloc) {
       if (cnt_host) cudaFreeHost(cnt_host);
-      if ((e = cudaMallocHost((void**)&cnt_host, sizeof(int64_t) * nloc)) != cudaSuccess) return e;
+      if ((e = cudaMallocHost((void**)&cnt_host, sizeof(int64_t) * 2 * nloc)) != cudaSuccess) return e;
       cnt_host_n = nloc;
     }
     cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(cnt_host, pools[0].cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(cnt_host + nloc, seg_tuples.p, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (!hdr_host->overflow) {
@@ -944,6 +1219,7 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
       for (int l = 0; l < D; ++l) res->candidates += (int64_t)hdr_host->cand_total[l];
       res->huge = (int64_t)hdr_host->huge;
       res->counts = cnt_host;
+      res->seg_tuples = cnt_host + nloc;
       int64_t tot = 0;
       for (int64_t i = 0; i < nloc; ++i) tot += cnt_host[i];
       res->total = tot;
@@ -977,18 +1253,19 @@ cudaError_t StepRunner::run(const StepDev& s0, cudaStream_t st, StepResult* res)
   }
 }
 
-cudaError_t StepRunner::gather(const StepDev& s, const StepResult& r, const int64_t* dst_off_host,
-                               int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st) {
-  const int64_t nloc = r.nloc;
-  if (nloc == 0) return cudaSuccess;
-  GROW(dst_off, int64_t, nloc);
-  cudaMemcpyAsync(dst_off.p, dst_off_host, sizeof(int64_t) * nloc, cudaMemcpyHostToDevice, st);
-  k_gather<<<grid_for(nloc, 1, 148 * 8), 128, 0, st>>>(s, r.pool, (const int64_t*)dst_off.p, om, ot,
-                                                      obp);
+cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResult& r,
+                               cudaStream_t st) {
+  if (r.nloc == 0) return cudaSuccess;
+  // the output pointers changed: refresh the step array (same batch layout)
+  cudaMemcpyAsync(steps_dev.p, steps.data(), sizeof(StepDev) * steps.size(), cudaMemcpyHostToDevice,
+                  st);
+  k_gather<<<grid_for(r.nloc, 1, 148 * 8), 128, 0, st>>>(batch, r.pool);
   return cudaGetLastError();
 }
 
 cudaError_t StepRunner::configure() {
+  if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
+  if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(64, std::min(C_DIRECT, atoi(e)));
   const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
   cudaError_t e = cudaFuncSetAttribute(k_bucket_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)lsm);

@@ -1,6 +1,7 @@
 // ft_step.h -- host interface of the per-step GPU pipeline (internal).
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "ft_kernels.cuh"
@@ -19,6 +20,7 @@ struct StepResult {
   float kernel_ms = 0;
   float plan_ms = 0, direct_ms = 0, filter_ms = 0, bucket_ms = 0, compact_ms = 0, host_ms = 0;
   const int64_t* counts = nullptr;  // host (pinned) per-segment survivor counts [nloc]
+  const int64_t* seg_tuples = nullptr;  // host (pinned) per-segment product tuples [nloc]
   Pool pool;                        // level-0 pool (device)
 };
 
@@ -32,15 +34,16 @@ class StepRunner {
   StepRunner();
   ~StepRunner();
   cudaError_t configure();
-  // Runs the step for segments [s.seg_lo, s.seg_hi); on success res->counts
-  // and res->pool describe the per-segment results (valid until the next run).
-  cudaError_t run(const StepDev& s, cudaStream_t st, StepResult* res);
-  // Gathers the level-0 pool into CSR arrays (dst_off_host[nloc]: offsets).
-  cudaError_t gather(const StepDev& s, const StepResult& r, const int64_t* dst_off_host,
-                     int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st);
+  // Runs a batch of independent steps, each for its segments [seg_lo,
+  // seg_hi); on success res->counts (local segments, in batch order) and
+  // res->pool describe the results (valid until the next run).
+  cudaError_t run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res);
+  // Gathers the level-0 pool into each step's CSR output (steps[j].out_*).
+  cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
 
   int slog = 3;                       // sample stride 8
+  int cdirect = C_DIRECT;             // direct-path capacity
   bool profile = false;               // events between kernel groups
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
   int64_t out_budget = 1 << 20;
@@ -51,11 +54,14 @@ class StepRunner {
     void* p = nullptr;
     size_t bytes = 0;
   };
-  Buf seg_d, blk_rel, seg_tuples, hdr;
+  Buf seg_d, seg_n, blk_rel, seg_tuples, hdr;
   Buf poolA_m, poolA_t, poolA_id, poolA_start, poolA_cnt;
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
   Buf cm, ct, cid, cgb, cpos, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
+  Buf steps_dev, base_dev;
+  std::vector<int64_t> h_base;
+  BatchDev batch{};
   StepHdr* hdr_host = nullptr;
   int64_t* cnt_host = nullptr;
   int64_t cnt_host_n = 0;

@@ -83,3 +83,22 @@ def test_c4_bert_2layers(ft):
 
 def test_c5_small(ft):
     compare(ft, G.c5(n_ops=200, K=16, B=8, Lmin=2, Lmax=6), strategies=32)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_invariance_loopback(ft, world):
+    """Multi-rank sharding (virtual ranks on one GPU): every step output and the
+    strategies are bit-identical to world = 1 (ids are shard-invariant, R6)."""
+    for w in (G.c3(), G.c4(layers=2), G.c5(n_ops=200, K=16, B=8, Lmin=2, Lmax=6)):
+        a = ft.load(w, keep_all=True)
+        a.eliminate()
+        am, at = a.frontier()
+        b = ft.load(w, keep_all=True, world=world, loopback=True)
+        b.eliminate()
+        bm, bt = b.frontier()
+        assert np.array_equal(am, bm) and np.array_equal(at, bt)
+        for s in range(len(a.stats())):
+            for x, y in zip(a.step_output(s), b.step_output(s)):
+                assert np.array_equal(x, y), (w.name, s)
+        for i in np.linspace(0, len(am) - 1, 16).astype(int):
+            assert np.array_equal(a.strategy(int(i)), b.strategy(int(i)))

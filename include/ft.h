@@ -85,7 +85,7 @@ typedef struct {
   int32_t pad;
   int64_t nseg;          /* output segments (configuration pairs / configs) */
   int64_t nblk;          /* blocks (union terms) per segment */
-  int64_t tuples;        /* product tuples sum |X||Y||Z| (the M1 numerator) */
+  int64_t tuples;        /* product tuples sum |X||Y||Z| over ALL ranks (the M1 numerator) */
   int64_t survivors;     /* frontier tuples written */
   int64_t candidates;    /* tuples that passed the dominance pre-filter (all levels);
                             wave-level numbers (candidates, launches, *_ms) are
@@ -93,6 +93,8 @@ typedef struct {
   int64_t retries;       /* capacity retries */
   int64_t launches;      /* kernels launched by this step on this rank */
   int64_t max_seg;       /* largest output segment (frontier) of the step */
+  int64_t filter_tuples; /* wave: sampled tuples streamed by the pre-filter kernel (this rank) */
+  int64_t direct_tuples; /* wave: sampled tuples sorted by the direct kernels (this rank) */
   float kernel_ms;       /* CUDA-event time of the step's kernels on this rank */
   float comm_ms;         /* all-gather time (world > 1) */
   float plan_ms, direct_ms, filter_ms, bucket_ms, compact_ms; /* opt.profile only */

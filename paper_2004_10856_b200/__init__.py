@@ -47,7 +47,8 @@ class ft_step_stats(C.Structure):
                 ("pad", C.c_int32), ("nseg", C.c_int64),
                 ("nblk", C.c_int64), ("tuples", C.c_int64), ("survivors", C.c_int64),
                 ("candidates", C.c_int64), ("retries", C.c_int64), ("launches", C.c_int64),
-                ("max_seg", C.c_int64), ("kernel_ms", C.c_float), ("comm_ms", C.c_float), ("plan_ms", C.c_float),
+                ("max_seg", C.c_int64), ("filter_tuples", C.c_int64), ("direct_tuples", C.c_int64),
+                ("kernel_ms", C.c_float), ("comm_ms", C.c_float), ("plan_ms", C.c_float),
                 ("direct_ms", C.c_float), ("filter_ms", C.c_float), ("bucket_ms", C.c_float),
                 ("compact_ms", C.c_float), ("host_ms", C.c_float)]
 
@@ -195,7 +196,8 @@ class Graph:
                         "launches": s.launches, "kernel_ms": s.kernel_ms, "comm_ms": s.comm_ms,
                         "plan_ms": s.plan_ms, "direct_ms": s.direct_ms, "filter_ms": s.filter_ms,
                         "bucket_ms": s.bucket_ms, "compact_ms": s.compact_ms,
-                        "host_ms": s.host_ms, "max_seg": s.max_seg})
+                        "host_ms": s.host_ms, "max_seg": s.max_seg,
+                        "filter_tuples": s.filter_tuples, "direct_tuples": s.direct_tuples})
         return out
 
     def step_output(self, step: int, with_mt: bool = True):

@@ -5,7 +5,9 @@
 // (Eq.5) and exact K=1 heuristic (Eq.7) eliminations, then LDP (Alg.3) and
 // unroll.  Every step's Product/Union/Reduce runs in ft_step.cu.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -29,7 +31,8 @@ struct FSet {
   int step = -1;
   int a_op = -1, b_op = -1;  // segment -> config mapping for unroll
   int64_t nseg = 0;
-  std::vector<int64_t> off;  // host copy of seg_off (filled when the step has run)
+  std::vector<int64_t> off;  // host copy of seg_off (lazy for single-rank step outputs)
+  bool off_ok = true;
   int64_t* d_off = nullptr;
   int64_t* d_m = nullptr;
   int64_t* d_t = nullptr;
@@ -108,7 +111,16 @@ struct ft_graph {
   std::vector<int64_t> h_pin_off;
   int64_t* h_pinned = nullptr;
   int64_t h_pinned_n = 0;
+  // host-side wall time by phase (FT_HOST_PROF=1 prints at destroy)
+  double hp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t nwaves = 0;
 };
+
+namespace {
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
 
 namespace ftk {
 static std::mutex g_reg_mu;
@@ -339,10 +351,24 @@ int nccl_fail(ft_graph* g, ncclResult_t nr) {
   return FT_ECUDA;
 }
 
+// Host copy of a set's seg_off (single-rank step outputs keep it on the device
+// until needed).
+int ensure_off(ft_graph* g, int set) {
+  FSet& S = g->sets[set];
+  if (S.off_ok) return FT_OK;
+  S.off.resize(S.nseg + 1);
+  CU(cudaMemcpy(S.off.data(), S.d_off, sizeof(int64_t) * (S.nseg + 1), cudaMemcpyDeviceToHost),
+     "seg_off d2h");
+  S.off_ok = true;
+  return FT_OK;
+}
+
 // Executes one wave of mutually independent steps as a single batch
 // (DESIGN.md 6): shard the wave's segments over ranks, run the pipeline,
 // all-gather counts and survivors, gather into the wave arena.
 int exec_wave(ft_graph* g, const std::vector<int>& ids) {
+  const double h0 = now_ms();
+  g->nwaves++;
   const int ns = (int)ids.size();
   // global segment numbering of the wave (step-major)
   std::vector<int64_t> sbase(ns + 1, 0);
@@ -403,23 +429,40 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   else
     vr.push_back(g->rank);
   ftk::StepResult res, agg;
+  const double h1 = now_ms();
   std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
   g->runner->profile = g->profile;
-  std::vector<int64_t> cnt(NS, 0), tup(NS, 0);
+  // single rank: offsets are computed on the device straight into the arena
+  const bool devoff = g->world == 1;
+  WaveBuf wb;
+  if (devoff)
+    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+  std::vector<int64_t> cnt(devoff ? 0 : NS, 0), tup(devoff ? 0 : NS, 0);
+  std::vector<int64_t> stot(ns, 0), smax(ns, 0), stup(ns, 0);
   std::vector<ftk::StepDev> sd;
   for (size_t v = 0; v < vr.size(); ++v) {
     const int64_t a = lo[vr[v]], b = lo[vr[v] + 1];
     sd = make_sd(a, b);
-    cudaError_t ce = g->runner->run(sd, g->stream, &res);
+    cudaError_t ce = g->runner->run(sd, g->stream, &res, devoff ? wb.off : nullptr);
     if (ce == cudaErrorInvalidConfiguration)
       return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
     if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
-    for (int64_t i = 0; i < res.nloc; ++i) {  // per-segment survivor counts
-      cnt[a + i] = res.counts[i];
-      tup[a + i] = res.seg_tuples[i];
+    if (devoff) {
+      for (int q = 0; q < ns; ++q) {
+        stot[q] = res.step_stats[3 * q];
+        smax[q] = res.step_stats[3 * q + 1];
+        stup[q] = res.step_stats[3 * q + 2];
+      }
+    } else {
+      for (int64_t i = 0; i < res.nloc; ++i) {  // per-segment survivor counts
+        cnt[a + i] = res.counts[i];
+        tup[a + i] = res.seg_tuples[i];
+      }
     }
     agg.levels = std::max(agg.levels, res.levels);
     agg.candidates += res.candidates;
+    agg.filter_tuples += res.filter_tuples;
+    agg.direct_tuples += res.direct_tuples;
     agg.kernel_ms += res.kernel_ms;
     agg.launches += res.launches;
     agg.retries += res.retries;
@@ -431,6 +474,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     agg.host_ms += res.host_ms;
   }
   float comm_ms = 0;
+  const double h2 = now_ms();
   cudaEvent_t ca = nullptr, cb = nullptr;
   if (g->world > 1 && !g->loopback) {
     cudaEventCreate(&ca);
@@ -460,23 +504,33 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     }
   }
   // wave arena: step-major CSR
-  std::vector<int64_t> hoff(NS + ns, 0);  // per step: nseg+1 offsets (relative to the step)
-  std::vector<int64_t> sbeg(ns + 1, 0);   // survivor start of each step in the arena
+  std::vector<int64_t> hoff(devoff ? 0 : NS + ns, 0);  // per step: nseg+1 offsets (relative)
+  std::vector<int64_t> sbeg(ns + 1, 0);                // survivor start of each step in the arena
   for (int q = 0; q < ns; ++q) {
+    if (devoff) {
+      sbeg[q + 1] = sbeg[q] + stot[q];
+      continue;
+    }
     int64_t* o = hoff.data() + sbase[q] + q;
     o[0] = 0;
     for (int64_t i = 0; i < g->steps[ids[q]].nseg; ++i) o[i + 1] = o[i] + cnt[sbase[q] + i];
     sbeg[q + 1] = sbeg[q] + o[g->steps[ids[q]].nseg];
+    stot[q] = o[g->steps[ids[q]].nseg];
+    for (int64_t i = 0; i < g->steps[ids[q]].nseg; ++i) {
+      stup[q] += tup[sbase[q] + i];
+      smax[q] = std::max<int64_t>(smax[q], cnt[sbase[q] + i]);
+    }
   }
   const int64_t total = sbeg[ns];
-  WaveBuf wb;
   const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
   CU(cudaMallocAsync((void**)&wb.m, nb, g->stream), "alloc frontier");
   CU(cudaMallocAsync((void**)&wb.t, nb, g->stream), "alloc frontier");
   CU(cudaMallocAsync((void**)&wb.bp, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
-  CU(cudaMemcpyAsync(wb.off, hoff.data(), sizeof(int64_t) * (NS + ns), cudaMemcpyHostToDevice,
-                     g->stream), "upload seg_off");
+  if (!devoff) {
+    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+    CU(cudaMemcpyAsync(wb.off, hoff.data(), sizeof(int64_t) * (NS + ns), cudaMemcpyHostToDevice,
+                       g->stream), "upload seg_off");
+  }
   auto set_out = [&](std::vector<ftk::StepDev>& v) {
     for (int q = 0; q < ns; ++q) {
       ftk::StepDev& d = v[q];
@@ -487,6 +541,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     }
   };
   set_out(sd);
+  const double h3 = now_ms();
   CU(g->runner->gather(sd, res, g->stream), "gather");  // last (or only) rank's pool
   for (size_t v = 0; v + 1 < vr.size(); ++v) {           // loopback: re-run the others
     std::vector<ftk::StepDev> sv = make_sd(lo[vr[v]], lo[vr[v] + 1]);
@@ -515,6 +570,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     cudaEventRecord(cb, g->stream);
   }
   CU(cudaStreamSynchronize(g->stream), "wave sync");
+  const double h4 = now_ms();
   if (g->world > 1 && !g->loopback) {
     cudaEventElapsedTime(&comm_ms, ca, cb);
     cudaEventDestroy(ca);
@@ -527,7 +583,12 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   for (int q = 0; q < ns; ++q) {
     StepRec& r = g->steps[ids[q]];
     FSet& o = g->sets[r.out];
-    o.off.assign(hoff.begin() + sbase[q] + q, hoff.begin() + sbase[q] + q + r.nseg + 1);
+    if (devoff) {
+      o.off_ok = false;  // fetched lazily (unroll, ft_step_output)
+    } else {
+      o.off.assign(hoff.begin() + sbase[q] + q, hoff.begin() + sbase[q] + q + r.nseg + 1);
+      o.off_ok = true;
+    }
     o.d_off = wb.off + sbase[q] + q;
     o.d_m = wb.m + sbeg[q];
     o.d_t = wb.t + sbeg[q];
@@ -540,16 +601,14 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     st.wave = wi;
     st.nseg = r.nseg;
     st.nblk = r.nblk;
-    st.tuples = 0;
-    st.max_seg = 0;
-    for (int64_t i = 0; i < r.nseg; ++i) {
-      st.tuples += tup[sbase[q] + i];
-      st.max_seg = std::max<int64_t>(st.max_seg, cnt[sbase[q] + i]);
-    }
-    st.survivors = o.off[r.nseg];
+    st.tuples = stup[q];
+    st.max_seg = smax[q];
+    st.survivors = stot[q];
     st.retries = agg.retries;
     if (q == 0) {  // wave-level numbers are booked on the wave's first step
       st.candidates = agg.candidates;
+      st.filter_tuples = agg.filter_tuples;
+      st.direct_tuples = agg.direct_tuples;
       st.kernel_ms = agg.kernel_ms;
       st.comm_ms = comm_ms;
       st.launches = agg.launches + (int64_t)vr.size();
@@ -567,6 +626,12 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     consume(g, r.Y);
     consume(g, r.Z);
   }
+  const double h5 = now_ms();
+  g->hp[0] += h1 - h0;  // shard plan + descriptors
+  g->hp[1] += h2 - h1;  // pipeline (2 syncs inside)
+  g->hp[2] += h3 - h2;  // counts -> arena offsets, alloc, upload
+  g->hp[3] += h4 - h3;  // gather + sync
+  g->hp[4] += h5 - h4;  // bookkeeping
   return FT_OK;
 }
 
@@ -575,6 +640,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
 // depend on the grouping (each step is a function of its inputs only).
 int flush(ft_graph* g) {
   if (g->pending.empty()) return FT_OK;
+  const double f0 = now_ms();
   std::vector<int> wave(g->steps.size(), 0);
   int maxw = 0;
   for (int id : g->pending) {
@@ -590,6 +656,7 @@ int flush(ft_graph* g) {
   std::vector<std::vector<int>> groups(maxw + 1);
   for (int id : g->pending) groups[wave[id]].push_back(id);
   g->pending.clear();
+  g->hp[5] += now_ms() - f0;  // wave assignment
   for (int w = 1; w <= maxw; ++w) {
     int rc = exec_wave(g, groups[w]);
     if (rc) return rc;
@@ -762,6 +829,7 @@ int run_ldp(ft_graph* g) {
   int rc = flush(g);
   if (rc) return rc;
   g->final_set = out;
+  if ((rc = ensure_off(g, out))) return rc;
   const FSet& F = g->sets[out];
   int64_t n = F.off[1];
   g->final_m.resize(n);
@@ -779,6 +847,12 @@ int run_ldp(ft_graph* g) {
 
 int fetch_bp(ft_graph* g, FSet& s) {
   if (s.h_bp_ok) return FT_OK;
+  if (!s.off_ok) {
+    s.off.resize(s.nseg + 1);
+    CU(cudaMemcpy(s.off.data(), s.d_off, sizeof(int64_t) * (s.nseg + 1), cudaMemcpyDeviceToHost),
+       "seg_off d2h");
+    s.off_ok = true;
+  }
   int64_t n = s.off[s.nseg];
   s.h_bp.resize(n);
   if (n) {
@@ -819,6 +893,7 @@ int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_
     if (S.kind != S_STEP) continue;
     if ((rc = fetch_bp(g, S))) return rc;
     const StepRec& r = g->steps[S.step];
+    if ((rc = ensure_off(g, r.X)) || (rc = ensure_off(g, r.Y)) || (rc = ensure_off(g, r.Z))) return rc;
     const uint64_t id = S.h_bp[S.off[it.seg] + it.idx];
     const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
     uint64_t acc = 0;
@@ -986,6 +1061,11 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
 
 void ft_graph_destroy(ft_graph* g) {
   if (!g) return;
+  if (getenv("FT_HOST_PROF"))
+    fprintf(stderr,
+            "[libft host ms] waves=%lld plan+desc %.2f pipeline %.2f offsets/alloc %.2f gather+sync %.2f "
+            "bookkeeping %.2f wave-assign %.2f policy %.2f\n",
+            (long long)g->nwaves, g->hp[0], g->hp[1], g->hp[2], g->hp[3], g->hp[4], g->hp[5], g->hp[6]);
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {
     if (w.m) cudaFree(w.m);
@@ -1064,11 +1144,13 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
   }
   int rc = start(g);
   if (rc) return rc;
+  const double a0 = now_ms();
   for (;;) {
     int r = auto_step(g);
     if (r < 0) return r;
     if (r == 0) break;
   }
+  g->hp[6] += now_ms() - a0;  // FT_AUTO policy (scheduling only)
   return flush(g);
 }
 
@@ -1178,6 +1260,8 @@ int ft_step_output(ft_graph* g, int64_t step, int64_t cap, int64_t* seg_off, int
   if (!g || !n_out) return FT_EINVAL;
   if (g->poisoned) return g->poisoned;
   if (step < 0 || step >= (int64_t)g->steps.size()) return setf(g, FT_EINVAL, "bad step");
+  int rc0 = ensure_off(g, g->steps[step].out);
+  if (rc0) return rc0;
   FSet& S = g->sets[g->steps[step].out];
   const int64_t n = S.off[S.nseg];
   *n_out = n;

@@ -163,7 +163,15 @@ __device__ __forceinline__ bool key_lt(int64_t am, int64_t at, uint64_t ai, int6
 __device__ __forceinline__ void block_factor_segs(const StepDev& s, int64_t sg, int64_t k,
                                                   int64_t& sx, int64_t& sy, int64_t& sz) {
   if (s.kind == K_NODE) {          // sigma = w*K_j + p ; X=F(e_hi,w,k) Y=F(o_i,k) Z=F(e_ij,k,p)
-    int64_t w = sg / s.KC, p = sg - w * s.KC;
+    int64_t w, p;
+    if ((sg >> 31) == 0 && (s.KC >> 31) == 0) {  // 32-bit division fast path
+      const unsigned q = (unsigned)sg / (unsigned)s.KC;
+      w = q;
+      p = sg - (int64_t)q * s.KC;
+    } else {
+      w = sg / s.KC;
+      p = sg - w * s.KC;
+    }
     sx = w * s.KB + k;
     sy = k;
     sz = k * s.KC + p;

@@ -97,9 +97,11 @@ void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap,
 // segment (ids, R6), sample sizes per level, the level at which the segment
 // is small enough for the direct path.
 
-__global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
-                                              int64_t* blk_rel, int64_t* seg_tuples,
-                                              StepHdr* hdr) {
+__device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int32_t* seg_n,
+                                         int64_t* blk_rel, int64_t* seg_tuples, StepHdr* hdr,
+                                         unsigned long long& sh_D, unsigned long long& sh_tuples,
+                                         unsigned long long* sh_filter,
+                                         unsigned long long* sh_direct) {
   // one warp per local output segment; lanes stride over its blocks
   const int lane = threadIdx.x & 31;
   const int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -109,50 +111,77 @@ __global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_
   const int64_t li = gs - B.seg_base[j];
   const int64_t sg = s.seg_lo + li;
   int64_t* rel_out = blk_rel + B.blk_base[j] + li * s.nblk;
-  unsigned long long samp[LMAX + 1];
-#pragma unroll
-  for (int l = 0; l <= LMAX; ++l) samp[l] = 0;
-  int64_t rel = 0;  // running block offset (ids, R6)
+  // level 0: block offsets relative to the segment (ids, R6) and the tuple count
+  int64_t rel = 0;
   for (int64_t k0 = 0; k0 < s.nblk; k0 += 32) {
     const int64_t k = k0 + lane;
     int64_t nk = 0;
     if (k < s.nblk) {
-      Blk b = load_blk(s, sg, k);
+      const Blk b = load_blk(s, sg, k);
       nk = b.n[0] * b.n[1] * b.n[2];
-#pragma unroll
-      for (int l = 0; l <= LMAX; ++l) {
-        const int sh = B.slog * l;
-        samp[l] += (unsigned long long)(samp_cnt(b.n[0], sh) * samp_cnt(b.n[1], sh) *
-                                        samp_cnt(b.n[2], sh));
-      }
     }
     const int64_t inc = warp_incl_sum<long long>(nk);
     if (k < s.nblk) rel_out[k] = rel + inc - nk;
     rel += __shfl_sync(0xffffffffu, inc, 31);
   }
-#pragma unroll
-  for (int l = 0; l <= LMAX; ++l) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) samp[l] += __shfl_xor_sync(0xffffffffu, samp[l], d);
-  }
-  if (lane != 0) return;
+  // levels l = 0, 1, ...: sample size until it fits the direct path
   int d = -1;
-  for (int l = 0; l <= LMAX; ++l)
-    if (samp[l] <= (unsigned long long)B.cdirect) {
+  unsigned long long samp = (unsigned long long)rel;
+  for (int l = 0; l <= LMAX; ++l) {
+    if (l > 0) {
+      const int sh = B.slog * l;
+      unsigned long long loc = 0;
+      for (int64_t k = lane; k < s.nblk; k += 32) {
+        const Blk b = load_blk(s, sg, k);
+        loc += (unsigned long long)(samp_cnt(b.n[0], sh) * samp_cnt(b.n[1], sh) * samp_cnt(b.n[2], sh));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+      samp = loc;
+    }
+    if (samp <= (unsigned long long)B.cdirect && s.nblk <= B.cdirect) {
       d = l;
       break;
     }
-  if (d < 0 || s.nblk > B.cdirect) {
-    atomicExch(&hdr->bad, 1ull);
-    d = LMAX;
+    if (lane == 0) atomicAdd(&sh_filter[l], samp);  // level l runs the filter path
   }
-  seg_d[gs] = d;
-  seg_n[gs] = (int32_t)min(samp[d], (unsigned long long)INT32_MAX);
-  seg_tuples[gs] = rel;
-  atomicMax(&hdr->D, (unsigned long long)d);
-  atomicAdd(&hdr->tuples, (unsigned long long)rel);
-  for (int l = 0; l < d; ++l) atomicAdd(&hdr->filter_samp[l], samp[l]);
-  atomicAdd(&hdr->direct_samp[d], samp[d]);
+  if (lane == 0) {
+    if (d < 0) {
+      atomicExch(&hdr->bad, 1ull);
+      d = LMAX;
+    }
+    seg_d[gs] = d;
+    seg_n[gs] = (int32_t)min(samp, (unsigned long long)INT32_MAX);
+    seg_tuples[gs] = rel;
+    atomicMax(&sh_D, (unsigned long long)d);
+    atomicAdd(&sh_tuples, (unsigned long long)rel);
+    atomicAdd(&sh_direct[d], samp);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
+                                              int64_t* blk_rel, int64_t* seg_tuples,
+                                              StepHdr* hdr) {
+  __shared__ unsigned long long sh_D, sh_tuples, sh_filter[LMAX + 1], sh_direct[LMAX + 1];
+  if (threadIdx.x == 0) {
+    sh_D = 0;
+    sh_tuples = 0;
+  }
+  if (threadIdx.x <= LMAX) {
+    sh_filter[threadIdx.x] = 0;
+    sh_direct[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  plan_seg(B, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (sh_D) atomicMax(&hdr->D, sh_D);
+    if (sh_tuples) atomicAdd(&hdr->tuples, sh_tuples);
+  }
+  if (threadIdx.x <= LMAX) {
+    if (sh_filter[threadIdx.x]) atomicAdd(&hdr->filter_samp[threadIdx.x], sh_filter[threadIdx.x]);
+    if (sh_direct[threadIdx.x]) atomicAdd(&hdr->direct_samp[threadIdx.x], sh_direct[threadIdx.x]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -328,8 +357,11 @@ __device__ __forceinline__ void warp_bitonic(int64_t (&m)[R], int64_t (&t)[R], u
   }
 }
 
+constexpr int WARP_BLK_CACHE = 64;  // block descriptors cached per warp
+
 template <int R>
-__device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre) {
+__device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre,
+                                Blk* wblk) {
   const int lane = threadIdx.x & 31;
   const int st = L.st;
   const int j = find_base(B.seg_base, B.nsteps, gs);
@@ -346,6 +378,7 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
     if (k < nblk) {
       Blk b = load_blk(s, sg, k);
       c = (int)(samp_cnt(b.n[0], st) * samp_cnt(b.n[1], st) * samp_cnt(b.n[2], st));
+      if (k < WARP_BLK_CACHE) wblk[k] = b;
     }
     const int inc = warp_incl_sum<int>(c);
     if (k < nblk) wpre[k + 1] = run + inc;
@@ -365,7 +398,7 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
         if (wpre[mid] <= e) lo = mid;
         else hi = mid;
       }
-      const Blk b = load_blk(s, sg, lo);
+      const Blk b = lo < WARP_BLK_CACHE ? wblk[lo] : load_blk(s, sg, lo);
       const int rr = e - wpre[lo];
       const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
       const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
@@ -423,8 +456,9 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
   }
 }
 
-__global__ void __launch_bounds__(256) k_direct_warp(BatchDev B, LevelDev L) {
+__global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) {
   __shared__ int pre_all[8][WARP_DIRECT + 1];
+  __shared__ Blk blk_all[8][WARP_BLK_CACHE];
   const int wid = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t gs = (int64_t)blockIdx.x * 8 + wid; gs < B.nseg; gs += nw) {
@@ -432,10 +466,10 @@ __global__ void __launch_bounds__(256) k_direct_warp(BatchDev B, LevelDev L) {
     const int n = L.seg_n[gs];
     if (n > WARP_DIRECT) continue;
     if (L.hdr->overflow) return;
-    if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid]);
-    else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid]);
-    else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid]);
-    else warp_direct_seg<8>(B, L, gs, n, pre_all[wid]);
+    if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+    else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+    else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+    else warp_direct_seg<8>(B, L, gs, n, pre_all[wid], blk_all[wid]);
     __syncwarp();
   }
 }
@@ -447,6 +481,16 @@ __global__ void k_level_prep(BatchDev B, LevelDev L) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B.nseg) return;
   L.nb[i] = L.seg_d[i] > L.level ? L.in.cnt[i] + 1 : 0;
+}
+
+// Clears the bucket counters of the live buckets only (B read on device).
+__global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
+  const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    L.bcount[i] = 0;
+    L.bmin[i] = INF;
+  }
 }
 
 __global__ void k_check_buckets(BatchDev Bt, LevelDev L) {
@@ -714,7 +758,7 @@ __device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int6
   }
 }
 
-__global__ void __launch_bounds__(256) k_bucket_small(BatchDev Bt, LevelDev L) {
+__global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L) {
   if (L.hdr->overflow) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
@@ -903,19 +947,82 @@ __global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos) {
   L.out.cnt[li] = gpos[hi] - gpos[lo];
 }
 
-// Final gather of the level-0 pool into every step's CSR output set.
-__global__ void k_gather(BatchDev B, Pool P) {
-  for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
+// Final gather of the level-0 pool into every step's CSR output set (one
+// warp per segment).
+__global__ void __launch_bounds__(256) k_gather(BatchDev B, Pool P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gs < B.nseg; gs += nw) {
     const int j = find_base(B.seg_base, B.nsteps, gs);
     const StepDev& s = B.steps[j];
     const int64_t li = gs - B.seg_base[j];
     const int64_t src = P.start[gs], n = P.cnt[gs], d = s.out_off[li];
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = lane; i < n; i += 32) {
       s.out_m[d + i] = P.m[src + i];
       s.out_t[d + i] = P.t[src + i];
       s.out_bp[d + i] = P.id[src + i];
     }
   }
+}
+
+// Single-rank gather: the arena is in `pos` order (step-major exclusive scan
+// of the survivor counts), so output element i belongs to the segment gs with
+// pos[gs] <= i < pos[gs+1].  Tiles of 2048 outputs: one binary search per CTA
+// for the tile's segment range, then a short search per element.
+__global__ void __launch_bounds__(256) k_gather_flat(BatchDev B, Pool P, const int64_t* pos,
+                                                     int64_t* om, int64_t* ot, uint64_t* obp) {
+  __shared__ int64_t seg_lo_s, seg_hi_s;
+  const int64_t total = pos[B.nseg];
+  const int64_t ntiles = (total + 2047) / 2048;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = tile * 2048, t1 = min(t0 + 2048, total);
+    if (threadIdx.x < 2) {  // segment containing t0 (thread 0) and t1-1 (thread 1)
+      const int64_t x = threadIdx.x == 0 ? t0 : t1 - 1;
+      int64_t lo = 0, hi = B.nseg;  // largest gs with pos[gs] <= x
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pos[mid] <= x) lo = mid;
+        else hi = mid;
+      }
+      if (threadIdx.x == 0) seg_lo_s = lo;
+      else seg_hi_s = lo;
+    }
+    __syncthreads();
+    const int64_t slo = seg_lo_s, shi = seg_hi_s;
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      int64_t lo = slo, hi = shi + 1;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pos[mid] <= i) lo = mid;
+        else hi = mid;
+      }
+      const int64_t src = P.start[lo] + (i - pos[lo]);
+      om[i] = P.m[src];
+      ot[i] = P.t[src];
+      obp[i] = P.id[src];
+    }
+    __syncthreads();
+  }
+}
+
+// Device-side wave offsets (single rank): from the level-0 survivor counts
+// and their exclusive scan `pos` (step-major = arena order), write every
+// step's relative CSR offsets into the arena offset array (step j's nseg+1
+// entries start at seg_base[j] + j) and per-step totals / max / tuples.
+__global__ void k_wave_off(BatchDev B, const int64_t* cnt, const int64_t* seg_tuples,
+                           const int64_t* pos, int64_t* off, int64_t* step_arr) {
+  const int64_t gs = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gs >= B.nseg) return;
+  const int j = find_base(B.seg_base, B.nsteps, gs);
+  const int64_t sb = B.seg_base[j], se = B.seg_base[j + 1];
+  const int64_t base = pos[sb];
+  off[sb + j + (gs - sb)] = pos[gs] - base;
+  if (gs == se - 1) {
+    off[sb + j + (gs - sb) + 1] = pos[se] - base;
+    step_arr[3 * j] = pos[se] - base;
+  }
+  atomicMax((unsigned long long*)&step_arr[3 * j + 1], (unsigned long long)cnt[gs]);
+  atomicAdd((unsigned long long*)&step_arr[3 * j + 2], (unsigned long long)seg_tuples[gs]);
 }
 
 // ---------------------------------------------------------------------------
@@ -951,7 +1058,7 @@ void StepRunner::release() {
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
                 &cgb, &cpos, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
-                &dst_off, &steps_dev, &base_dev};
+                &dst_off, &steps_dev, &base_dev, &pos, &step_arr};
   for (Buf* b : all) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;
@@ -962,6 +1069,9 @@ void StepRunner::release() {
   if (cnt_host) cudaFreeHost(cnt_host);
   cnt_host = nullptr;
   cnt_host_n = 0;
+  if (step_host_p) cudaFreeHost(step_host_p);
+  step_host_p = nullptr;
+  step_host.clear();
   for (auto& e : pev)
     if (e) {
       cudaEventDestroy(e);
@@ -979,7 +1089,8 @@ static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
   return (int)g;
 }
 
-cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res) {
+cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
+                            int64_t* dev_off) {
   int64_t nl = 0;  // kernel launches
   int pgroup[64];
   npev = 0;
@@ -1169,8 +1280,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
         scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
         k_check_buckets<<<1, 1, 0, st>>>(s, L);
-        cudaMemsetAsync(L.bcount, 0, sizeof(unsigned int) * bcap, st);
-        cudaMemsetAsync(L.bmin, BMIN_FILL, sizeof(long long) * bcap, st);
+        k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
         cudaMemsetAsync(L.cand_cursor, 0, sizeof(unsigned long long), st);
         k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
         scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
@@ -1208,20 +1318,51 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       if ((e = cudaMallocHost((void**)&cnt_host, sizeof(int64_t) * 2 * nloc)) != cudaSuccess) return e;
       cnt_host_n = nloc;
     }
-    cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(cnt_host, pools[0].cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(cnt_host + nloc, seg_tuples.p, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
+    if (dev_off) {  // offsets on the device; only per-step totals come back
+      GROW(pos, int64_t, nloc + 1);
+      GROW(step_arr, int64_t, 3 * nsteps);
+      if ((int64_t)step_host.size() < 3 * nsteps) {
+        if (step_host_p) cudaFreeHost(step_host_p);
+        if ((e = cudaMallocHost((void**)&step_host_p, sizeof(int64_t) * 3 * nsteps)) != cudaSuccess) return e;
+        step_host.assign(3 * nsteps, 0);
+      }
+      scan_excl<int64_t>(pools[0].cnt, (int64_t*)pos.p, nullptr, nloc, (int64_t*)scan_tmp.p, st);
+      cudaMemsetAsync(step_arr.p, 0, sizeof(int64_t) * 3 * nsteps, st);
+      k_wave_off<<<grid_for(nloc, 256, 1 << 30), 256, 0, st>>>(s, pools[0].cnt, (int64_t*)seg_tuples.p,
+                                                               (int64_t*)pos.p, dev_off,
+                                                               (int64_t*)step_arr.p);
+      nl += 4;
+      cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(step_host_p, step_arr.p, sizeof(int64_t) * 3 * nsteps, cudaMemcpyDeviceToHost, st);
+    } else {
+      cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(cnt_host, pools[0].cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(cnt_host + nloc, seg_tuples.p, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
+    }
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (!hdr_host->overflow) {
       res->pool = pools[0];
       res->candidates = 0;
       for (int l = 0; l < D; ++l) res->candidates += (int64_t)hdr_host->cand_total[l];
+      res->filter_tuples = res->direct_tuples = 0;
+      for (int l = 0; l <= D; ++l) {
+        res->filter_tuples += (int64_t)plan_copy[LMAX + 1 + l];
+        res->direct_tuples += (int64_t)plan_copy[l];
+      }
       res->huge = (int64_t)hdr_host->huge;
-      res->counts = cnt_host;
-      res->seg_tuples = cnt_host + nloc;
       int64_t tot = 0;
-      for (int64_t i = 0; i < nloc; ++i) tot += cnt_host[i];
+      if (dev_off) {
+        res->counts = nullptr;
+        res->seg_tuples = nullptr;
+        res->step_stats = step_host_p;
+        for (int q = 0; q < nsteps; ++q) tot += step_host_p[3 * q];
+      } else {
+        res->counts = cnt_host;
+        res->seg_tuples = cnt_host + nloc;
+        res->step_stats = nullptr;
+        for (int64_t i = 0; i < nloc; ++i) tot += cnt_host[i];
+      }
       res->total = tot;
       float ms = 0;
       cudaEventElapsedTime(&ms, ev0, ev1);
@@ -1256,10 +1397,15 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
 cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResult& r,
                                cudaStream_t st) {
   if (r.nloc == 0) return cudaSuccess;
+  if (r.step_stats) {  // device-offset mode: arena is contiguous in pos order
+    k_gather_flat<<<grid_for(r.total, 2048, 148 * 16), 256, 0, st>>>(
+        batch, r.pool, (const int64_t*)pos.p, steps[0].out_m, steps[0].out_t, steps[0].out_bp);
+    return cudaGetLastError();
+  }
   // the output pointers changed: refresh the step array (same batch layout)
   cudaMemcpyAsync(steps_dev.p, steps.data(), sizeof(StepDev) * steps.size(), cudaMemcpyHostToDevice,
                   st);
-  k_gather<<<grid_for(r.nloc, 1, 148 * 8), 128, 0, st>>>(batch, r.pool);
+  k_gather<<<grid_for(r.nloc, 8, 148 * 16), 256, 0, st>>>(batch, r.pool);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@ struct StepResult {
   int64_t total = 0;       // survivors over those segments
   int64_t tuples = 0;      // product tuples over those segments
   int64_t candidates = 0;  // pre-filter survivors over all levels
+  int64_t filter_tuples = 0, direct_tuples = 0;  // sampled tuples per kernel family
   int64_t huge = 0;        // buckets that took the global-memory sort
   int64_t retries = 0;
   int levels = 0;
@@ -21,6 +22,7 @@ struct StepResult {
   float plan_ms = 0, direct_ms = 0, filter_ms = 0, bucket_ms = 0, compact_ms = 0, host_ms = 0;
   const int64_t* counts = nullptr;  // host (pinned) per-segment survivor counts [nloc]
   const int64_t* seg_tuples = nullptr;  // host (pinned) per-segment product tuples [nloc]
+  const int64_t* step_stats = nullptr;  // device-offset mode: per step {survivors, max, tuples}
   Pool pool;                        // level-0 pool (device)
 };
 
@@ -37,7 +39,10 @@ class StepRunner {
   // Runs a batch of independent steps, each for its segments [seg_lo,
   // seg_hi); on success res->counts (local segments, in batch order) and
   // res->pool describe the results (valid until the next run).
-  cudaError_t run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res);
+  // dev_off != nullptr (single rank): write the wave's CSR offsets on the device
+  // (arena layout) and return only per-step totals in res->step_stats.
+  cudaError_t run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
+                  int64_t* dev_off = nullptr);
   // Gathers the level-0 pool into each step's CSR output (steps[j].out_*).
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
@@ -59,7 +64,9 @@ class StepRunner {
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
   Buf cm, ct, cid, cgb, cpos, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
-  Buf steps_dev, base_dev;
+  Buf steps_dev, base_dev, pos, step_arr;
+  std::vector<int64_t> step_host;
+  int64_t* step_host_p = nullptr;
   std::vector<int64_t> h_base;
   BatchDev batch{};
   StepHdr* hdr_host = nullptr;

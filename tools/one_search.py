@@ -1,5 +1,8 @@
-"""One FT search of a workload on cuda:0 (for ncu); prints the k_filter
-launch index of the largest step (ncu --launch-skip target) when --target."""
+"""One FT search of a workload on cuda:0 (for ncu).  With --target KERNEL,
+prints the ncu launch-skip count that lands on KERNEL's level-0 launch in the
+wave with the largest work for that kernel family:
+  k_filter / k_bucket_small: launched once per filter level (levels-1 per wave)
+  k_direct_warp / k_direct:  launched once per level (levels per wave)"""
 import sys
 
 sys.path.insert(0, ".")
@@ -12,7 +15,14 @@ g.eliminate()
 m, t = g.frontier()
 st = g.stats()
 if "--target" in sys.argv:
-    best = max(range(len(st)), key=lambda i: st[i]["tuples"])
-    skip = sum(max(0, s["levels"] - 1) for s in st[:best]) + max(0, st[best]["levels"] - 2)
-    print(f"largest step {best} tuples {st[best]['tuples']} levels {st[best]['levels']} filter_skip {skip}")
+    kern = sys.argv[sys.argv.index("--target") + 1]
+    waves = {}
+    for s in st:
+        waves.setdefault(s["wave"], s)  # first step of each wave carries the wave numbers
+    order = [waves[w] for w in sorted(waves)]
+    per = (lambda s: max(0, s["levels"] - 1)) if kern in ("k_filter", "k_bucket_small") else (lambda s: s["levels"])
+    key = "filter_tuples" if kern in ("k_filter", "k_bucket_small") else "direct_tuples"
+    best = max(range(len(order)), key=lambda i: order[i][key])
+    skip = sum(per(s) for s in order[:best]) + max(0, per(order[best]) - 1)
+    print(f"target {kern} wave {best} {key} {order[best][key]} levels {order[best]['levels']} skip {skip}")
 print("frontier", len(m))

@@ -76,6 +76,7 @@ struct ft_graph {
   bool own_stream = false;
   int rank = 0, world = 1;
   bool loopback = false;  // world > 1 simulated on one GPU (tests)
+  bool no_shared = false;  // FT_NO_SHARED=1 disables the shared-order node path (A/B tests)
   ncclComm_t comm = nullptr;
   bool keep_all = false;
   int n_ops = 0, n_orig_edges = 0;
@@ -100,6 +101,7 @@ struct ft_graph {
   std::vector<WaveBuf> waves;
   std::vector<std::vector<int64_t>> op_m, op_t, e_m, e_t;
   std::vector<char> op_ok, e_ok;
+  std::vector<char> e_mzero;  // original edge has m = 0 everywhere (Eq. 2)
   bool started = false, have_final = false;
   int final_set = -1;
   std::vector<int64_t> final_m, final_t;
@@ -401,6 +403,43 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     }
     ft_shard_plan(NS, w.data(), g->world, lo.data());
   }
+  // shared-order node path eligibility (k_node_shared): Y all singletons,
+  // Z an original edge with m = 0
+  std::vector<char> shared(ns, 0);
+  for (int q = 0; q < ns; ++q) {
+    const StepRec& r = g->steps[ids[q]];
+    if (r.kind != ftk::K_NODE || r.nblk > ftk::NS_MAXBLK) continue;
+    const FSet &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+    const bool y1 = Y.kind == S_OP || (Y.kind == S_STEP && g->steps[Y.step].done &&
+                                       g->steps[Y.step].st.survivors == Y.nseg);
+    bool zok = false;
+    if (Z.kind == S_EDGE)
+      for (int e = 0; e < g->n_orig_edges; ++e)
+        if (g->edges[e].set == r.Z) zok = g->e_mzero[e] != 0;
+    shared[q] = y1 && zok && !g->no_shared;
+  }
+  auto make_groups = [&](const std::vector<ftk::StepDev>& v) {
+    std::vector<ftk::NodeGroupH> gr;
+    int64_t base = 0;
+    for (int q = 0; q < ns; ++q) {
+      const ftk::StepDev& d = v[q];
+      if (d.node_shared && d.seg_hi > d.seg_lo) {
+        for (int64_t w = d.seg_lo / d.KC; w <= (d.seg_hi - 1) / d.KC; ++w) {
+          const int64_t a0 = std::max(d.seg_lo, w * d.KC), a1 = std::min(d.seg_hi, (w + 1) * d.KC);
+          ftk::NodeGroupH G;
+          G.step = q;
+          G.pad = 0;
+          G.w = w;
+          G.p_lo = a0 - w * d.KC;
+          G.p_hi = a1 - w * d.KC;
+          G.gs0 = base + (a0 - d.seg_lo);
+          gr.push_back(G);
+        }
+      }
+      base += d.seg_hi - d.seg_lo;
+    }
+    return gr;
+  };
   // step descriptors for the global segment range [a, b) of the wave
   auto make_sd = [&](int64_t a, int64_t b) {
   std::vector<ftk::StepDev> sd(ns);
@@ -409,6 +448,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     ftk::StepDev& d = sd[q];
     std::memset(&d, 0, sizeof(d));
     d.kind = r.kind;
+    d.node_shared = shared[q];
     d.KA = r.KA;
     d.KB = r.KB;
     d.KC = r.KC;
@@ -443,7 +483,8 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   for (size_t v = 0; v < vr.size(); ++v) {
     const int64_t a = lo[vr[v]], b = lo[vr[v] + 1];
     sd = make_sd(a, b);
-    cudaError_t ce = g->runner->run(sd, g->stream, &res, devoff ? wb.off : nullptr);
+    const std::vector<ftk::NodeGroupH> grp = make_groups(sd);
+    cudaError_t ce = g->runner->run(sd, g->stream, &res, devoff ? wb.off : nullptr, &grp);
     if (ce == cudaErrorInvalidConfiguration)
       return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
     if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
@@ -545,7 +586,8 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   CU(g->runner->gather(sd, res, g->stream), "gather");  // last (or only) rank's pool
   for (size_t v = 0; v + 1 < vr.size(); ++v) {           // loopback: re-run the others
     std::vector<ftk::StepDev> sv = make_sd(lo[vr[v]], lo[vr[v] + 1]);
-    cudaError_t ce = g->runner->run(sv, g->stream, &res);
+    const std::vector<ftk::NodeGroupH> grp = make_groups(sv);
+    cudaError_t ce = g->runner->run(sv, g->stream, &res, nullptr, &grp);
     if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline (loopback)");
     set_out(sv);
     CU(g->runner->gather(sv, res, g->stream), "gather");
@@ -981,6 +1023,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
   g->e_m.resize(n_edges);
   g->e_t.resize(n_edges);
   g->e_ok.assign(n_edges, 0);
+  g->e_mzero.assign(n_edges, 0);
   FSet unit;
   unit.kind = S_UNIT;
   unit.nseg = 1;
@@ -1032,6 +1075,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     g->stream = (cudaStream_t)opt->stream;
   }
   if (opt && g->world > 1 && !g->comm && opt->loopback) g->loopback = true;
+  g->no_shared = getenv("FT_NO_SHARED") != nullptr;
   if (g->world > 1 && !g->loopback && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
     delete g;
     return FT_EINVAL;
@@ -1107,6 +1151,9 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
   }
   if (m) g->e_m[edge].assign(m, m + n);
   else g->e_m[edge].assign(n, 0);
+  g->e_mzero[edge] = 1;
+  for (int64_t q = 0; q < n; ++q)
+    if (g->e_m[edge][q] != 0) g->e_mzero[edge] = 0;
   g->e_t[edge].assign(t, t + n);
   g->e_ok[edge] = 1;
   return FT_OK;

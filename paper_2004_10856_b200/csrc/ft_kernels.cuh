@@ -31,6 +31,9 @@ constexpr int64_t INF = INT64_MAX;
 constexpr int LMAX = 12;            // max sample level
 constexpr int C_DIRECT = 1024;      // direct (single-CTA) segment capacity
 constexpr int WARP_DIRECT = 256;    // direct segments up to this size: one warp each
+constexpr int NS_CAP = 2048;        // shared-order node path: tuples per (step, w) group
+constexpr int NS_MAXBLK = 128;      // ... and blocks (K_i)
+constexpr int SPECIAL_LEVEL = 60;   // seg_d of segments handled by the shared-order node path
 constexpr int DIRECT_NT = 256;      // threads of the direct / bucket CTA kernels
 constexpr int CHUNK = 16;           // run elements per filter work item
 constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
@@ -48,7 +51,7 @@ struct FacSet {
 // One FT step of a batch ("wave" of independent steps).
 struct StepDev {
   int kind;
-  int pad_;
+  int node_shared;  // NODE step with singleton F(o_i,k) and original m=0 edge F(e_ij,k,p)
   int64_t KA, KB, KC, nseg, nblk;
   int64_t seg_lo, seg_hi;  // this rank's output segments [seg_lo, seg_hi)
   FacSet X, Y, Z;

@@ -20,6 +20,12 @@ namespace ftk {
 
 constexpr int SCAN_NT = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_NT * SCAN_ITEMS;
 
+// Segment runs the filter path at this level (its direct level is deeper;
+// SPECIAL_LEVEL segments are handled by k_node_shared).
+__device__ __forceinline__ bool is_filter(int32_t d, int level) {
+  return d > level && d < SPECIAL_LEVEL;
+}
+
 template <typename TIn>
 __global__ void __launch_bounds__(SCAN_NT) k_scan_tiles(const TIn* in, const int64_t* n_dev,
                                                         int64_t n_host, int64_t* tile_sums) {
@@ -123,6 +129,18 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int3
     const int64_t inc = warp_incl_sum<long long>(nk);
     if (k < s.nblk) rel_out[k] = rel + inc - nk;
     rel += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  // shared-order node path (k_node_shared): every segment of row w has the same
+  // n = sum_k |X_{w,k}| (Y, Z singletons)
+  if (s.node_shared && rel <= NS_CAP && s.nblk <= NS_MAXBLK) {
+    if (lane == 0) {
+      seg_d[gs] = SPECIAL_LEVEL;
+      seg_n[gs] = (int32_t)rel;
+      seg_tuples[gs] = rel;
+      atomicAdd(&sh_tuples, (unsigned long long)rel);
+      atomicAdd(&sh_direct[0], (unsigned long long)rel);  // level-0 pool capacity
+    }
+    return;
   }
   // levels l = 0, 1, ...: sample size until it fits the direct path
   int d = -1;
@@ -474,13 +492,256 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
   }
 }
 
+// Shared-order node elimination (Eq. 4) for steps whose Y = F(o_i,k) are
+// singletons and Z = F(e_ij,k,p) is an original edge with m = 0 (Eq. 2): for a
+// fixed w, every segment (w,p) holds the same tuples (k, x) with the same m and
+// id = rel_k + x; only t = t_x + t_y + t_z(k,p) depends on p.  The (m, id)
+// order is sorted once per w; if no two tuples share m it equals the
+// (m, t, id) order of every p and Alg. 1 is one sweep per p.  With m ties the
+// exact group rule below is used instead.  One CTA per (step, w).
+constexpr size_t NS_SMEM = (size_t)NS_CAP * (5 * 8 + 4 + 2 + 2);
+static_assert(sizeof(NodeGroup) == sizeof(NodeGroupH), "NodeGroup layout");
+
+__global__ void __launch_bounds__(DIRECT_NT) k_node_shared(BatchDev B, LevelDev L,
+                                                           const NodeGroup* groups, int ngroups) {
+  extern __shared__ int64_t dyn_ns[];
+  int64_t* sm = dyn_ns;                            // [NS_CAP] m (sorted by (m, id))
+  uint64_t* sid = (uint64_t*)(sm + NS_CAP);        // [NS_CAP] id
+  int64_t* stxy = (int64_t*)(sid + NS_CAP);        // [NS_CAP] t_x + t_y
+  int64_t* tt = stxy + NS_CAP;                     // [NS_CAP] t for this p
+  int64_t* mincl = tt + NS_CAP;                    // [NS_CAP] inclusive prefix-min of tt (ties)
+  int* kf = (int*)(mincl + NS_CAP);                // [NS_CAP] keep flags -> positions
+  int16_t* sk = (int16_t*)(kf + NS_CAP);           // [NS_CAP] block of each tuple
+  int16_t* gst = sk + NS_CAP;                      // [NS_CAP] start of the equal-m group
+  __shared__ int64_t zt[NS_MAXBLK];
+  __shared__ int64_t wzt[DIRECT_NT / 32][NS_MAXBLK];  // per-warp t_z(k, p)
+  __shared__ int pre[NS_MAXBLK + 1];
+  __shared__ int64_t bo[NS_MAXBLK];
+  __shared__ int64_t bym[NS_MAXBLK], byt[NS_MAXBLK];
+  __shared__ long long sh[33];
+  __shared__ int s_tie;
+  __shared__ int64_t s_start;
+  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+    const NodeGroup G = groups[gi];
+    if (L.seg_d[G.gs0] != SPECIAL_LEVEL) continue;  // uniform per group
+    if (L.hdr->overflow) return;
+    const StepDev& s = B.steps[G.step];
+    const int nblk = (int)s.nblk;
+    // blocks: X = F(e_hi, w, k) (runs), Y = F(o_i, k), Z = F(e_ij, k, p)
+    for (int k = threadIdx.x; k < nblk; k += DIRECT_NT) {
+      const int64_t sx = G.w * s.KB + k;
+      const int64_t o = s.X.off[sx];
+      bo[k] = o;
+      pre[k + 1] = (int)(s.X.off[sx + 1] - o);
+      const int64_t oy = s.Y.off[k];
+      bym[k] = s.Y.m[oy];
+      byt[k] = s.Y.t[oy];
+    }
+    if (threadIdx.x == 0) {
+      pre[0] = 0;
+      s_tie = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nblk; ++k) pre[k + 1] += pre[k];
+    __syncthreads();
+    const int n = pre[nblk];
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
+      if (i < n) {
+        int lo = 0, hi = nblk;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= i) lo = mid;
+          else hi = mid;
+        }
+        const int x = i - pre[lo];
+        sm[i] = __ldg(s.X.m + bo[lo] + x) + bym[lo];
+        stxy[i] = __ldg(s.X.t + bo[lo] + x) + byt[lo];
+        sid[i] = (uint64_t)(pre[lo] + x);  // id = rel_k + x  (|Y| = |Z| = 1, R6)
+        sk[i] = (int16_t)lo;
+      } else {
+        sm[i] = INF;
+        stxy[i] = INF;
+        sid[i] = ~0ull;
+        sk[i] = 0;
+      }
+    }
+    __syncthreads();
+    // bitonic sort by (m, id), carrying (t_xy, k)
+    for (int kk = 2; kk <= N; kk <<= 1) {
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const bool up = (i & kk) == 0;
+            const bool gt = sm[l] < sm[i] || (sm[l] == sm[i] && sid[l] < sid[i]);
+            if (gt == up) {
+              int64_t a = sm[i]; sm[i] = sm[l]; sm[l] = a;
+              a = stxy[i]; stxy[i] = stxy[l]; stxy[l] = a;
+              uint64_t b = sid[i]; sid[i] = sid[l]; sid[l] = b;
+              int16_t c = sk[i]; sk[i] = sk[l]; sk[l] = c;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // equal-m groups (rare): gst[i] = first index of i's group
+    for (int i = threadIdx.x; i < n; i += DIRECT_NT) {
+      int g0 = i;
+      while (g0 > 0 && sm[g0 - 1] == sm[i]) --g0;
+      gst[i] = (int16_t)g0;
+      if (g0 != i) s_tie = 1;
+    }
+    __syncthreads();
+    const bool tie = s_tie != 0;
+    if (!tie) {
+      // distinct m: the (m, id) order is every p's (m, t, id) order; one warp
+      // per p runs Alg. 1 as a warp-scan sweep (count pass, then write pass)
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      for (int64_t p = G.p_lo + wid; p < G.p_hi; p += DIRECT_NT / 32) {
+        const int64_t gs = G.gs0 + (p - G.p_lo);
+        for (int k = lane; k < nblk; k += 32) wzt[wid][k] = s.Z.t[s.Z.off[(int64_t)k * s.KC + p]];
+        __syncwarp();
+        long long carry = INF;
+        int cnt = 0;
+        for (int c0 = 0; c0 < n; c0 += 32) {
+          const int i = c0 + lane;
+          const long long t = i < n ? stxy[i] + wzt[wid][sk[i]] : INF;
+          const long long inc = warp_incl_min(t);
+          long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+          if (lane == 0) ex = INF;
+          const bool keep = i < n && t < (ex < carry ? ex : carry);
+          cnt += __popc(__ballot_sync(0xffffffffu, keep));
+          const long long rm = __shfl_sync(0xffffffffu, inc, 31);
+          carry = rm < carry ? rm : carry;
+        }
+        int64_t base = 0;
+        if (lane == 0) {
+          unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
+          if ((int64_t)(st0 + cnt) > L.out.cap) {
+            atomicExch(&L.hdr->overflow, 1ull);
+            base = -1;
+          } else {
+            base = (int64_t)st0;
+          }
+          atomicAdd(&L.hdr->out_total[0], (unsigned long long)cnt);
+          L.out.start[gs] = base;
+          L.out.cnt[gs] = cnt;
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= 0) {
+          carry = INF;
+          int off = 0;
+          for (int c0 = 0; c0 < n; c0 += 32) {
+            const int i = c0 + lane;
+            const long long t = i < n ? stxy[i] + wzt[wid][sk[i]] : INF;
+            const long long inc = warp_incl_min(t);
+            long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane == 0) ex = INF;
+            const bool keep = i < n && t < (ex < carry ? ex : carry);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+              const int64_t d = base + off + __popc(bal & ((1u << lane) - 1u));
+              L.out.m[d] = sm[i];
+              L.out.t[d] = t;
+              L.out.id[d] = sid[i];
+            }
+            off += __popc(bal);
+            const long long rm = __shfl_sync(0xffffffffu, inc, 31);
+            carry = rm < carry ? rm : carry;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int64_t p = G.p_lo; p < G.p_hi; ++p) {
+      const int64_t gs = G.gs0 + (p - G.p_lo);
+      for (int k = threadIdx.x; k < nblk; k += DIRECT_NT) {
+        const int64_t sz = (int64_t)k * s.KC + p;
+        zt[k] = s.Z.t[s.Z.off[sz]];
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += DIRECT_NT) tt[i] = stxy[i] + zt[sk[i]];
+      __syncthreads();
+      int cnt;
+      if (!tie) {
+        // distinct m: the (m, id) order is the (m, t, id) order -> Alg. 1 directly
+        cnt = alg1_sweep_smem<DIRECT_NT>(tt, n, INF, kf, sh);
+      } else {
+        // Alg. 1 under (m, t, id) on the (m, id) order: only the (t, id)-least
+        // tuple of an equal-m group can survive, iff its t is below every t of
+        // the earlier groups.
+        {
+          const int per = (n + DIRECT_NT - 1) / DIRECT_NT;
+          const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+          long long lmin = INF;
+          for (int i = lo; i < hi; ++i) lmin = tt[i] < lmin ? tt[i] : lmin;
+          long long v = block_excl_min<DIRECT_NT>(lmin, sh);
+          for (int i = lo; i < hi; ++i) {
+            v = tt[i] < v ? tt[i] : v;
+            mincl[i] = v;
+          }
+        }
+        __syncthreads();
+        int c = 0;
+        const int per = (n + DIRECT_NT - 1) / DIRECT_NT;
+        const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+        for (int i = lo; i < hi; ++i) {
+          const int g0 = gst[i];
+          bool best = true;
+          for (int jx = g0; jx < n && sm[jx] == sm[i]; ++jx)
+            if (jx != i && (tt[jx] < tt[i] || (tt[jx] == tt[i] && sid[jx] < sid[i]))) best = false;
+          const long long before = g0 > 0 ? mincl[g0 - 1] : INF;
+          kf[i] = best && tt[i] < before;
+          c += kf[i];
+        }
+        long long tot;
+        long long off = block_excl_sum<DIRECT_NT>(c, sh, &tot);
+        int q = (int)off;
+        for (int i = lo; i < hi; ++i)
+          if (kf[i]) kf[i] = ++q;
+        __syncthreads();
+        cnt = (int)tot;
+      }
+      if (threadIdx.x == 0) {
+        unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
+        if ((int64_t)(st0 + cnt) > L.out.cap) {
+          atomicExch(&L.hdr->overflow, 1ull);
+          s_start = -1;
+        } else {
+          s_start = (int64_t)st0;
+        }
+        atomicAdd(&L.hdr->out_total[0], (unsigned long long)cnt);
+        L.out.start[gs] = s_start;
+        L.out.cnt[gs] = cnt;
+      }
+      __syncthreads();
+      const int64_t o = s_start;
+      if (o >= 0)
+        for (int i = threadIdx.x; i < n; i += DIRECT_NT)
+          if (kf[i]) {
+            const int64_t d = o + kf[i] - 1;
+            L.out.m[d] = sm[i];
+            L.out.t[d] = tt[i];
+            L.out.id[d] = sid[i];
+          }
+      __syncthreads();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Filter path, level l < d_sigma.
 
 __global__ void k_level_prep(BatchDev B, LevelDev L) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B.nseg) return;
-  L.nb[i] = L.seg_d[i] > L.level ? L.in.cnt[i] + 1 : 0;
+  L.nb[i] = is_filter(L.seg_d[i], L.level) ? L.in.cnt[i] + 1 : 0;
 }
 
 // Clears the bucket counters of the live buckets only (B read on device).
@@ -526,7 +787,7 @@ __global__ void k_work_count(BatchDev B, LevelDev L) {
   const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
   const int64_t gs = B.seg_base[j] + li;
   int64_t w = 0;
-  if (L.seg_d[gs] > L.level) {
+  if (is_filter(L.seg_d[gs], L.level)) {
     Blk b = load_blk(s, s.seg_lo + li, k);
     int lf, fa, fb;
     int64_t c[3];
@@ -684,7 +945,7 @@ __global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L) {
   if (L.hdr->overflow) return;
   const int64_t nloc = B.nseg;
   for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
-    if (L.seg_d[li] <= L.level) continue;
+    if (!is_filter(L.seg_d[li], L.level)) continue;
     const int64_t b0 = L.bucket_base[li], nb = L.nb[li];
     long long carry = INF;
     for (int64_t c0 = 0; c0 < nb; c0 += 256) {
@@ -940,7 +1201,7 @@ __global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand)
 __global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos) {
   const int64_t nloc = B.nseg;
   const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (li >= nloc || L.seg_d[li] <= L.level) return;
+  if (li >= nloc || !is_filter(L.seg_d[li], L.level)) return;
   const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
   const int64_t lo = L.boff[b0], hi = L.boff[b1];
   L.out.start[li] = L.wcnt[0] + gpos[lo];
@@ -1058,7 +1319,7 @@ void StepRunner::release() {
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
                 &cgb, &cpos, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
-                &dst_off, &steps_dev, &base_dev, &pos, &step_arr};
+                &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev};
   for (Buf* b : all) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;
@@ -1090,7 +1351,7 @@ static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
 }
 
 cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
-                            int64_t* dev_off) {
+                            int64_t* dev_off, const std::vector<NodeGroupH>* groups) {
   int64_t nl = 0;  // kernel launches
   int pgroup[64];
   npev = 0;
@@ -1146,6 +1407,11 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   batch = s;
   GROW(seg_d, int32_t, nloc);
   GROW(seg_n, int32_t, nloc);
+  const int ngroups = groups ? (int)groups->size() : 0;
+  if (ngroups) {
+    GROW(groups_dev, NodeGroup, ngroups);
+    cudaMemcpyAsync(groups_dev.p, groups->data(), sizeof(NodeGroup) * ngroups, cudaMemcpyHostToDevice, st);
+  }
   GROW(blk_rel, int64_t, nbl);
   GROW(seg_tuples, int64_t, nloc);
   GROW(hdr, StepHdr, 1);
@@ -1246,6 +1512,11 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       cudaMemsetAsync(L.out.cursor, 0, sizeof(unsigned long long), st);
       mark(1);
       nl += 2;
+      if (l == 0 && ngroups) {
+        ++nl;
+        k_node_shared<<<std::min(ngroups, 148 * 4), DIRECT_NT, NS_SMEM, st>>>(
+            s, L, (const NodeGroup*)groups_dev.p, ngroups);
+      }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, 0, st>>>(s, L);
       if (l < D) {
@@ -1410,6 +1681,11 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 }
 
 cudaError_t StepRunner::configure() {
+  {
+    cudaError_t e0 = cudaFuncSetAttribute(k_node_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)NS_SMEM);
+    if (e0 != cudaSuccess) return e0;
+  }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(64, std::min(C_DIRECT, atoi(e)));
   const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));

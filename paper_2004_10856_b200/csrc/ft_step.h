@@ -31,6 +31,15 @@ struct StepResult {
 class StepRunner;
 StepRunner* device_runner(int device);
 
+// One (step, w) row of a shared-order node elimination (k_node_shared).
+struct NodeGroup {
+  int32_t step;
+  int32_t pad;
+  int64_t w, p_lo, p_hi;  // p range [p_lo, p_hi) of this rank's segments in row w
+  int64_t gs0;            // local segment index of (w, p_lo)
+};
+using NodeGroupH = NodeGroup;
+
 class StepRunner {
  public:
   StepRunner();
@@ -42,7 +51,7 @@ class StepRunner {
   // dev_off != nullptr (single rank): write the wave's CSR offsets on the device
   // (arena layout) and return only per-step totals in res->step_stats.
   cudaError_t run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
-                  int64_t* dev_off = nullptr);
+                  int64_t* dev_off = nullptr, const std::vector<NodeGroupH>* groups = nullptr);
   // Gathers the level-0 pool into each step's CSR output (steps[j].out_*).
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
@@ -64,7 +73,7 @@ class StepRunner {
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
   Buf cm, ct, cid, cgb, cpos, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
-  Buf steps_dev, base_dev, pos, step_arr;
+  Buf steps_dev, base_dev, pos, step_arr, groups_dev;
   std::vector<int64_t> step_host;
   int64_t* step_host_p = nullptr;
   std::vector<int64_t> h_base;

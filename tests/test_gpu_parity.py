@@ -102,3 +102,28 @@ def test_partition_invariance_loopback(ft, world):
                 assert np.array_equal(x, y), (w.name, s)
         for i in np.linspace(0, len(am) - 1, 16).astype(int):
             assert np.array_equal(a.strategy(int(i)), b.strategy(int(i)))
+
+
+def test_bert_no_jitter_ties(ft):
+    """Exact m/t ties (no cost jitter): shared-order node path's tie rule."""
+    compare(ft, G.c4(layers=3, jitter=False), strategies=16)
+
+
+def test_shared_path_ab(ft, monkeypatch):
+    """Shared-order node path vs the generic pipeline (FT_NO_SHARED): identical."""
+    import os
+    w = G.c5(n_ops=300, K=32, B=8, Lmin=3, Lmax=8)
+    a = ft.load(w, keep_all=True)
+    a.eliminate()
+    am, at = a.frontier()
+    os.environ["FT_NO_SHARED"] = "1"
+    try:
+        b = ft.load(w, keep_all=True)
+        b.eliminate()
+        bm, bt = b.frontier()
+    finally:
+        del os.environ["FT_NO_SHARED"]
+    assert np.array_equal(am, bm) and np.array_equal(at, bt)
+    for s in range(len(a.stats())):
+        for x, y in zip(a.step_output(s), b.step_output(s)):
+            assert np.array_equal(x, y), s

@@ -115,6 +115,16 @@ void ft_graph_destroy(ft_graph* g);
  * time the search with inputs already resident in HBM. */
 int ft_prepare(ft_graph* g);
 
+/* All costs at once (fast path; HOST arrays, pinned memory recommended):
+ *  op_m/op_t: concatenation over operators 0..n_ops-1 of K_i entries each;
+ *  edge_t (and edge_m, NULL = 0 per Eq. 2): concatenation over edges
+ *  0..n_edges-1 of K_src*K_dst entries each, row-major [s_src][s_dst].
+ * Copied to the device (asynchronously, then validated on the device) before
+ * the call returns.  Exclusive with the per-operator / per-edge setters.
+ * Errors: FT_EINVAL (negative), FT_EOVERFLOW (>= 2^40), FT_ESTATE, FT_ECUDA. */
+int ft_set_costs_all(ft_graph* g, const int64_t* op_m, const int64_t* op_t,
+                     const int64_t* edge_m, const int64_t* edge_t);
+
 /* Operator costs, Eq. 1: m[K_op] bytes, t[K_op] ns (host arrays,
  * copied to the device).  Must precede the first ft_eliminate/ft_frontier. */
 int ft_set_op_costs(ft_graph* g, int32_t op, const int64_t* m, const int64_t* t);

@@ -71,6 +71,7 @@ def _load():
     L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
     L.ft_shard_plan.argtypes = [C.c_int64, P64, C.c_int32, P64]
     L.ft_prepare.argtypes = [C.c_void_p]
+    L.ft_set_costs_all.argtypes = [C.c_void_p, P64, P64, P64, P64]
     L.ft_step_inputs.argtypes = [C.c_void_p, C.c_int64, P64, P64]
     L.ft_nccl_unique_id.argtypes = [C.c_char_p]
     L.ft_nccl_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.c_int32,
@@ -86,7 +87,7 @@ def _load():
 lib = _load()
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
            "ft_eliminate", "ft_frontier", "ft_strategy", "ft_get_stats", "ft_step_output",
-           "ft_prepare", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
+           "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version"]
 
 
@@ -151,6 +152,16 @@ class Graph:
         t = np.ascontiguousarray(t, dtype=np.int64)
         m = None if m is None else np.ascontiguousarray(m, dtype=np.int64)
         self._chk(lib.ft_set_edge_costs(self.h, e, _p(m, C.c_int64), _p(t, C.c_int64)))
+
+    def set_costs_all(self, op_m, op_t, edge_m, edge_t):
+        """Concatenated cost arrays (see ft_set_costs_all); pinned numpy views
+        (e.g. torch.empty(..., pin_memory=True).numpy()) give the fastest copy."""
+        op_m = np.ascontiguousarray(op_m, dtype=np.int64)
+        op_t = np.ascontiguousarray(op_t, dtype=np.int64)
+        edge_t = np.ascontiguousarray(edge_t, dtype=np.int64)
+        edge_m = None if edge_m is None else np.ascontiguousarray(edge_m, dtype=np.int64)
+        self._chk(lib.ft_set_costs_all(self.h, _p(op_m, C.c_int64), _p(op_t, C.c_int64),
+                                       _p(edge_m, C.c_int64), _p(edge_t, C.c_int64)))
 
     def prepare(self):
         self._chk(lib.ft_prepare(self.h))
@@ -235,9 +246,22 @@ def nccl_comm_destroy(comm):
     lib.ft_nccl_comm_destroy(C.c_void_p(comm))
 
 
-def load(w, **kw) -> Graph:
-    """Create a graph from a ``synth.graphs.Workload`` and upload its costs."""
+def concat_costs(w):
+    """(op_m, op_t, edge_m | None, edge_t) concatenated for ft_set_costs_all."""
+    op_m = np.concatenate(w.op_m)
+    op_t = np.concatenate(w.op_t)
+    edge_t = np.concatenate(w.edge_t) if w.n_edges else np.zeros(0, np.int64)
+    edge_m = None if w.edge_m is None else np.concatenate(w.edge_m)
+    return op_m, op_t, edge_m, edge_t
+
+
+def load(w, bulk: bool = True, costs=None, **kw) -> Graph:
+    """Create a graph from a ``synth.graphs.Workload`` and upload its costs
+    (one ft_set_costs_all call, or per-operator/per-edge setters)."""
     g = Graph(w.n_cfgs, w.src, w.dst, **kw)
+    if bulk:
+        g.set_costs_all(*(costs if costs is not None else concat_costs(w)))
+        return g
     for i in range(w.n_ops):
         g.set_op_costs(i, w.op_m[i], w.op_t[i])
     for e in range(w.n_edges):

@@ -109,7 +109,12 @@ struct ft_graph {
   std::string err;
   ftk::StepRunner* runner = nullptr;  // process-wide per device
   bool profile = false;
-  int64_t* d_costs = nullptr;  // all original costs + iota offsets + unit
+  int64_t* d_costs = nullptr;  // all original costs + iota offsets + unit (alloc_costs)
+  std::vector<int64_t> op_off, e_off;  // concatenation offsets of op / edge costs
+  int64_t c_unit = 0, c_opm = 0, c_opt = 0, c_em = 0, c_et = 0;
+  std::vector<int> op_set0;          // original op sets
+  bool host_costs_pending = false;   // per-op/edge setters used: upload at start()
+  bool bulk_done = false;            // ft_set_costs_all put every cost on the device
   std::vector<int64_t> h_pin_off;
   int64_t* h_pinned = nullptr;
   int64_t h_pinned_n = 0;
@@ -260,57 +265,90 @@ void mark_backbone(ft_graph* g) {
 
 // ---- device side ----------------------------------------------------------
 
+// Device cost buffer layout: iota offsets | unit (m,t) | OPM | OPT | EM | ET,
+// where OPM/OPT concatenate every operator's Eq.1 costs (K_i each) and EM/ET
+// every edge's Eq.2 costs (K_src*K_dst each).  Singleton sets point into it.
+int alloc_costs(ft_graph* g) {
+  if (g->d_costs) return FT_OK;
+  int64_t maxseg = 2, nop = 0, ned = 0;
+  g->op_off.assign(g->n_ops + 1, 0);
+  g->e_off.assign(g->n_orig_edges + 1, 0);
+  for (int i = 0; i < g->n_ops; ++i) {
+    maxseg = std::max<int64_t>(maxseg, g->K[i]);
+    g->op_off[i + 1] = g->op_off[i] + g->K[i];
+  }
+  for (int e = 0; e < g->n_orig_edges; ++e) {
+    const int64_t n = (int64_t)g->K[g->edges[e].src] * g->K[g->edges[e].dst];
+    maxseg = std::max<int64_t>(maxseg, n);
+    g->e_off[e + 1] = g->e_off[e] + n;
+  }
+  nop = g->op_off[g->n_ops];
+  ned = g->e_off[g->n_orig_edges];
+  g->c_unit = maxseg + 1;
+  g->c_opm = g->c_unit + 2;
+  g->c_opt = g->c_opm + nop;
+  g->c_em = g->c_opt + nop;
+  g->c_et = g->c_em + ned;
+  const int64_t total = g->c_et + ned;
+  CU(cudaSetDevice(g->dev), "cudaSetDevice");
+  CU(cudaMalloc(&g->d_costs, sizeof(int64_t) * total), "cudaMalloc(costs)");
+  std::vector<int64_t> head(maxseg + 3);
+  for (int64_t i = 0; i <= maxseg; ++i) head[i] = i;
+  head[maxseg + 1] = 0;
+  head[maxseg + 2] = 0;
+  CU(cudaMemcpyAsync(g->d_costs, head.data(), sizeof(int64_t) * head.size(), cudaMemcpyHostToDevice,
+                     g->stream), "upload costs");
+  CU(cudaStreamSynchronize(g->stream), "upload costs");
+  int64_t* base = g->d_costs;
+  FSet& u = g->sets[0];
+  u.d_off = base;
+  u.d_m = base + g->c_unit;
+  u.d_t = base + g->c_unit + 1;
+  for (int i = 0; i < g->n_ops; ++i) {
+    FSet& st = g->sets[g->op_set0[i]];
+    st.d_off = base;
+    st.d_m = base + g->c_opm + g->op_off[i];
+    st.d_t = base + g->c_opt + g->op_off[i];
+  }
+  for (int e = 0; e < g->n_orig_edges; ++e) {
+    FSet& st = g->sets[g->edges[e].set];
+    st.d_off = base;
+    st.d_m = base + g->c_em + g->e_off[e];
+    st.d_t = base + g->c_et + g->e_off[e];
+  }
+  return FT_OK;
+}
+
 int start(ft_graph* g) {
   if (g->started) return FT_OK;
   for (int i = 0; i < g->n_ops; ++i)
     if (!g->op_ok[i]) return setf(g, FT_ESTATE, "operator costs missing (op " + std::to_string(i) + ")");
   for (int e = 0; e < g->n_orig_edges; ++e)
     if (!g->e_ok[e]) return setf(g, FT_ESTATE, "edge costs missing (edge " + std::to_string(e) + ")");
-  // one device buffer: iota offsets | unit (m,t) | op m,t | edge m,t
-  int64_t maxseg = 2;
-  for (int i = 0; i < g->n_ops; ++i) maxseg = std::max<int64_t>(maxseg, g->K[i]);
-  for (int e = 0; e < g->n_orig_edges; ++e)
-    maxseg = std::max<int64_t>(maxseg, (int64_t)g->K[g->edges[e].src] * g->K[g->edges[e].dst]);
-  std::vector<int64_t> h;
-  h.reserve(maxseg + 1);
-  for (int64_t i = 0; i <= maxseg; ++i) h.push_back(i);
-  const size_t unit_at = h.size();
-  h.push_back(0);
-  h.push_back(0);
-  std::vector<size_t> op_at(g->n_ops), e_at(g->n_orig_edges);
+  int rc = alloc_costs(g);
+  if (rc) return rc;
+  if (!g->host_costs_pending) {  // costs already on the device (ft_set_costs_all)
+    g->started = true;
+    return FT_OK;
+  }
+  // per-operator / per-edge setters: concatenate on the host, 4 copies
+  std::vector<int64_t> a(g->op_off[g->n_ops]), b(g->op_off[g->n_ops]);
   for (int i = 0; i < g->n_ops; ++i) {
-    op_at[i] = h.size();
-    h.insert(h.end(), g->op_m[i].begin(), g->op_m[i].end());
-    h.insert(h.end(), g->op_t[i].begin(), g->op_t[i].end());
+    std::copy(g->op_m[i].begin(), g->op_m[i].end(), a.begin() + g->op_off[i]);
+    std::copy(g->op_t[i].begin(), g->op_t[i].end(), b.begin() + g->op_off[i]);
   }
+  std::vector<int64_t> c(g->e_off[g->n_orig_edges]), d(g->e_off[g->n_orig_edges]);
   for (int e = 0; e < g->n_orig_edges; ++e) {
-    e_at[e] = h.size();
-    h.insert(h.end(), g->e_m[e].begin(), g->e_m[e].end());
-    h.insert(h.end(), g->e_t[e].begin(), g->e_t[e].end());
+    std::copy(g->e_m[e].begin(), g->e_m[e].end(), c.begin() + g->e_off[e]);
+    std::copy(g->e_t[e].begin(), g->e_t[e].end(), d.begin() + g->e_off[e]);
   }
-  CU(cudaSetDevice(g->dev), "cudaSetDevice");
-  CU(cudaMalloc(&g->d_costs, h.size() * sizeof(int64_t)), "cudaMalloc(costs)");
-  CU(cudaMemcpyAsync(g->d_costs, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
-                     g->stream), "upload costs");
-  CU(cudaStreamSynchronize(g->stream), "upload costs");
   int64_t* base = g->d_costs;
-  FSet& u = g->sets[0];
-  u.d_off = base;
-  u.d_m = base + unit_at;
-  u.d_t = base + unit_at + 1;
-  for (int i = 0; i < g->n_ops; ++i) {
-    FSet& s = g->sets[g->op_set[i]];
-    s.d_off = base;
-    s.d_m = base + op_at[i];
-    s.d_t = base + op_at[i] + g->K[i];
-  }
-  for (int e = 0; e < g->n_orig_edges; ++e) {
-    FSet& s = g->sets[g->edges[e].set];
-    int64_t n = (int64_t)g->K[g->edges[e].src] * g->K[g->edges[e].dst];
-    s.d_off = base;
-    s.d_m = base + e_at[e];
-    s.d_t = base + e_at[e] + n;
-  }
+  CU(cudaMemcpyAsync(base + g->c_opm, a.data(), sizeof(int64_t) * a.size(), cudaMemcpyHostToDevice, g->stream), "upload");
+  CU(cudaMemcpyAsync(base + g->c_opt, b.data(), sizeof(int64_t) * b.size(), cudaMemcpyHostToDevice, g->stream), "upload");
+  CU(cudaMemcpyAsync(base + g->c_em, c.data(), sizeof(int64_t) * c.size(), cudaMemcpyHostToDevice, g->stream), "upload");
+  CU(cudaMemcpyAsync(base + g->c_et, d.data(), sizeof(int64_t) * d.size(), cudaMemcpyHostToDevice, g->stream), "upload");
+  CU(cudaStreamSynchronize(g->stream), "upload costs");
+  g->host_costs_pending = false;
   g->started = true;
   return FT_OK;
 }
@@ -1030,6 +1068,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
   unit.off = {0, 1};
   g->sets.push_back(unit);
   for (int i = 0; i < n_ops; ++i) {
+    g->op_set0.push_back((int)g->sets.size());
     FSet s;
     s.kind = S_OP;
     s.a_op = i;
@@ -1127,6 +1166,7 @@ int ft_set_op_costs(ft_graph* g, int32_t op, const int64_t* m, const int64_t* t)
   if (g->poisoned) return g->poisoned;
   if (g->started) return setf(g, FT_ESTATE, "costs set after elimination began");
   if (op < 0 || op >= g->n_ops || !m || !t) return setf(g, FT_EINVAL, "bad operator or null costs");
+  if (g->bulk_done) return setf(g, FT_ESTATE, "costs already set by ft_set_costs_all");
   const int k = g->K[op];
   for (int q = 0; q < k; ++q) {
     if (m[q] < 0 || t[q] < 0) return setf(g, FT_EINVAL, "negative cost");
@@ -1135,6 +1175,7 @@ int ft_set_op_costs(ft_graph* g, int32_t op, const int64_t* m, const int64_t* t)
   g->op_m[op].assign(m, m + k);
   g->op_t[op].assign(t, t + k);
   g->op_ok[op] = 1;
+  g->host_costs_pending = true;
   return FT_OK;
 }
 
@@ -1143,6 +1184,7 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
   if (g->poisoned) return g->poisoned;
   if (g->started) return setf(g, FT_ESTATE, "costs set after elimination began");
   if (edge < 0 || edge >= g->n_orig_edges || !t) return setf(g, FT_EINVAL, "bad edge or null costs");
+  if (g->bulk_done) return setf(g, FT_ESTATE, "costs already set by ft_set_costs_all");
   const int64_t n = (int64_t)g->K[g->edges[edge].src] * g->K[g->edges[edge].dst];
   for (int64_t q = 0; q < n; ++q) {
     const int64_t mm = m ? m[q] : 0;
@@ -1156,6 +1198,42 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
     if (g->e_m[edge][q] != 0) g->e_mzero[edge] = 0;
   g->e_t[edge].assign(t, t + n);
   g->e_ok[edge] = 1;
+  g->host_costs_pending = true;
+  return FT_OK;
+}
+
+int ft_set_costs_all(ft_graph* g, const int64_t* op_m, const int64_t* op_t, const int64_t* edge_m,
+                     const int64_t* edge_t) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (g->started) return setf(g, FT_ESTATE, "costs set after elimination began");
+  if (!op_m || !op_t || (g->n_orig_edges > 0 && !edge_t)) return setf(g, FT_EINVAL, "null cost array");
+  if (g->host_costs_pending || g->bulk_done)
+    return setf(g, FT_ESTATE, "ft_set_costs_all must be the only cost setter");
+  int rc = alloc_costs(g);
+  if (rc) return rc;
+  const int64_t nop = g->op_off[g->n_ops], ned = g->e_off[g->n_orig_edges];
+  int64_t* base = g->d_costs;
+  CU(cudaMemcpyAsync(base + g->c_opm, op_m, sizeof(int64_t) * nop, cudaMemcpyHostToDevice, g->stream), "upload");
+  CU(cudaMemcpyAsync(base + g->c_opt, op_t, sizeof(int64_t) * nop, cudaMemcpyHostToDevice, g->stream), "upload");
+  if (edge_m)
+    CU(cudaMemcpyAsync(base + g->c_em, edge_m, sizeof(int64_t) * ned, cudaMemcpyHostToDevice, g->stream), "upload");
+  else
+    CU(cudaMemsetAsync(base + g->c_em, 0, sizeof(int64_t) * ned, g->stream), "upload");
+  CU(cudaMemcpyAsync(base + g->c_et, edge_t, sizeof(int64_t) * ned, cudaMemcpyHostToDevice, g->stream), "upload");
+  // validation on the device: R10 bounds, and which edges carry m = 0 (Eq. 2)
+  int32_t status = 0;
+  std::vector<char> mz(g->n_orig_edges, 1);
+  CU(ftk::validate_costs(base + g->c_opm, 2 * nop + 2 * ned, base + g->c_em, g->e_off, g->n_orig_edges,
+                         &status, mz.data(), g->stream), "validate costs");
+  if (status & 1) return setf(g, FT_EINVAL, "negative cost");
+  if (status & 2) return setf(g, FT_EOVERFLOW, "cost >= 2^40");
+  for (int i = 0; i < g->n_ops; ++i) g->op_ok[i] = 1;
+  for (int e = 0; e < g->n_orig_edges; ++e) {
+    g->e_ok[e] = 1;
+    g->e_mzero[e] = mz[e];
+  }
+  g->bulk_done = true;
   return FT_OK;
 }
 

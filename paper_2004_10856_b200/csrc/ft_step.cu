@@ -1286,6 +1286,57 @@ __global__ void k_wave_off(BatchDev B, const int64_t* cnt, const int64_t* seg_tu
   atomicAdd((unsigned long long*)&step_arr[3 * j + 2], (unsigned long long)seg_tuples[gs]);
 }
 
+static int grid_for(int64_t n, int nt, int maxg);
+
+// ---------------------------------------------------------------------------
+// Cost validation for ft_set_costs_all (R10 bounds; edges with m = 0).
+
+__global__ void k_validate(const int64_t* d, int64_t n, int32_t* status) {
+  int bits = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = d[i];
+    if (v < 0) bits |= 1;
+    if (v >= ((int64_t)1 << 40)) bits |= 2;
+  }
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(status, bits);
+}
+
+__global__ void k_edge_mzero(const int64_t* em, const int64_t* e_off, int ne, char* mz) {
+  for (int e = blockIdx.x; e < ne; e += gridDim.x) {
+    int nz = 0;
+    for (int64_t i = e_off[e] + threadIdx.x; i < e_off[e + 1]; i += blockDim.x) nz |= em[i] != 0;
+    nz = __syncthreads_or(nz);
+    if (threadIdx.x == 0) mz[e] = nz ? 0 : 1;
+  }
+}
+
+cudaError_t validate_costs(const int64_t* d, int64_t n, const int64_t* em,
+                           const std::vector<int64_t>& e_off, int ne, int32_t* status_host,
+                           char* mz_host, cudaStream_t st) {
+  int32_t* dstat = nullptr;
+  int64_t* doff = nullptr;
+  char* dmz = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dstat, sizeof(int32_t) + 16, st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(dstat, 0, sizeof(int32_t), st);
+  if (n > 0) k_validate<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(d, n, dstat);
+  if (ne > 0) {
+    if ((e = cudaMallocAsync((void**)&doff, sizeof(int64_t) * (ne + 1), st)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void**)&dmz, ne, st)) != cudaSuccess) return e;
+    cudaMemcpyAsync(doff, e_off.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice, st);
+    k_edge_mzero<<<std::min(ne, 148 * 8), 128, 0, st>>>(em, doff, ne, dmz);
+    cudaMemcpyAsync(mz_host, dmz, ne, cudaMemcpyDeviceToHost, st);
+  }
+  cudaMemcpyAsync(status_host, dstat, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dstat, st);
+  if (doff) cudaFreeAsync(doff, st);
+  if (dmz) cudaFreeAsync(dmz, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Host side
 
@@ -1343,7 +1394,7 @@ void StepRunner::release() {
   ev0 = ev1 = nullptr;
 }
 
-static int grid_for(int64_t n, int nt, int maxg = 148 * 16) {
+static int grid_for(int64_t n, int nt, int maxg) {
   int64_t g = (n + nt - 1) / nt;
   if (g < 1) g = 1;
   if (g > maxg) g = maxg;

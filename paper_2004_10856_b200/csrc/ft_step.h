@@ -40,6 +40,12 @@ struct NodeGroup {
 };
 using NodeGroupH = NodeGroup;
 
+// Validates costs on the device (bit 0: negative, bit 1: >= 2^40) and reports
+// per edge whether its memory costs are all zero.
+cudaError_t validate_costs(const int64_t* d, int64_t n, const int64_t* em,
+                           const std::vector<int64_t>& e_off, int ne, int32_t* status_host,
+                           char* mz_host, cudaStream_t st);
+
 class StepRunner {
  public:
   StepRunner();

@@ -127,3 +127,31 @@ def test_shared_path_ab(ft, monkeypatch):
     for s in range(len(a.stats())):
         for x, y in zip(a.step_output(s), b.step_output(s)):
             assert np.array_equal(x, y), s
+
+
+def test_bulk_vs_per_op_setters(ft):
+    """ft_set_costs_all (device-validated bulk upload) == per-op/per-edge setters."""
+    w = G.c3()
+    a = ft.load(w, bulk=True)
+    a.eliminate()
+    b = ft.load(w, bulk=False)
+    b.eliminate()
+    for x, y in zip(a.frontier(), b.frontier()):
+        assert np.array_equal(x, y)
+
+
+def test_bulk_validation_errors(ft):
+    w = G.c1(0)
+    op_m, op_t, em, et = ft.concat_costs(w)
+    for bad, code in (((-1), ft.EINVAL), ((1 << 40), ft.EOVERFLOW)):
+        g = ft.Graph(w.n_cfgs, w.src, w.dst)
+        et2 = et.copy()
+        et2[3] = bad
+        with pytest.raises(ft.FTError) as e:
+            g.set_costs_all(op_m, op_t, em, et2)
+        assert e.value.code == code
+    g = ft.Graph(w.n_cfgs, w.src, w.dst)
+    g.set_costs_all(op_m, op_t, em, et)
+    with pytest.raises(ft.FTError) as e:
+        g.set_op_costs(0, w.op_m[0], w.op_t[0])
+    assert e.value.code == ft.ESTATE

@@ -1149,6 +1149,10 @@ void ft_graph_destroy(ft_graph* g) {
             "[libft host ms] waves=%lld plan+desc %.2f pipeline %.2f offsets/alloc %.2f gather+sync %.2f "
             "bookkeeping %.2f wave-assign %.2f policy %.2f\n",
             (long long)g->nwaves, g->hp[0], g->hp[1], g->hp[2], g->hp[3], g->hp[4], g->hp[5], g->hp[6]);
+  if (getenv("FT_FILTER_STATS") && g->runner)
+    fprintf(stderr, "[libft filter] items %llu chunk_tests %llu skipped_elems %llu tested_elems %llu\n",
+            g->runner->fstat_acc[0], g->runner->fstat_acc[1], g->runner->fstat_acc[2],
+            g->runner->fstat_acc[3]);
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {
     if (w.m) cudaFree(w.m);

@@ -88,6 +88,9 @@ struct StepHdr {
   unsigned long long out_total[LMAX + 1];     // level outputs
   unsigned long long bucket_total[LMAX + 1];  // buckets per level
   unsigned long long huge;                    // buckets sorted by the global-memory path
+  unsigned long long fstat[4];                // filter work counters (FT_FILTER_STATS): work
+                                              // items, chunk tests, skipped chunks' elements,
+                                              // elements tested one by one
 };
 
 // Per-level pool of per-segment results (G of the next finer level, or the
@@ -106,6 +109,7 @@ struct LevelDev {
   int level;
   int st;      // log2 of the sample stride
   int run_item;  // filter work-item length (sampled run elements)
+  int fstats;    // collect filter work counters
   const int32_t* seg_d;
   const int32_t* seg_n;  // sample size at the direct level
   const int64_t* blk_rel;

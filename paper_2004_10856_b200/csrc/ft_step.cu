@@ -864,7 +864,9 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     // q: #G points with m < m of the current chunk start (galloping lower bound)
     int64_t q = 0;
     int64_t jj = j0;
+    unsigned long long c_tests = 0, c_skip = 0, c_elem = 0;
     while (jj < j1) {
+      ++c_tests;
       const int64_t je = min(jj + CHUNK, j1);
       const int64_t mf = ms + __ldg(Lm + samp_idx(jj, nL, sh));
       const int64_t tl = ts + __ldg(Lt + samp_idx(je - 1, nL, sh));
@@ -894,9 +896,11 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
           if (ts + __ldg(Lt + samp_idx(mid, nL, sh)) >= tg) a0 = mid + 1;
           else a1 = mid;
         }
+        c_skip += a0 - jj;
         jj = a0;
         continue;
       }
+      c_elem += je - jj;
       // element-level test of the chunk: p = #G points with m <= m_x
       int64_t p = q;
       for (int64_t j = jj; j < je; ++j) {
@@ -927,6 +931,12 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
         }
       }
       jj = je;
+    }
+    if (L.fstats) {
+      atomicAdd(&L.hdr->fstat[0], 1ull);
+      atomicAdd(&L.hdr->fstat[1], c_tests);
+      atomicAdd(&L.hdr->fstat[2], c_skip);
+      atomicAdd(&L.hdr->fstat[3], c_elem);
     }
   }
 }
@@ -1548,6 +1558,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       std::memset(&L, 0, sizeof(L));
       L.level = l;
       L.st = slog * l;
+      L.fstats = fstats;
       {  // ~2 work items per resident thread (148 SMs x 2048 threads) at this level
         const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
         int64_t ri = tot / (int64_t)(148 * 2048 * 2);
@@ -1667,6 +1678,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       res->pool = pools[0];
       res->candidates = 0;
       for (int l = 0; l < D; ++l) res->candidates += (int64_t)hdr_host->cand_total[l];
+      if (fstats) {
+        fstat_acc[0] += hdr_host->fstat[0];
+        fstat_acc[1] += hdr_host->fstat[1];
+        fstat_acc[2] += hdr_host->fstat[2];
+        fstat_acc[3] += hdr_host->fstat[3];
+      }
       res->filter_tuples = res->direct_tuples = 0;
       for (int l = 0; l <= D; ++l) {
         res->filter_tuples += (int64_t)plan_copy[LMAX + 1 + l];
@@ -1732,6 +1749,7 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 }
 
 cudaError_t StepRunner::configure() {
+  fstats = getenv("FT_FILTER_STATS") != nullptr;
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_node_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)NS_SMEM);

@@ -64,6 +64,8 @@ class StepRunner {
 
   int slog = 3;                       // sample stride 8
   int cdirect = C_DIRECT;             // direct-path capacity
+  int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
+  unsigned long long fstat_acc[4] = {0, 0, 0, 0};
   bool profile = false;               // events between kernel groups
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
   int64_t out_budget = 1 << 20;

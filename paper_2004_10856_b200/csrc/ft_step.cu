@@ -812,8 +812,28 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
   const int64_t W = L.wo[nbl];
   const int sh = L.st;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gstride) {
-    int64_t lo = 0, hi = nbl;  // block: largest beta with wo[beta] <= w
+  const int lane = threadIdx.x & 31;
+  for (int64_t wbase = (int64_t)blockIdx.x * blockDim.x; wbase < W; wbase += gstride) {
+    const int64_t w0 = wbase + (threadIdx.x & ~31);  // first item of this warp
+    if (w0 >= W) break;
+    // blocks of the warp's first and last items (two full binary searches per
+    // warp), then a bounded binary search per lane
+    int64_t lo = 0;
+    if (lane == 0 || lane == 31) {
+      const int64_t x = lane == 0 ? w0 : min(w0 + 31, W - 1);
+      int64_t hi = nbl;  // largest beta with wo[beta] <= x
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (L.wo[mid] <= x) lo = mid;
+        else hi = mid;
+      }
+    }
+    const int64_t blo = __shfl_sync(0xffffffffu, lo, 0);
+    const int64_t bhi = __shfl_sync(0xffffffffu, lo, 31);
+    const int64_t w = w0 + lane;
+    if (w >= W) continue;
+    lo = blo;
+    int64_t hi = bhi + 1;  // wo[lo] <= w < wo[hi]
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
       if (L.wo[mid] <= w) lo = mid;
@@ -843,8 +863,20 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     const int64_t cB = fb == 2 ? c[2] : c[1];
     const int64_t RI = L.run_item;
     const int64_t nch = (cL + RI - 1) / RI;
-    const int64_t run = wl / nch, ch = wl - run * nch;
-    const int64_t ja = run / cB, jb = run - ja * cB;
+    int64_t run, ch, ja, jb;
+    if (((wl | nch | cB) >> 31) == 0) {  // 32-bit division fast path
+      const unsigned r32 = (unsigned)wl / (unsigned)nch;
+      run = r32;
+      ch = wl - (int64_t)r32 * nch;
+      const unsigned a32 = r32 / (unsigned)cB;
+      ja = a32;
+      jb = run - (int64_t)a32 * cB;
+    } else {
+      run = wl / nch;
+      ch = wl - run * nch;
+      ja = run / cB;
+      jb = run - ja * cB;
+    }
     const int64_t ia = samp_idx(ja, nA, sh), ib = samp_idx(jb, nB, sh);
     const int64_t* Am = fa == 0 ? fm[0] : fm[1];
     const int64_t* At = fa == 0 ? ft[0] : ft[1];
@@ -1559,10 +1591,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       L.level = l;
       L.st = slog * l;
       L.fstats = fstats;
-      {  // ~2 work items per resident thread (148 SMs x 2048 threads) at this level
+      {  // ~item_div work items per resident thread (148 SMs x 2048 threads)
         const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
-        int64_t ri = tot / (int64_t)(148 * 2048 * 2);
-        ri = std::max<int64_t>(CHUNK, std::min<int64_t>(512, ri));
+        int64_t ri = tot / (int64_t)(148 * 2048) / item_div;
+        ri = std::max<int64_t>(CHUNK, std::min<int64_t>(item_max, ri));
         L.run_item = (int)((ri + CHUNK - 1) / CHUNK * CHUNK);
       }
       L.seg_d = (const int32_t*)seg_d.p;
@@ -1617,7 +1649,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         cudaMemsetAsync(L.cand_cursor, 0, sizeof(unsigned long long), st);
         k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
         scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
-        k_filter<<<148 * 8, 256, 0, st>>>(s, L);
+        k_filter<<<filter_grid, 256, 0, st>>>(s, L);
         k_check_cand<<<1, 1, 0, st>>>(L);
         k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
@@ -1750,6 +1782,9 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
+  if (const char* e = getenv("FT_FILTER_GRID")) filter_grid = std::max(148, atoi(e));
+  if (const char* e = getenv("FT_ITEM_MAX")) item_max = std::max(16, atoi(e));
+  if (const char* e = getenv("FT_ITEM_DIV")) item_div = std::max(1, atoi(e));
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_node_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)NS_SMEM);

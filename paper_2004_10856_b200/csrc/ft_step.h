@@ -65,6 +65,9 @@ class StepRunner {
   int slog = 3;                       // sample stride 8
   int cdirect = C_DIRECT;             // direct-path capacity
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
+  int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
+  int item_max = 512;                 // filter work item: max sampled run elements
+  int item_div = 4;                   // ... and target items per resident thread
   unsigned long long fstat_acc[4] = {0, 0, 0, 0};
   bool profile = false;               // events between kernel groups
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)

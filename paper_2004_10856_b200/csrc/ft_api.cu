@@ -1153,6 +1153,12 @@ void ft_graph_destroy(ft_graph* g) {
     fprintf(stderr, "[libft filter] items %llu chunk_tests %llu skipped_elems %llu tested_elems %llu\n",
             g->runner->fstat_acc[0], g->runner->fstat_acc[1], g->runner->fstat_acc[2],
             g->runner->fstat_acc[3]);
+  if (getenv("FT_FILTER_STATS") && g->runner) {
+    fprintf(stderr, "[libft buckets] size-class: count/candidates 1 | 2-4 | 5-8 | 9-16 | 17-32 | 33-64 | 65-128 | 129-256 | <=4096 | >4096\n ");
+    for (int q = 0; q < 10; ++q)
+      fprintf(stderr, " %llu/%llu", g->runner->bstat_acc[0][q], g->runner->bstat_acc[1][q]);
+    fprintf(stderr, "\n");
+  }
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {
     if (w.m) cudaFree(w.m);

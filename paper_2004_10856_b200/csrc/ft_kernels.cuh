@@ -70,7 +70,8 @@ struct BatchDev {
   const int64_t* seg_base;  // [nsteps+1]
   const int64_t* blk_base;  // [nsteps+1]
   int nsteps;
-  int slog;                 // sample stride at level l = 2^(slog*l)
+  int slog;                 // sample stride at level l >= 1: 2^(slog0 + slog*(l-1))
+  int slog0;
   int cdirect;              // direct-path capacity (<= C_DIRECT)
   int64_t nseg;             // local segments over all steps
   int64_t nblk;             // local blocks over all steps
@@ -88,6 +89,7 @@ struct StepHdr {
   unsigned long long out_total[LMAX + 1];     // level outputs
   unsigned long long bucket_total[LMAX + 1];  // buckets per level
   unsigned long long huge;                    // buckets sorted by the global-memory path
+  unsigned long long bstat[2][10];            // bucket count / candidates by size class (stats)
   unsigned long long fstat[4];                // filter work counters (FT_FILTER_STATS): work
                                               // items, chunk tests, skipped chunks' elements,
                                               // elements tested one by one
@@ -213,6 +215,11 @@ __device__ __forceinline__ Blk load_blk(const StepDev& s, int64_t sg, int64_t k)
   b.o[2] = s.Z.off[sz];
   b.n[2] = s.Z.off[sz + 1] - b.o[2];
   return b;
+}
+
+// log2 of the sample stride of level l (level 0 = everything).
+__host__ __device__ __forceinline__ int level_shift(int l, int slog0, int slog) {
+  return l == 0 ? 0 : slog0 + slog * (l - 1);
 }
 
 // Sampled index set at stride st = 2^sh: {0, st, 2st, ...} U {n-1}.

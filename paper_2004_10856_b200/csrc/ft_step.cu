@@ -147,7 +147,7 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int3
   unsigned long long samp = (unsigned long long)rel;
   for (int l = 0; l <= LMAX; ++l) {
     if (l > 0) {
-      const int sh = B.slog * l;
+      const int sh = level_shift(l, B.slog0, B.slog);
       unsigned long long loc = 0;
       for (int64_t k = lane; k < s.nblk; k += 32) {
         const Blk b = load_blk(s, sg, k);
@@ -1069,6 +1069,12 @@ __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L
   for (int64_t bkt = (int64_t)blockIdx.x * 8 + wid; bkt < B; bkt += nw) {
     const int64_t c = L.bcount[bkt];
     if (c == 0) continue;
+    if (L.fstats && lane == 0) {
+      const int cls = c == 1 ? 0 : c <= 4 ? 1 : c <= 8 ? 2 : c <= 16 ? 3 : c <= 32 ? 4 : c <= 64 ? 5
+                      : c <= 128 ? 6 : c <= 256 ? 7 : c <= 4096 ? 8 : 9;
+      atomicAdd(&L.hdr->bstat[0][cls], 1ull);
+      atomicAdd(&L.hdr->bstat[1][cls], (unsigned long long)c);
+    }
     if (c > WARP_DIRECT) {
       if (lane == 0) L.large_list[atomicAdd(L.large_n, 1ull)] = bkt;
       continue;
@@ -1494,6 +1500,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   s.blk_base = (const int64_t*)base_dev.p + nsteps + 1;
   s.nsteps = nsteps;
   s.slog = slog;
+  s.slog0 = slog0;
   s.cdirect = cdirect;
   s.nseg = nloc;
   s.nblk = nbl;
@@ -1589,7 +1596,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       LevelDev L;
       std::memset(&L, 0, sizeof(L));
       L.level = l;
-      L.st = slog * l;
+      L.st = level_shift(l, slog0, slog);
       L.fstats = fstats;
       {  // ~item_div work items per resident thread (148 SMs x 2048 threads)
         const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
@@ -1711,6 +1718,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       res->candidates = 0;
       for (int l = 0; l < D; ++l) res->candidates += (int64_t)hdr_host->cand_total[l];
       if (fstats) {
+        for (int q = 0; q < 10; ++q) {
+          bstat_acc[0][q] += hdr_host->bstat[0][q];
+          bstat_acc[1][q] += hdr_host->bstat[1][q];
+        }
         fstat_acc[0] += hdr_host->fstat[0];
         fstat_acc[1] += hdr_host->fstat[1];
         fstat_acc[2] += hdr_host->fstat[2];
@@ -1791,6 +1802,7 @@ cudaError_t StepRunner::configure() {
     if (e0 != cudaSuccess) return e0;
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
+  if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(64, std::min(C_DIRECT, atoi(e)));
   const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
   cudaError_t e = cudaFuncSetAttribute(k_bucket_large, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -62,13 +62,15 @@ class StepRunner {
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
 
-  int slog = 3;                       // sample stride 8
+  int slog = 4;                       // sample stride x16 per level beyond level 1
+  int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
   int cdirect = C_DIRECT;             // direct-path capacity
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int item_max = 512;                 // filter work item: max sampled run elements
   int item_div = 4;                   // ... and target items per resident thread
   unsigned long long fstat_acc[4] = {0, 0, 0, 0};
+  unsigned long long bstat_acc[2][10] = {};
   bool profile = false;               // events between kernel groups
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
   int64_t out_budget = 1 << 20;

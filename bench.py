@@ -118,7 +118,7 @@ def cpu_sample_workload(name, seconds):
     C5 -> the same generator with fewer ops; C1-C3 -> the full graph."""
     from synth import graphs as G
     if name == "C4":
-        layers = max(1, min(24, int(round(seconds / 2.5))))
+        layers = max(1, min(24, int(round(seconds * 0.6))))
         return G.c4(layers=layers), f"C4 BERT-large cost model, {layers} of 24 encoder layers"
     if name == "C5":
         n = max(100, min(2000, int(seconds * 25)))
@@ -316,162 +316,6 @@ def main():
             "yardstick": ("40 B/tuple = SURVEY 8(d) materialised expand->sort->scan->compact cost; the "
                           "pruned kernel moves far fewer DRAM bytes (ncu traffic in profiles/), so "
                           "frac > 1 means faster than that design's HBM ceiling")}
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "impl": "reference", "config": cfg,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": sample + f"; {tuples} product tuples per step"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-# ---------------------------------------------------------------- our arm
-
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    import numpy as np
-    import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    comm = None
-    import paper_2004_10856_b200 as ft
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(ft.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        comm = ft.nccl_comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()), local)
-    w, cfg = workload_config(args.workload)
-    cfg.update({"graphs_per_step": 1, "parallelism": f"config-pair sharding x{world} + NCCL all-gather",
-                "l2_flush": not args.no_flush})
-    stream = torch.cuda.current_stream()
-    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
-
-    def flush():
-        if not args.no_flush:
-            flush_buf.zero_()
-
-    def search(profile, keep=None):
-        g = ft.load(w, profile=profile, **kw)
-        g.prepare()
-        return g
-
-    # warm-up (module load, scratch growth, NCCL)
-    for _ in range(args.warmup):
-        g = search(False)
-        g.eliminate()
-        g.frontier()
-        g.close()
-    torch.cuda.synchronize()
-
-    # timed region: inputs resident in HBM (ft_prepare before the events)
-    clk = ClockSampler(local)
-    clk.start()
-    ev_ms, stats_all, nfront = [], [], 0
-    for _ in range(args.steps):
-        g = search(True)
-        flush()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        g.eliminate()
-        m, t = g.frontier()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        ev_ms.append(e0.elapsed_time(e1))
-        stats_all.append(g.stats())
-        nfront = len(m)
-        g.close()
-    clocks = clk.stop()
-    total_ms = sum(ev_ms)
-    st = stats_all[-1]
-    local_tuples = sum(s["tuples"] for s in st)
-    launches = sum(s["launches"] for s in st)
-    groups = {k: sum(s[k + "_ms"] for s in st) for k in ("plan", "direct", "filter", "bucket", "compact")}
-    # ft_step_stats.tuples already counts every rank's segments (the per-segment
-    # counts are all-gathered with the survivors), so this is the whole job
-    tuples = local_tuples
-    if dist is not None:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    ms_per_step = total_ms / args.steps
-    value = tuples / (ms_per_step / 1e3)
-
-    # end-to-end through the public API with host buffers: the step's inputs
-    # (concatenated Eq. 1 / Eq. 2 cost tables) sit in pinned host memory; the
-    # timed region creates the graph, copies the costs H2D (ft_set_costs_all),
-    # runs the search and reads the frontier back (D2H).
-    e2e_ms = []
-    pinned = []
-    for a in ft.concat_costs(w):
-        if a is None:
-            pinned.append(None)
-            continue
-        pt = torch.empty(len(a), dtype=torch.int64, pin_memory=True)
-        pt.numpy()[:] = a
-        pinned.append(pt.numpy())
-    h2d = sum(a.nbytes for a in pinned if a is not None)
-    d2h = 0
-    for _ in range(args.steps):
-        flush()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        g = ft.load(w, costs=pinned, **kw)
-        g.eliminate()
-        m, t = g.frontier()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms.append(e0.elapsed_time(e1))
-        d2h = m.nbytes + t.nbytes
-        g.close()
-    e2e_tot = sum(e2e_ms)
-    if dist is not None:
-        tt = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_tot = float(tt.item())
-    e2e_value = tuples / (e2e_tot / args.steps / 1e3)
-
-    # roofline of the dominant kernel group
-    dom = max(groups, key=groups.get)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    filter_tuples = sum(s["tuples"] for s in st if s["levels"] > 1)
-    roof = {"kernel": f"k_{dom}", "bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-            "traffic": None}
-    # per-unit algorithmic bytes: 40 B per product tuple; units =
-    # product tuples of the steps whose kernels ran in this group
-    if dom == "filter":
-        roof["units"] = filter_tuples
-    else:
-        roof["units"] = tuples
-    roof["bytes_per_unit"] = 40
-    roof["achieved"] = roof["units"] * 40 / (groups[dom] / 1e3) / 1e9 if groups[dom] > 0 else None
-    roof["frac"] = roof["achieved"] / hbm_peak if roof["achieved"] else None
-    roof["share_of_step"] = groups[dom] / (ms_per_step) if ms_per_step else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

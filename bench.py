@@ -34,6 +34,10 @@ METRIC = "frontier tuples/sec (Product+Reduce) and FT search time per graph at 1
 UNIT = "product tuples/s"
 
 
+def print_line(line):
+    print(json.dumps(line), flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -161,7 +165,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": sample + f"; {tuples} product tuples per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print_line(line)
     return 0
 
 
@@ -169,6 +173,13 @@ def run_reference(args):
 
 def main():
     args = parse()
+    # exactly one JSON line on stdout: libraries (NCCL prints its version on
+    # init) write to fd 1 too, so everything else goes to stderr
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
+    global print_line
+    print_line = lambda line: (out.write(json.dumps(line) + "\n"), out.flush())
     if args.impl == "reference":
         return run_reference(args)
     import numpy as np
@@ -336,7 +347,7 @@ def main():
         for s in st:
             print(json.dumps(s), file=sys.stderr)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print_line(line)
     if comm is not None:
         ft.nccl_comm_destroy(comm)
     if dist is not None:

@@ -77,6 +77,7 @@ struct ft_graph {
   int rank = 0, world = 1;
   bool loopback = false;  // world > 1 simulated on one GPU (tests)
   bool no_shared = false;  // FT_NO_SHARED=1 disables the shared-order node path (A/B tests)
+  double replicate_tau = 2e6;  // waves below this estimated tuple count are replicated
   ncclComm_t comm = nullptr;
   bool keep_all = false;
   int n_ops = 0, n_orig_edges = 0;
@@ -414,32 +415,44 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   std::vector<int64_t> sbase(ns + 1, 0);
   for (int q = 0; q < ns; ++q) sbase[q + 1] = sbase[q] + g->steps[ids[q]].nseg;
   const int64_t NS = sbase[ns];
-  std::vector<int64_t> lo(g->world + 1, 0);
-  lo[g->world] = NS;
-  if (g->world > 1) {
-    // weights = product tuples per segment (exact when cheap, else uniform per step);
-    // any partition gives identical results (ids are shard-invariant, R6)
-    int64_t work = 0;
-    for (int q = 0; q < ns; ++q) work += g->steps[ids[q]].nseg * g->steps[ids[q]].nblk;
+  // Replicated small waves: below tau estimated product tuples
+  // every rank computes the whole wave (identical results, no collective).
+  // The estimate uses host-known mean segment sizes, identical on all ranks.
+  bool replicate = g->world > 1 && !g->loopback;
+  if (replicate) {
+    double est = 0;
+    auto mean_size = [&](int set) {
+      const FSet& S = g->sets[set];
+      if (S.kind != S_STEP) return 1.0;
+      return (double)g->steps[S.step].st.survivors / (double)std::max<int64_t>(S.nseg, 1);
+    };
+    for (int q = 0; q < ns; ++q) {
+      const StepRec& r = g->steps[ids[q]];
+      est += (double)r.nseg * (double)r.nblk * mean_size(r.X) * mean_size(r.Y) * mean_size(r.Z);
+    }
+    replicate = est < g->replicate_tau;
+  }
+  const int world = replicate ? 1 : g->world;
+  const int rank = replicate ? 0 : g->rank;
+  std::vector<int64_t> lo(world + 1, 0);
+  lo[world] = NS;
+  if (world > 1) {
+    // weights = estimated product tuples per segment from host-known mean
+    // segment sizes (uniform within a step); any partition gives identical
+    // results (ids are shard-invariant, R6) -- the plan only balances load
+    auto mean_sz = [&](int set) {
+      const FSet& S = g->sets[set];
+      if (S.kind != S_STEP) return 1.0;
+      return (double)g->steps[S.step].st.survivors / (double)std::max<int64_t>(S.nseg, 1);
+    };
     std::vector<int64_t> w(NS, 1);
     for (int q = 0; q < ns; ++q) {
       const StepRec& r = g->steps[ids[q]];
-      const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
-      for (int64_t sg = 0; sg < r.nseg; ++sg) {
-        int64_t tot = 0;
-        if (work <= (1 << 21)) {
-          for (int64_t k = 0; k < r.nblk; ++k) {
-            int64_t sx, sy, sz;
-            host_block_segs(r, sg, k, sx, sy, sz);
-            tot += (X.off[sx + 1] - X.off[sx]) * (Y.off[sy + 1] - Y.off[sy]) * (Z.off[sz + 1] - Z.off[sz]);
-          }
-        } else {
-          tot = r.nblk;
-        }
-        w[sbase[q] + sg] = tot;
-      }
+      const double e = (double)r.nblk * mean_sz(r.X) * mean_sz(r.Y) * mean_sz(r.Z);
+      const int64_t wi = std::max<int64_t>(1, (int64_t)std::min(e, 4e18 / (double)std::max<int64_t>(NS, 1)));
+      for (int64_t sg = 0; sg < r.nseg; ++sg) w[sbase[q] + sg] = wi;
     }
-    ft_shard_plan(NS, w.data(), g->world, lo.data());
+    ft_shard_plan(NS, w.data(), world, lo.data());
   }
   // shared-order node path eligibility (k_node_shared): Y all singletons,
   // Z an original edge with m = 0
@@ -500,18 +513,147 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   }
   return sd;
   };
+  // Multi-rank wave with the device-side exchange: per-segment
+  // counts are all-gathered on the device, every rank scans them into the
+  // same arena offsets, gathers its own contiguous arena range and broadcasts it.
+  if (world > 1 && !g->loopback) {
+    std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
+    g->runner->profile = g->profile;
+    std::vector<ftk::StepDev> sd = make_sd(lo[rank], lo[rank + 1]);
+    const std::vector<ftk::NodeGroupH> grp = make_groups(sd);
+    ftk::StepResult res;
+    const double h1 = now_ms();
+    cudaError_t ce = g->runner->run(sd, g->stream, &res, nullptr, &grp, true);
+    if (ce == cudaErrorInvalidConfiguration)
+      return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
+    if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
+    const double h2 = now_ms();
+    cudaEvent_t ca, cb;
+    cudaEventCreate(&ca);
+    cudaEventCreate(&cb);
+    cudaEventRecord(ca, g->stream);
+    WaveBuf wb;
+    int64_t *cntg = nullptr, *tupg = nullptr, *pos = nullptr, *sb = nullptr, *stats = nullptr,
+            *tmp = nullptr;
+    const int64_t nloc = lo[rank + 1] - lo[rank];
+    CU(cudaMallocAsync((void**)&cntg, sizeof(int64_t) * std::max<int64_t>(NS, 1), g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&tupg, sizeof(int64_t) * std::max<int64_t>(NS, 1), g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&pos, sizeof(int64_t) * (NS + 1), g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&sb, sizeof(int64_t) * (ns + 1), g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&stats, sizeof(int64_t) * 3 * ns, g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&tmp, sizeof(int64_t) * ftk::scan_tmp_elems(NS + 1), g->stream), "alloc");
+    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+    if (nloc > 0) {
+      CU(cudaMemcpyAsync(cntg + lo[rank], res.dev_cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice,
+                         g->stream), "counts");
+      CU(cudaMemcpyAsync(tupg + lo[rank], res.dev_tup, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice,
+                         g->stream), "counts");
+    }
+    ncclResult_t nr = ncclGroupStart();
+    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
+      const int64_t n = lo[q + 1] - lo[q];
+      if (n <= 0) continue;
+      nr = ncclBroadcast(cntg + lo[q], cntg + lo[q], n, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(tupg + lo[q], tupg + lo[q], n, ncclInt64, q, g->comm, g->stream);
+    }
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    CU(cudaMemcpyAsync(sb, sbase.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, g->stream), "sbase");
+    CU(ftk::wave_offsets(cntg, tupg, NS, ns, sb, pos, wb.off, stats, tmp, g->stream), "wave offsets");
+    std::vector<int64_t> hstat(3 * ns), posb(world + 1);
+    CU(cudaMemcpyAsync(hstat.data(), stats, sizeof(int64_t) * 3 * ns, cudaMemcpyDeviceToHost, g->stream), "stats");
+    for (int q = 0; q <= world; ++q)
+      CU(cudaMemcpyAsync(&posb[q], pos + lo[q], sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream), "pos");
+    CU(cudaStreamSynchronize(g->stream), "wave offsets");
+    std::vector<int64_t> sbeg(ns + 1, 0);
+    for (int q = 0; q < ns; ++q) sbeg[q + 1] = sbeg[q] + hstat[3 * q];
+    const int64_t total = sbeg[ns];
+    const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
+    CU(cudaMallocAsync((void**)&wb.m, nb, g->stream), "alloc frontier");
+    CU(cudaMallocAsync((void**)&wb.t, nb, g->stream), "alloc frontier");
+    CU(cudaMallocAsync((void**)&wb.bp, nb, g->stream), "alloc frontier");
+    CU(ftk::gather_range(res.pool, pos, lo[rank], lo[rank + 1], posb[rank + 1] - posb[rank], wb.m, wb.t,
+                         wb.bp, g->stream), "gather");
+    nr = ncclGroupStart();
+    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
+      const int64_t a0 = posb[q], a1 = posb[q + 1];
+      if (a1 <= a0) continue;
+      nr = ncclBroadcast(wb.m + a0, wb.m + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(wb.t + a0, wb.t + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
+      if (nr == ncclSuccess) nr = ncclBroadcast(wb.bp + a0, wb.bp + a0, a1 - a0, ncclUint64, q, g->comm, g->stream);
+    }
+    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    cudaEventRecord(cb, g->stream);
+    for (int64_t* p : {cntg, tupg, pos, sb, stats, tmp}) cudaFreeAsync(p, g->stream);
+    CU(cudaStreamSynchronize(g->stream), "wave sync");
+    float comm_ms = 0;
+    cudaEventElapsedTime(&comm_ms, ca, cb);
+    cudaEventDestroy(ca);
+    cudaEventDestroy(cb);
+    const double h4 = now_ms();
+    const int wi = (int)g->waves.size();
+    wb.live = ns;
+    g->waves.push_back(wb);
+    for (int q = 0; q < ns; ++q) {
+      StepRec& r = g->steps[ids[q]];
+      FSet& o = g->sets[r.out];
+      o.off_ok = false;
+      o.d_off = wb.off + sbase[q] + q;
+      o.d_m = wb.m + sbeg[q];
+      o.d_t = wb.t + sbeg[q];
+      o.d_bp = wb.bp + sbeg[q];
+      o.wave_buf = wi;
+      r.done = true;
+      ft_step_stats& st = r.st;
+      st.kind = r.kind;
+      st.levels = res.levels;
+      st.wave = wi;
+      st.nseg = r.nseg;
+      st.nblk = r.nblk;
+      st.tuples = hstat[3 * q + 2];
+      st.max_seg = hstat[3 * q + 1];
+      st.survivors = hstat[3 * q];
+      st.retries = res.retries;
+      if (q == 0) {
+        st.candidates = res.candidates;
+        st.filter_tuples = res.filter_tuples;
+        st.direct_tuples = res.direct_tuples;
+        st.kernel_ms = res.kernel_ms;
+        st.comm_ms = comm_ms;
+        st.launches = res.launches + 3;
+        st.plan_ms = res.plan_ms;
+        st.direct_ms = res.direct_ms;
+        st.filter_ms = res.filter_ms;
+        st.bucket_ms = res.bucket_ms;
+        st.compact_ms = res.compact_ms;
+        st.host_ms = res.host_ms;
+      }
+    }
+    for (int q = 0; q < ns; ++q) {
+      const StepRec& r = g->steps[ids[q]];
+      consume(g, r.X);
+      consume(g, r.Y);
+      consume(g, r.Z);
+    }
+    g->hp[0] += h1 - h0;
+    g->hp[1] += h2 - h1;
+    g->hp[3] += h4 - h2;
+    g->hp[4] += now_ms() - h4;
+    return FT_OK;
+  }
   // real ranks run their own range; loopback runs every virtual rank here
   std::vector<int> vr;
   if (g->loopback)
     for (int q = 0; q < g->world; ++q) vr.push_back(q);
   else
-    vr.push_back(g->rank);
+    vr.push_back(rank);
   ftk::StepResult res, agg;
   const double h1 = now_ms();
   std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
   g->runner->profile = g->profile;
-  // single rank: offsets are computed on the device straight into the arena
-  const bool devoff = g->world == 1;
+  // single rank (or replicated wave): offsets computed on the device straight into the arena
+  const bool devoff = world == 1 && !g->loopback;
   WaveBuf wb;
   if (devoff)
     CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
@@ -555,7 +697,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   float comm_ms = 0;
   const double h2 = now_ms();
   cudaEvent_t ca = nullptr, cb = nullptr;
-  if (g->world > 1 && !g->loopback) {
+  if (world > 1 && !g->loopback) {
     cudaEventCreate(&ca);
     cudaEventCreate(&cb);
     cudaEventRecord(ca, g->stream);
@@ -568,7 +710,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     }
     CU(cudaMemcpyAsync(dc, both.data(), sizeof(int64_t) * 2 * NS, cudaMemcpyHostToDevice, g->stream), "counts");
     ncclResult_t nr = ncclGroupStart();
-    for (int q = 0; q < g->world && nr == ncclSuccess; ++q)
+    for (int q = 0; q < world && nr == ncclSuccess; ++q)
       if (lo[q + 1] > lo[q])
         nr = ncclBroadcast(dc + 2 * lo[q], dc + 2 * lo[q], 2 * (lo[q + 1] - lo[q]), ncclInt64, q,
                            g->comm, g->stream);
@@ -630,7 +772,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     set_out(sv);
     CU(g->runner->gather(sv, res, g->stream), "gather");
   }
-  if (g->world > 1 && !g->loopback) {
+  if (world > 1 && !g->loopback) {
     // all-gather-v of survivors: rank q owns arena range [A(lo[q]), A(lo[q+1]))
     auto arena_pos = [&](int64_t gseg) -> int64_t {  // arena offset of global segment gseg
       int q = (int)(std::upper_bound(sbase.begin(), sbase.end(), gseg) - sbase.begin()) - 1;
@@ -638,7 +780,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       return sbeg[q] + hoff[sbase[q] + q + (gseg - sbase[q])];
     };
     ncclResult_t nr = ncclGroupStart();
-    for (int q = 0; q < g->world && nr == ncclSuccess; ++q) {
+    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
       const int64_t a0 = arena_pos(lo[q]), a1 = arena_pos(lo[q + 1]);
       if (a1 <= a0) continue;
       nr = ncclBroadcast(wb.m + a0, wb.m + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
@@ -651,7 +793,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   }
   CU(cudaStreamSynchronize(g->stream), "wave sync");
   const double h4 = now_ms();
-  if (g->world > 1 && !g->loopback) {
+  if (world > 1 && !g->loopback) {
     cudaEventElapsedTime(&comm_ms, ca, cb);
     cudaEventDestroy(ca);
     cudaEventDestroy(cb);
@@ -1115,6 +1257,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
   }
   if (opt && g->world > 1 && !g->comm && opt->loopback) g->loopback = true;
   g->no_shared = getenv("FT_NO_SHARED") != nullptr;
+  if (const char* e = getenv("FT_REPLICATE_TAU")) g->replicate_tau = atof(e);
   if (g->world > 1 && !g->loopback && (!g->comm || g->rank < 0 || g->rank >= g->world)) {
     delete g;
     return FT_EINVAL;

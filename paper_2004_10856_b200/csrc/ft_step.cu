@@ -1385,6 +1385,65 @@ cudaError_t validate_costs(const int64_t* d, int64_t n, const int64_t* em,
   return cudaGetLastError();
 }
 
+// Multi-rank exchange helpers (device offsets over the whole wave).
+__global__ void __launch_bounds__(256) k_gather_range(Pool P, const int64_t* pos, int64_t lo, int64_t hi,
+                                                      int64_t* om, int64_t* ot, uint64_t* obp) {
+  __shared__ int64_t seg_lo_s, seg_hi_s;
+  const int64_t a0 = pos[lo], a1 = pos[hi];
+  const int64_t ntiles = (a1 - a0 + 2047) / 2048;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = a0 + tile * 2048, t1 = min(t0 + 2048, a1);
+    if (threadIdx.x < 2) {
+      const int64_t x = threadIdx.x == 0 ? t0 : t1 - 1;
+      int64_t l = lo, h = hi;  // largest gs in [lo, hi) with pos[gs] <= x
+      while (h - l > 1) {
+        const int64_t mid = (l + h) >> 1;
+        if (pos[mid] <= x) l = mid;
+        else h = mid;
+      }
+      if (threadIdx.x == 0) seg_lo_s = l;
+      else seg_hi_s = l;
+    }
+    __syncthreads();
+    const int64_t slo = seg_lo_s, shi = seg_hi_s;
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      int64_t l = slo, h = shi + 1;
+      while (h - l > 1) {
+        const int64_t mid = (l + h) >> 1;
+        if (pos[mid] <= i) l = mid;
+        else h = mid;
+      }
+      const int64_t src = P.start[l - lo] + (i - pos[l]);
+      om[i] = P.m[src];
+      ot[i] = P.t[src];
+      obp[i] = P.id[src];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t wave_offsets(const int64_t* cnt, const int64_t* tup, int64_t NS, int ns,
+                         const int64_t* sbase_dev, int64_t* pos, int64_t* off, int64_t* stats,
+                         int64_t* scan_tmp, cudaStream_t st) {
+  BatchDev B{};
+  B.seg_base = sbase_dev;
+  B.nsteps = ns;
+  B.nseg = NS;
+  scan_excl<int64_t>(cnt, pos, nullptr, NS, scan_tmp, st);
+  cudaMemsetAsync(stats, 0, sizeof(int64_t) * 3 * ns, st);
+  k_wave_off<<<grid_for(NS, 256, 1 << 30), 256, 0, st>>>(B, cnt, tup, pos, off, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_range(const Pool& P, const int64_t* pos, int64_t lo, int64_t hi, int64_t nout,
+                         int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st) {
+  if (hi <= lo || nout <= 0) return cudaSuccess;
+  k_gather_range<<<grid_for(nout, 2048, 148 * 16), 256, 0, st>>>(P, pos, lo, hi, om, ot, obp);
+  return cudaGetLastError();
+}
+
+int64_t scan_tmp_elems(int64_t n) { return n / SCAN_TILE + 8; }
+
 // ---------------------------------------------------------------------------
 // Host side
 
@@ -1450,7 +1509,7 @@ static int grid_for(int64_t n, int nt, int maxg) {
 }
 
 cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
-                            int64_t* dev_off, const std::vector<NodeGroupH>* groups) {
+                            int64_t* dev_off, const std::vector<NodeGroupH>* groups, bool keep_dev) {
   int64_t nl = 0;  // kernel launches
   int pgroup[64];
   npev = 0;
@@ -1706,6 +1765,8 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       nl += 4;
       cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
       cudaMemcpyAsync(step_host_p, step_arr.p, sizeof(int64_t) * 3 * nsteps, cudaMemcpyDeviceToHost, st);
+    } else if (keep_dev) {  // multi-rank device exchange: counts stay on the device
+      cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
     } else {
       cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
       cudaMemcpyAsync(cnt_host, pools[0].cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToHost, st);
@@ -1739,6 +1800,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         res->seg_tuples = nullptr;
         res->step_stats = step_host_p;
         for (int q = 0; q < nsteps; ++q) tot += step_host_p[3 * q];
+      } else if (keep_dev) {
+        res->counts = nullptr;
+        res->seg_tuples = nullptr;
+        res->step_stats = nullptr;
+        res->dev_cnt = pools[0].cnt;
+        res->dev_tup = (const int64_t*)seg_tuples.p;
       } else {
         res->counts = cnt_host;
         res->seg_tuples = cnt_host + nloc;

@@ -23,6 +23,8 @@ struct StepResult {
   const int64_t* counts = nullptr;  // host (pinned) per-segment survivor counts [nloc]
   const int64_t* seg_tuples = nullptr;  // host (pinned) per-segment product tuples [nloc]
   const int64_t* step_stats = nullptr;  // device-offset mode: per step {survivors, max, tuples}
+  const int64_t* dev_cnt = nullptr;     // keep_dev mode: per-local-segment counts (device)
+  const int64_t* dev_tup = nullptr;     // keep_dev mode: per-local-segment tuples (device)
   Pool pool;                        // level-0 pool (device)
 };
 
@@ -39,6 +41,17 @@ struct NodeGroup {
   int64_t gs0;            // local segment index of (w, p_lo)
 };
 using NodeGroupH = NodeGroup;
+
+// Multi-rank device exchange: exclusive scan of the wave's per-segment counts
+// (step-major) into pos[0..NS], CSR offsets into `off` (arena layout) and
+// per-step {survivors, max, tuples} into stats[3*ns] (device).
+cudaError_t wave_offsets(const int64_t* cnt, const int64_t* tup, int64_t NS, int ns,
+                         const int64_t* sbase_dev, int64_t* pos, int64_t* off, int64_t* stats,
+                         int64_t* scan_tmp, cudaStream_t st);
+// Copies this rank's level-0 pool (global segments [lo, hi)) into the arena at pos.
+cudaError_t gather_range(const Pool& P, const int64_t* pos, int64_t lo, int64_t hi, int64_t nout,
+                         int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st);
+int64_t scan_tmp_elems(int64_t n);
 
 // Validates costs on the device (bit 0: negative, bit 1: >= 2^40) and reports
 // per edge whether its memory costs are all zero.
@@ -57,7 +70,8 @@ class StepRunner {
   // dev_off != nullptr (single rank): write the wave's CSR offsets on the device
   // (arena layout) and return only per-step totals in res->step_stats.
   cudaError_t run(const std::vector<StepDev>& steps, cudaStream_t st, StepResult* res,
-                  int64_t* dev_off = nullptr, const std::vector<NodeGroupH>* groups = nullptr);
+                  int64_t* dev_off = nullptr, const std::vector<NodeGroupH>* groups = nullptr,
+                  bool keep_dev = false);
   // Gathers the level-0 pool into each step's CSR output (steps[j].out_*).
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();

@@ -468,6 +468,9 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       for (int e = 0; e < g->n_orig_edges; ++e)
         if (g->edges[e].set == r.Z) zok = g->e_mzero[e] != 0;
     shared[q] = y1 && zok && !g->no_shared;
+    if (getenv("FT_DEBUG_SHARED"))
+      fprintf(stderr, "[shared] step %d kind %d nblk %lld Y.kind %d y1 %d Z.kind %d zok %d -> %d\n", ids[q],
+              r.kind, (long long)r.nblk, Y.kind, (int)y1, Z.kind, (int)zok, (int)shared[q]);
   }
   auto make_groups = [&](const std::vector<ftk::StepDev>& v) {
     std::vector<ftk::NodeGroupH> gr;

@@ -207,13 +207,15 @@ __global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_
 // one CTA: product -> bitonic sort on (m,t,id) -> Alg.1 sweep -> compaction.
 
 constexpr int DIRECT_MAXBLK = 128;  // per-block info cached in smem up to this many blocks
+static size_t direct_smem(int cap) { return (size_t)cap * (3 * 8 + 4 + 4) + 8; }
 
 __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
-  __shared__ int64_t sm[C_DIRECT];
-  __shared__ int64_t stt[C_DIRECT];
-  __shared__ uint64_t sid[C_DIRECT];
-  __shared__ int kf[C_DIRECT];
-  __shared__ int pre[C_DIRECT + 1];
+  extern __shared__ int64_t dyn_direct[];  // capacity B.cdirect (runtime)
+  int64_t* sm = dyn_direct;
+  int64_t* stt = sm + B.cdirect;
+  uint64_t* sid = (uint64_t*)(stt + B.cdirect);
+  int* kf = (int*)(sid + B.cdirect);
+  int* pre = kf + B.cdirect;  // [B.cdirect + 1]
   __shared__ int64_t bo[DIRECT_MAXBLK][3];  // factor offsets
   __shared__ int bn[DIRECT_MAXBLK][3];      // factor sizes
   __shared__ int bc[DIRECT_MAXBLK][3];      // sampled counts
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
   __shared__ int64_t s_start;
   const int st = L.st;
   for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
-    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= WARP_DIRECT) continue;
+    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= WARP_DIRECT2) continue;
     if (L.hdr->overflow) return;
     const int j = find_base(B.seg_base, B.nsteps, gs);
     const StepDev& s = B.steps[j];
@@ -471,6 +473,22 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
       L.out.id[d] = id[r];
     }
     off += __popc(bal);
+  }
+}
+
+// Segments of 257..512 tuples: R = 16 rows per warp (own kernel: more registers).
+__global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
+  __shared__ int pre_all[4][WARP_DIRECT2 + 1];
+  __shared__ Blk blk_all[4][WARP_BLK_CACHE];
+  const int wid = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * 4;
+  for (int64_t gs = (int64_t)blockIdx.x * 4 + wid; gs < B.nseg; gs += nw) {
+    if (L.seg_d[gs] != L.level) continue;
+    const int n = L.seg_n[gs];
+    if (n <= WARP_DIRECT || n > WARP_DIRECT2) continue;
+    if (L.hdr->overflow) return;
+    warp_direct_seg<16>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+    __syncwarp();
   }
 }
 
@@ -1678,7 +1696,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
             s, L, (const NodeGroup*)groups_dev.p, ngroups);
       }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
-      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, 0, st>>>(s, L);
+      k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, 0, st>>>(s, L);
+      ++nl;
+      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cdirect), st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
         L.bucket_base = (int64_t*)bucket_base.p;
@@ -1870,7 +1890,12 @@ cudaError_t StepRunner::configure() {
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
-  if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(64, std::min(C_DIRECT, atoi(e)));
+  if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(256, std::min(C_DIRECT, atoi(e)));
+  {
+    cudaError_t e0 = cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)direct_smem(C_DIRECT));
+    if (e0 != cudaSuccess) return e0;
+  }
   const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
   cudaError_t e = cudaFuncSetAttribute(k_bucket_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)lsm);

@@ -23,6 +23,8 @@ if "--target" in sys.argv:
     per = (lambda s: max(0, s["levels"] - 1)) if kern in ("k_filter", "k_bucket_small") else (lambda s: s["levels"])
     key = "filter_tuples" if kern in ("k_filter", "k_bucket_small") else "direct_tuples"
     best = max(range(len(order)), key=lambda i: order[i][key])
+    if "--wave" in sys.argv:
+        best = int(sys.argv[sys.argv.index("--wave") + 1])
     skip = sum(per(s) for s in order[:best]) + max(0, per(order[best]) - 1)
     print(f"target {kern} wave {best} {key} {order[best][key]} levels {order[best]['levels']} skip {skip}")
 print("frontier", len(m))

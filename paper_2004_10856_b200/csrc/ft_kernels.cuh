@@ -112,6 +112,7 @@ struct LevelDev {
   int level;
   int st;      // log2 of the sample stride
   int run_item;  // filter work-item length (sampled run elements)
+  int warp2;     // largest direct segment handled by the warp kernels
   int fstats;    // collect filter work counters
   const int32_t* seg_d;
   const int32_t* seg_n;  // sample size at the direct level

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
   __shared__ int64_t s_start;
   const int st = L.st;
   for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
-    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= WARP_DIRECT2) continue;
+    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= L.warp2) continue;
     if (L.hdr->overflow) return;
     const int j = find_base(B.seg_base, B.nsteps, gs);
     const StepDev& s = B.steps[j];
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
   for (int64_t gs = (int64_t)blockIdx.x * 4 + wid; gs < B.nseg; gs += nw) {
     if (L.seg_d[gs] != L.level) continue;
     const int n = L.seg_n[gs];
-    if (n <= WARP_DIRECT || n > WARP_DIRECT2) continue;
+    if (n <= WARP_DIRECT || n > L.warp2) continue;
     if (L.hdr->overflow) return;
     warp_direct_seg<16>(B, L, gs, n, pre_all[wid], blk_all[wid]);
     __syncwarp();
@@ -1674,6 +1674,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       std::memset(&L, 0, sizeof(L));
       L.level = l;
       L.st = level_shift(l, slog0, slog);
+      L.warp2 = warp16 ? WARP_DIRECT2 : WARP_DIRECT;
       L.fstats = fstats;
       {  // ~item_div work items per resident thread (148 SMs x 2048 threads)
         const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
@@ -1696,8 +1697,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
             s, L, (const NodeGroup*)groups_dev.p, ngroups);
       }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
-      k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, 0, st>>>(s, L);
-      ++nl;
+      if (warp16) {
+        k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, 0, st>>>(s, L);
+        ++nl;
+      }
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cdirect), st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
@@ -1890,6 +1893,7 @@ cudaError_t StepRunner::configure() {
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
+  if (const char* e = getenv("FT_WARP16")) warp16 = atoi(e) != 0;
   if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(256, std::min(C_DIRECT, atoi(e)));
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -79,6 +79,7 @@ class StepRunner {
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
   int cdirect = 1024;                 // direct-path capacity (<= C_DIRECT)
+  bool warp16 = false;                // 257..512-tuple direct segments on one warp (R = 16; A/B: slower)
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int item_max = 512;                 // filter work item: max sampled run elements

@@ -94,6 +94,7 @@ struct StepHdr {
   unsigned long long fstat[4];                // filter work counters (FT_FILTER_STATS): work
                                               // items, chunk tests, skipped chunks' elements,
                                               // elements tested one by one
+  unsigned long long ns_big;                  // rows handed from k_node_pack to k_node_shared
 };
 
 // Per-level pool of per-segment results (G of the next finer level, or the

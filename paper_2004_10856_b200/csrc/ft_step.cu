@@ -334,27 +334,40 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
 // Direct path for small segments (<= WARP_DIRECT tuples): one warp, R rows of
 // 32 tuples in registers (element e = r*32 + lane), bitonic sort on (m,t,id)
 // by shuffles, Alg. 1 sweep by warp scans, ballot compaction.  No barriers.
+// Stages run as runtime loops (only the R rows are unrolled): a fully
+// unrolled network for R = 1..8 inlined into every caller made the kernels
+// ~600 KB of SASS and instruction-fetch bound.
+template <int R, int JR>
+__device__ __forceinline__ void warp_bitonic_rows(int64_t (&m)[R], int64_t (&t)[R], uint64_t (&id)[R],
+                                                  int k) {
+  // partner rows r and r|JR (j = 32*JR >= 32; k >= 64 so `up` depends on r only)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r & JR) continue;
+    const int r2 = r | JR;
+    const bool up = ((r << 5) & k) == 0;
+    const bool gt = key_lt(m[r2], t[r2], id[r2], m[r], t[r], id[r]);
+    if (gt == up) {
+      int64_t a = m[r]; m[r] = m[r2]; m[r2] = a;
+      a = t[r]; t[r] = t[r2]; t[r2] = a;
+      uint64_t b = id[r]; id[r] = id[r2]; id[r2] = b;
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void warp_bitonic(int64_t (&m)[R], int64_t (&t)[R], uint64_t (&id)[R]) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
+#pragma unroll 1
   for (int k = 2; k <= R * 32; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j >= 32) {
         const int jr = j >> 5;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (r & jr) continue;
-          const int r2 = r | jr;
-          const bool up = (((r << 5) | lane) & k) == 0;
-          const bool gt = key_lt(m[r2], t[r2], id[r2], m[r], t[r], id[r]);
-          if (gt == up) {
-            int64_t a = m[r]; m[r] = m[r2]; m[r2] = a;
-            a = t[r]; t[r] = t[r2]; t[r2] = a;
-            uint64_t b = id[r]; id[r] = id[r2]; id[r2] = b;
-          }
-        }
+        if (jr == 1) warp_bitonic_rows<R, 1>(m, t, id, k);
+        else if (R >= 4 && jr == 2) warp_bitonic_rows<R, (R >= 4 ? 2 : 1)>(m, t, id, k);
+        else if (R >= 8 && jr == 4) warp_bitonic_rows<R, (R >= 8 ? 4 : 1)>(m, t, id, k);
+        else if (R >= 16) warp_bitonic_rows<R, (R >= 16 ? 8 : 1)>(m, t, id, k);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -410,6 +423,13 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
   uint64_t id[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
+    m[r] = INF;
+    t[r] = INF;
+    id[r] = ~0ull;
+  }
+  // runtime row loop (small code); the value lands in row r via static selects
+#pragma unroll 1
+  for (int r = 0; r < R && (r << 5) < n; ++r) {
     const int e = (r << 5) | lane;
     if (e < n) {
       int lo = 0, hi = nblk;
@@ -422,12 +442,17 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
       const int rr = e - wpre[lo];
       const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
       const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
+      int64_t vm, vt;
+      uint64_t vi;
       make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
-                 samp_idx(jz, b.n[2], st), m[r], t[r], id[r]);
-    } else {
-      m[r] = INF;
-      t[r] = INF;
-      id[r] = ~0ull;
+                 samp_idx(jz, b.n[2], st), vm, vt, vi);
+#pragma unroll
+      for (int q2 = 0; q2 < R; ++q2)
+        if (q2 == r) {
+          m[q2] = vm;
+          t[q2] = vt;
+          id[q2] = vi;
+        }
     }
   }
   __syncwarp();
@@ -515,13 +540,254 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
 // fixed w, every segment (w,p) holds the same tuples (k, x) with the same m and
 // id = rel_k + x; only t = t_x + t_y + t_z(k,p) depends on p.  The (m, id)
 // order is sorted once per w; if no two tuples share m it equals the
-// (m, t, id) order of every p and Alg. 1 is one sweep per p.  With m ties the
-// exact group rule below is used instead.  One CTA per (step, w).
+// (m, t, id) order of every p and Alg. 1 is one running-min sweep per p.
+//
+// k_node_pack (common case): a CTA takes a pack of up to 256/ceil32(K_j) rows
+// w of one step; each row (<= WARP_DIRECT tuples) is sorted by one warp in
+// registers, t_z(k, p) is staged once per step in shared memory and reused
+// across the CTA's packs, and one thread per (w, p) runs Alg. 1 as a
+// sequential running min, recording keep bits; survivors are then written
+// warp-cooperatively (coalesced).  Rows with equal m values, more than
+// WARP_DIRECT tuples or an oversized t_z table go to k_node_shared (one CTA per
+// row, exact group rule for ties) through a device list.
+constexpr int NP_NT = 256;
+constexpr int NP_WORDS = WARP_DIRECT / 32;
+constexpr int NP_ROWS = 8;
+constexpr int64_t NP_ZT_CAP = 8192;  // t_z table entries staged per step (64 KB)
+
+__host__ __device__ inline int np_tpr(int64_t np) { return (int)((np + 31) / 32 * 32); }
+__host__ __device__ inline size_t np_smem(int rmax, int64_t ztn) {
+  return (size_t)ztn * 8 + (size_t)rmax * (WARP_DIRECT * 20 + NS_MAXBLK * 8 + (NS_MAXBLK + 1) * 4) +
+         (size_t)NP_WORDS * NP_NT * 4;
+}
+
+template <int R>
+__device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, const int64_t* bo,
+                                            const int64_t* ym, const int64_t* yt, int nblk, int n,
+                                            int64_t* sm, int64_t* stxy, uint32_t* sidk) {
+  const int lane = threadIdx.x & 31;
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    m[r] = INF;
+    t[r] = INF;
+    id[r] = ~0ull;
+  }
+#pragma unroll 1
+  for (int r = 0; r < R && (r << 5) < n; ++r) {
+    const int e = (r << 5) | lane;
+    if (e < n) {
+      int lo = 0, hi = nblk;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      const int x = e - pre[lo];
+      const int64_t vm = __ldg(s.X.m + bo[lo] + x) + ym[lo];
+      const int64_t vt = __ldg(s.X.t + bo[lo] + x) + yt[lo];
+      // id = rel_k + x (|Y| = |Z| = 1, R6); k rides in bits 32.. (monotone in id)
+      const uint64_t vi = ((uint64_t)lo << 32) | (uint64_t)e;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == r) {
+          m[q] = vm;
+          t[q] = vt;
+          id[q] = vi;
+        }
+    }
+  }
+  warp_bitonic<R>(m, t, id);
+  bool tie = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t nm = __shfl_down_sync(0xffffffffu, m[r], 1);
+    const int64_t n0 = r + 1 < R ? __shfl_sync(0xffffffffu, m[r + 1 < R ? r + 1 : r], 0) : INF;
+    if (lane == 31) nm = n0;
+    const int e = (r << 5) | lane;
+    if (e + 1 < n && nm == m[r]) tie = true;
+    if (e < n) {
+      sm[e] = m[r];
+      stxy[e] = t[r];
+      sidk[e] = (uint32_t)(id[r] & 0xffffu) | (uint32_t)((id[r] >> 32) << 16);
+    }
+  }
+  return __any_sync(0xffffffffu, tie);
+}
+
+__global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, const NodeGroup* packs,
+                                                     int npacks, int rmax, int64_t ztn,
+                                                     NodeGroup* big) {
+  extern __shared__ int64_t dyn_np[];
+  int64_t* ztab = dyn_np;                                        // [ztn] t_z(k, p) at k*tpr+pl
+  int64_t* sm = ztab + ztn;                                      // [rmax][WARP_DIRECT]
+  int64_t* stxy = sm + (size_t)rmax * WARP_DIRECT;               // [rmax][WARP_DIRECT]
+  int64_t* bo = stxy + (size_t)rmax * WARP_DIRECT;               // [rmax][NS_MAXBLK]
+  uint32_t* sidk = (uint32_t*)(bo + (size_t)rmax * NS_MAXBLK);   // [rmax][WARP_DIRECT]
+  int* pre = (int*)(sidk + (size_t)rmax * WARP_DIRECT);          // [rmax][NS_MAXBLK + 1]
+  uint32_t* kbits = (uint32_t*)(pre + (size_t)rmax * (NS_MAXBLK + 1));  // [NP_WORDS][NP_NT]
+  __shared__ int64_t ym[NS_MAXBLK], yt[NS_MAXBLK];
+  __shared__ int soff[NP_NT];
+  __shared__ int row_n[NP_ROWS];
+  __shared__ long long sh[33];
+  __shared__ int64_t s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p0 = (int)((int64_t)npacks * blockIdx.x / gridDim.x);
+  const int p1 = (int)((int64_t)npacks * (blockIdx.x + 1) / gridDim.x);
+  int cur = -1;
+  for (int pi = p0; pi < p1; ++pi) {
+    if (L.hdr->overflow) return;
+    const NodeGroup P = packs[pi];
+    const StepDev& s = B.steps[P.step];
+    const int nblk = (int)s.nblk;
+    const int64_t np = P.p_hi - P.p_lo;
+    const int tpr = np_tpr(np);
+    const int nw = P.pad;
+    const bool fits = np <= NP_NT && (int64_t)nblk * tpr <= ztn && nw <= rmax;
+    if (P.step != cur && fits) {  // per-step tables: t_z(k, p) and Y = F(o_i, k)
+      for (int64_t q = threadIdx.x; q < (int64_t)nblk * tpr; q += NP_NT) {
+        const int k = (int)(q / tpr), pl = (int)(q - (int64_t)k * tpr);
+        ztab[q] = pl < np ? s.Z.t[s.Z.off[(int64_t)k * s.KC + P.p_lo + pl]] : 0;
+      }
+      for (int k = threadIdx.x; k < nblk; k += NP_NT) {
+        const int64_t oy = s.Y.off[k];
+        ym[k] = s.Y.m[oy];
+        yt[k] = s.Y.t[oy];
+      }
+      cur = P.step;
+    }
+    __syncthreads();
+    // one warp per row: block prefix, register sort, tie check
+    for (int r = wid; r < nw; r += NP_NT / 32) {
+      const int64_t gsr = P.gs0 + (int64_t)r * np;
+      int n = 0;
+      if (L.seg_d[gsr] == SPECIAL_LEVEL) {
+        n = L.seg_n[gsr];
+        bool ok = fits && n <= WARP_DIRECT;
+        if (ok) {
+          int* pr = pre + r * (NS_MAXBLK + 1);
+          int64_t* b = bo + r * NS_MAXBLK;
+          int run = 0;
+          for (int k0 = 0; k0 < nblk; k0 += 32) {
+            const int k = k0 + lane;
+            int c = 0;
+            if (k < nblk) {
+              const int64_t sx = (P.w + r) * s.KB + k;
+              const int64_t o = s.X.off[sx];
+              b[k] = o;
+              c = (int)(s.X.off[sx + 1] - o);
+            }
+            const int inc = warp_incl_sum<int>(c);
+            if (k < nblk) pr[k + 1] = run + inc;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+          }
+          if (lane == 0) pr[0] = 0;
+          __syncwarp();
+          int64_t* rm = sm + r * WARP_DIRECT;
+          int64_t* rt = stxy + r * WARP_DIRECT;
+          uint32_t* ri = sidk + r * WARP_DIRECT;
+          bool tie;
+          if (n <= 32) tie = np_row_sort<1>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
+          else if (n <= 64) tie = np_row_sort<2>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
+          else if (n <= 128) tie = np_row_sort<4>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
+          else tie = np_row_sort<8>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
+          ok = !tie;
+        }
+        if (!ok) {  // exact tie rule / large rows: one CTA per row in k_node_shared
+          if (lane == 0) {
+            NodeGroup G;
+            G.step = P.step;
+            G.pad = 0;
+            G.w = P.w + r;
+            G.p_lo = P.p_lo;
+            G.p_hi = P.p_hi;
+            G.gs0 = gsr;
+            big[atomicAdd(&L.hdr->ns_big, 1ull)] = G;
+          }
+          n = 0;
+        }
+      }
+      if (lane == 0) row_n[r] = n;
+    }
+    __syncthreads();
+    // Alg. 1 for segment (w, p): running min over the shared (m, id) order
+    const int r = threadIdx.x / tpr, pl = threadIdx.x - r * tpr;
+    const int n = r < nw ? row_n[r] : 0;
+    const bool act = n > 0 && pl < np;
+    int cnt = 0;
+    if (act) {
+      const int64_t* rt = stxy + r * WARP_DIRECT;
+      const uint32_t* ri = sidk + r * WARP_DIRECT;
+      long long carry = INF;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        uint32_t word = 0;
+        const int ce = min(32, n - c0);
+#pragma unroll 4
+        for (int b = 0; b < ce; ++b) {
+          const int i = c0 + b;
+          const long long t = rt[i] + ztab[(ri[i] >> 16) * tpr + pl];
+          if (t < carry) {
+            word |= 1u << b;
+            carry = t;
+          }
+        }
+        kbits[(c0 >> 5) * NP_NT + threadIdx.x] = word;
+        cnt += __popc(word);
+      }
+    }
+    long long tot;
+    const int ex = (int)block_excl_sum<NP_NT>(cnt, sh, &tot);
+    soff[threadIdx.x] = ex;
+    if (threadIdx.x == 0) {
+      int64_t base = -1;
+      const unsigned long long st0 = tot ? atomicAdd(L.out.cursor, (unsigned long long)tot) : 0ull;
+      if ((int64_t)(st0 + tot) > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+      else base = (int64_t)st0;
+      if (tot) atomicAdd(&L.hdr->out_total[0], (unsigned long long)tot);
+      s_base = base;
+    }
+    __syncthreads();
+    const int64_t base = s_base;
+    if (act) {
+      const int64_t gs = P.gs0 + (int64_t)r * np + pl;
+      L.out.start[gs] = base < 0 ? -1 : base + ex;
+      L.out.cnt[gs] = cnt;
+    }
+    if (base >= 0) {
+      // survivors of (r, pl), coalesced: lane = bit within a 32-tuple word
+      for (int j = wid; j < nw * tpr; j += NP_NT / 32) {
+        const int rr = j / tpr, pp = j - rr * tpr;
+        const int nn = row_n[rr];
+        if (nn == 0 || pp >= np) continue;
+        int off = soff[j];
+        const int64_t* rm = sm + rr * WARP_DIRECT;
+        const int64_t* rt = stxy + rr * WARP_DIRECT;
+        const uint32_t* ri = sidk + rr * WARP_DIRECT;
+        for (int c0 = 0; c0 < nn; c0 += 32) {
+          const uint32_t word = kbits[(c0 >> 5) * NP_NT + j];
+          if ((word >> lane) & 1u) {
+            const int i = c0 + lane;
+            const uint32_t v = ri[i];
+            const int64_t d = base + off + __popc(word & ((1u << lane) - 1u));
+            L.out.m[d] = rm[i];
+            L.out.t[d] = rt[i] + ztab[(v >> 16) * tpr + pp];
+            L.out.id[d] = (uint64_t)(v & 0xffffu);
+          }
+          off += __popc(word);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 constexpr size_t NS_SMEM = (size_t)NS_CAP * (5 * 8 + 4 + 2 + 2);
 static_assert(sizeof(NodeGroup) == sizeof(NodeGroupH), "NodeGroup layout");
 
 __global__ void __launch_bounds__(DIRECT_NT) k_node_shared(BatchDev B, LevelDev L,
-                                                           const NodeGroup* groups, int ngroups) {
+                                                           const NodeGroup* groups) {
+  const int ngroups = (int)L.hdr->ns_big;  // rows k_node_pack handed over
   extern __shared__ int64_t dyn_ns[];
   int64_t* sm = dyn_ns;                            // [NS_CAP] m (sorted by (m, id))
   uint64_t* sid = (uint64_t*)(sm + NS_CAP);        // [NS_CAP] id
@@ -1585,9 +1851,35 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   GROW(seg_d, int32_t, nloc);
   GROW(seg_n, int32_t, nloc);
   const int ngroups = groups ? (int)groups->size() : 0;
+  // k_node_pack: consecutive full rows w of one step, up to NP_NT/ceil32(K_j) per pack
+  std::vector<NodeGroup> packs;
+  int np_rmax = 1;
+  int64_t np_ztn = 0;
   if (ngroups) {
-    GROW(groups_dev, NodeGroup, ngroups);
-    cudaMemcpyAsync(groups_dev.p, groups->data(), sizeof(NodeGroup) * ngroups, cudaMemcpyHostToDevice, st);
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const NodeGroup& G = (*groups)[gi];
+      const StepDev& d = steps[G.step];
+      const int64_t np = G.p_hi - G.p_lo;
+      const int tpr = np_tpr(np);
+      const int64_t zt = d.nblk * (int64_t)tpr;
+      if (np <= NP_NT && zt <= NP_ZT_CAP) np_ztn = std::max(np_ztn, zt);
+      const int rcap = np <= NP_NT ? std::min(NP_ROWS, NP_NT / tpr) : 1;
+      if (!packs.empty()) {
+        NodeGroup& P = packs.back();
+        if (P.step == G.step && P.p_lo == G.p_lo && P.p_hi == G.p_hi && G.p_lo == 0 && G.p_hi == d.KC &&
+            G.w == P.w + P.pad && G.gs0 == P.gs0 + P.pad * np && P.pad < rcap) {
+          ++P.pad;
+          np_rmax = std::max(np_rmax, P.pad);
+          continue;
+        }
+      }
+      NodeGroup P = G;
+      P.pad = 1;
+      packs.push_back(P);
+    }
+    GROW(groups_dev, NodeGroup, ngroups);  // rows handed to k_node_shared
+    GROW(packs_dev, NodeGroup, packs.size());
+    cudaMemcpyAsync(packs_dev.p, packs.data(), sizeof(NodeGroup) * packs.size(), cudaMemcpyHostToDevice, st);
   }
   GROW(blk_rel, int64_t, nbl);
   GROW(seg_tuples, int64_t, nloc);
@@ -1693,8 +1985,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       nl += 2;
       if (l == 0 && ngroups) {
         ++nl;
-        k_node_shared<<<std::min(ngroups, 148 * 4), DIRECT_NT, NS_SMEM, st>>>(
-            s, L, (const NodeGroup*)groups_dev.p, ngroups);
+        ++nl;
+        const int npk = (int)packs.size();
+        k_node_pack<<<std::min(npk, 148 * 4), NP_NT, np_smem(np_rmax, np_ztn), st>>>(
+            s, L, (const NodeGroup*)packs_dev.p, npk, np_rmax, np_ztn, (NodeGroup*)groups_dev.p);
+        k_node_shared<<<std::min(ngroups, 148 * 2), DIRECT_NT, NS_SMEM, st>>>(
+            s, L, (const NodeGroup*)groups_dev.p);
       }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
       if (warp16) {
@@ -1889,6 +2185,9 @@ cudaError_t StepRunner::configure() {
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_node_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)NS_SMEM);
+    if (e0 != cudaSuccess) return e0;
+    e0 = cudaFuncSetAttribute(k_node_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)np_smem(NP_ROWS, NP_ZT_CAP));
     if (e0 != cudaSuccess) return e0;
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));

@@ -117,6 +117,22 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int3
   const int64_t li = gs - B.seg_base[j];
   const int64_t sg = s.seg_lo + li;
   int64_t* rel_out = blk_rel + B.blk_base[j] + li * s.nblk;
+  // shared-order node path (k_node_pack / k_node_shared): Y, Z singletons, so
+  // n = sum_k |X_{w,k}| = X.off[(w+1)K_i] - X.off[w K_i] for every p of row w
+  if (s.node_shared && s.nblk <= NS_MAXBLK && s.KB == s.nblk) {
+    const int64_t w = sg / s.KC;
+    const int64_t rel = s.X.off[(w + 1) * s.KB] - s.X.off[w * s.KB];
+    if (rel <= NS_CAP) {
+      if (lane == 0) {
+        seg_d[gs] = SPECIAL_LEVEL;
+        seg_n[gs] = (int32_t)rel;
+        seg_tuples[gs] = rel;
+        atomicAdd(&sh_tuples, (unsigned long long)rel);
+        atomicAdd(&sh_direct[0], (unsigned long long)rel);  // level-0 pool capacity
+      }
+      return;
+    }
+  }
   // level 0: block offsets relative to the segment (ids, R6) and the tuple count
   int64_t rel = 0;
   for (int64_t k0 = 0; k0 < s.nblk; k0 += 32) {
@@ -206,10 +222,172 @@ __global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_
 // Direct path: the whole level-l sample of a segment (<= C_DIRECT tuples) in
 // one CTA: product -> bitonic sort on (m,t,id) -> Alg.1 sweep -> compaction.
 
+// Register-blocked CTA sort + Alg. 1 for N = 32 R x (DIRECT_NT / 32) tuples:
+// element e = warp*32R + r*32 + lane lives in registers; bitonic stages with
+// j < 32 use shuffles, j < 32R register swaps, and only the log2(#warps)
+// cross-warp stages per merge exchange through shared memory (x*).  The sweep
+// is warp scans with a cross-warp carry; survivors are written by ballot.
+template <int R, int JR>
+__device__ __forceinline__ void cta_rows_xchg(int64_t (&m)[R], int64_t (&t)[R], uint64_t (&id)[R], int k,
+                                              int eb) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r & JR) continue;
+    const int r2 = r | JR;
+    const bool up = ((eb | (r << 5)) & k) == 0;
+    const bool gt = key_lt(m[r2], t[r2], id[r2], m[r], t[r], id[r]);
+    if (gt == up) {
+      int64_t a = m[r]; m[r] = m[r2]; m[r2] = a;
+      a = t[r]; t[r] = t[r2]; t[r2] = a;
+      uint64_t b = id[r]; id[r] = id[r2]; id[r2] = b;
+    }
+  }
+}
+
+template <int R, typename Gen>
+__device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
+                                               long long* sh, const LevelDev& L, int64_t gs,
+                                               int64_t* s_start) {
+  constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eb = wid * 32 * R;
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    m[r] = INF;
+    t[r] = INF;
+    id[r] = ~0ull;
+  }
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const int e = eb + (r << 5) + lane;
+    if (e < n) {
+      int64_t vm, vt;
+      uint64_t vi;
+      gen(e, vm, vt, vi);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == r) {
+          m[q] = vm;
+          t[q] = vt;
+          id[q] = vi;
+        }
+    }
+  }
+#pragma unroll 1
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32 * R) {  // partner in another warp
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = eb + (r << 5) + lane;
+          xm[e] = m[r];
+          xt[e] = t[r];
+          xid[e] = id[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = eb + (r << 5) + lane, p = e ^ j;
+          const int64_t pm = xm[p], pt = xt[p];
+          const uint64_t pi = xid[p];
+          const bool up = (e & k) == 0, lower = (e & j) == 0;
+          const bool p_lt = key_lt(pm, pt, pi, m[r], t[r], id[r]);
+          if ((lower == up) ? p_lt : !p_lt) {
+            m[r] = pm;
+            t[r] = pt;
+            id[r] = pi;
+          }
+        }
+        __syncthreads();
+      } else if (j >= 32) {
+        const int jr = j >> 5;
+        if (jr == 1) cta_rows_xchg<R, 1>(m, t, id, k, eb);
+        else if (R >= 4 && jr == 2) cta_rows_xchg<R, (R >= 4 ? 2 : 1)>(m, t, id, k, eb);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t pm = __shfl_xor_sync(0xffffffffu, m[r], j);
+          const int64_t pt = __shfl_xor_sync(0xffffffffu, t[r], j);
+          const uint64_t pi = __shfl_xor_sync(0xffffffffu, id[r], j);
+          const int e = eb + (r << 5) + lane;
+          const bool up = (e & k) == 0, lower = (e & j) == 0;
+          const bool p_lt = key_lt(pm, pt, pi, m[r], t[r], id[r]);
+          if ((lower == up) ? p_lt : !p_lt) {
+            m[r] = pm;
+            t[r] = pt;
+            id[r] = pi;
+          }
+        }
+      }
+    }
+  }
+  // Alg. 1: keep iff t < min of all earlier t (earlier warps via sh)
+  long long wmin = INF;
+#pragma unroll
+  for (int r = 0; r < R; ++r) wmin = t[r] < wmin ? t[r] : wmin;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long u = __shfl_xor_sync(0xffffffffu, wmin, o);
+    wmin = u < wmin ? u : wmin;
+  }
+  if (lane == 0) sh[wid] = wmin;
+  __syncthreads();
+  long long carry = INF;
+  for (int w = 0; w < wid; ++w) carry = sh[w] < carry ? sh[w] : carry;
+  unsigned bal[R];
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long inc = warp_incl_min(t[r]);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    bal[r] = __ballot_sync(0xffffffffu, eb + (r << 5) + lane < n && t[r] < v);
+    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
+    carry = rowmin < carry ? rowmin : carry;
+    cnt += __popc(bal[r]);
+  }
+  __syncthreads();  // sh reused for the per-warp counts
+  if (lane == 0) sh[wid] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < NW; ++w) tot += sh[w];
+    const unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)tot);
+    int64_t base = -1;
+    if ((int64_t)(st0 + tot) > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+    else base = (int64_t)st0;
+    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
+    L.out.start[gs] = base;
+    L.out.cnt[gs] = tot;
+    *s_start = base;
+  }
+  __syncthreads();
+  const int64_t base = *s_start;
+  if (base >= 0) {
+    int64_t off = base;
+    for (int w = 0; w < wid; ++w) off += sh[w];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if ((bal[r] >> lane) & 1u) {
+        const int64_t d = off + __popc(bal[r] & ((1u << lane) - 1u));
+        L.out.m[d] = m[r];
+        L.out.t[d] = t[r];
+        L.out.id[d] = id[r];
+      }
+      off += __popc(bal[r]);
+    }
+  }
+  __syncthreads();  // sh / x* / s_start reuse
+}
+
 constexpr int DIRECT_MAXBLK = 128;  // per-block info cached in smem up to this many blocks
 static size_t direct_smem(int cap) { return (size_t)cap * (3 * 8 + 4 + 4) + 8; }
 
-__global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
+__global__ void __launch_bounds__(DIRECT_NT, 3) k_direct(BatchDev B, LevelDev L) {
   extern __shared__ int64_t dyn_direct[];  // capacity B.cdirect (runtime)
   int64_t* sm = dyn_direct;
   int64_t* stt = sm + B.cdirect;
@@ -221,9 +399,27 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
   __shared__ int bc[DIRECT_MAXBLK][3];      // sampled counts
   __shared__ long long sh[33];
   __shared__ int64_t s_start;
+  __shared__ int64_t s_list[DIRECT_NT];
+  __shared__ int s_nl;
   const int st = L.st;
-  for (int64_t gs = blockIdx.x; gs < B.nseg; gs += gridDim.x) {
-    if (L.seg_d[gs] != L.level || L.seg_n[gs] <= L.warp2) continue;
+  // one parallel pass over tw segments' seg_d picks this level's CTA-direct
+  // segments (most waves have few among many)
+  int64_t tw = B.nseg / ((int64_t)gridDim.x * 4);
+  tw = tw < 1 ? 1 : (tw > DIRECT_NT ? DIRECT_NT : tw);
+  // the CTA's segments are b, b + G, b + 2G, ... (G = grid; spreads a step's
+  // heavy segments over CTAs), examined tw at a time
+  for (int64_t t0 = 0; (int64_t)blockIdx.x + t0 * gridDim.x < B.nseg; t0 += tw) {
+    if (threadIdx.x == 0) s_nl = 0;
+    __syncthreads();
+    {
+      const int64_t g = (int64_t)blockIdx.x + (t0 + threadIdx.x) * gridDim.x;
+      if (threadIdx.x < tw && g < B.nseg && L.seg_d[g] == L.level && L.seg_n[g] > L.warp2)
+        s_list[atomicAdd(&s_nl, 1)] = g;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    for (int q = 0; q < nl; ++q) {
+    const int64_t gs = s_list[q];
     if (L.hdr->overflow) return;
     const int j = find_base(B.seg_base, B.nsteps, gs);
     const StepDev& s = B.steps[j];
@@ -267,35 +463,44 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
     const int n = pre[nblk];
     int N = 1;
     while (N < n) N <<= 1;
+    // tuple i of the level-l sample (block k = largest with pre[k] <= i)
+    auto gen = [&](int i, int64_t& om, int64_t& ot, uint64_t& oid) {
+      int lo = 0, hi = nblk;
+      while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (pre[mid] <= i) lo = mid;
+        else hi = mid;
+      }
+      const int k = lo;
+      Blk b;
+      int cy, cz;
+      if (cached) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          b.o[f] = bo[k][f];
+          b.n[f] = bn[k][f];
+        }
+        cy = bc[k][1];
+        cz = bc[k][2];
+      } else {
+        b = load_blk(s, sg, k);
+        cy = (int)samp_cnt(b.n[1], st);
+        cz = (int)samp_cnt(b.n[2], st);
+      }
+      const int r = i - pre[k];  // < C_DIRECT: 32-bit index math
+      const int jz = r % cz, q2 = r / cz, jy = q2 % cy, jx = q2 / cy;
+      const int64_t x = samp_idx(jx, b.n[0], st), y = samp_idx(jy, b.n[1], st),
+                    z = samp_idx(jz, b.n[2], st);
+      make_tuple(s, b, rel[k], x, y, z, om, ot, oid);
+    };
+    if (N == 2 * DIRECT_NT || N == 4 * DIRECT_NT) {
+      if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, sh, L, gs, &s_start);
+      else cta_sort_sweep<4>(n, gen, sm, stt, sid, sh, L, gs, &s_start);
+      continue;
+    }
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
       if (i < n) {
-        int lo = 0, hi = nblk;  // largest k with pre[k] <= i
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if (pre[mid] <= i) lo = mid;
-          else hi = mid;
-        }
-        const int k = lo;
-        Blk b;
-        int cy, cz;
-        if (cached) {
-#pragma unroll
-          for (int f = 0; f < 3; ++f) {
-            b.o[f] = bo[k][f];
-            b.n[f] = bn[k][f];
-          }
-          cy = bc[k][1];
-          cz = bc[k][2];
-        } else {
-          b = load_blk(s, sg, k);
-          cy = (int)samp_cnt(b.n[1], st);
-          cz = (int)samp_cnt(b.n[2], st);
-        }
-        const int r = i - pre[k];  // < C_DIRECT: 32-bit index math
-        const int jz = r % cz, q = r / cz, jy = q % cy, jx = q / cy;
-        const int64_t x = samp_idx(jx, b.n[0], st), y = samp_idx(jy, b.n[1], st),
-                      z = samp_idx(jz, b.n[2], st);
-        make_tuple(s, b, rel[k], x, y, z, sm[i], stt[i], sid[i]);
+        gen(i, sm[i], stt[i], sid[i]);
       } else {
         sm[i] = INF;
         stt[i] = INF;
@@ -328,6 +533,8 @@ __global__ void __launch_bounds__(DIRECT_NT) k_direct(BatchDev B, LevelDev L) {
           L.out.id[d] = sid[i];
         }
     __syncthreads();
+    }
+    __syncthreads();  // s_nl / s_list reuse
   }
 }
 
@@ -521,17 +728,28 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
   __shared__ int pre_all[8][WARP_DIRECT + 1];
   __shared__ Blk blk_all[8][WARP_BLK_CACHE];
   const int wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * 8;
-  for (int64_t gs = (int64_t)blockIdx.x * 8 + wid; gs < B.nseg; gs += nw) {
-    if (L.seg_d[gs] != L.level) continue;
-    const int n = L.seg_n[gs];
-    if (n > WARP_DIRECT) continue;
-    if (L.hdr->overflow) return;
-    if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-    else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-    else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-    else warp_direct_seg<8>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-    __syncwarp();
+  int64_t tw = B.nseg / nw;
+  tw = tw < 1 ? 1 : (tw > 32 ? 32 : tw);
+  const int64_t w0 = (int64_t)blockIdx.x * 8 + wid;  // segments w0 + j * nw, tw per ballot
+  for (int64_t t0 = 0; w0 + t0 * nw < B.nseg; t0 += tw) {
+    const int64_t g = w0 + (t0 + lane) * nw;
+    int nn = 0;
+    if (lane < tw && g < B.nseg && L.seg_d[g] == L.level) nn = L.seg_n[g];
+    unsigned bal = __ballot_sync(0xffffffffu, nn > 0 && nn <= WARP_DIRECT);
+    while (bal) {
+      const int b = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int64_t gs = w0 + (t0 + b) * nw;
+      const int n = __shfl_sync(0xffffffffu, nn, b);
+      if (L.hdr->overflow) return;
+      if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+      else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+      else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+      else warp_direct_seg<8>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+      __syncwarp();
+    }
   }
 }
 
@@ -606,11 +824,13 @@ __device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, co
     const int64_t n0 = r + 1 < R ? __shfl_sync(0xffffffffu, m[r + 1 < R ? r + 1 : r], 0) : INF;
     if (lane == 31) nm = n0;
     const int e = (r << 5) | lane;
-    if (e + 1 < n && nm == m[r]) tie = true;
-    if (e < n) {
+    const bool same_next = e + 1 < n && nm == m[r];
+    if (same_next) tie = true;
+    if (e < n)  {  // id | k << 16 | (last of its equal-m group) << 31
       sm[e] = m[r];
       stxy[e] = t[r];
-      sidk[e] = (uint32_t)(id[r] & 0xffffu) | (uint32_t)((id[r] >> 32) << 16);
+      sidk[e] = (uint32_t)(id[r] & 0xffffu) | (uint32_t)((id[r] >> 32) << 16) |
+                (same_next ? 0u : 0x80000000u);
     }
   }
   return __any_sync(0xffffffffu, tie);
@@ -630,6 +850,7 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
   __shared__ int64_t ym[NS_MAXBLK], yt[NS_MAXBLK];
   __shared__ int soff[NP_NT];
   __shared__ int row_n[NP_ROWS];
+  __shared__ bool row_tie[NP_ROWS];
   __shared__ long long sh[33];
   __shared__ int64_t s_base;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -692,9 +913,9 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
           else if (n <= 64) tie = np_row_sort<2>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
           else if (n <= 128) tie = np_row_sort<4>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
           else tie = np_row_sort<8>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          ok = !tie;
+          if (lane == 0) row_tie[r] = tie;
         }
-        if (!ok) {  // exact tie rule / large rows: one CTA per row in k_node_shared
+        if (!ok) {  // large rows / tables: one CTA per row in k_node_shared
           if (lane == 0) {
             NodeGroup G;
             G.step = P.step;
@@ -716,7 +937,7 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
     const int n = r < nw ? row_n[r] : 0;
     const bool act = n > 0 && pl < np;
     int cnt = 0;
-    if (act) {
+    if (act && !row_tie[r]) {
       const int64_t* rt = stxy + r * WARP_DIRECT;
       const uint32_t* ri = sidk + r * WARP_DIRECT;
       long long carry = INF;
@@ -726,7 +947,7 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
 #pragma unroll 4
         for (int b = 0; b < ce; ++b) {
           const int i = c0 + b;
-          const long long t = rt[i] + ztab[(ri[i] >> 16) * tpr + pl];
+          const long long t = rt[i] + ztab[((ri[i] >> 16) & 0x7fffu) * tpr + pl];
           if (t < carry) {
             word |= 1u << b;
             carry = t;
@@ -734,6 +955,34 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
         }
         kbits[(c0 >> 5) * NP_NT + threadIdx.x] = word;
         cnt += __popc(word);
+      }
+    } else if (act) {
+      // equal m values: Alg. 1 under (m, t, id) keeps only the (t, id)-least
+      // tuple of an equal-m group, iff its t is below every earlier t
+      const int64_t* rt = stxy + r * WARP_DIRECT;
+      const uint32_t* ri = sidk + r * WARP_DIRECT;
+      for (int c0 = 0; c0 < n; c0 += 32) kbits[(c0 >> 5) * NP_NT + threadIdx.x] = 0;
+      long long carry = INF, bt = INF;
+      int bi = 0;
+      uint32_t bid = 0xffffffffu;
+      for (int i = 0; i < n; ++i) {
+        const uint32_t v = ri[i];
+        const long long t = rt[i] + ztab[((v >> 16) & 0x7fffu) * tpr + pl];
+        const uint32_t id = v & 0xffffu;
+        if (t < bt || (t == bt && id < bid)) {
+          bt = t;
+          bi = i;
+          bid = id;
+        }
+        if (v >> 31) {
+          if (bt < carry) {
+            kbits[(bi >> 5) * NP_NT + threadIdx.x] |= 1u << (bi & 31);
+            carry = bt;
+            ++cnt;
+          }
+          bt = INF;
+          bid = 0xffffffffu;
+        }
       }
     }
     long long tot;
@@ -771,7 +1020,7 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
             const uint32_t v = ri[i];
             const int64_t d = base + off + __popc(word & ((1u << lane) - 1u));
             L.out.m[d] = rm[i];
-            L.out.t[d] = rt[i] + ztab[(v >> 16) * tpr + pp];
+            L.out.t[d] = rt[i] + ztab[((v >> 16) & 0x7fffu) * tpr + pp];
             L.out.id[d] = (uint64_t)(v & 0xffffu);
           }
           off += __popc(word);
@@ -1614,8 +1863,24 @@ __global__ void k_wave_off(BatchDev B, const int64_t* cnt, const int64_t* seg_tu
     off[sb + j + (gs - sb) + 1] = pos[se] - base;
     step_arr[3 * j] = pos[se] - base;
   }
-  atomicMax((unsigned long long*)&step_arr[3 * j + 1], (unsigned long long)cnt[gs]);
-  atomicAdd((unsigned long long*)&step_arr[3 * j + 2], (unsigned long long)seg_tuples[gs]);
+  // per-step max / sum: one atomic per run of equal j within the warp
+  unsigned long long mx = (unsigned long long)cnt[gs], sm = (unsigned long long)seg_tuples[gs];
+  const unsigned act = __activemask();
+  const unsigned same = __match_any_sync(act, j);
+  // segments are step-major, so `same` is a contiguous run of lanes [a, b];
+  // after offset o lane i holds [i, min(i + 2o - 1, b)]
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long m2 = __shfl_down_sync(act, mx, o), s2 = __shfl_down_sync(act, sm, o);
+    const int src = (threadIdx.x & 31) + o;
+    if (src < 32 && ((same >> src) & 1u)) {
+      mx = m2 > mx ? m2 : mx;
+      sm += s2;
+    }
+  }
+  if ((threadIdx.x & 31) == __ffs(same) - 1) {
+    atomicMax((unsigned long long*)&step_arr[3 * j + 1], mx);
+    atomicAdd((unsigned long long*)&step_arr[3 * j + 2], sm);
+  }
 }
 
 static int grid_for(int64_t n, int nt, int maxg);

@@ -1594,29 +1594,115 @@ __device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int6
   }
 }
 
+// Buckets of 2..32 candidates: the 32/S buckets of one size class
+// (S/2, S] of a 32-bucket tile are sorted together, one per S-lane group
+// (bitonic with shuffles inside the group, segmented warp scans for Alg. 1).
+template <int S>
+__device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int64_t b0, int* slist) {
+  const int lane = threadIdx.x & 31;
+  const bool mine = c > S / 2 && c <= S;
+  const unsigned mask = __ballot_sync(0xffffffffu, mine);
+  if (mask == 0) return;
+  if (mine) slist[__popc(mask & ((1u << lane) - 1u))] = lane;
+  __syncwarp();
+  const int n = __popc(mask);
+  constexpr int G = 32 / S;
+  const int g = lane / S, e = lane & (S - 1);
+  for (int p0 = 0; p0 < n; p0 += G) {
+    const int q = p0 + g;
+    const int src = q < n ? slist[q] : 0;
+    const int64_t cc = __shfl_sync(0xffffffffu, c, src);
+    int64_t m = INF, t = INF, base = 0;
+    uint64_t id = ~0ull;
+    long long carry = INF;
+    const int64_t bk = b0 + src;
+    if (q < n) {
+      base = L.boff[bk];
+      carry = L.bcarry[bk];
+      if (e < cc) {
+        m = L.gm[base + e];
+        t = L.gt[base + e];
+        id = L.gid[base + e];
+      }
+    }
+#pragma unroll
+    for (int k = 2; k <= S; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const int64_t pm = __shfl_xor_sync(0xffffffffu, m, j);
+        const int64_t pt = __shfl_xor_sync(0xffffffffu, t, j);
+        const uint64_t pi = __shfl_xor_sync(0xffffffffu, id, j);
+        const bool up = (e & k) == 0, lower = (e & j) == 0;
+        const bool p_lt = key_lt(pm, pt, pi, m, t, id);
+        if ((lower == up) ? p_lt : !p_lt) {
+          m = pm;
+          t = pt;
+          id = pi;
+        }
+      }
+    }
+    long long inc = t;
+#pragma unroll
+    for (int d = 1; d < S; d <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, inc, d, S);
+      if (e >= d) inc = u < inc ? u : inc;
+    }
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1, S);
+    if (e == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    if (q < n && e < cc) {
+      L.gm[base + e] = m;
+      L.gt[base + e] = t;
+      L.gid[base + e] = id;
+      L.gflag[base + e] = t < v ? 1 : 0;
+    }
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L) {
   if (L.hdr->overflow) return;
+  __shared__ int slist_all[8][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int* slist = slist_all[wid];
   const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
   const int64_t nw = (int64_t)gridDim.x * 8;
-  for (int64_t bkt = (int64_t)blockIdx.x * 8 + wid; bkt < B; bkt += nw) {
-    const int64_t c = L.bcount[bkt];
-    if (c == 0) continue;
-    if (L.fstats && lane == 0) {
+  // tiles of T buckets per warp: T = 1 (a warp per bucket) while there are
+  // few buckets, up to 32 when there are many (size classes batch up)
+  int64_t T = B / (2 * nw);
+  T = T < 1 ? 1 : (T > 32 ? 32 : T);
+  const int64_t ntile = (B + T - 1) / T;
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + wid; tile < ntile; tile += nw) {
+    const int64_t b0 = tile * T;
+    const int64_t bkt = b0 + lane;
+    const int64_t c = lane < T && bkt < B ? (int64_t)L.bcount[bkt] : 0;
+    if (L.fstats && c > 0) {
       const int cls = c == 1 ? 0 : c <= 4 ? 1 : c <= 8 ? 2 : c <= 16 ? 3 : c <= 32 ? 4 : c <= 64 ? 5
                       : c <= 128 ? 6 : c <= 256 ? 7 : c <= 4096 ? 8 : 9;
       atomicAdd(&L.hdr->bstat[0][cls], 1ull);
       atomicAdd(&L.hdr->bstat[1][cls], (unsigned long long)c);
     }
-    if (c > WARP_DIRECT) {
-      if (lane == 0) L.large_list[atomicAdd(L.large_n, 1ull)] = bkt;
-      continue;
+    if (c > WARP_DIRECT) L.large_list[atomicAdd(L.large_n, 1ull)] = bkt;
+    if (c == 1) {  // a single candidate: kept iff below the carry
+      const int64_t base = L.boff[bkt];
+      L.gflag[base] = L.gt[base] < L.bcarry[bkt] ? 1 : 0;
     }
-    const int64_t base = L.boff[bkt];
-    if (c <= 32) warp_bucket<1>(L, bkt, c, base);
-    else if (c <= 64) warp_bucket<2>(L, bkt, c, base);
-    else if (c <= 128) warp_bucket<4>(L, bkt, c, base);
-    else warp_bucket<8>(L, bkt, c, base);
+    bucket_groups<2>(L, c, b0, slist);
+    bucket_groups<4>(L, c, b0, slist);
+    bucket_groups<8>(L, c, b0, slist);
+    bucket_groups<16>(L, c, b0, slist);
+    bucket_groups<32>(L, c, b0, slist);
+    unsigned big = __ballot_sync(0xffffffffu, c > 32 && c <= WARP_DIRECT);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int64_t cb = __shfl_sync(0xffffffffu, c, src);
+      const int64_t bk = b0 + src;
+      const int64_t base = L.boff[bk];
+      if (cb <= 64) warp_bucket<2>(L, bk, cb, base);
+      else if (cb <= 128) warp_bucket<4>(L, bk, cb, base);
+      else warp_bucket<8>(L, bk, cb, base);
+    }
   }
 }
 
@@ -2299,7 +2385,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         cudaMemsetAsync(L.cand_cursor, 0, sizeof(unsigned long long), st);
         k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
         scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
-        k_filter<<<filter_grid, 256, 0, st>>>(s, L);
+        k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
         k_check_cand<<<1, 1, 0, st>>>(L);
         k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
@@ -2444,6 +2530,8 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
+  if (const char* e = getenv("FT_FILTER_NT")) filter_nt = std::max(32, std::min(256, atoi(e) / 32 * 32));
+  filter_grid = 148 * 128 * (256 / filter_nt);
   if (const char* e = getenv("FT_FILTER_GRID")) filter_grid = std::max(148, atoi(e));
   if (const char* e = getenv("FT_ITEM_MAX")) item_max = std::max(16, atoi(e));
   if (const char* e = getenv("FT_ITEM_DIV")) item_div = std::max(1, atoi(e));

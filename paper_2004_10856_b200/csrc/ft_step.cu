@@ -1426,6 +1426,7 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     const int64_t* Gt = L.in.t + L.in.start[li];
     const int64_t g = L.in.cnt[li];
     const int64_t bb = L.bucket_base[li];
+    const int64_t gml = g > 0 ? Gm[g - 1] : INF;  // largest G m (interpolation)
     // q: #G points with m < m of the current chunk start (galloping lower bound)
     int64_t q = 0;
     int64_t jj = j0;
@@ -1436,6 +1437,32 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
       const int64_t mf = ms + __ldg(Lm + samp_idx(jj, nL, sh));
       const int64_t tl = ts + __ldg(Lt + samp_idx(je - 1, nL, sh));
       if (q < g && Gm[q] < mf) {  // gallop + binary search to lower_bound(mf)
+        if (g - q > 16) {
+          // one interpolation probe between Gm[q] and Gm[g-1] (G's m values are
+          // spread over the segment's range); the gallop then starts there
+          const int64_t mq = Gm[q];
+          if (gml < mf) {
+            q = g;
+            goto g_done;
+          }
+          int64_t e = q + (int64_t)((double)(mf - mq) / (double)(gml - mq) * (double)(g - 1 - q));
+          e = e <= q ? q + 1 : (e > g - 1 ? g - 1 : e);
+          if (Gm[e] < mf) {
+            q = e;
+          } else {  // lower bound in (q, e]: gallop down from e
+            int64_t stp = 1;
+            while (e - stp > q && Gm[e - stp] >= mf) stp <<= 1;
+            int64_t a0 = e - stp < q ? q + 1 : e - stp + 1, a1 = e - (stp >> 1);
+            // Gm[a1] >= mf (or a1 == e), lower bound in [a0, a1]
+            while (a0 < a1) {
+              const int64_t mid = (a0 + a1) >> 1;
+              if (Gm[mid] < mf) a0 = mid + 1;
+              else a1 = mid;
+            }
+            q = a0;
+            goto g_done;
+          }
+        }
         int64_t step = 1;
         while (q + step < g && Gm[q + step] < mf) step <<= 1;
         int64_t a0 = q + (step >> 1) + 1, a1 = min(q + step, g);
@@ -1446,10 +1473,16 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
         }
         q = a0;
       }
+    g_done:
       if (q > 0 && Gt[q - 1] <= tl) {
         // G[q-1] (m < mf) strictly dominates the whole chunk and every later
         // element with t >= its t: gallop along the run to the first t below it.
         const int64_t tg = Gt[q - 1];
+        if (ts + __ldg(Lt + samp_idx(j1 - 1, nL, sh)) >= tg) {  // common: the rest of the item
+          c_skip += j1 - jj;
+          jj = j1;
+          continue;
+        }
         int64_t step = 1, last = je - 1;  // t(last) >= tg
         while (last + step < j1 && ts + __ldg(Lt + samp_idx(last + step, nL, sh)) >= tg) {
           last += step;

@@ -99,6 +99,10 @@ typedef struct {
   float comm_ms;         /* all-gather time (world > 1) */
   float plan_ms, direct_ms, filter_ms, bucket_ms, compact_ms; /* opt.profile only */
   float host_ms;         /* opt.profile only: host readback + scratch sizing inside the step */
+  int64_t path[4];       /* wave: kernel-path counters (this rank) -- shared-order node rows
+                            reduced by the packed kernel, ... of them with equal m values,
+                            rows sent to the one-CTA-per-row kernel, direct segments sorted
+                            by the register-blocked CTA kernel */
 } ft_step_stats;
 
 /* Create a graph: n_ops operators, K_i = n_cfgs[i] (1 <= K_i <= 4096)

@@ -50,7 +50,7 @@ class ft_step_stats(C.Structure):
                 ("max_seg", C.c_int64), ("filter_tuples", C.c_int64), ("direct_tuples", C.c_int64),
                 ("kernel_ms", C.c_float), ("comm_ms", C.c_float), ("plan_ms", C.c_float),
                 ("direct_ms", C.c_float), ("filter_ms", C.c_float), ("bucket_ms", C.c_float),
-                ("compact_ms", C.c_float), ("host_ms", C.c_float)]
+                ("compact_ms", C.c_float), ("host_ms", C.c_float), ("path", C.c_int64 * 4)]
 
 
 def _load():
@@ -208,7 +208,9 @@ class Graph:
                         "plan_ms": s.plan_ms, "direct_ms": s.direct_ms, "filter_ms": s.filter_ms,
                         "bucket_ms": s.bucket_ms, "compact_ms": s.compact_ms,
                         "host_ms": s.host_ms, "max_seg": s.max_seg,
-                        "filter_tuples": s.filter_tuples, "direct_tuples": s.direct_tuples})
+                        "filter_tuples": s.filter_tuples, "direct_tuples": s.direct_tuples,
+                        "path": {"shared_rows": s.path[0], "shared_tie_rows": s.path[1],
+                                 "shared_cta_rows": s.path[2], "direct_reg_segs": s.path[3]}})
         return out
 
     def step_output(self, step: int, with_mt: bool = True):

@@ -622,6 +622,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
         st.candidates = res.candidates;
         st.filter_tuples = res.filter_tuples;
         st.direct_tuples = res.direct_tuples;
+        for (int u = 0; u < 4; ++u) st.path[u] = res.path[u];
         st.kernel_ms = res.kernel_ms;
         st.comm_ms = comm_ms;
         st.launches = res.launches + 3;
@@ -687,6 +688,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     agg.candidates += res.candidates;
     agg.filter_tuples += res.filter_tuples;
     agg.direct_tuples += res.direct_tuples;
+    for (int u = 0; u < 4; ++u) agg.path[u] += res.path[u];
     agg.kernel_ms += res.kernel_ms;
     agg.launches += res.launches;
     agg.retries += res.retries;
@@ -834,6 +836,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       st.candidates = agg.candidates;
       st.filter_tuples = agg.filter_tuples;
       st.direct_tuples = agg.direct_tuples;
+      for (int u = 0; u < 4; ++u) st.path[u] = agg.path[u];
       st.kernel_ms = agg.kernel_ms;
       st.comm_ms = comm_ms;
       st.launches = agg.launches + (int64_t)vr.size();

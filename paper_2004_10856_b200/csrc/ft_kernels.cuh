@@ -95,6 +95,9 @@ struct StepHdr {
                                               // items, chunk tests, skipped chunks' elements,
                                               // elements tested one by one
   unsigned long long ns_big;                  // rows handed from k_node_pack to k_node_shared
+  unsigned long long ns_rows;                 // rows reduced by k_node_pack
+  unsigned long long ns_tie;                  // ... of which with equal m values (group rule)
+  unsigned long long dreg;                    // k_direct segments sorted register-blocked
 };
 
 // Per-level pool of per-segment results (G of the next finer level, or the

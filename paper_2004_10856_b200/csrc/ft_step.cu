@@ -364,6 +364,7 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     L.out.start[gs] = base;
     L.out.cnt[gs] = tot;
     *s_start = base;
+    atomicAdd(&L.hdr->dreg, 1ull);
   }
   __syncthreads();
   const int64_t base = *s_start;
@@ -913,7 +914,11 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
           else if (n <= 64) tie = np_row_sort<2>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
           else if (n <= 128) tie = np_row_sort<4>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
           else tie = np_row_sort<8>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          if (lane == 0) row_tie[r] = tie;
+          if (lane == 0) {
+            row_tie[r] = tie;
+            atomicAdd(&L.hdr->ns_rows, 1ull);
+            if (tie) atomicAdd(&L.hdr->ns_tie, 1ull);
+          }
         }
         if (!ok) {  // large rows / tables: one CTA per row in k_node_shared
           if (lane == 0) {
@@ -2497,6 +2502,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         res->direct_tuples += (int64_t)plan_copy[l];
       }
       res->huge = (int64_t)hdr_host->huge;
+      res->path[0] = (int64_t)hdr_host->ns_rows;
+      res->path[1] = (int64_t)hdr_host->ns_tie;
+      res->path[2] = (int64_t)hdr_host->ns_big;
+      res->path[3] = (int64_t)hdr_host->dreg;
       int64_t tot = 0;
       if (dev_off) {
         res->counts = nullptr;

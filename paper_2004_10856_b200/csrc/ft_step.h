@@ -15,6 +15,8 @@ struct StepResult {
   int64_t candidates = 0;  // pre-filter survivors over all levels
   int64_t filter_tuples = 0, direct_tuples = 0;  // sampled tuples per kernel family
   int64_t huge = 0;        // buckets that took the global-memory sort
+  int64_t path[4] = {0, 0, 0, 0};  // shared rows: packed, packed with m ties, CTA fallback;
+                                   // register-blocked k_direct segments
   int64_t retries = 0;
   int levels = 0;
   int64_t launches = 0;

@@ -155,3 +155,36 @@ def test_bulk_validation_errors(ft):
     with pytest.raises(ft.FTError) as e:
         g.set_op_costs(0, w.op_m[0], w.op_t[0])
     assert e.value.code == ft.ESTATE
+
+
+def _paths(st):
+    tot = {}
+    for s in st:
+        for k, v in s["path"].items():
+            tot[k] = tot.get(k, 0) + v
+    return tot
+
+
+def test_kernel_paths_with_ties(ft):
+    """Costs in [0, 4): heavy m ties.  Exercises every reduce path -- packed
+    shared-order rows (k_node_pack), its equal-m group rule, the one-CTA-per-row
+    fallback (k_node_shared) and the register-blocked CTA sort (k_direct) --
+    and requires each to be bit-exact against the oracle."""
+    tot = {}
+    for seed in (7, 11, 19):
+        _, st = compare(ft, G.random_sp(seed, n_ops=30, kmax=24, cost_hi=4), strategies=16)
+        for k, v in _paths(st).items():
+            tot[k] = tot.get(k, 0) + v
+    assert tot["shared_rows"] > 0 and tot["shared_tie_rows"] > 0
+    assert tot["shared_cta_rows"] > 0 and tot["direct_reg_segs"] > 0
+
+
+def test_kernel_paths_wide_costs(ft):
+    """Wide cost range (few ties): large shared rows (> 256 tuples, CTA
+    fallback) and register-blocked direct segments without the tie rule."""
+    tot = {}
+    for seed in (8, 9):
+        _, st = compare(ft, G.random_sp(seed, n_ops=30, kmax=32, cost_hi=1 << 20), strategies=16)
+        for k, v in _paths(st).items():
+            tot[k] = tot.get(k, 0) + v
+    assert tot["shared_rows"] > 0 and tot["shared_cta_rows"] > 0 and tot["direct_reg_segs"] > 0

@@ -19,6 +19,8 @@ namespace ftk {
 // from *n_dev when given (device-resident counts), else n_host.
 
 constexpr int SCAN_NT = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_NT * SCAN_ITEMS;
+// scratch layout of a scan over <= n_cap elements: tile states, then the tile counter
+__host__ __device__ inline int64_t ntiles_cap_slot(int64_t n_cap) { return (n_cap + SCAN_TILE - 1) / SCAN_TILE; }
 
 // Segment runs the filter path at this level (its direct level is deeper;
 // SPECIAL_LEVEL segments are handled by k_node_shared).
@@ -26,76 +28,88 @@ __device__ __forceinline__ bool is_filter(int32_t d, int level) {
   return d > level && d < SPECIAL_LEVEL;
 }
 
-template <typename TIn>
-__global__ void __launch_bounds__(SCAN_NT) k_scan_tiles(const TIn* in, const int64_t* n_dev,
-                                                        int64_t n_host, int64_t* tile_sums) {
-  __shared__ long long sh[33];
-  const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
-  const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
-    long long s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i)
-      if (base + i < n) s += (long long)in[base + i];
-    long long tot;
-    block_excl_sum<SCAN_NT>(s, sh, &tot);
-    if (threadIdx.x == 0) tile_sums[tile] = tot;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_scan_sums(int64_t* tile_sums, const int64_t* n_dev,
-                                                    int64_t n_host) {
-  __shared__ long long sh[33];
-  const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
-  const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-  long long carry = 0;
-  for (int64_t b = 0; b < ntiles; b += 1024) {
-    int64_t i = b + threadIdx.x;
-    long long v = i < ntiles ? tile_sums[i] : 0;
-    long long tot;
-    long long ex = block_excl_sum<1024>(v, sh, &tot);
-    if (i < ntiles) tile_sums[i] = ex + carry;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) tile_sums[ntiles] = carry;
-}
+// Single-pass scan with decoupled look-back: CTAs take tiles in order from
+// an atomic counter, publish their tile sum (AGG) and, once the exclusive
+// prefix is known, the inclusive prefix (PREF) in one 64-bit word
+// (flag << 62 | value); warp 0 looks back 32 predecessors at a time.  The
+// tile states and the two counters are zeroed by a memset before each scan.
+#define SC_AGG (1ull << 62)
+#define SC_PREF (2ull << 62)
+#define SC_VAL ((1ull << 62) - 1)
 
 template <typename TIn>
-__global__ void __launch_bounds__(SCAN_NT) k_scan_apply(const TIn* in, const int64_t* n_dev,
-                                                        int64_t n_host, const int64_t* tile_sums,
-                                                        int64_t* out) {
+__global__ void __launch_bounds__(SCAN_NT) k_scan1(const TIn* in, const int64_t* n_dev, int64_t n_host,
+                                                   int64_t* out, unsigned long long* state) {
   __shared__ long long sh[33];
+  __shared__ int64_t s_tile;
+  __shared__ long long s_pre;
   const int64_t n = n_dev ? min(*n_dev, n_host) : n_host;
   const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  unsigned long long* ctr = state + ntiles_cap_slot(n_host);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ctr, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     long long v[SCAN_ITEMS];
-    long long s = 0;
+    long long sum = 0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
       v[i] = base + i < n ? (long long)in[base + i] : 0;
-      s += v[i];
+      sum += v[i];
     }
     long long tot;
-    long long ex = block_excl_sum<SCAN_NT>(s, sh, &tot) + tile_sums[tile];
+    long long ex = block_excl_sum<SCAN_NT>(sum, sh, &tot);
+    if (wid == 0) {
+      long long pre = 0;
+      if (tile == 0) {
+        if (lane == 0) atomicExch(state + tile, SC_PREF | (unsigned long long)tot);
+      } else {
+        if (lane == 0) atomicExch(state + tile, SC_AGG | (unsigned long long)tot);
+        int64_t p = tile - 1;
+        for (;;) {
+          const int64_t q = p - lane;  // lane 0 = nearest predecessor
+          const unsigned long long x =
+              q >= 0 ? *(volatile unsigned long long*)(state + q) : SC_PREF;
+          const unsigned long long fl = x & ~SC_VAL;
+          const unsigned pref = __ballot_sync(0xffffffffu, fl == SC_PREF);
+          const unsigned ready = __ballot_sync(0xffffffffu, fl != 0);
+          const int fp = pref ? __ffs(pref) - 1 : 32;  // nearest inclusive prefix
+          const unsigned need = fp == 32 ? 0xffffffffu : (fp == 31 ? 0xffffffffu : ((2u << fp) - 1u));
+          if ((ready & need) != need) continue;  // a predecessor has not published yet
+          long long c = lane <= fp ? (long long)(x & SC_VAL) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+          pre += c;
+          if (fp < 32) break;
+          p -= 32;
+        }
+        if (lane == 0) atomicExch(state + tile, SC_PREF | (unsigned long long)(pre + tot));
+      }
+      if (lane == 0) s_pre = pre;
+    }
+    __syncthreads();
+    ex += s_pre;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
       if (base + i < n) out[base + i] = ex;
       ex += v[i];
     }
+    if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
+    __syncthreads();  // s_tile / s_pre reuse
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_sums[ntiles];
 }
 
 template <typename TIn>
 void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
                cudaStream_t st) {
-  int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 8));
-  k_scan_tiles<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, tmp);
-  k_scan_sums<<<1, 1024, 0, st>>>(tmp, n_dev, n_cap);
-  k_scan_apply<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, tmp, out);
+  const int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
+  cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 1), st);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
+  k_scan1<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, out, (unsigned long long*)tmp);
 }
 
 // ---------------------------------------------------------------------------
@@ -103,16 +117,13 @@ void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap,
 // segment (ids, R6), sample sizes per level, the level at which the segment
 // is small enough for the direct path.
 
-__device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int32_t* seg_n,
+__device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, int32_t* seg_d, int32_t* seg_n,
                                          int64_t* blk_rel, int64_t* seg_tuples, StepHdr* hdr,
                                          unsigned long long& sh_D, unsigned long long& sh_tuples,
                                          unsigned long long* sh_filter,
                                          unsigned long long* sh_direct) {
-  // one warp per local output segment; lanes stride over its blocks
+  // one warp per local output segment (gs, of step j); lanes stride over its blocks
   const int lane = threadIdx.x & 31;
-  const int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gs >= B.nseg) return;
-  const int j = find_base(B.seg_base, B.nsteps, gs);
   const StepDev& s = B.steps[j];
   const int64_t li = gs - B.seg_base[j];
   const int64_t sg = s.seg_lo + li;
@@ -193,10 +204,13 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int32_t* seg_d, int3
   }
 }
 
-__global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
+constexpr int PLAN_BASE_CAP = 2048;  // step bases cached in shared memory by k_plan
+
+__global__ void __launch_bounds__(256) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
                                               int64_t* blk_rel, int64_t* seg_tuples,
                                               StepHdr* hdr) {
   __shared__ unsigned long long sh_D, sh_tuples, sh_filter[LMAX + 1], sh_direct[LMAX + 1];
+  __shared__ int64_t s_base[PLAN_BASE_CAP + 1];
   if (threadIdx.x == 0) {
     sh_D = 0;
     sh_tuples = 0;
@@ -205,8 +219,36 @@ __global__ void __launch_bounds__(128) k_plan(BatchDev B, int32_t* seg_d, int32_
     sh_filter[threadIdx.x] = 0;
     sh_direct[threadIdx.x] = 0;
   }
+  // step bases in shared memory (a 9-level global binary search per segment
+  // dominated node waves with ~1e6 segments); each warp also remembers the
+  // step range of its previous segment
+  const bool cached = B.nsteps <= PLAN_BASE_CAP;
+  if (cached)
+    for (int i = threadIdx.x; i <= B.nsteps; i += blockDim.x) s_base[i] = B.seg_base[i];
   __syncthreads();
-  plan_seg(B, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int j = 0;
+  int64_t sb = 0, se = -1;
+  for (int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gs < B.nseg; gs += nwarps) {
+    if (gs < sb || gs >= se) {
+      if (cached) {
+        int lo = 0, hi = B.nsteps;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_base[mid] <= gs) lo = mid;
+          else hi = mid;
+        }
+        j = lo;
+        sb = s_base[j];
+        se = s_base[j + 1];
+      } else {
+        j = find_base(B.seg_base, B.nsteps, gs);
+        sb = B.seg_base[j];
+        se = B.seg_base[j + 1];
+      }
+    }
+    plan_seg(B, gs, j, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     if (sh_D) atomicMax(&hdr->D, sh_D);
@@ -2115,7 +2157,7 @@ cudaError_t gather_range(const Pool& P, const int64_t* pos, int64_t lo, int64_t 
   return cudaGetLastError();
 }
 
-int64_t scan_tmp_elems(int64_t n) { return n / SCAN_TILE + 8; }
+int64_t scan_tmp_elems(int64_t n) { return ntiles_cap_slot(n) + 8; }
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -2278,7 +2320,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   mark(0);
   cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
   ++nl;
-  k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
+  k_plan<<<grid_for(nloc * 32, 256, 148 * 8), 256, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                             (int64_t*)blk_rel.p,
                                                             (int64_t*)seg_tuples.p, H);
   cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
@@ -2341,7 +2383,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {
       cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
-      k_plan<<<grid_for(nloc * 32, 128, 1 << 30), 128, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
+      k_plan<<<grid_for(nloc * 32, 256, 148 * 8), 256, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                                 (int64_t*)blk_rel.p,
                                                                 (int64_t*)seg_tuples.p, H);
     }
@@ -2415,7 +2457,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(2);
-        nl += 15;  // prep, 3 scan, check, work_count, 3 scan, filter, 2 checks (+ memsets)
+        nl += 9;  // prep, scan, check, bucket_init, work_count, scan, filter, 2 checks
         k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
         scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
         k_check_buckets<<<1, 1, 0, st>>>(s, L);
@@ -2428,7 +2470,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
         mark(3);
-        nl += 8;
+        nl += 6;  // scan, carry, scatter, 3 bucket sorts
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
         k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L);
         k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
@@ -2438,7 +2480,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_bucket_huge<<<148, 1024, (size_t)BUCKET_SMEM * 3 * sizeof(int64_t), st>>>(L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
         mark(4);
-        nl += 6;
+        nl += 4;  // scan, compact_base, compact, seg_out
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
         scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
         // k_compact_base reads the total at gpos[n]; pass via gflag alias
@@ -2470,7 +2512,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       k_wave_off<<<grid_for(nloc, 256, 1 << 30), 256, 0, st>>>(s, pools[0].cnt, (int64_t*)seg_tuples.p,
                                                                (int64_t*)pos.p, dev_off,
                                                                (int64_t*)step_arr.p);
-      nl += 4;
+      nl += 2;  // scan, wave_off
       cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
       cudaMemcpyAsync(step_host_p, step_arr.p, sizeof(int64_t) * 3 * nsteps, cudaMemcpyDeviceToHost, st);
     } else if (keep_dev) {  // multi-rank device exchange: counts stay on the device

@@ -314,13 +314,25 @@ def main():
              "compact": (cand, 24, "candidates scanned/compacted"),
              "plan": (len(st), 0, "steps")}[dom]
     n_units, bpu, what = units
+    # DRAM bytes of one launch of the dominant kernel from a committed ncu
+    # --set full capture (profiles/r1_traffic.json, tools/ncu_final.sh)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if dom == "filter" and os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj["traffic_bytes"]
+        traffic_src = (f"ncu --set full, {tj['launch']}: {tj['traffic_bytes']/1e6:.1f} MB DRAM in "
+                       f"{tj['duration_s']*1e3:.3f} ms; that wave streams {tj['wave_filter_tuples_all_levels']:.3e} "
+                       f"sampled tuples over all levels ({40 * tj['wave_filter_tuples_all_levels']/1e9:.1f} GB "
+                       f"at 40 B/tuple)")
     gsec = groups[dom] / 1e3
     achieved = n_units * bpu / gsec / 1e9 if gsec > 0 and bpu else None
     roof = {"kernel": {"filter": "k_filter", "direct": "k_direct_warp+k_direct", "bucket":
                        "k_bucket_small/large/huge+k_carry+k_scatter", "compact": "k_compact+scans",
                        "plan": "k_plan"}[dom],
             "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak if achieved else None, "traffic": None,
+            "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s",
             "units_per_step": n_units, "bytes_per_unit": bpu, "unit_desc": what,
             "kernel_ms_per_step": groups[dom], "share_of_step": groups[dom] / ms_per_step,

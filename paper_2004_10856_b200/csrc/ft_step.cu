@@ -900,6 +900,7 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
   const int p0 = (int)((int64_t)npacks * blockIdx.x / gridDim.x);
   const int p1 = (int)((int64_t)npacks * (blockIdx.x + 1) / gridDim.x);
   int cur = -1;
+  int64_t cur_lo = -1, cur_hi = -1;
   for (int pi = p0; pi < p1; ++pi) {
     if (L.hdr->overflow) return;
     const NodeGroup P = packs[pi];
@@ -909,7 +910,9 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
     const int tpr = np_tpr(np);
     const int nw = P.pad;
     const bool fits = np <= NP_NT && (int64_t)nblk * tpr <= ztn && nw <= rmax;
-    if (P.step != cur && fits) {  // per-step tables: t_z(k, p) and Y = F(o_i, k)
+    // per-step tables t_z(k, p_lo + pl), Y = F(o_i, k); a rank boundary can cut
+    // a row, so the cache key includes the p range
+    if ((P.step != cur || P.p_lo != cur_lo || P.p_hi != cur_hi) && fits) {
       for (int64_t q = threadIdx.x; q < (int64_t)nblk * tpr; q += NP_NT) {
         const int k = (int)(q / tpr), pl = (int)(q - (int64_t)k * tpr);
         ztab[q] = pl < np ? s.Z.t[s.Z.off[(int64_t)k * s.KC + P.p_lo + pl]] : 0;
@@ -920,6 +923,8 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
         yt[k] = s.Y.t[oy];
       }
       cur = P.step;
+      cur_lo = P.p_lo;
+      cur_hi = P.p_hi;
     }
     __syncthreads();
     // one warp per row: block prefix, register sort, tie check
@@ -2418,7 +2423,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         ++nl;
         ++nl;
         const int npk = (int)packs.size();
-        k_node_pack<<<std::min(npk, 148 * 4), NP_NT, np_smem(np_rmax, np_ztn), st>>>(
+        k_node_pack<<<std::min(npk, pack_grid), NP_NT, np_smem(np_rmax, np_ztn), st>>>(
             s, L, (const NodeGroup*)packs_dev.p, npk, np_rmax, np_ztn, (NodeGroup*)groups_dev.p);
         k_node_shared<<<std::min(ngroups, 148 * 2), DIRECT_NT, NS_SMEM, st>>>(
             s, L, (const NodeGroup*)groups_dev.p);
@@ -2614,6 +2619,7 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
+  if (const char* e = getenv("FT_PACK_GRID")) pack_grid = std::max(1, atoi(e));  // tests: packs per CTA
   if (const char* e = getenv("FT_FILTER_NT")) filter_nt = std::max(32, std::min(256, atoi(e) / 32 * 32));
   filter_grid = 148 * 128 * (256 / filter_nt);
   if (const char* e = getenv("FT_FILTER_GRID")) filter_grid = std::max(148, atoi(e));

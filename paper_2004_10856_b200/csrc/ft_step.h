@@ -84,6 +84,7 @@ class StepRunner {
   bool warp16 = false;                // 257..512-tuple direct segments on one warp (R = 16; A/B: slower)
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
+  int pack_grid = 148 * 4;             // CTAs of k_node_pack (each takes a contiguous pack range)
   int filter_nt = 128;                 // threads per k_filter CTA (A/B: 128 >= 256 > 64)
   int item_max = 512;                 // filter work item: max sampled run elements
   int item_div = 4;                   // ... and target items per resident thread

@@ -188,3 +188,38 @@ def test_kernel_paths_wide_costs(ft):
         for k, v in _paths(st).items():
             tot[k] = tot.get(k, 0) + v
     assert tot["shared_rows"] > 0 and tot["shared_cta_rows"] > 0 and tot["direct_reg_segs"] > 0
+
+
+_PACK_REUSE = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2004_10856_b200 as ft
+from synth import graphs as G
+w = G.c5(n_ops=200, K=16, B=8, Lmin=2, Lmax=6)
+a = ft.load(w, keep_all=True); a.eliminate()
+bad = 0
+for world in (2, 3):
+    b = ft.load(w, keep_all=True, world=world, loopback=True); b.eliminate()
+    for s in range(len(a.stats())):
+        if not all(np.array_equal(x, y) for x, y in zip(a.step_output(s), b.step_output(s))):
+            bad += 1
+rows = sum(s["path"]["shared_rows"] for s in a.stats())
+print("BAD", bad, "ROWS", rows)
+"""
+
+
+def test_partition_invariance_pack_reuse():
+    """Rank boundaries cut shared-order rows into partial p ranges; with few
+    k_node_pack CTAs (FT_PACK_GRID) each CTA reuses its staged t_z table across
+    packs, which must be re-staged when the p range changes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FT_PACK_GRID="3")
+    out = subprocess.run([sys.executable, "-c", _PACK_REUSE.format(root=root)], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    tok = out.stdout.split()
+    assert int(tok[tok.index("ROWS") + 1]) > 0
+    assert int(tok[tok.index("BAD") + 1]) == 0, out.stdout

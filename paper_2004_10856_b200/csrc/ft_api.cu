@@ -77,7 +77,8 @@ struct ft_graph {
   int rank = 0, world = 1;
   bool loopback = false;  // world > 1 simulated on one GPU (tests)
   bool no_shared = false;  // FT_NO_SHARED=1 disables the shared-order node path (A/B tests)
-  double replicate_tau = 2e6;  // waves below this estimated tuple count are replicated
+  double replicate_tau = 1e8;  // waves below this estimated cost (tuples) are replicated
+  std::vector<int> set_edge;   // original edge index of each original edge set (-1 otherwise)
   ncclComm_t comm = nullptr;
   bool keep_all = false;
   int n_ops = 0, n_orig_edges = 0;
@@ -415,6 +416,31 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   std::vector<int64_t> sbase(ns + 1, 0);
   for (int q = 0; q < ns; ++q) sbase[q + 1] = sbase[q] + g->steps[ids[q]].nseg;
   const int64_t NS = sbase[ns];
+  // shared-order node path eligibility (k_node_pack / k_node_shared): Y all singletons,
+  // Z an original edge with m = 0
+  std::vector<char> shared(ns, 0);
+  for (int q = 0; q < ns; ++q) {
+    const StepRec& r = g->steps[ids[q]];
+    if (r.kind != ftk::K_NODE || r.nblk > ftk::NS_MAXBLK) continue;
+    const FSet &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+    const bool y1 = Y.kind == S_OP || (Y.kind == S_STEP && g->steps[Y.step].done &&
+                                       g->steps[Y.step].st.survivors == Y.nseg);
+    bool zok = false;
+    if (Z.kind == S_EDGE) {
+      if (g->set_edge.empty()) {  // original edge of each edge set (built once)
+        g->set_edge.assign(g->sets.size(), -1);
+        for (int e = 0; e < g->n_orig_edges; ++e)
+          if (g->edges[e].set >= 0 && g->edges[e].set < (int)g->set_edge.size())
+            g->set_edge[g->edges[e].set] = e;
+      }
+      const int e = r.Z < (int)g->set_edge.size() ? g->set_edge[r.Z] : -1;
+      zok = e >= 0 && g->e_mzero[e] != 0;
+    }
+    shared[q] = y1 && zok && !g->no_shared;
+    if (getenv("FT_DEBUG_SHARED"))
+      fprintf(stderr, "[shared] step %d kind %d nblk %lld Y.kind %d y1 %d Z.kind %d zok %d -> %d\n", ids[q],
+              r.kind, (long long)r.nblk, Y.kind, (int)y1, Z.kind, (int)zok, (int)shared[q]);
+  }
   // Replicated small waves: below tau estimated product tuples
   // every rank computes the whole wave (identical results, no collective).
   // The estimate uses host-known mean segment sizes, identical on all ranks.
@@ -426,9 +452,12 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       if (S.kind != S_STEP) return 1.0;
       return (double)g->steps[S.step].st.survivors / (double)std::max<int64_t>(S.nseg, 1);
     };
+    // shared-order node steps cost ~1/16 per tuple of the generic path
+    // (one sort per row, running-min sweeps): sharding them did not pay
     for (int q = 0; q < ns; ++q) {
       const StepRec& r = g->steps[ids[q]];
-      est += (double)r.nseg * (double)r.nblk * mean_size(r.X) * mean_size(r.Y) * mean_size(r.Z);
+      est += (shared[q] ? 1.0 / 16 : 1.0) * (double)r.nseg * (double)r.nblk * mean_size(r.X) *
+             mean_size(r.Y) * mean_size(r.Z);
     }
     replicate = est < g->replicate_tau;
   }
@@ -453,24 +482,6 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       for (int64_t sg = 0; sg < r.nseg; ++sg) w[sbase[q] + sg] = wi;
     }
     ft_shard_plan(NS, w.data(), world, lo.data());
-  }
-  // shared-order node path eligibility (k_node_shared): Y all singletons,
-  // Z an original edge with m = 0
-  std::vector<char> shared(ns, 0);
-  for (int q = 0; q < ns; ++q) {
-    const StepRec& r = g->steps[ids[q]];
-    if (r.kind != ftk::K_NODE || r.nblk > ftk::NS_MAXBLK) continue;
-    const FSet &Y = g->sets[r.Y], &Z = g->sets[r.Z];
-    const bool y1 = Y.kind == S_OP || (Y.kind == S_STEP && g->steps[Y.step].done &&
-                                       g->steps[Y.step].st.survivors == Y.nseg);
-    bool zok = false;
-    if (Z.kind == S_EDGE)
-      for (int e = 0; e < g->n_orig_edges; ++e)
-        if (g->edges[e].set == r.Z) zok = g->e_mzero[e] != 0;
-    shared[q] = y1 && zok && !g->no_shared;
-    if (getenv("FT_DEBUG_SHARED"))
-      fprintf(stderr, "[shared] step %d kind %d nblk %lld Y.kind %d y1 %d Z.kind %d zok %d -> %d\n", ids[q],
-              r.kind, (long long)r.nblk, Y.kind, (int)y1, Z.kind, (int)zok, (int)shared[q]);
   }
   auto make_groups = [&](const std::vector<ftk::StepDev>& v) {
     std::vector<ftk::NodeGroupH> gr;

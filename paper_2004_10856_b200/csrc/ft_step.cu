@@ -101,13 +101,27 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(const TIn* in, const int64_t*
     if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
     __syncthreads();  // s_tile / s_pre reuse
   }
+  // the last CTA out leaves the tile states and counters zeroed for the next
+  // scan (every CTA has finished its tiles and look-backs by then)
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    for (int64_t i = threadIdx.x; i < ntiles; i += SCAN_NT) state[i] = 0;
+    if (threadIdx.x == 0) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
 }
 
+// tmp: >= scan_tmp_elems(n_cap) int64 slots, zero on first use (`fresh`
+// zeroes it here); every scan leaves it zeroed again.
 template <typename TIn>
 void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
-               cudaStream_t st) {
+               cudaStream_t st, bool fresh = false) {
   const int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
-  cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 1), st);
+  if (fresh) cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 2), st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
   k_scan1<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, out, (unsigned long long*)tmp);
 }
@@ -1331,20 +1345,20 @@ __global__ void k_level_prep(BatchDev B, LevelDev L) {
 
 // Clears the bucket counters of the live buckets only (B read on device).
 __global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // bucket totals, list/cursor resets
+    const int64_t Bt0 = L.bucket_base[Bt.nseg];
+    L.hdr->bucket_total[L.level] = Bt0;
+    if (Bt0 > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
+    *L.large_n = 0;
+    *L.huge_n = 0;
+    *L.cand_cursor = 0;
+  }
   const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B;
        i += (int64_t)gridDim.x * blockDim.x) {
     L.bcount[i] = 0;
     L.bmin[i] = INF;
   }
-}
-
-__global__ void k_check_buckets(BatchDev Bt, LevelDev L) {
-  const int64_t B = L.bucket_base[Bt.nseg];
-  L.hdr->bucket_total[L.level] = B;
-  if (B > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
-  *L.large_n = 0;
-  *L.huge_n = 0;
 }
 
 // Long factor = the one with most sampled indices; runs = product of the other two.
@@ -1591,10 +1605,11 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
   }
 }
 
-__global__ void k_check_cand(LevelDev L) {
+__global__ void k_check_cand(LevelDev L, int64_t* ncand) {
   unsigned long long c = *L.cand_cursor;
   L.hdr->cand_total[L.level] = c;
   if ((int64_t)c > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
+  *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
 }
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
@@ -1633,10 +1648,6 @@ __global__ void k_scatter(LevelDev L, const int64_t* ncand) {
   }
 }
 
-__global__ void k_clamp_cand(LevelDev L, int64_t* ncand) {
-  unsigned long long c = *L.cand_cursor;
-  *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
-}
 
 // K2+K3 for buckets of <= WARP_DIRECT candidates: one warp per bucket,
 // register bitonic sort by shuffles (R rows of 32), Alg.1 sweep with the
@@ -1926,22 +1937,15 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
   }
 }
 
-__global__ void k_compact_base(LevelDev L, const int64_t* ncand) {
-  const int64_t n = *ncand;
-  const int64_t tot = L.gflag[n];  // after in-place scan: gflag holds positions, [n] = total
-  unsigned long long b = atomicAdd(L.out.cursor, (unsigned long long)tot);
-  if ((int64_t)(b + tot) > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
-  atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
-  L.wcnt[0] = (int64_t)b;  // stash base (wcnt is dead after the work scan)
-}
-
-__global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand) {
+// Survivors of the filter path go to the level pool at the fixed offset
+// `base` = this level's direct-sample total (the direct kernels' outputs,
+// reserved by cursor atomics, never exceed it; the pool holds both).
+__global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand, int64_t base) {
   if (L.hdr->overflow) return;
   const int64_t n = *ncand;
-  const int64_t base = L.wcnt[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (gpos[i + 1] != gpos[i]) {
+    if (gpos[i + 1] != gpos[i] && base + gpos[i] < L.out.cap) {
       const int64_t d = base + gpos[i];
       L.out.m[d] = L.gm[i];
       L.out.t[d] = L.gt[i];
@@ -1950,13 +1954,19 @@ __global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand)
   }
 }
 
-__global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos) {
+__global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos, const int64_t* ncand,
+                          int64_t base) {
   const int64_t nloc = B.nseg;
   const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (li == 0) {
+    const int64_t tot = gpos[*ncand];
+    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
+    if (base + tot > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+  }
   if (li >= nloc || !is_filter(L.seg_d[li], L.level)) return;
   const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
   const int64_t lo = L.boff[b0], hi = L.boff[b1];
-  L.out.start[li] = L.wcnt[0] + gpos[lo];
+  L.out.start[li] = base + gpos[lo];
   L.out.cnt[li] = gpos[hi] - gpos[lo];
 }
 
@@ -2149,7 +2159,7 @@ cudaError_t wave_offsets(const int64_t* cnt, const int64_t* tup, int64_t NS, int
   B.seg_base = sbase_dev;
   B.nsteps = ns;
   B.nseg = NS;
-  scan_excl<int64_t>(cnt, pos, nullptr, NS, scan_tmp, st);
+  scan_excl<int64_t>(cnt, pos, nullptr, NS, scan_tmp, st, true);  // freshly allocated scratch
   cudaMemsetAsync(stats, 0, sizeof(int64_t) * 3 * ns, st);
   k_wave_off<<<grid_for(NS, 256, 1 << 30), 256, 0, st>>>(B, cnt, tup, pos, off, stats);
   return cudaGetLastError();
@@ -2384,7 +2394,11 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(ncand, int64_t, 2);
     }
     const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
-    GROW(scan_tmp, int64_t, scan_n / SCAN_TILE + 8);
+    {  // scan scratch: zeroed when (re)allocated; scans leave it zeroed
+      void* old = scan_tmp.p;
+      GROW(scan_tmp, int64_t, scan_n / SCAN_TILE + 8);
+      if (scan_tmp.p != old) cudaMemsetAsync(scan_tmp.p, 0, scan_tmp.bytes, st);
+    }
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {
       cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
@@ -2462,17 +2476,14 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(2);
-        nl += 9;  // prep, scan, check, bucket_init, work_count, scan, filter, 2 checks
+        nl += 7;  // prep, scan, bucket_init, work_count, scan, filter, check_cand
         k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
         scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
-        k_check_buckets<<<1, 1, 0, st>>>(s, L);
         k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
-        cudaMemsetAsync(L.cand_cursor, 0, sizeof(unsigned long long), st);
         k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
         scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
         k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
-        k_check_cand<<<1, 1, 0, st>>>(L);
-        k_clamp_cand<<<1, 1, 0, st>>>(L, nc);
+        k_check_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
         mark(3);
         nl += 6;  // scan, carry, scatter, 3 bucket sorts
@@ -2485,15 +2496,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_bucket_huge<<<148, 1024, (size_t)BUCKET_SMEM * 3 * sizeof(int64_t), st>>>(L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
         mark(4);
-        nl += 4;  // scan, compact_base, compact, seg_out
+        nl += 3;  // scan, compact, seg_out
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
         scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
-        // k_compact_base reads the total at gpos[n]; pass via gflag alias
-        LevelDev L2 = L;
-        L2.gflag = gpos;
-        k_compact_base<<<1, 1, 0, st>>>(L2, nc);
-        k_compact<<<148 * 8, 256, 0, st>>>(L2, gpos, nc);
-        k_seg_out<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L2, gpos);
+        const int64_t cbase = (int64_t)plan_copy[l];  // direct outputs of level l stay below
+        k_compact<<<148 * 8, 256, 0, st>>>(L, gpos, nc, cbase);
+        k_seg_out<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L, gpos, nc, cbase);
       }
     }
     mark(-1);

@@ -137,7 +137,6 @@ struct LevelDev {
   int64_t* ct;
   uint64_t* cid;
   int64_t* cgb;
-  unsigned int* cpos;
   unsigned long long* cand_cursor;
   int64_t cand_cap;
   int64_t* gm;           // grouped (bucket-ordered) candidates

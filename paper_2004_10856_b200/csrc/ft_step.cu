@@ -1585,13 +1585,12 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
         base = grp.shfl(base, 0);
         const unsigned long long idx = base + grp.thread_rank();
         if ((int64_t)idx < L.cand_cap) {
-          const unsigned pos = atomicAdd(L.bcount + gb, 1u);
+          atomicAdd(L.bcount + gb, 1u);  // no return value: slots are taken in k_scatter
           atomicMin(L.bmin + gb, (long long)t);
           L.cm[idx] = m;
           L.ct[idx] = t;
           L.cid[idx] = id;
           L.cgb[idx] = gb;
-          L.cpos[idx] = pos;
         }
       }
       jj = je;
@@ -1641,7 +1640,10 @@ __global__ void k_scatter(LevelDev L, const int64_t* ncand) {
   const int64_t n = *ncand;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t d = L.boff[L.cgb[i]] + L.cpos[i];
+    // slot inside the bucket: the count is handed back down (order inside a
+    // bucket is irrelevant, buckets are sorted by (m, t, id) next)
+    const int64_t gb = L.cgb[i];
+    const int64_t d = L.boff[gb] + (int64_t)(atomicSub(L.bcount + gb, 1u) - 1u);
     L.gm[d] = L.cm[i];
     L.gt[d] = L.ct[i];
     L.gid[d] = L.cid[i];
@@ -1771,7 +1773,7 @@ __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L
   for (int64_t tile = (int64_t)blockIdx.x * 8 + wid; tile < ntile; tile += nw) {
     const int64_t b0 = tile * T;
     const int64_t bkt = b0 + lane;
-    const int64_t c = lane < T && bkt < B ? (int64_t)L.bcount[bkt] : 0;
+    const int64_t c = lane < T && bkt < B ? L.boff[bkt + 1] - L.boff[bkt] : 0;
     if (L.fstats && c > 0) {
       const int cls = c == 1 ? 0 : c <= 4 ? 1 : c <= 8 ? 2 : c <= 16 ? 3 : c <= 32 ? 4 : c <= 64 ? 5
                       : c <= 128 ? 6 : c <= 256 ? 7 : c <= 4096 ? 8 : 9;
@@ -1814,7 +1816,7 @@ __global__ void __launch_bounds__(DIRECT_NT) k_bucket_large(LevelDev L) {
   const int64_t nl = *L.large_n;
   for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
     const int64_t bkt = L.large_list[e];
-    const int64_t c = L.bcount[bkt];
+    const int64_t c = L.boff[bkt + 1] - L.boff[bkt];
     if (c > BUCKET_SMEM) {
       if (threadIdx.x == 0) L.huge_list[atomicAdd(L.huge_n, 1ull)] = bkt;
       continue;
@@ -1858,7 +1860,7 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
   const int64_t nh = *L.huge_n;
   for (int64_t e = blockIdx.x; e < nh; e += gridDim.x) {
     const int64_t bkt = L.huge_list[e];
-    const int64_t c = L.bcount[bkt];
+    const int64_t c = L.boff[bkt + 1] - L.boff[bkt];
     const int64_t base = L.boff[bkt];
     if (threadIdx.x == 0) atomicAdd(&L.hdr->huge, 1ull);
     // 1) sort tiles of BUCKET_SMEM
@@ -2206,7 +2208,7 @@ void StepRunner::release() {
   Buf* all[] = {&seg_d, &seg_n, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
-                &cgb, &cpos, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
+                &cgb, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
                 &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev};
   for (Buf* b : all) {
     if (b->p) cudaFree(b->p);
@@ -2384,7 +2386,6 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(ct, int64_t, cand_cap);
       GROW(cid, uint64_t, cand_cap);
       GROW(cgb, int64_t, cand_cap + 1);
-      GROW(cpos, unsigned int, cand_cap);
       GROW(gm, int64_t, cand_cap);
       GROW(gt, int64_t, cand_cap);
       GROW(gid, uint64_t, cand_cap);
@@ -2462,7 +2463,6 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         L.ct = (int64_t*)ct.p;
         L.cid = (uint64_t*)cid.p;
         L.cgb = (int64_t*)cgb.p;
-        L.cpos = (unsigned int*)cpos.p;
         L.cand_cursor = cur + 2;
         L.cand_cap = cand_cap;
         L.gm = (int64_t*)gm.p;

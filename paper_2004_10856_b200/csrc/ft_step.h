@@ -104,7 +104,7 @@ class StepRunner {
   Buf poolA_m, poolA_t, poolA_id, poolA_start, poolA_cnt;
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
-  Buf cm, ct, cid, cgb, cpos, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
+  Buf cm, ct, cid, cgb, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
   Buf steps_dev, base_dev, pos, step_arr, groups_dev, packs_dev, big_dev;
   std::vector<int64_t> step_host;
   int64_t* step_host_p = nullptr;

@@ -300,37 +300,12 @@ __device__ __forceinline__ void cta_rows_xchg(int64_t (&m)[R], int64_t (&t)[R], 
   }
 }
 
-template <int R, typename Gen>
-__device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
-                                               long long* sh, const LevelDev& L, int64_t gs,
-                                               int64_t* s_start) {
+template <int R>
+__device__ __forceinline__ void cta_bitonic_regs(int64_t (&m)[R], int64_t (&t)[R], uint64_t (&id)[R],
+                                                 int64_t* xm, int64_t* xt, uint64_t* xid) {
   constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eb = wid * 32 * R;
-  int64_t m[R], t[R];
-  uint64_t id[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    m[r] = INF;
-    t[r] = INF;
-    id[r] = ~0ull;
-  }
-#pragma unroll 1
-  for (int r = 0; r < R; ++r) {
-    const int e = eb + (r << 5) + lane;
-    if (e < n) {
-      int64_t vm, vt;
-      uint64_t vi;
-      gen(e, vm, vt, vi);
-#pragma unroll
-      for (int q = 0; q < R; ++q)
-        if (q == r) {
-          m[q] = vm;
-          t[q] = vt;
-          id[q] = vi;
-        }
-    }
-  }
 #pragma unroll 1
   for (int k = 2; k <= N; k <<= 1) {
 #pragma unroll 1
@@ -380,6 +355,40 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
       }
     }
   }
+}
+
+template <int R, typename Gen>
+__device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
+                                               long long* sh, const LevelDev& L, int64_t gs,
+                                               int64_t* s_start) {
+  constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eb = wid * 32 * R;
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    m[r] = INF;
+    t[r] = INF;
+    id[r] = ~0ull;
+  }
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const int e = eb + (r << 5) + lane;
+    if (e < n) {
+      int64_t vm, vt;
+      uint64_t vi;
+      gen(e, vm, vt, vi);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == r) {
+          m[q] = vm;
+          t[q] = vt;
+          id[q] = vi;
+        }
+    }
+  }
+  cta_bitonic_regs<R>(m, t, id, xm, xt, xid);
   // Alg. 1: keep iff t < min of all earlier t (earlier warps via sh)
   long long wmin = INF;
 #pragma unroll
@@ -1805,7 +1814,64 @@ __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L
 }
 
 // K2+K3 for buckets of 33..BUCKET_SMEM candidates: one CTA, bitonic in smem.
-__global__ void __launch_bounds__(DIRECT_NT) k_bucket_large(LevelDev L) {
+// Register-blocked sort + Alg. 1 of one bucket of c <= 32 R x 8 candidates
+// (in place in gm/gt/gid, keep flags in gflag; carry from earlier buckets).
+template <int R>
+__device__ __forceinline__ void cta_bucket_regs(const LevelDev& L, int64_t bkt, int64_t c, int64_t base,
+                                                int64_t* xm, int64_t* xt, uint64_t* xid,
+                                                long long* sh) {
+  constexpr int NW = DIRECT_NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eb = wid * 32 * R;
+  int64_t m[R], t[R];
+  uint64_t id[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = eb + (r << 5) + lane;
+    if (e < c) {
+      m[r] = L.gm[base + e];
+      t[r] = L.gt[base + e];
+      id[r] = L.gid[base + e];
+    } else {
+      m[r] = INF;
+      t[r] = INF;
+      id[r] = ~0ull;
+    }
+  }
+  cta_bitonic_regs<R>(m, t, id, xm, xt, xid);
+  long long wmin = INF;
+#pragma unroll
+  for (int r = 0; r < R; ++r) wmin = t[r] < wmin ? t[r] : wmin;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long u = __shfl_xor_sync(0xffffffffu, wmin, o);
+    wmin = u < wmin ? u : wmin;
+  }
+  if (lane == 0) sh[wid] = wmin;
+  __syncthreads();
+  long long carry = L.bcarry[bkt];
+  for (int w = 0; w < wid; ++w) carry = sh[w] < carry ? sh[w] : carry;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = eb + (r << 5) + lane;
+    const long long inc = warp_incl_min(t[r]);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    if (e < c) {
+      L.gm[base + e] = m[r];
+      L.gt[base + e] = t[r];
+      L.gid[base + e] = id[r];
+      L.gflag[base + e] = t[r] < v ? 1 : 0;
+    }
+    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
+    carry = rowmin < carry ? rowmin : carry;
+  }
+  (void)NW;
+  __syncthreads();  // sh / x* reuse
+}
+
+__global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
   extern __shared__ int64_t dyn[];
   int64_t* sm = dyn;
   int64_t* stt = sm + BUCKET_SMEM;
@@ -1824,6 +1890,14 @@ __global__ void __launch_bounds__(DIRECT_NT) k_bucket_large(LevelDev L) {
     const int64_t base = L.boff[bkt];
     int N = 1;
     while (N < c) N <<= 1;
+    if (N <= 2 * DIRECT_NT) {  // c <= 512
+      cta_bucket_regs<2>(L, bkt, c, base, sm, stt, sid, sh);
+      continue;
+    }
+    if (N == 4 * DIRECT_NT) {  // c <= 1024
+      cta_bucket_regs<4>(L, bkt, c, base, sm, stt, sid, sh);
+      continue;
+    }
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
       if (i < c) {
         sm[i] = L.gm[base + i];

@@ -357,10 +357,59 @@ __device__ __forceinline__ void cta_bitonic_regs(int64_t (&m)[R], int64_t (&t)[R
   }
 }
 
+// Register-blocked CTA bitonic on single 64-bit keys (same layout as
+// cta_bitonic_regs); xk: N keys of shared memory for the cross-warp stages.
+template <int R>
+__device__ __forceinline__ void cta_bitonic_keys(uint64_t (&k)[R], uint64_t* xk) {
+  constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eb = wid * 32 * R;
+#pragma unroll 1
+  for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32 * R) {  // partner in another warp
+#pragma unroll
+        for (int r = 0; r < R; ++r) xk[eb + (r << 5) + lane] = k[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = eb + (r << 5) + lane;
+          const uint64_t pk = xk[e ^ j];
+          const bool up = (e & kk) == 0, lower = (e & j) == 0;
+          k[r] = (lower == up) ? (pk < k[r] ? pk : k[r]) : (pk > k[r] ? pk : k[r]);
+        }
+        __syncthreads();
+      } else if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r & jr) continue;  // jr is a power of two < R
+          const int r2 = r | jr;
+          if (r2 >= R) continue;
+          const bool up = ((eb | (r << 5)) & kk) == 0;
+          const uint64_t a = k[r], b = k[r2];
+          const bool sw = up ? (b < a) : (a < b);
+          k[r] = sw ? b : a;
+          k[r2] = sw ? a : b;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint64_t pk = __shfl_xor_sync(0xffffffffu, k[r], j);
+          const int e = eb + (r << 5) + lane;
+          const bool up = (e & kk) == 0, lower = (e & j) == 0;
+          k[r] = (lower == up) ? (pk < k[r] ? pk : k[r]) : (pk > k[r] ? pk : k[r]);
+        }
+      }
+    }
+  }
+}
+
 template <int R, typename Gen>
 __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
-                                               long long* sh, const LevelDev& L, int64_t gs,
-                                               int64_t* s_start) {
+                                               uint64_t* xk, long long* sh, const LevelDev& L,
+                                               int64_t gs, int64_t* s_start) {
   constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eb = wid * 32 * R;
@@ -372,6 +421,13 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     t[r] = INF;
     id[r] = ~0ull;
   }
+  // Tuples are staged in x*; the sort runs on 64-bit keys (m << 10 | e)
+  // (m < 3 * 2^40 by R10, e < N <= 1024) and t, id are gathered by e.  The
+  // key order is the (m, t, id) order unless two tuples share m: then the
+  // staged tuples are re-sorted on the full key.
+  uint64_t k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) k[r] = ~0ull;
 #pragma unroll 1
   for (int r = 0; r < R; ++r) {
     const int e = eb + (r << 5) + lane;
@@ -379,16 +435,45 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
       int64_t vm, vt;
       uint64_t vi;
       gen(e, vm, vt, vi);
+      xm[e] = vm;
+      xt[e] = vt;
+      xid[e] = vi;
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (q == r) {
-          m[q] = vm;
-          t[q] = vt;
-          id[q] = vi;
-        }
+        if (q == r) k[q] = ((uint64_t)vm << 10) | (uint64_t)e;
     }
   }
-  cta_bitonic_regs<R>(m, t, id, xm, xt, xid);
+  __syncthreads();
+  cta_bitonic_keys<R>(k, xk);
+  bool tie = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = eb + (r << 5) + lane;
+    if (e < n) {
+      const int src = (int)(k[r] & 1023u);
+      m[r] = (int64_t)(k[r] >> 10);
+      t[r] = xt[src];
+      id[r] = xid[src];
+    }
+    uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+    const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
+    if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
+    if (e < n && prev != ~0ull && (prev >> 10) == (k[r] >> 10)) tie = true;
+  }
+  if (lane == 31) sh[wid] = (long long)(k[R - 1] >> 10);  // last m of the warp (INF-padded: huge)
+  __syncthreads();
+  if (wid > 0 && lane == 0 && eb < n && (long long)(k[0] >> 10) == sh[wid - 1]) tie = true;
+  if (__syncthreads_or(tie)) {  // equal m values: exact sort on (m, t, id)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = eb + (r << 5) + lane;
+      m[r] = e < n ? xm[e] : INF;
+      t[r] = e < n ? xt[e] : INF;
+      id[r] = e < n ? xid[e] : ~0ull;
+    }
+    __syncthreads();
+    cta_bitonic_regs<R>(m, t, id, xm, xt, xid);
+  }
   // Alg. 1: keep iff t < min of all earlier t (earlier warps via sh)
   long long wmin = INF;
 #pragma unroll
@@ -559,9 +644,10 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_direct(BatchDev B, LevelDev L)
                     z = samp_idx(jz, b.n[2], st);
       make_tuple(s, b, rel[k], x, y, z, om, ot, oid);
     };
-    if (N == 2 * DIRECT_NT || N == 4 * DIRECT_NT) {
-      if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, sh, L, gs, &s_start);
-      else cta_sort_sweep<4>(n, gen, sm, stt, sid, sh, L, gs, &s_start);
+    if ((N == 2 * DIRECT_NT || N == 4 * DIRECT_NT) && N <= B.cdirect) {
+      uint64_t* xk = (uint64_t*)kf;  // kf + pre (>= 8 N bytes) are free after generation
+      if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start);
+      else cta_sort_sweep<4>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start);
       continue;
     }
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {

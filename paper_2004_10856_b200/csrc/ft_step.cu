@@ -749,11 +749,46 @@ __device__ __forceinline__ void warp_bitonic(int64_t (&m)[R], int64_t (&t)[R], u
   }
 }
 
-constexpr int WARP_BLK_CACHE = 64;  // block descriptors cached per warp
+// Warp bitonic on single 64-bit keys, R rows of 32 (element e = r*32 + lane).
+template <int R>
+__device__ __forceinline__ void warp_bitonic_keys(uint64_t (&k)[R]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int kk = 2; kk <= R * 32; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r & jr) continue;
+          const int r2 = r | jr;
+          if (r2 >= R) continue;
+          const bool up = ((r << 5) & kk) == 0;
+          const uint64_t a = k[r], b = k[r2];
+          const bool sw = up ? (b < a) : (a < b);
+          k[r] = sw ? b : a;
+          k[r2] = sw ? a : b;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint64_t pk = __shfl_xor_sync(0xffffffffu, k[r], j);
+          const int e = (r << 5) | lane;
+          const bool up = (e & kk) == 0, lower = (e & j) == 0;
+          k[r] = (lower == up) ? (pk < k[r] ? pk : k[r]) : (pk > k[r] ? pk : k[r]);
+        }
+      }
+    }
+  }
+}
+
+constexpr int WARP_BLK_CACHE = 64;
+constexpr size_t DW_SMEM = 8 * 2 * WARP_DIRECT * 8, DW16_SMEM = 4 * 2 * WARP_DIRECT2 * 8;  // t/id staging  // block descriptors cached per warp
 
 template <int R>
 __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre,
-                                Blk* wblk) {
+                                Blk* wblk, int64_t* wt, uint64_t* wi) {
   const int lane = threadIdx.x & 31;
   const int st = L.st;
   const int j = find_base(B.seg_base, B.nsteps, gs);
@@ -780,13 +815,67 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
   __syncwarp();
   int64_t m[R], t[R];
   uint64_t id[R];
+  // tuple e of the sample (block: largest lo with wpre[lo] <= e)
+  auto gen = [&](int e, int64_t& vm, int64_t& vt, uint64_t& vi) {
+    int lo = 0, hi = nblk;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (wpre[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const Blk b = lo < WARP_BLK_CACHE ? wblk[lo] : load_blk(s, sg, lo);
+    const int rr = e - wpre[lo];
+    const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
+    const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
+    make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
+               samp_idx(jz, b.n[2], st), vm, vt, vi);
+  };
+  // sort 64-bit keys (m << 9 | e), t and id staged in wt/wi (m < 3 * 2^40,
+  // R10); equal m values (detected after the sort) -> full (m, t, id) sort
+  uint64_t k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) k[r] = ~0ull;
+#pragma unroll 1
+  for (int r = 0; r < R && (r << 5) < n; ++r) {
+    const int e = (r << 5) | lane;
+    if (e < n) {
+      int64_t vm, vt;
+      uint64_t vi;
+      gen(e, vm, vt, vi);
+      wt[e] = vt;
+      wi[e] = vi;
+#pragma unroll
+      for (int q2 = 0; q2 < R; ++q2)
+        if (q2 == r) k[q2] = ((uint64_t)vm << 9) | (uint64_t)e;
+    }
+  }
+  __syncwarp();
+  warp_bitonic_keys<R>(k);
+  bool tie = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
     m[r] = INF;
     t[r] = INF;
     id[r] = ~0ull;
+    if (e < n) {
+      const int src = (int)(k[r] & 511u);
+      m[r] = (int64_t)(k[r] >> 9);
+      t[r] = wt[src];
+      id[r] = wi[src];
+    }
+    uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+    const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
+    if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
+    if (e < n && prev != ~0ull && (prev >> 9) == (k[r] >> 9)) tie = true;
   }
-  // runtime row loop (small code); the value lands in row r via static selects
+  if (__any_sync(0xffffffffu, tie)) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      m[r] = INF;
+      t[r] = INF;
+      id[r] = ~0ull;
+    }
 #pragma unroll 1
   for (int r = 0; r < R && (r << 5) < n; ++r) {
     const int e = (r << 5) | lane;
@@ -814,8 +903,9 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
         }
     }
   }
-  __syncwarp();
-  warp_bitonic<R>(m, t, id);
+    __syncwarp();
+    warp_bitonic<R>(m, t, id);
+  }
   // Alg. 1 sweep in e order: keep iff t < min of all earlier t
   long long carry = INF;
   bool keep[R];
@@ -864,6 +954,7 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
 __global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
   __shared__ int pre_all[4][WARP_DIRECT2 + 1];
   __shared__ Blk blk_all[4][WARP_BLK_CACHE];
+  extern __shared__ int64_t dyn_dw16[];  // per warp: t[WARP_DIRECT2], id[WARP_DIRECT2]
   const int wid = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * 4;
   for (int64_t gs = (int64_t)blockIdx.x * 4 + wid; gs < B.nseg; gs += nw) {
@@ -871,7 +962,8 @@ __global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
     const int n = L.seg_n[gs];
     if (n <= WARP_DIRECT || n > L.warp2) continue;
     if (L.hdr->overflow) return;
-    warp_direct_seg<16>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+    warp_direct_seg<16>(B, L, gs, n, pre_all[wid], blk_all[wid], dyn_dw16 + wid * 2 * WARP_DIRECT2,
+                        (uint64_t*)(dyn_dw16 + wid * 2 * WARP_DIRECT2 + WARP_DIRECT2));
     __syncwarp();
   }
 }
@@ -879,6 +971,9 @@ __global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
 __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) {
   __shared__ int pre_all[8][WARP_DIRECT + 1];
   __shared__ Blk blk_all[8][WARP_BLK_CACHE];
+  extern __shared__ int64_t dyn_dw[];  // per warp: t[WARP_DIRECT], id[WARP_DIRECT]
+  int64_t* wt = dyn_dw + (threadIdx.x >> 5) * 2 * WARP_DIRECT;
+  uint64_t* wi = (uint64_t*)(wt + WARP_DIRECT);
   const int wid = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * 8;
@@ -896,10 +991,10 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
       const int64_t gs = w0 + (t0 + b) * nw;
       const int n = __shfl_sync(0xffffffffu, nn, b);
       if (L.hdr->overflow) return;
-      if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-      else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-      else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid], blk_all[wid]);
-      else warp_direct_seg<8>(B, L, gs, n, pre_all[wid], blk_all[wid]);
+      if (n <= 32) warp_direct_seg<1>(B, L, gs, n, pre_all[wid], blk_all[wid], wt, wi);
+      else if (n <= 64) warp_direct_seg<2>(B, L, gs, n, pre_all[wid], blk_all[wid], wt, wi);
+      else if (n <= 128) warp_direct_seg<4>(B, L, gs, n, pre_all[wid], blk_all[wid], wt, wi);
+      else warp_direct_seg<8>(B, L, gs, n, pre_all[wid], blk_all[wid], wt, wi);
       __syncwarp();
     }
   }
@@ -2603,9 +2698,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_node_shared<<<std::min(ngroups, 148 * 2), DIRECT_NT, NS_SMEM, st>>>(
             s, L, (const NodeGroup*)groups_dev.p);
       }
-      k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, 0, st>>>(s, L);
+      k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, DW_SMEM, st>>>(s, L);
       if (warp16) {
-        k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, 0, st>>>(s, L);
+        k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, DW16_SMEM, st>>>(s, L);
         ++nl;
       }
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cdirect), st>>>(s, L);
@@ -2799,6 +2894,10 @@ cudaError_t StepRunner::configure() {
     if (e0 != cudaSuccess) return e0;
     e0 = cudaFuncSetAttribute(k_node_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)np_smem(NP_ROWS, NP_ZT_CAP));
+    if (e0 != cudaSuccess) return e0;
+    e0 = cudaFuncSetAttribute(k_direct_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DW_SMEM);
+    if (e0 != cudaSuccess) return e0;
+    e0 = cudaFuncSetAttribute(k_direct_warp16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DW16_SMEM);
     if (e0 != cudaSuccess) return e0;
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));

@@ -347,7 +347,8 @@ def main():
             "frontier_size": nfront, "ft_steps": len(st), "gpu_launches": launches * args.steps,
             "kernel_group_ms": {k: round(v, 3) for k, v in groups.items()},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot / args.steps},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot / args.steps,
+                    "ms_steps": [round(x, 2) for x in e2e_ms]},
             "clocks": clocks, "roofline": roof}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sw, sample = cpu_sample_workload(args.workload, args.cpu_seconds)

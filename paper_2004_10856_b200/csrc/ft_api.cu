@@ -293,7 +293,9 @@ int alloc_costs(ft_graph* g) {
   g->c_et = g->c_em + ned;
   const int64_t total = g->c_et + ned;
   CU(cudaSetDevice(g->dev), "cudaSetDevice");
-  CU(cudaMalloc(&g->d_costs, sizeof(int64_t) * total), "cudaMalloc(costs)");
+  // stream-ordered pool (release threshold: unlimited) -- a plain
+  // cudaMalloc/cudaFree per graph showed ~100 ms driver stalls
+  CU(cudaMallocAsync((void**)&g->d_costs, sizeof(int64_t) * total, g->stream), "cudaMallocAsync(costs)");
   std::vector<int64_t> head(maxseg + 3);
   for (int64_t i = 0; i <= maxseg; ++i) head[i] = i;
   head[maxseg + 1] = 0;
@@ -399,6 +401,11 @@ int ensure_off(ft_graph* g, int set) {
   FSet& S = g->sets[set];
   if (S.off_ok) return FT_OK;
   S.off.resize(S.nseg + 1);
+  if (S.kind == S_OP || S.kind == S_EDGE) {  // original sets: one tuple per segment (built lazily)
+    for (int64_t q = 0; q <= S.nseg; ++q) S.off[q] = q;
+    S.off_ok = true;
+    return FT_OK;
+  }
   CU(cudaMemcpy(S.off.data(), S.d_off, sizeof(int64_t) * (S.nseg + 1), cudaMemcpyDeviceToHost),
      "seg_off d2h");
   S.off_ok = true;
@@ -1232,8 +1239,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     s.kind = S_OP;
     s.a_op = i;
     s.nseg = g->K[i];
-    s.off.resize(s.nseg + 1);
-    for (int64_t q = 0; q <= s.nseg; ++q) s.off[q] = q;
+    s.off_ok = false;  // iota, built on demand (ensure_off)
     g->op_set.push_back((int)g->sets.size());
     g->sets.push_back(std::move(s));
   }
@@ -1243,8 +1249,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     s.a_op = src[e];
     s.b_op = dst[e];
     s.nseg = (int64_t)g->K[src[e]] * g->K[dst[e]];
-    s.off.resize(s.nseg + 1);
-    for (int64_t q = 0; q <= s.nseg; ++q) s.off[q] = q;
+    s.off_ok = false;  // iota, built on demand (ensure_off; C5: 9.4e6 entries)
     add_edge(g, src[e], dst[e], (int)g->sets.size());
     g->sets.push_back(std::move(s));
   }
@@ -1321,12 +1326,13 @@ void ft_graph_destroy(ft_graph* g) {
   }
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {
-    if (w.m) cudaFree(w.m);
-    if (w.t) cudaFree(w.t);
-    if (w.bp) cudaFree(w.bp);
-    if (w.off) cudaFree(w.off);
+    if (w.m) cudaFreeAsync(w.m, g->stream);
+    if (w.t) cudaFreeAsync(w.t, g->stream);
+    if (w.bp) cudaFreeAsync(w.bp, g->stream);
+    if (w.off) cudaFreeAsync(w.off, g->stream);
   }
-  if (g->d_costs) cudaFree(g->d_costs);
+  if (g->d_costs) cudaFreeAsync(g->d_costs, g->stream);
+  if (g->stream) cudaStreamSynchronize(g->stream);  // back to the pool (not the driver)
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
 }

@@ -183,9 +183,14 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, i
     }
     return;
   }
-  // levels l = 0, 1, ...: sample size until it fits the direct path
+  // levels l = 0, 1, ...: sample size until it fits the direct path.  A
+  // segment of more than cdirect blocks never fits (every block keeps >= 1
+  // sampled tuple): once the sample stops shrinking, level d has no direct
+  // work and an empty output, and level d-1 filters its whole sample against
+  // the empty staircase (one bucket per segment, exact in the bucket sorts).
   int d = -1;
-  unsigned long long samp = (unsigned long long)rel;
+  bool empty = false;
+  unsigned long long samp = (unsigned long long)rel, prev = ~0ull;
   for (int l = 0; l <= LMAX; ++l) {
     if (l > 0) {
       const int sh = level_shift(l, B.slog0, B.slog);
@@ -202,8 +207,15 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, i
       d = l;
       break;
     }
+    if (l > 0 && (samp >= prev || l == LMAX)) {
+      d = l;
+      empty = true;
+      break;
+    }
     if (lane == 0) atomicAdd(&sh_filter[l], samp);  // level l runs the filter path
+    prev = samp;
   }
+  if (empty) samp = 0;
   if (lane == 0) {
     if (d < 0) {
       atomicExch(&hdr->bad, 1ull);
@@ -983,7 +995,13 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
   for (int64_t t0 = 0; w0 + t0 * nw < B.nseg; t0 += tw) {
     const int64_t g = w0 + (t0 + lane) * nw;
     int nn = 0;
-    if (lane < tw && g < B.nseg && L.seg_d[g] == L.level) nn = L.seg_n[g];
+    if (lane < tw && g < B.nseg && L.seg_d[g] == L.level) {
+      nn = L.seg_n[g];
+      if (nn == 0) {  // empty-staircase level of a very wide segment (k_plan)
+        L.out.start[g] = 0;
+        L.out.cnt[g] = 0;
+      }
+    }
     unsigned bal = __ballot_sync(0xffffffffu, nn > 0 && nn <= WARP_DIRECT);
     while (bal) {
       const int b = __ffs(bal) - 1;

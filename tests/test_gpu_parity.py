@@ -223,3 +223,31 @@ def test_partition_invariance_pack_reuse():
     tok = out.stdout.split()
     assert int(tok[tok.index("ROWS") + 1]) > 0
     assert int(tok[tok.index("BAD") + 1]) == 0, out.stdout
+
+
+def _wide(K, edges, seed=0, hi=1 << 30):
+    """Explicit graph with the given configuration counts and edges."""
+    from synth.graphs import Workload
+    rng = np.random.default_rng(seed)
+    src = np.array([a for a, _ in edges], np.int32)
+    dst = np.array([b for _, b in edges], np.int32)
+    op_m = [rng.integers(0, hi, k).astype(np.int64) for k in K]
+    op_t = [rng.integers(0, hi, k).astype(np.int64) for k in K]
+    edge_t = [rng.integers(0, hi, K[a] * K[b]).astype(np.int64) for a, b in edges]
+    return Workload(f"wide{K}", np.array(K, np.int32), src, dst, op_m, op_t, edge_t).check()
+
+
+@pytest.mark.parametrize("K,edges", [
+    ([4096], []),                                   # final reduce over 4096 singleton blocks
+    ([4096, 4096], [(0, 1)]),                       # LDP: 4096 segments x 4096 blocks
+    ([2000, 3000], [(0, 1)]),
+    ([1, 4096, 1], [(0, 1), (1, 2)]),
+    ([64, 4096, 64], [(0, 1), (1, 2), (0, 2)]),     # node elimination over 4096 blocks
+    ([300, 300], [(0, 1), (0, 1), (0, 1)]),         # parallel multi-edges (Eq. 5 merges)
+    ([1, 1, 1], [(0, 1), (1, 2), (0, 2)]),          # K = 1 everywhere
+])
+def test_extreme_shapes(ft, K, edges):
+    """K up to the documented maximum (4096) and degenerate graphs: segments
+    with more union terms than the direct capacity take the empty-staircase
+    level (k_plan) and are reduced exactly by the bucket sorts."""
+    compare(ft, _wide(K, edges), strategies=8)

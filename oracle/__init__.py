@@ -26,7 +26,7 @@ LIB_PATH = os.path.join(_HERE, "liboracle_ft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -6, -7, -8
 NODE, EDGE, AUTO = 1, 2, 3
-STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final"}
+STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair"}
 
 
 def build(force: bool = False) -> str:
@@ -59,6 +59,7 @@ def lib():
         L.oft_set_edge_costs.argtypes = [C.c_void_p, C.c_int32, P64, P64]
         L.oft_eliminate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P32]
         L.oft_frontier.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
+        L.oft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
         L.oft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
         L.oft_num_steps.argtypes = [C.c_void_p]
         L.oft_num_steps.restype = C.c_int64
@@ -129,15 +130,16 @@ class Graph:
         self._chk(self._L.oft_eliminate(self.h, kind, id, C.byref(ne)))
         return ne.value
 
-    def frontier(self):
+    def frontier(self, algo="ldp"):
+        """Final frontier by FT-LDP (Alg. 3) or, algo="elim", FT-Elimination."""
+        fn = self._L.oft_frontier if algo == "ldp" else self._L.oft_frontier_elim
         n = C.c_int64(0)
-        rc = self._L.oft_frontier(self.h, 0, None, None, C.byref(n))
+        rc = fn(self.h, 0, None, None, C.byref(n))
         if rc not in (OK, ESIZE):
             self._chk(rc)
         m = np.empty(n.value, np.int64)
         t = np.empty(n.value, np.int64)
-        self._chk(self._L.oft_frontier(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64),
-                                       C.byref(n)))
+        self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
 
     def strategy(self, idx):

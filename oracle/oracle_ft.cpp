@@ -95,6 +95,7 @@ struct oft_graph {
   std::vector<int> pos0;         // position in the original graph's topological order (R9)
   bool started = false;
   bool have_final = false;
+  int final_mode = 0;  // 1 = LDP (Alg. 3), 2 = FT-Elimination
   int final_set = -1;
   std::string err;
 };
@@ -135,6 +136,11 @@ void block_segs(const Step& s, int64_t sigma, int64_t k, int64_t* sx, int64_t* s
     }
     case OFT_STEP_FINAL:  // Alg.3 line 9 P:648: reduce(U_s CF(o_n, s))
       *sx = k; *sy = 0; *sz = 0;
+      break;
+    case OFT_STEP_PAIR:  // FT-Elimination P:628: k = s_1 * K_n + s_n over the 2-op graph
+      *sx = k;             // F(e_1n, s_1, s_n)
+      *sy = k / s.KB;      // F(o_1, s_1)
+      *sz = k % s.KB;      // F(o_n, s_n)
       break;
     default:
       *sx = *sy = *sz = 0;
@@ -475,6 +481,47 @@ int run_ldp(oft_graph* g) {
   if (rc) return rc;
   g->final_set = g->steps.back().out;
   g->have_final = true;
+  g->final_mode = 1;
+  return OFT_OK;
+}
+
+// FT-Elimination (Theorem 2): on the linear graph,
+// node-eliminate (Eq.4) the second op of the remaining chain until only
+// o_1 and o_n are left, then find the frontier of the two-op graph by
+// enumerating every configuration pair: reduce(U_{s_1,s_n} F(e_1n,s_1,s_n)
+// (x) F(o_1,s_1) (x) F(o_n,s_n)).  One op: reduce(U_s F(o_1, s)).
+int run_elim(oft_graph* g) {
+  std::vector<int> chain, ce;
+  int rc = chain_of(g, &chain, &ce);
+  if (rc) return rc;
+  for (size_t i = 1; i + 1 < chain.size(); ++i) {
+    Adj a = build_adj(g);
+    if ((rc = do_node(g, a, chain[i], nullptr))) return rc;
+  }
+  Step f;
+  if (chain.size() == 1) {
+    f.kind = OFT_STEP_FINAL;
+    f.X = g->op_set[chain[0]];
+    f.Y = 0;
+    f.Z = 0;
+    f.KA = g->K[chain[0]];
+    f.nblk = f.KA;
+  } else {
+    Adj a = build_adj(g);
+    f.kind = OFT_STEP_PAIR;
+    f.X = g->edges[a.out[chain[0]][0]].set;
+    f.Y = g->op_set[chain[0]];
+    f.Z = g->op_set[chain.back()];
+    f.KA = g->K[chain[0]];
+    f.KB = g->K[chain.back()];
+    f.nblk = f.KA * f.KB;
+  }
+  f.nseg = 1;
+  rc = run_step(g, f);
+  if (rc) return rc;
+  g->final_set = g->steps.back().out;
+  g->have_final = true;
+  g->final_mode = 2;
   return OFT_OK;
 }
 
@@ -650,7 +697,24 @@ int oft_frontier(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int6
   if (!g || !n_out) return OFT_EINVAL;
   int rc = check_started(g);
   if (rc) return rc;
+  if (g->have_final && g->final_mode != 1) return fail(g, OFT_ESTATE, "frontier computed by FT-Elimination");
   if (!g->have_final && (rc = run_ldp(g))) return rc;
+  const Frontier& F = g->sets[g->final_set].seg[0];
+  *n_out = (int64_t)F.size();
+  if (cap < (int64_t)F.size()) return OFT_ESIZE;
+  for (size_t i = 0; i < F.size(); ++i) {
+    if (m_out) m_out[i] = F[i].m;
+    if (t_out) t_out[i] = F[i].t;
+  }
+  return OFT_OK;
+}
+
+int oft_frontier_elim(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out) {
+  if (!g || !n_out) return OFT_EINVAL;
+  int rc = check_started(g);
+  if (rc) return rc;
+  if (g->have_final && g->final_mode != 2) return fail(g, OFT_ESTATE, "frontier computed by LDP");
+  if (!g->have_final && (rc = run_elim(g))) return rc;
   const Frontier& F = g->sets[g->final_set].seg[0];
   *n_out = (int64_t)F.size();
   if (cap < (int64_t)F.size()) return OFT_ESIZE;

@@ -33,7 +33,7 @@ enum { OFT_OK = 0, OFT_EINVAL = -1, OFT_ESTATE = -2, OFT_EPRECOND = -3, OFT_ENOM
 enum { OFT_NODE = 1, OFT_EDGE = 2, OFT_AUTO = 3 };
 /* step kinds reported by oft_step_info */
 enum { OFT_STEP_NODE = 1, OFT_STEP_EDGE = 2, OFT_STEP_FOLD = 3, OFT_STEP_LDP = 4,
-       OFT_STEP_FINAL = 5 };
+       OFT_STEP_FINAL = 5, OFT_STEP_PAIR = 6 };
 
 typedef struct oft_graph oft_graph;
 
@@ -52,6 +52,11 @@ int oft_set_edge_costs(oft_graph* g, int32_t edge, const int64_t* m, const int64
 int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);
 /* LDP + final reduce (cached).  Two-call size pattern: OFT_ESIZE with *n_out. */
 int oft_frontier(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
+/* FT-Elimination instead of LDP: node-eliminate the
+ * chain's second op until two ops remain, then reduce over every
+ * configuration pair (s_1, s_n) (cached; the graph then has a frontier and
+ * oft_frontier returns OFT_ESTATE, and vice versa). */
+int oft_frontier_elim(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
 /* Unrolled strategy (config per original op) of final-frontier tuple idx. */
 int oft_strategy(oft_graph* g, int64_t tuple_idx, int32_t* cfg_out);
 int64_t oft_num_steps(const oft_graph* g);

@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline budget")
     ap.add_argument("--details", action="store_true", help="print per-kind breakdown to stderr")
+    ap.add_argument("--algo", choices=["ldp", "elim"], default="ldp",
+                    help="final frontier by FT-LDP (Alg. 3, default) or FT-Elimination (P:628)")
     return ap.parse_args()
 
 
@@ -130,10 +132,15 @@ def cpu_sample_workload(name, seconds):
     return G.get(name), f"{name} full graph"
 
 
-def oracle_run(w, threads):
+ALGO = {"ldp": "FT-LDP (Alg. 3)", "elim": "FT-Elimination (P:628)"}
+
+
+def oracle_run(w, threads, algo="ldp"):
     import oracle
     t0 = time.perf_counter()
-    g, m, t = oracle.run_ft(w, threads=threads)
+    g = oracle.load(w, threads)
+    g.eliminate()
+    m, t = g.frontier(algo=algo)
     dt = time.perf_counter() - t0
     tuples = sum(g.step_info(s)["tuples"] for s in range(g.num_steps()))
     return tuples, dt, len(m)
@@ -148,12 +155,13 @@ def run_reference(args):
     threads = len(os.sched_getaffinity(0))
     w, _cfg = workload_config(args.workload)
     _, cfg = workload_config(args.workload)
+    cfg["algo"] = ALGO[args.algo]
     sw, sample = cpu_sample_workload(args.workload, args.cpu_seconds)
     for _ in range(max(0, min(args.warmup, 1))):
-        oracle_run(sw, threads)
+        oracle_run(sw, threads, args.algo)
     times, tuples = [], 0
     for _ in range(args.steps):
-        tp, dt, _n = oracle_run(sw, threads)
+        tp, dt, _n = oracle_run(sw, threads, args.algo)
         times.append(dt)
         tuples = tp
     tot = sum(times)
@@ -200,7 +208,8 @@ def main():
         dist.broadcast(uid, 0)
         comm = ft.nccl_comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()), local)
     w, cfg = workload_config(args.workload)
-    cfg.update({"graphs_per_step": 1, "parallelism": f"config-pair sharding x{world} + NCCL all-gather",
+    cfg.update({"algo": ALGO[args.algo], "graphs_per_step": 1,
+                "parallelism": f"config-pair sharding x{world} + NCCL all-gather",
                 "l2_flush": not args.no_flush})
     stream = torch.cuda.current_stream()
     kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm)
@@ -225,7 +234,7 @@ def main():
     for _ in range(args.warmup):
         g = search(False)
         g.eliminate()
-        g.frontier()
+        g.frontier(algo=args.algo)
         g.close()
     torch.cuda.synchronize()
 
@@ -241,7 +250,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         g.eliminate()
-        m, t = g.frontier()
+        m, t = g.frontier(algo=args.algo)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -288,7 +297,7 @@ def main():
         e0.record(stream)
         g = ft.load(w, costs=pinned, **kw)
         g.eliminate()
-        m, t = g.frontier()
+        m, t = g.frontier(algo=args.algo)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -353,7 +362,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sw, sample = cpu_sample_workload(args.workload, args.cpu_seconds)
         threads = len(os.sched_getaffinity(0))
-        tp, dt, _ = oracle_run(sw, threads)
+        tp, dt, _ = oracle_run(sw, threads, args.algo)
         line["cpu_baseline"] = {"value": tp / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "sample": sample + f"; {tp} product tuples in {dt:.2f} s"}
     if args.details and rank == 0:

@@ -60,7 +60,8 @@ enum {
 enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3 };
 
 /* Step kinds in ft_step_stats records. */
-enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5 };
+enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5,
+       FT_STEP_PAIR = 6 /* FT-Elimination's reduce over configuration pairs */ };
 
 typedef struct ft_graph ft_graph; /* opaque, library-owned */
 
@@ -152,6 +153,16 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);
  * (m, t) unique; cap = capacity of m_out/t_out (host).  FT_EPRECOND if the
  * remaining graph is not a chain. */
 int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
+
+/* FT-Elimination (Theorem 2) instead of LDP: on the
+ * remaining chain o_1 -> ... -> o_n, node-eliminate (Eq. 4) the second op
+ * until two ops remain, then reduce over every configuration pair
+ * U_{s_1,s_n} F(e_1n,s_1,s_n) (x) F(o_1,s_1) (x) F(o_n,s_n) (FT_STEP_PAIR:
+ * one segment, K_1*K_n blocks).  Same output contract as ft_frontier (the
+ * (m, t) frontier is identical: both are exact); computed once and cached.
+ * A graph has one final frontier: after ft_frontier_elim, ft_frontier
+ * returns FT_ESTATE, and vice versa.  FT_EPRECOND if not a chain. */
+int ft_frontier_elim(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
 
 /* Unroll: configuration index of every ORIGINAL operator for final
  * frontier tuple tuple_idx; cfg_out[n_ops] host.  Requires ft_frontier. */

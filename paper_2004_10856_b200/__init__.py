@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "libft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, ECUDA, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8
 NODE, EDGE, AUTO = 1, 2, 3
-STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final"}
+STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair"}
 
 
 class FTError(RuntimeError):
@@ -66,6 +66,7 @@ def _load():
     L.ft_set_edge_costs.argtypes = [C.c_void_p, C.c_int32, P64, P64]
     L.ft_eliminate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P32]
     L.ft_frontier.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
+    L.ft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
     L.ft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
     L.ft_get_stats.argtypes = [C.c_void_p, C.POINTER(ft_step_stats), C.c_int64, P64]
     L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
@@ -86,7 +87,7 @@ def _load():
 
 lib = _load()
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
-           "ft_eliminate", "ft_frontier", "ft_strategy", "ft_get_stats", "ft_step_output",
+           "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version"]
 
@@ -177,14 +178,17 @@ class Graph:
         self._chk(lib.ft_eliminate(self.h, kind, id, C.byref(ne)))
         return ne.value
 
-    def frontier(self):
+    def frontier(self, algo: str = "ldp"):
+        """Final frontier by FT-LDP (Alg. 3, ft_frontier) or, with algo="elim",
+        FT-Elimination (P:628, ft_frontier_elim)."""
+        fn = lib.ft_frontier if algo == "ldp" else lib.ft_frontier_elim
         n = C.c_int64(0)
-        rc = lib.ft_frontier(self.h, 0, None, None, C.byref(n))
+        rc = fn(self.h, 0, None, None, C.byref(n))
         if rc not in (OK, ESIZE):
             self._chk(rc)
         m = np.empty(n.value, np.int64)
         t = np.empty(n.value, np.int64)
-        self._chk(lib.ft_frontier(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
+        self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
 
     def strategy(self, idx: int) -> np.ndarray:

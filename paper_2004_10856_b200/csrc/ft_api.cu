@@ -105,6 +105,7 @@ struct ft_graph {
   std::vector<char> op_ok, e_ok;
   std::vector<char> e_mzero;  // original edge has m = 0 everywhere (Eq. 2)
   bool started = false, have_final = false;
+  int final_mode = 0;  // 1 = LDP (Alg. 3), 2 = FT-Elimination
   int final_set = -1;
   std::vector<int64_t> final_m, final_t;
   int poisoned = 0;
@@ -384,6 +385,8 @@ void host_block_segs(const StepRec& r, int64_t sg, int64_t k, int64_t& sx, int64
     sx = k * r.KB + sg; sy = k; sz = sg;
   } else if (r.kind == ftk::K_FINAL) {
     sx = k; sy = 0; sz = 0;
+  } else if (r.kind == ftk::K_PAIR) {
+    sx = k; sy = k / r.KB; sz = k % r.KB;
   } else {
     sx = sg; sy = sg; sz = 0;
   }
@@ -1024,9 +1027,8 @@ int auto_step(ft_graph* g) {
   return 0;
 }
 
-// Alg. 3 (P:635-652) on the remaining chain, then the final reduce (line 9).
-int run_ldp(ft_graph* g) {
-  std::vector<int> chain, ce;
+// The live graph as a chain o_1 -> ... -> o_n (LDP / FT-Elimination precondition).
+int linear_chain(ft_graph* g, std::vector<int>& chain, std::vector<int>& ce) {
   int src = -1, live = 0;
   for (int v = 0; v < g->n_ops; ++v) {
     if (!g->op_alive[v]) continue;
@@ -1048,6 +1050,34 @@ int run_ldp(ft_graph* g) {
     v = d;
   }
   if ((int)chain.size() != live) return setf(g, FT_EPRECOND, "graph is not linear (disconnected)");
+  return FT_OK;
+}
+
+// Runs the scheduled steps and fetches the final frontier (one segment).
+int finish_final(ft_graph* g, int out, int mode) {
+  int rc = flush(g);
+  if (rc) return rc;
+  g->final_set = out;
+  if ((rc = ensure_off(g, out))) return rc;
+  const FSet& F = g->sets[out];
+  int64_t n = F.off[1];
+  g->final_m.resize(n);
+  g->final_t.resize(n);
+  if (n) {
+    CU(cudaMemcpyAsync(g->final_m.data(), F.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    CU(cudaMemcpyAsync(g->final_t.data(), F.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    CU(cudaStreamSynchronize(g->stream), "d2h");
+  }
+  g->have_final = true;
+  g->final_mode = mode;
+  return FT_OK;
+}
+
+// Alg. 3 (P:635-652) on the remaining chain, then the final reduce (line 9).
+int run_ldp(ft_graph* g) {
+  std::vector<int> chain, ce;
+  int rc = linear_chain(g, chain, ce);
+  if (rc) return rc;
   int cf = g->op_set[chain[0]];  // CF(o_1, s) = F(o_1, s)  (line 3)
   for (size_t i = 1; i < chain.size(); ++i) {
     StepRec r;
@@ -1071,22 +1101,38 @@ int run_ldp(ft_graph* g) {
   f.KA = g->K[chain.back()];
   f.nseg = 1;
   f.nblk = f.KA;
-  int out = schedule(g, f);
-  int rc = flush(g);
+  return finish_final(g, schedule(g, f), 1);
+}
+
+// FT-Elimination (Theorem 2): node-eliminate (Eq. 4) the
+// second op of the remaining chain until o_1 and o_n are left, then reduce
+// over every configuration pair: U_{s_1,s_n} F(e_1n,s_1,s_n) (x) F(o_1,s_1)
+// (x) F(o_n,s_n) (one segment, K_1*K_n blocks).  One op: reduce(U_s F(o_1,s)).
+int run_elim(ft_graph* g) {
+  std::vector<int> chain, ce;
+  int rc = linear_chain(g, chain, ce);
   if (rc) return rc;
-  g->final_set = out;
-  if ((rc = ensure_off(g, out))) return rc;
-  const FSet& F = g->sets[out];
-  int64_t n = F.off[1];
-  g->final_m.resize(n);
-  g->final_t.resize(n);
-  if (n) {
-    CU(cudaMemcpyAsync(g->final_m.data(), F.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
-    CU(cudaMemcpyAsync(g->final_t.data(), F.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
-    CU(cudaStreamSynchronize(g->stream), "d2h");
+  for (size_t i = 1; i + 1 < chain.size(); ++i)
+    if ((rc = do_node(g, chain[i], nullptr))) return rc;
+  StepRec f;
+  if (chain.size() == 1) {
+    f.kind = ftk::K_FINAL;
+    f.X = g->op_set[chain[0]];
+    f.Y = 0;
+    f.Z = 0;
+    f.KA = g->K[chain[0]];
+    f.nblk = f.KA;
+  } else {
+    f.kind = ftk::K_PAIR;
+    f.X = g->edges[*g->out_e[chain[0]].begin()].set;
+    f.Y = g->op_set[chain[0]];
+    f.Z = g->op_set[chain.back()];
+    f.KA = g->K[chain[0]];
+    f.KB = g->K[chain.back()];
+    f.nblk = f.KA * f.KB;
   }
-  g->have_final = true;
-  return FT_OK;
+  f.nseg = 1;
+  return finish_final(g, schedule(g, f), 2);
 }
 
 // ---- unroll -----------------------------------------------------------
@@ -1153,6 +1199,8 @@ int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_
         sx = k * r.KB + it.seg; sy = k; sz = it.seg;
       } else if (r.kind == ftk::K_FINAL) {
         sx = k; sy = 0; sz = 0;
+      } else if (r.kind == ftk::K_PAIR) {
+        sx = k; sy = k / r.KB; sz = k % r.KB;
       } else {
         sx = it.seg; sy = it.seg; sz = 0;
       }
@@ -1460,7 +1508,23 @@ int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_
   if (g->poisoned) return g->poisoned;
   int rc = start(g);
   if (rc) return rc;
+  if (g->have_final && g->final_mode != 1) return setf(g, FT_ESTATE, "frontier computed by FT-Elimination");
   if (!g->have_final && (rc = run_ldp(g))) return rc;
+  const int64_t n = (int64_t)g->final_m.size();
+  *n_out = n;
+  if (cap < n) return FT_ESIZE;
+  if (m_out) std::memcpy(m_out, g->final_m.data(), sizeof(int64_t) * n);
+  if (t_out) std::memcpy(t_out, g->final_t.data(), sizeof(int64_t) * n);
+  return FT_OK;
+}
+
+int ft_frontier_elim(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out) {
+  if (!g || !n_out) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  int rc = start(g);
+  if (rc) return rc;
+  if (g->have_final && g->final_mode != 2) return setf(g, FT_ESTATE, "frontier computed by LDP");
+  if (!g->have_final && (rc = run_elim(g))) return rc;
   const int64_t n = (int64_t)g->final_m.size();
   *n_out = n;
   if (cap < n) return FT_ESIZE;

@@ -251,3 +251,44 @@ def test_extreme_shapes(ft, K, edges):
     with more union terms than the direct capacity take the empty-staircase
     level (k_plan) and are reduced exactly by the bucket sorts."""
     compare(ft, _wide(K, edges), strategies=8)
+
+
+def compare_elim(ft, w, threads=8, strategies=16):
+    """FT-Elimination: every step bit-identical to the oracle's, and
+    the frontier equal to FT-LDP's (both exact)."""
+    og = oracle.load(w, threads)
+    og.eliminate()
+    om, ot = og.frontier(algo="elim")
+    gg = ft.load(w, keep_all=True)
+    gg.eliminate()
+    gm, gt = gg.frontier(algo="elim")
+    st = gg.stats()
+    assert og.num_steps() == len(st)
+    for s in range(len(st)):
+        assert og.step_info(s)["kind"] == st[s]["kind"], s
+        for x, y in zip(og.step_output(s), gg.step_output(s)):
+            assert np.array_equal(x, y), (w.name, s)
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+    for i in np.linspace(0, len(om) - 1, strategies).astype(int):
+        assert np.array_equal(og.strategy(int(i)), gg.strategy(int(i)))
+    lg = ft.load(w)
+    lg.eliminate()
+    lm, lt = lg.frontier()
+    assert np.array_equal(lm, gm) and np.array_equal(lt, gt)
+    return st
+
+
+def test_ft_elimination(ft):
+    for seed in range(20):
+        compare_elim(ft, G.random_sp(700 + seed, n_ops=3 + seed % 10, kmax=6, cost_hi=1 << 12))
+    for var in ("chain", "parallel", "diamond"):
+        compare_elim(ft, G.c1(3, var))
+    compare_elim(ft, G.c2())
+    compare_elim(ft, G.c3())
+    st = compare_elim(ft, G.c4(layers=2))
+    assert st[-1]["kind"] == "pair" and st[-1]["nblk"] == 36 * 36
+    with pytest.raises(ft.FTError):
+        g = ft.load(G.c1(0, "chain"))
+        g.eliminate()
+        g.frontier(algo="elim")
+        g.frontier()  # the graph's frontier was computed by FT-Elimination

@@ -137,6 +137,12 @@ void block_segs(const Step& s, int64_t sigma, int64_t k, int64_t* sx, int64_t* s
     case OFT_STEP_FINAL:  // Alg.3 line 9 P:648: reduce(U_s CF(o_n, s))
       *sx = k; *sy = 0; *sz = 0;
       break;
+    case OFT_STEP_BRANCH: {  // Eq.6 P:606-613 (reading R14): sigma = s_h, k = s_i
+      *sx = sigma;                                            // F(o_h, s_h)
+      *sy = s.KC ? k * s.KA + sigma : sigma * s.KB + k;       // F(e, s_i, s_h) | F(e, s_h, s_i)
+      *sz = k;                                                // F(o_i, s_i)
+      break;
+    }
     case OFT_STEP_PAIR:  // FT-Elimination P:628: k = s_1 * K_n + s_n over the 2-op graph
       *sx = k;             // F(e_1n, s_1, s_n)
       *sy = k / s.KB;      // F(o_1, s_1)
@@ -362,6 +368,35 @@ int do_fold(oft_graph* g, const Adj& a, int src, const std::vector<int>& topo) {
   return OFT_OK;
 }
 
+// Eq. 6, reading R14: o_i's only remaining edge is e (to or from
+// o_h), so it is merged into o_h.  The paper keeps composite configurations
+// (s_h, s_i); since o_i reaches the rest of the graph only through e, the
+// union over s_i is reduced at once -- the same (m, t) frontier:
+//   F(o_h, s_h) <- reduce(U_{s_i} F(o_h, s_h) (x) F(e, .) (x) F(o_i, s_i)).
+int do_branch(oft_graph* g, const Adj& a, int i) {
+  const bool src = a.in[i].empty();  // o_i -> o_h, else o_h -> o_i
+  const int e = src ? a.out[i][0] : a.in[i][0];
+  const int h = src ? g->edges[e].dst : g->edges[e].src;
+  Step s;
+  s.kind = OFT_STEP_BRANCH;
+  s.X = g->op_set[h];
+  s.Y = g->edges[e].set;
+  s.Z = g->op_set[i];
+  s.KA = g->K[h];
+  s.KB = g->K[i];
+  s.KC = src ? 1 : 0;
+  s.nseg = g->K[h];
+  s.nblk = g->K[i];
+  int rc = run_step(g, s);
+  if (rc) return rc;
+  int so = g->steps.back().out;
+  g->sets[so].a_op = h;
+  g->op_set[h] = so;
+  g->edges[e].alive = false;
+  g->op_alive[i] = false;
+  return OFT_OK;
+}
+
 int check_started(oft_graph* g) {
   if (g->started) return OFT_OK;
   for (int i = 0; i < g->n_ops; ++i)
@@ -410,7 +445,14 @@ int auto_one(oft_graph* g) {
       int rc = do_node(g, a, i, nullptr);
       return rc ? rc : 1;
     }
-  // (c) fold a K=1 source (exact Eq. 7).
+  // (c) branch elimination (Eq. 6): topologically-first unmarked op whose
+  //     only edge connects it to one neighbour.
+  for (int i : topo)
+    if (g->op_alive[i] && !marked[i] && a.in[i].size() + a.out[i].size() == 1) {
+      int rc = do_branch(g, a, i);
+      return rc ? rc : 1;
+    }
+  // (d) fold a K=1 source (exact Eq. 7).
   for (int i : topo)
     if (g->op_alive[i] && g->K[i] == 1 && a.in[i].empty() && !a.out[i].empty()) {
       int rc = do_fold(g, a, i, topo);

@@ -413,6 +413,25 @@ def get(name: str, **kw) -> Workload:
     return CONFIGS[name](**kw)
 
 
+def random_leafy(seed: int, n_ops: int = 5, kmax: int = 3, leaves: int = 2, cost_hi: int = 8,
+                 edge_mem: bool = False) -> Workload:
+    """A random SP graph with `leaves` extra ops attached by a single edge
+    (an input feeding, or an output read from, a random op) -- shapes that
+    need branch elimination (Eq. 6).  Costs U{0..cost_hi}, seeded."""
+    base = random_sp(seed, n_ops=n_ops, kmax=kmax, cost_hi=cost_hi, edge_mem=edge_mem)
+    rng = np.random.default_rng(seed + 7919)
+    K = [int(k) for k in base.n_cfgs]
+    edges = list(zip(base.src.tolist(), base.dst.tolist()))
+    for _ in range(leaves):
+        h = int(rng.integers(0, len(K)))
+        i = len(K)
+        K.append(int(rng.integers(1, kmax + 1)))
+        edges.append((i, h) if rng.integers(0, 2) == 0 else (h, i))
+    w = random_graph(len(K), edges, K, seed + 104729, cost_hi=cost_hi, edge_mem=edge_mem,
+                     name=f"leafy{seed}")
+    return w
+
+
 def random_sp(seed: int, n_ops: int = 6, kmax: int = 3, p_parallel: float = 0.35,
               p_mask: float = 0.3, cost_hi: int = 8, edge_mem: bool = False) -> Workload:
     """Small random two-terminal series-parallel DAG (brute-force fixtures).

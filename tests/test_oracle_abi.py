@@ -38,8 +38,9 @@ def test_errors():
 
 
 def test_not_linear():
-    # two independent sources feeding one sink with K>1 cannot be linearised
-    w = G.random_graph(3, [(0, 2), (1, 2)], 2, 0)
+    # the bridge DAG (non-series-parallel, every op of degree >= 2, K > 1):
+    # no node, edge, K=1-fold or branch elimination applies
+    w = G.random_graph(4, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], 2, 0)
     g = oracle.load(w)
     g.eliminate()
     with pytest.raises(oracle.OracleError) as e:

@@ -61,7 +61,8 @@ enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3 };
 
 /* Step kinds in ft_step_stats records. */
 enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5,
-       FT_STEP_PAIR = 6 /* FT-Elimination's reduce over configuration pairs */ };
+       FT_STEP_PAIR = 6 /* FT-Elimination's reduce over configuration pairs */,
+       FT_STEP_BRANCH = 7 /* branch elimination, Eq. 6 (merge a one-edge op into its neighbour) */ };
 
 typedef struct ft_graph ft_graph; /* opaque, library-owned */
 
@@ -143,7 +144,11 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
  *  FT_EDGE: id = edge; merged with the lowest-id other edge of the same
  *           (src, dst) (Eq. 5, binary; X = lower id) -> new edge.
  *  FT_AUTO: id ignored; the deterministic policy of DESIGN.md R9 until no
- *           exact elimination applies.
+ *           exact elimination applies: parallel edges (Eq. 5), node
+ *           elimination (Eq. 4), the K=1 source fold (Eq. 7, exact for
+ *           K=1), then branch elimination (Eq. 6: an unmarked op whose only
+ *           edge joins it to o_h is merged into o_h, reducing over its
+ *           configurations -- reading R14).
  * New edge ids are n_edges, n_edges+1, ... in creation order (*new_edge,
  * nullable).  Errors: FT_EINVAL, FT_ESTATE, FT_EPRECOND, FT_ENOMEM, FT_ECUDA. */
 int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);

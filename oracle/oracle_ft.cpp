@@ -445,17 +445,18 @@ int auto_one(oft_graph* g) {
       int rc = do_node(g, a, i, nullptr);
       return rc ? rc : 1;
     }
-  // (c) branch elimination (Eq. 6): topologically-first unmarked op whose
-  //     only edge connects it to one neighbour.
-  for (int i : topo)
-    if (g->op_alive[i] && !marked[i] && a.in[i].size() + a.out[i].size() == 1) {
-      int rc = do_branch(g, a, i);
-      return rc ? rc : 1;
-    }
-  // (d) fold a K=1 source (exact Eq. 7).
+  // (c) fold a K=1 source (exact Eq. 7).
   for (int i : topo)
     if (g->op_alive[i] && g->K[i] == 1 && a.in[i].empty() && !a.out[i].empty()) {
       int rc = do_fold(g, a, i, topo);
+      return rc ? rc : 1;
+    }
+  // (d) branch elimination (Eq. 6): topologically-first unmarked op whose
+  //     only edge connects it to one neighbour (after the K=1 fold, which keeps
+  //     the backbone intact: DESIGN.md R14).
+  for (int i : topo)
+    if (g->op_alive[i] && !marked[i] && a.in[i].size() + a.out[i].size() == 1) {
+      int rc = do_branch(g, a, i);
       return rc ? rc : 1;
     }
   return 0;

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "libft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, ECUDA, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8
 NODE, EDGE, AUTO = 1, 2, 3
-STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair"}
+STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch"}
 
 
 class FTError(RuntimeError):

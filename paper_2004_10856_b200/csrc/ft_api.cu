@@ -92,6 +92,7 @@ struct ft_graph {
   std::vector<int> pos0, order0;
   std::set<std::pair<int, int>> live_ops;   // (pos0, op)
   std::set<std::pair<int, int>> one_one;    // live ops with one in- and one out-edge
+  std::set<std::pair<int, int>> leaf;       // live ops with exactly one edge (branch elimination)
   std::set<std::pair<int, int>> k1src;      // live K=1 sources with out-edges
   std::map<std::pair<int, int>, std::set<int>> pair_edges;  // (src, dst) -> live edges
   std::set<std::pair<int, int>> multi;      // (pos0 src, pos0 dst) with >= 2 live edges
@@ -203,12 +204,14 @@ void refresh(ft_graph* g, int v) {
   const std::pair<int, int> key{g->pos0[v], v};
   g->one_one.erase(key);
   g->k1src.erase(key);
+  g->leaf.erase(key);
   if (!g->op_alive[v]) {
     g->live_ops.erase(key);
     return;
   }
   if (g->in_e[v].size() == 1 && g->out_e[v].size() == 1) g->one_one.insert(key);
   if (g->K[v] == 1 && g->in_e[v].empty() && !g->out_e[v].empty()) g->k1src.insert(key);
+  if (g->in_e[v].size() + g->out_e[v].size() == 1) g->leaf.insert(key);
 }
 
 void kill_edge(ft_graph* g, int e) {
@@ -387,6 +390,8 @@ void host_block_segs(const StepRec& r, int64_t sg, int64_t k, int64_t& sx, int64
     sx = k; sy = 0; sz = 0;
   } else if (r.kind == ftk::K_PAIR) {
     sx = k; sy = k / r.KB; sz = k % r.KB;
+  } else if (r.kind == ftk::K_BRANCH) {
+    sx = sg; sy = r.KC ? k * r.KA + sg : sg * r.KB + k; sz = k;
   } else {
     sx = sg; sy = sg; sz = 0;
   }
@@ -1001,6 +1006,31 @@ int do_fold(ft_graph* g, int src) {
   return FT_OK;
 }
 
+// Eq. 6, reading R14: o_i's only edge e connects it to o_h; it is
+// merged into o_h and the union over s_i is reduced at once:
+//   F(o_h, s_h) <- reduce(U_{s_i} F(o_h, s_h) (x) F(e, .) (x) F(o_i, s_i)).
+int do_branch(ft_graph* g, int i) {
+  const bool src = g->in_e[i].empty();  // o_i -> o_h, else o_h -> o_i
+  const int e = src ? *g->out_e[i].begin() : *g->in_e[i].begin();
+  const int h = src ? g->edges[e].dst : g->edges[e].src;
+  StepRec r;
+  r.kind = ftk::K_BRANCH;
+  r.X = g->op_set[h];
+  r.Y = g->edges[e].set;
+  r.Z = g->op_set[i];
+  r.KA = g->K[h];
+  r.KB = g->K[i];
+  r.KC = src ? 1 : 0;
+  r.nseg = g->K[h];
+  r.nblk = g->K[i];
+  int out = schedule(g, r);
+  g->sets[out].a_op = h;
+  g->op_set[h] = out;
+  kill_edge(g, e);
+  kill_op(g, i);
+  return FT_OK;
+}
+
 // One FT_AUTO elimination (R9).  1 = scheduled, 0 = none applies, <0 error.
 int auto_step(ft_graph* g) {
   mark_backbone(g);
@@ -1019,11 +1049,18 @@ int auto_step(ft_graph* g) {
       int rc = do_node(g, kv.second, nullptr);
       return rc ? rc : 1;
     }
-  // (c) K=1 source fold
+  // (c) K=1 source fold (Eq. 7, exact for K=1)
   if (!g->k1src.empty()) {
     int rc = do_fold(g, g->k1src.begin()->second);
     return rc ? rc : 1;
   }
+  // (d) branch elimination (Eq. 6): topologically first unmarked op with one
+  //     edge (after the fold, which keeps the backbone intact: DESIGN.md R14)
+  for (const auto& kv : g->leaf)
+    if (g->mark_stamp[kv.second] != g->stamp) {
+      int rc = do_branch(g, kv.second);
+      return rc ? rc : 1;
+    }
   return 0;
 }
 
@@ -1201,6 +1238,8 @@ int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_
         sx = k; sy = 0; sz = 0;
       } else if (r.kind == ftk::K_PAIR) {
         sx = k; sy = k / r.KB; sz = k % r.KB;
+      } else if (r.kind == ftk::K_BRANCH) {
+        sx = it.seg; sy = r.KC ? k * r.KA + it.seg : it.seg * r.KB + k; sz = k;
       } else {
         sx = it.seg; sy = it.seg; sz = 0;
       }

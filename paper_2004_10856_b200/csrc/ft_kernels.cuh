@@ -40,7 +40,7 @@ constexpr int CHUNK = 16;           // run elements per filter work item
 constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
 constexpr int BMIN_FILL = 0x7F;     // memset byte: 0x7F7F..7F > any t (< 2^60)
 
-enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5, K_PAIR = 6 };
+enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5, K_PAIR = 6, K_BRANCH = 7 };
 
 // A frontier set on the device (CSR): segment s = [off[s], off[s+1]).
 struct FacSet {
@@ -197,6 +197,10 @@ __device__ __forceinline__ void block_factor_segs(const StepDev& s, int64_t sg, 
     sx = k;
     sy = 0;
     sz = 0;
+  } else if (s.kind == K_BRANCH) { // Eq. 6 (R14): sigma = s_h, k = s_i; KC = o_i is the edge's source
+    sx = sg;                         // F(o_h, s_h)
+    sy = s.KC ? k * s.KA + sg : sg * s.KB + k;  // F(e, s_i, s_h) | F(e, s_h, s_i)
+    sz = k;                          // F(o_i, s_i)
   } else if (s.kind == K_PAIR) {   // FT-Elimination: k = s_1*K_n + s_n
     const int64_t s1 = (k >> 31) == 0 && (s.KB >> 31) == 0 ? (int64_t)((unsigned)k / (unsigned)s.KB) : k / s.KB;
     sx = k;                          // F(e_1n, s_1, s_n)

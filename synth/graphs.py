@@ -418,15 +418,25 @@ def random_leafy(seed: int, n_ops: int = 5, kmax: int = 3, leaves: int = 2, cost
     """A random SP graph with `leaves` extra ops attached by a single edge
     (an input feeding, or an output read from, a random op) -- shapes that
     need branch elimination (Eq. 6).  Costs U{0..cost_hi}, seeded."""
-    base = random_sp(seed, n_ops=n_ops, kmax=kmax, cost_hi=cost_hi, edge_mem=edge_mem)
+    base = random_sp(seed, n_ops=n_ops, kmax=kmax, p_mask=0.0, cost_hi=cost_hi, edge_mem=edge_mem)
     rng = np.random.default_rng(seed + 7919)
     K = [int(k) for k in base.n_cfgs]
     edges = list(zip(base.src.tolist(), base.dst.tolist()))
+    has_in = {d for _, d in edges}
+    has_out = {a for a, _ in edges}
     for _ in range(leaves):
-        h = int(rng.integers(0, len(K)))
+        # an input leaf goes to an op that already has an input, an output leaf
+        # to one that already has an output (the graph's source stays the
+        # backbone head, P:630), both to ops with K >= 2 (a K=1 source with an
+        # extra output would be folded first, Eq. 7, disconnecting its consumers)
+        as_input = rng.integers(0, 2) == 0
+        cand = [v for v in range(len(K)) if K[v] >= 2 and (v in has_in if as_input else v in has_out)]
+        if not cand:
+            continue
+        h = int(cand[int(rng.integers(0, len(cand)))])
         i = len(K)
-        K.append(int(rng.integers(1, kmax + 1)))
-        edges.append((i, h) if rng.integers(0, 2) == 0 else (h, i))
+        K.append(int(rng.integers(2, max(2, kmax) + 1)))
+        edges.append((i, h) if as_input else (h, i))
     w = random_graph(len(K), edges, K, seed + 104729, cost_hi=cost_hi, edge_mem=edge_mem,
                      name=f"leafy{seed}")
     return w

@@ -292,3 +292,17 @@ def test_ft_elimination(ft):
         g.eliminate()
         g.frontier(algo="elim")
         g.frontier()  # the graph's frontier was computed by FT-Elimination
+
+
+def test_branch_elimination(ft):
+    """Branch elimination (Eq. 6) in FT_AUTO: graphs with attached input and
+    output ops; every step bit-identical to the oracle, for FT-LDP and
+    FT-Elimination."""
+    kinds = set()
+    for seed in range(30):
+        w = G.random_leafy(seed, n_ops=2 + seed % 6, kmax=6, leaves=1 + seed % 4, cost_hi=1 << 12)
+        _, st = compare(ft, w, strategies=8)
+        kinds |= {s["kind"] for s in st}
+        compare_elim(ft, w, strategies=4)
+    assert "branch" in kinds
+    compare(ft, G.random_graph(3, [(0, 2), (1, 2)], 40, 5, cost_hi=1 << 20), strategies=8)

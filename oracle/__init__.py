@@ -25,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle_ft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -6, -7, -8
-NODE, EDGE, AUTO = 1, 2, 3
+NODE, EDGE, AUTO, AUTO_HEUR = 1, 2, 3, 4
 STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch"}
 
 
@@ -60,6 +60,7 @@ def lib():
         L.oft_eliminate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P32]
         L.oft_frontier.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
         L.oft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
+        L.oft_query_mini_time.argtypes = [C.c_void_p, C.c_int64, P64]
         L.oft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
         L.oft_num_steps.argtypes = [C.c_void_p]
         L.oft_num_steps.restype = C.c_int64
@@ -141,6 +142,12 @@ class Graph:
         t = np.empty(n.value, np.int64)
         self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
+
+    def mini_time(self, memory_limit):
+        """SS4.1 mini-time: index of the fastest frontier tuple with m <= limit, or -1."""
+        i = C.c_int64(-1)
+        self._chk(self._L.oft_query_mini_time(self.h, int(memory_limit), C.byref(i)))
+        return i.value
 
     def strategy(self, idx):
         out = np.empty(self.n_ops, np.int32)

@@ -124,8 +124,8 @@ void block_segs(const Step& s, int64_t sigma, int64_t k, int64_t* sx, int64_t* s
     case OFT_STEP_EDGE:  // Eq.5 P:600 (binary, R7)
       *sx = sigma; *sy = sigma; *sz = 0;
       break;
-    case OFT_STEP_FOLD:  // Eq.7 P:620 with K_src = 1 (R13): F(o_j,p) (x) F(e,0,p) [(x) F(o_src,0)]
-      *sx = sigma; *sy = sigma; *sz = 0;
+    case OFT_STEP_FOLD:  // Eq.7, source fixed to k* = KB: F(o_j,p) (x) F(e,k*,p) [(x) F(o_src,k*)]
+      *sx = sigma; *sy = s.KB * s.KA + sigma; *sz = s.KC;  // K=1 fold: KB = KC = 0 (R13)
       break;
     case OFT_STEP_LDP: {  // Alg.3 line 6 P:645; KA=K_{i-1} KB=K_i
       int64_t p = sigma;
@@ -338,7 +338,7 @@ int do_edge(oft_graph* g, int e1, int e2, int* out_edge) {
 // Eq. 7 for a K=1 source (exact, R13): every consumer o_j gets
 // F(o_j, p) <- F(o_j, p) (x) F(e, 0, p); the source's own cost is added once,
 // to its topologically first consumer.
-int do_fold(oft_graph* g, const Adj& a, int src, const std::vector<int>& topo) {
+int do_fold(oft_graph* g, const Adj& a, int src, const std::vector<int>& topo, int64_t kstar = 0) {
   const std::vector<int> out = a.out[src];
   std::vector<int> pos(g->n_ops, 0);
   for (size_t i = 0; i < topo.size(); ++i) pos[topo[i]] = (int)i;
@@ -355,6 +355,8 @@ int do_fold(oft_graph* g, const Adj& a, int src, const std::vector<int>& topo) {
     s.Y = g->edges[e].set;
     s.Z = (c == first) ? g->op_set[src] : 0;
     s.KA = g->K[c];
+    s.KB = kstar;                      // edge segment k* * K_c + p
+    s.KC = (c == first) ? kstar : 0;   // op segment k* (unit set: 0)
     s.nseg = g->K[c];
     s.nblk = 1;
     int rc = run_step(g, s);
@@ -460,6 +462,32 @@ int auto_one(oft_graph* g) {
       return rc ? rc : 1;
     }
   return 0;
+}
+
+// Heuristic elimination (Eq. 7; lossy, opt-in): the unmarked
+// source op with the most out-edges (ties: topological order), K >= 2, gets
+// the configuration of least memory -- min over k of the first (least-m)
+// tuple of F(o_i, k), ties by its t, then k ("minimizing the memory
+// consumption of o_i") -- and is folded into its consumers.  1 = done, 0 =
+// no candidate.
+int heur_one(oft_graph* g) {
+  Adj a = build_adj(g);
+  auto topo = live_order(g);
+  auto marked = marking(g, a, topo);
+  int best = -1;
+  for (int i : topo)
+    if (g->op_alive[i] && !marked[i] && g->K[i] >= 2 && a.in[i].empty() && !a.out[i].empty() &&
+        (best < 0 || a.out[i].size() > a.out[best].size()))
+      best = i;
+  if (best < 0) return 0;
+  const FSet& S = g->sets[g->op_set[best]];
+  int64_t ks = 0;
+  for (int64_t k = 1; k < (int64_t)S.seg.size(); ++k) {
+    const Tup &x = S.seg[k][0], &y = S.seg[ks][0];
+    if (x.m < y.m || (x.m == y.m && x.t < y.t)) ks = k;
+  }
+  int rc = do_fold(g, a, best, topo, ks);
+  return rc ? rc : 1;
 }
 
 // The live graph as a chain o_1 -> ... -> o_n (LDP precondition).
@@ -725,9 +753,16 @@ int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* out_edge) {
     if (other < 0) return fail(g, OFT_EPRECOND, "edge elimination needs a parallel edge");
     return do_edge(g, std::min(id, other), std::max(id, other), out_edge);
   }
-  if (kind == OFT_AUTO) {
+  if (kind == OFT_AUTO || kind == OFT_AUTO_HEUR) {
     for (;;) {
       int r = auto_one(g);
+      if (r < 0) return r;
+      if (r == 1) continue;
+      if (kind == OFT_AUTO) break;
+      std::vector<int> ch, ce;
+      if (chain_of(g, &ch, &ce) == OFT_OK) break;  // linear: LDP can run
+      g->err.clear();
+      r = heur_one(g);
       if (r < 0) return r;
       if (r == 0) break;
     }
@@ -765,6 +800,17 @@ int oft_frontier_elim(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out,
     if (m_out) m_out[i] = F[i].m;
     if (t_out) t_out[i] = F[i].t;
   }
+  return OFT_OK;
+}
+
+int oft_query_mini_time(oft_graph* g, int64_t memory_limit, int64_t* idx_out) {
+  if (!g || !idx_out) return OFT_EINVAL;
+  if (!g->have_final) return fail(g, OFT_ESTATE, "call oft_frontier first");
+  const Frontier& F = g->sets[g->final_set].seg[0];
+  int64_t best = -1;  // plain scan: t strictly descends, so the last feasible tuple wins
+  for (size_t i = 0; i < F.size(); ++i)
+    if (F[i].m <= memory_limit && (best < 0 || F[i].t < F[best].t)) best = (int64_t)i;
+  *idx_out = best;
   return OFT_OK;
 }
 

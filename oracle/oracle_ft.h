@@ -30,7 +30,7 @@ extern "C" {
 
 enum { OFT_OK = 0, OFT_EINVAL = -1, OFT_ESTATE = -2, OFT_EPRECOND = -3, OFT_ENOMEM = -4,
        OFT_EOVERFLOW = -6, OFT_ESIZE = -7, OFT_EINTERNAL = -8 };
-enum { OFT_NODE = 1, OFT_EDGE = 2, OFT_AUTO = 3 };
+enum { OFT_NODE = 1, OFT_EDGE = 2, OFT_AUTO = 3, OFT_AUTO_HEUR = 4 };
 /* step kinds reported by oft_step_info */
 enum { OFT_STEP_NODE = 1, OFT_STEP_EDGE = 2, OFT_STEP_FOLD = 3, OFT_STEP_LDP = 4,
        OFT_STEP_FINAL = 5, OFT_STEP_PAIR = 6, OFT_STEP_BRANCH = 7 };
@@ -48,7 +48,11 @@ void oft_graph_destroy(oft_graph* g);
 int oft_set_op_costs(oft_graph* g, int32_t op, const int64_t* m, const int64_t* t);
 /* Eq. 2 edge costs, row-major [s_src][s_dst]; m may be NULL (= 0). */
 int oft_set_edge_costs(oft_graph* g, int32_t edge, const int64_t* m, const int64_t* t);
-/* OFT_NODE (id = op), OFT_EDGE (id = edge), OFT_AUTO (id ignored). */
+/* OFT_NODE (id = op), OFT_EDGE (id = edge), OFT_AUTO (id ignored),
+ * OFT_AUTO_HEUR: OFT_AUTO, then while the graph is not linear and no exact
+ * elimination applies, one heuristic elimination (Eq. 7; lossy)
+ * of the unmarked source op with the most out-edges, its configuration
+ * fixed to the one of least memory (ties: time, index). */
 int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);
 /* LDP + final reduce (cached).  Two-call size pattern: OFT_ESIZE with *n_out. */
 int oft_frontier(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
@@ -57,6 +61,10 @@ int oft_frontier(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int6
  * configuration pair (s_1, s_n) (cached; the graph then has a frontier and
  * oft_frontier returns OFT_ESTATE, and vice versa). */
 int oft_frontier_elim(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
+/* Mini-time query (SS4.1): index of the smallest-time final-frontier
+ * tuple with m <= memory_limit (the last such tuple: m ascending, t strictly
+ * descending), or -1 if none (infeasible).  Requires a computed frontier. */
+int oft_query_mini_time(oft_graph* g, int64_t memory_limit, int64_t* idx_out);
 /* Unrolled strategy (config per original op) of final-frontier tuple idx. */
 int oft_strategy(oft_graph* g, int64_t tuple_idx, int32_t* cfg_out);
 int64_t oft_num_steps(const oft_graph* g);

@@ -297,10 +297,11 @@ def c3(seed: int = 0, jitter: bool = True) -> Workload:
     return _dnn_workload("C3-resnet50", specs, edges, 16, seed, jitter)
 
 
-def c4(seed: int = 0, jitter: bool = True, layers: int = 24) -> Workload:
+def c4(seed: int = 0, jitter: bool = True, layers: int = 24, mask_k1: bool = True) -> Workload:
     """C4: BERT-large encoder (342 ops / 460 edges at 24 layers), D=32.
     The attention mask is a K=1 source feeding every scores op (P:618);
-    mask edges carry t = 10,000 ns."""
+    mask edges carry t = 10,000 ns.  mask_k1=False gives the mask the full
+    configuration space (the case heuristic elimination, Eq. 7, exists for)."""
     N, S, H, heads = N_BATCH, 128, 1024, 16
     rows = N * S
     specs: List[OpSpec] = []
@@ -348,7 +349,7 @@ def c4(seed: int = 0, jitter: bool = True, layers: int = 24) -> Workload:
     if layers == 24:
         assert len(specs) == 342 and len(edges) == 460, (len(specs), len(edges))
     return _dnn_workload(f"C4-bert-large-L{layers}", specs, edges, 32, seed, jitter,
-                         k1_ops=(mask,), const_edge_t=const_t)
+                         k1_ops=(mask,) if mask_k1 else (), const_edge_t=const_t)
 
 
 # --------------------------------------------------------------------------
@@ -440,6 +441,23 @@ def random_leafy(seed: int, n_ops: int = 5, kmax: int = 3, leaves: int = 2, cost
     w = random_graph(len(K), edges, K, seed + 104729, cost_hi=cost_hi, edge_mem=edge_mem,
                      name=f"leafy{seed}")
     return w
+
+
+def random_masked(seed: int, n_ops: int = 5, kmax: int = 3, mask_k: int = 2, fanout: int = 2,
+                  cost_hi: int = 8) -> Workload:
+    """A random SP graph plus a BERT-mask-like source (the last op id, so
+    not the backbone head) with `mask_k` >= 2 configurations feeding
+    `fanout` random non-source ops -- the shape heuristic elimination (Eq. 7)
+    is for.  Costs U{0..cost_hi}, seeded."""
+    base = random_sp(seed, n_ops=n_ops, kmax=kmax, p_mask=0.0, cost_hi=cost_hi)
+    rng = np.random.default_rng(seed + 15485863)
+    K = [int(k) for k in base.n_cfgs] + [int(mask_k)]
+    edges = list(zip(base.src.tolist(), base.dst.tolist()))
+    targets = sorted({d for _, d in edges})
+    m = len(K) - 1
+    for d in rng.choice(targets, size=min(fanout, len(targets)), replace=False).tolist():
+        edges.append((m, int(d)))
+    return random_graph(len(K), edges, K, seed + 32452843, cost_hi=cost_hi, name=f"masked{seed}")
 
 
 def random_sp(seed: int, n_ops: int = 6, kmax: int = 3, p_parallel: float = 0.35,

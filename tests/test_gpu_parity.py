@@ -306,3 +306,19 @@ def test_branch_elimination(ft):
         compare_elim(ft, w, strategies=4)
     assert "branch" in kinds
     compare(ft, G.random_graph(3, [(0, 2), (1, 2)], 40, 5, cost_hi=1 << 20), strategies=8)
+
+
+def test_mini_time_query(ft):
+    """ft_query_mini_time (SS4.1) returns the oracle's index at every limit."""
+    for w in (G.c2(), G.c3(), G.random_sp(77, n_ops=12, kmax=6, cost_hi=1 << 16)):
+        og = oracle.load(w, 8)
+        og.eliminate()
+        om, _ = og.frontier()
+        g = ft.load(w)
+        g.eliminate()
+        gm, _ = g.frontier()
+        lims = [int(om[0]) - 1] + om.tolist() + (om + 1).tolist() + [1 << 62]
+        for lim in lims:
+            assert g.mini_time(lim) == og.mini_time(lim), lim
+        i = g.mini_time(int(om[len(om) // 2]))
+        assert np.array_equal(g.strategy(i), og.strategy(i))

@@ -1,0 +1,106 @@
+"""Pins for heuristic elimination (Eq. 7),
+opt-in via OFT_AUTO_HEUR.  It is lossy in general, so the exact pin is on
+the RESTRICTED problem: with the mask op fixed to the configuration the rule
+picks (least memory, ties by time then index -- computed here from the cost
+tables), the frontier must equal brute force over that restricted strategy
+space; and every point must be achievable in the full problem (quality is
+reported as the share of the exact frontier it reproduces)."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import bruteforce as bf
+from synth import graphs as G
+
+
+def _restricted(w, op, k):
+    """Workload with op's configuration fixed to k (Eq. 1 / Eq. 2 slices)."""
+    K = w.n_cfgs.copy()
+    op_m = list(w.op_m)
+    op_t = list(w.op_t)
+    op_m[op] = w.op_m[op][k:k + 1].copy()
+    op_t[op] = w.op_t[op][k:k + 1].copy()
+    edge_t = list(w.edge_t)
+    edge_m = None if w.edge_m is None else list(w.edge_m)
+    for e in range(w.n_edges):
+        s, d = int(w.src[e]), int(w.dst[e])
+        if s == op:
+            sl = slice(k * int(K[d]), (k + 1) * int(K[d]))
+        elif d == op:
+            sl = slice(k, None, int(K[op]))
+        else:
+            continue
+        edge_t[e] = w.edge_t[e][sl].copy()
+        if edge_m is not None:
+            edge_m[e] = w.edge_m[e][sl].copy()
+    K[op] = 1
+    return G.Workload(w.name + "-fixed", K, w.src, w.dst, op_m, op_t, edge_t, edge_m).check()
+
+
+def _ok(w):
+    g = oracle.load(w, 2)
+    g.eliminate(oracle.AUTO_HEUR)
+    try:
+        m, t = g.frontier()
+    except oracle.OracleError as e:
+        assert e.code == oracle.EPRECOND  # heuristics only remove sources
+        return None
+    return g, m, t
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_heuristic_restricted_brute_force(seed):
+    w = G.random_masked(seed, n_ops=3 + seed % 4, kmax=3, mask_k=2 + seed % 2, fanout=2 + seed % 2)
+    r = _ok(w)
+    if r is None:
+        pytest.skip("not linearisable by source heuristics")
+    g, m, t = r
+    mask = w.n_ops - 1
+    exact_only = oracle.load(w, 2)
+    exact_only.eliminate(oracle.AUTO)
+    try:  # FT_AUTO alone linearised it: no heuristic step, the result is exact
+        exact_only.frontier()
+        ma, ta, _ = bf.enumerate_costs(w)
+        assert bf.check_frontier(m, t, ma, ta) == []
+        return
+    except oracle.OracleError:
+        pass
+    om, ot = w.op_m[mask], w.op_t[mask]
+    ks = min(range(len(om)), key=lambda k: (int(om[k]), int(ot[k]), k))
+    wr = _restricted(w, mask, ks)
+    ma, ta, _ = bf.enumerate_costs(wr)
+    assert bf.check_frontier(m, t, ma, ta) == []       # exact on the restricted space
+    for i in range(len(m)):
+        s = g.strategy(i)
+        assert s[mask] == ks
+        assert bf.total_cost(w, s) == (int(m[i]), int(t[i]))  # achievable in the full problem
+
+
+def test_heuristic_quality_report():
+    """Share of the exact frontier the heuristic reproduces (lossy by design)."""
+    got = tot = 0
+    for seed in range(20):
+        w = G.random_masked(seed, n_ops=4, kmax=3, mask_k=3, fanout=3)
+        r = _ok(w)
+        if r is None:
+            continue
+        _, m, t = r
+        ex = bf.brute_force(w)
+        pts = set(zip(m.tolist(), t.tolist()))
+        got += sum((a, b) in pts for a, b in ex)
+        tot += len(ex)
+    assert tot > 0 and 0 < got <= tot
+
+
+def test_heuristic_off_by_default():
+    """FT_AUTO never applies it: the K>1-mask BERT graph stays non-linear."""
+    w = G.c4(layers=2, mask_k1=False)  # (one layer: the mask is a leaf -> exact branch elimination)
+    g = oracle.load(w, 8)
+    g.eliminate(oracle.AUTO)
+    with pytest.raises(oracle.OracleError) as e:
+        g.frontier()
+    assert e.value.code == oracle.EPRECOND
+    g = oracle.load(w, 8)
+    g.eliminate(oracle.AUTO_HEUR)
+    m, t = g.frontier()
+    assert len(m) > 0

@@ -57,7 +57,7 @@ enum {
   FT_EINTERNAL = -8   /* broken provenance or internal invariant (poisons the handle) */
 };
 
-enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3 };
+enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3, FT_AUTO_HEUR = 4 };
 
 /* Step kinds in ft_step_stats records. */
 enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5,
@@ -149,6 +149,11 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
  *           K=1), then branch elimination (Eq. 6: an unmarked op whose only
  *           edge joins it to o_h is merged into o_h, reducing over its
  *           configurations -- reading R14).
+ *  FT_AUTO_HEUR: FT_AUTO, then, while the graph is not linear and no exact
+ *           elimination applies, one heuristic elimination (Eq. 7,
+ *           P:618-622; lossy): the unmarked source op with the most
+ *           out-edges is fixed to its least-memory configuration (ties:
+ *           time, index) and folded into its consumers.
  * New edge ids are n_edges, n_edges+1, ... in creation order (*new_edge,
  * nullable).  Errors: FT_EINVAL, FT_ESTATE, FT_EPRECOND, FT_ENOMEM, FT_ECUDA. */
 int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);
@@ -168,6 +173,14 @@ int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_
  * A graph has one final frontier: after ft_frontier_elim, ft_frontier
  * returns FT_ESTATE, and vice versa.  FT_EPRECOND if not a chain. */
 int ft_frontier_elim(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
+
+/* Mini-time query (SS4.1: "minimizes the per-iteration time while
+ * satisfying the memory constraint"): *idx_out = index of the smallest-time
+ * final-frontier tuple with m <= memory_limit -- binary search on the
+ * staircase (m ascending, t strictly descending: the last feasible tuple) --
+ * or -1 when no strategy fits (infeasible is a value, not an error).
+ * Requires ft_frontier / ft_frontier_elim (else FT_ESTATE). */
+int ft_query_mini_time(ft_graph* g, int64_t memory_limit, int64_t* idx_out);
 
 /* Unroll: configuration index of every ORIGINAL operator for final
  * frontier tuple tuple_idx; cfg_out[n_ops] host.  Requires ft_frontier. */

@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, ECUDA, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8
-NODE, EDGE, AUTO = 1, 2, 3
+NODE, EDGE, AUTO, AUTO_HEUR = 1, 2, 3, 4
 STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch"}
 
 
@@ -67,6 +67,7 @@ def _load():
     L.ft_eliminate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P32]
     L.ft_frontier.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
     L.ft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
+    L.ft_query_mini_time.argtypes = [C.c_void_p, C.c_int64, P64]
     L.ft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
     L.ft_get_stats.argtypes = [C.c_void_p, C.POINTER(ft_step_stats), C.c_int64, P64]
     L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
@@ -87,7 +88,7 @@ def _load():
 
 lib = _load()
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
-           "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_strategy", "ft_get_stats", "ft_step_output",
+           "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version"]
 
@@ -190,6 +191,12 @@ class Graph:
         t = np.empty(n.value, np.int64)
         self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
+
+    def mini_time(self, memory_limit: int) -> int:
+        """SS4.1 mini-time: index of the fastest frontier tuple with m <= limit, or -1."""
+        i = C.c_int64(-1)
+        self._chk(lib.ft_query_mini_time(self.h, int(memory_limit), C.byref(i)))
+        return i.value
 
     def strategy(self, idx: int) -> np.ndarray:
         out = np.empty(self.n_ops, np.int32)

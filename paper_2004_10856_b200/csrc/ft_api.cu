@@ -392,6 +392,8 @@ void host_block_segs(const StepRec& r, int64_t sg, int64_t k, int64_t& sx, int64
     sx = k; sy = k / r.KB; sz = k % r.KB;
   } else if (r.kind == ftk::K_BRANCH) {
     sx = sg; sy = r.KC ? k * r.KA + sg : sg * r.KB + k; sz = k;
+  } else if (r.kind == ftk::K_FOLD) {
+    sx = sg; sy = r.KB * r.KA + sg; sz = r.KC;
   } else {
     sx = sg; sy = sg; sz = 0;
   }
@@ -980,7 +982,7 @@ int do_merge(ft_graph* g, int e1, int e2, int* new_edge) {  // Eq.5,
 
 // Exact K=1 case of Eq.7: fold the source into every consumer;
 // the source's own cost goes to its topologically first consumer (R13).
-int do_fold(ft_graph* g, int src) {
+int do_fold(ft_graph* g, int src, int64_t kstar = 0) {
   std::vector<int> outs(g->out_e[src].begin(), g->out_e[src].end());  // ascending ids
   int first = -1;
   for (int e : outs) {
@@ -995,6 +997,8 @@ int do_fold(ft_graph* g, int src) {
     r.Y = g->edges[e].set;
     r.Z = c == first ? g->op_set[src] : 0;
     r.KA = g->K[c];
+    r.KB = kstar;                     // edge segment k* * K_c + p
+    r.KC = c == first ? kstar : 0;    // op segment k* (unit set: 0)
     r.nseg = g->K[c];
     r.nblk = 1;
     int out = schedule(g, r);
@@ -1062,6 +1066,39 @@ int auto_step(ft_graph* g) {
       return rc ? rc : 1;
     }
   return 0;
+}
+
+// Heuristic elimination (Eq. 7; lossy, FT_AUTO_HEUR only): the
+// unmarked source op with the most out-edges (ties: topological order),
+// K >= 2, gets the configuration of least memory -- min over k of the first
+// (least-m) tuple of F(o_i, k), ties by its t, then k -- and is folded into
+// its consumers.  1 = done, 0 = no candidate, < 0 error.
+int heur_step(ft_graph* g) {
+  mark_backbone(g);
+  int best = -1;
+  for (const auto& kv : g->live_ops) {
+    const int v = kv.second;
+    if (g->mark_stamp[v] == g->stamp || g->K[v] < 2 || !g->in_e[v].empty() || g->out_e[v].empty())
+      continue;
+    if (best < 0 || g->out_e[v].size() > g->out_e[best].size()) best = v;
+  }
+  if (best < 0) return 0;
+  int rc = flush(g);  // the op's frontier may come from a pending step
+  if (rc) return rc;
+  const int set = g->op_set[best];
+  if ((rc = ensure_off(g, set))) return rc;
+  const FSet& S = g->sets[set];
+  const int64_t n = S.off[S.nseg];
+  std::vector<int64_t> hm(n), ht(n);
+  CU(cudaMemcpy(hm.data(), S.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+  CU(cudaMemcpy(ht.data(), S.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+  int64_t ks = 0;
+  for (int64_t k = 1; k < S.nseg; ++k) {
+    const int64_t a = S.off[k], b = S.off[ks];
+    if (hm[a] < hm[b] || (hm[a] == hm[b] && ht[a] < ht[b])) ks = k;
+  }
+  rc = do_fold(g, best, ks);
+  return rc ? rc : 1;
 }
 
 // The live graph as a chain o_1 -> ... -> o_n (LDP / FT-Elimination precondition).
@@ -1240,6 +1277,8 @@ int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_
         sx = k; sy = k / r.KB; sz = k % r.KB;
       } else if (r.kind == ftk::K_BRANCH) {
         sx = it.seg; sy = r.KC ? k * r.KA + it.seg : it.seg * r.KB + k; sz = k;
+      } else if (r.kind == ftk::K_FOLD) {
+        sx = it.seg; sy = r.KB * r.KA + it.seg; sz = r.KC;
       } else {
         sx = it.seg; sy = it.seg; sz = 0;
       }
@@ -1504,7 +1543,8 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
   if (!g) return FT_EINVAL;
   if (g->poisoned) return g->poisoned;
   if (new_edge) *new_edge = -1;
-  if (kind != FT_NODE && kind != FT_EDGE && kind != FT_AUTO) return setf(g, FT_EINVAL, "bad kind");
+  if (kind != FT_NODE && kind != FT_EDGE && kind != FT_AUTO && kind != FT_AUTO_HEUR)
+    return setf(g, FT_EINVAL, "bad kind");
   if (g->have_final) return setf(g, FT_ESTATE, "frontier already computed");
   if (kind == FT_NODE) {
     if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return setf(g, FT_EINVAL, "bad operator");
@@ -1535,6 +1575,13 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
   const double a0 = now_ms();
   for (;;) {
     int r = auto_step(g);
+    if (r < 0) return r;
+    if (r == 1) continue;
+    if (kind != FT_AUTO_HEUR) break;
+    std::vector<int> ch, ce;
+    if (linear_chain(g, ch, ce) == FT_OK) break;  // linear: LDP can run
+    g->err.clear();
+    r = heur_step(g);
     if (r < 0) return r;
     if (r == 0) break;
   }
@@ -1569,6 +1616,16 @@ int ft_frontier_elim(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, i
   if (cap < n) return FT_ESIZE;
   if (m_out) std::memcpy(m_out, g->final_m.data(), sizeof(int64_t) * n);
   if (t_out) std::memcpy(t_out, g->final_t.data(), sizeof(int64_t) * n);
+  return FT_OK;
+}
+
+int ft_query_mini_time(ft_graph* g, int64_t memory_limit, int64_t* idx_out) {
+  if (!g || !idx_out) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (!g->have_final) return setf(g, FT_ESTATE, "call ft_frontier first");
+  // last index with m <= limit (m strictly ascending on the staircase)
+  const auto& M = g->final_m;
+  *idx_out = (int64_t)(std::upper_bound(M.begin(), M.end(), memory_limit) - M.begin()) - 1;
   return FT_OK;
 }
 

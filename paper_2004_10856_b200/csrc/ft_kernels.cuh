@@ -206,7 +206,11 @@ __device__ __forceinline__ void block_factor_segs(const StepDev& s, int64_t sg, 
     sx = k;                          // F(e_1n, s_1, s_n)
     sy = s1;                         // F(o_1, s_1)
     sz = k - s1 * s.KB;              // F(o_n, s_n)
-  } else {                         // K_EDGE (X=e1, Y=e2) / K_FOLD (X=o_j, Y=e, Z=o_src|unit)
+  } else if (s.kind == K_FOLD) {   // Eq. 7, source fixed to k* = KB: X=o_j, Y=F(e,k*,p), Z=o_src(k*)|unit
+    sx = sg;
+    sy = s.KB * s.KA + sg;           // K=1 fold: KB = KC = 0 (R13)
+    sz = s.KC;
+  } else {                         // K_EDGE (X=e1, Y=e2)
     sx = sg;
     sy = sg;
     sz = 0;

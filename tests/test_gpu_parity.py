@@ -322,3 +322,38 @@ def test_mini_time_query(ft):
             assert g.mini_time(lim) == og.mini_time(lim), lim
         i = g.mini_time(int(om[len(om) // 2]))
         assert np.array_equal(g.strategy(i), og.strategy(i))
+
+
+def test_heuristic_elimination(ft):
+    """FT_AUTO_HEUR (Eq. 7 heuristic elimination, lossy): the GPU applies the
+    oracle's rule and matches it step by step; includes BERT with a K=36 mask."""
+    import paper_2004_10856_b200 as ftm
+    n = 0
+    for seed in range(24):
+        w = G.random_masked(seed, n_ops=3 + seed % 5, kmax=4, mask_k=2 + seed % 3, fanout=2 + seed % 2)
+        og = oracle.load(w, 4)
+        og.eliminate(oracle.AUTO_HEUR)
+        try:
+            om, ot = og.frontier()
+        except oracle.OracleError:
+            continue
+        g = ft.load(w, keep_all=True)
+        g.eliminate(ftm.AUTO_HEUR)
+        gm, gt = g.frontier()
+        assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+        assert og.num_steps() == len(g.stats())
+        for s in range(og.num_steps()):
+            for x, y in zip(og.step_output(s), g.step_output(s)):
+                assert np.array_equal(x, y), (seed, s)
+        for i in range(len(om)):
+            assert np.array_equal(og.strategy(i), g.strategy(i))
+        n += 1
+    assert n > 10
+    w = G.c4(layers=2, mask_k1=False)
+    og = oracle.load(w, 8)
+    og.eliminate(oracle.AUTO_HEUR)
+    om, ot = og.frontier()
+    g = ft.load(w)
+    g.eliminate(ftm.AUTO_HEUR)
+    gm, gt = g.frontier()
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)

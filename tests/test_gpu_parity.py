@@ -357,3 +357,26 @@ def test_heuristic_elimination(ft):
     g.eliminate(ftm.AUTO_HEUR)
     gm, gt = g.frontier()
     assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_invariance_new_kinds(ft, world):
+    """Sharded execution (loopback virtual ranks) of branch elimination,
+    heuristic elimination and FT-Elimination's pair reduce is bit-identical
+    to world = 1."""
+    import paper_2004_10856_b200 as ftm
+    cases = [(G.random_leafy(5, n_ops=7, kmax=6, leaves=3, cost_hi=1 << 12), ftm.AUTO, "ldp"),
+             (G.random_leafy(9, n_ops=6, kmax=6, leaves=2, cost_hi=1 << 12), ftm.AUTO, "elim"),
+             (G.c4(layers=2, mask_k1=False), ftm.AUTO_HEUR, "ldp"),
+             (G.c3(), ftm.AUTO, "elim")]
+    for w, kind, algo in cases:
+        a = ft.load(w, keep_all=True)
+        a.eliminate(kind)
+        am, at = a.frontier(algo=algo)
+        b = ft.load(w, keep_all=True, world=world, loopback=True)
+        b.eliminate(kind)
+        bm, bt = b.frontier(algo=algo)
+        assert np.array_equal(am, bm) and np.array_equal(at, bt), w.name
+        for s in range(len(a.stats())):
+            for x, y in zip(a.step_output(s), b.step_output(s)):
+                assert np.array_equal(x, y), (w.name, s)

@@ -2668,10 +2668,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(ncand, int64_t, 2);
     }
     const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
-    {  // scan scratch: zeroed when (re)allocated; scans leave it zeroed
-      void* old = scan_tmp.p;
+    {  // scan scratch: zeroed when (re)allocated -- compare the capacity, not the
+       // address (a larger allocation can come back at the same address); scans
+       // leave it zeroed
+      const size_t old_bytes = scan_tmp.bytes;
       GROW(scan_tmp, int64_t, scan_n / SCAN_TILE + 8);
-      if (scan_tmp.p != old) cudaMemsetAsync(scan_tmp.p, 0, scan_tmp.bytes, st);
+      if (scan_tmp.bytes != old_bytes) cudaMemsetAsync(scan_tmp.p, 0, scan_tmp.bytes, st);
     }
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {

@@ -1266,22 +1266,7 @@ int unroll(ft_graph* g, int set0, int64_t seg0, int64_t idx0, std::vector<int32_
     bool found = false;
     for (int64_t k = 0; k < r.nblk && !found; ++k) {
       int64_t sx, sy, sz;
-      if (r.kind == ftk::K_NODE) {
-        int64_t wv = it.seg / r.KC, p = it.seg % r.KC;
-        sx = wv * r.KB + k; sy = k; sz = k * r.KC + p;
-      } else if (r.kind == ftk::K_LDP) {
-        sx = k * r.KB + it.seg; sy = k; sz = it.seg;
-      } else if (r.kind == ftk::K_FINAL) {
-        sx = k; sy = 0; sz = 0;
-      } else if (r.kind == ftk::K_PAIR) {
-        sx = k; sy = k / r.KB; sz = k % r.KB;
-      } else if (r.kind == ftk::K_BRANCH) {
-        sx = it.seg; sy = r.KC ? k * r.KA + it.seg : it.seg * r.KB + k; sz = k;
-      } else if (r.kind == ftk::K_FOLD) {
-        sx = it.seg; sy = r.KB * r.KA + it.seg; sz = r.KC;
-      } else {
-        sx = it.seg; sy = it.seg; sz = 0;
-      }
+      host_block_segs(r, it.seg, k, sx, sy, sz);
       uint64_t nx = X.off[sx + 1] - X.off[sx], ny = Y.off[sy + 1] - Y.off[sy],
                nz = Z.off[sz + 1] - Z.off[sz];
       uint64_t n = nx * ny * nz;

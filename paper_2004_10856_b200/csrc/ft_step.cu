@@ -422,7 +422,7 @@ template <int R, typename Gen>
 __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
                                                uint64_t* xk, long long* sh, const LevelDev& L,
                                                int64_t gs, int64_t* s_start) {
-  constexpr int NW = DIRECT_NT / 32, N = 32 * R * NW;
+  constexpr int NW = DIRECT_NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eb = wid * 32 * R;
   int64_t m[R], t[R];

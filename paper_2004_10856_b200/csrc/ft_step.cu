@@ -37,8 +37,16 @@ __device__ __forceinline__ bool is_filter(int32_t d, int level) {
 #define SC_PREF (2ull << 62)
 #define SC_VAL ((1ull << 62) - 1)
 
-template <typename TIn>
-__global__ void __launch_bounds__(SCAN_NT) k_scan1(const TIn* in, const int64_t* n_dev, int64_t n_host,
+// Element loaders for the scan: a plain array, or a functor that computes
+// the element (and stores it for later kernels) while the scan reads it.
+template <typename T>
+struct LoadArr {
+  const T* p;
+  __device__ __forceinline__ long long operator()(int64_t i) const { return (long long)p[i]; }
+};
+
+template <typename Load>
+__global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev, int64_t n_host,
                                                    int64_t* out, unsigned long long* state) {
   __shared__ long long sh[33];
   __shared__ int64_t s_tile;
@@ -58,7 +66,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(const TIn* in, const int64_t*
     long long sum = 0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-      v[i] = base + i < n ? (long long)in[base + i] : 0;
+      v[i] = base + i < n ? ld(base + i) : 0;
       sum += v[i];
     }
     long long tot;
@@ -117,13 +125,19 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(const TIn* in, const int64_t*
 
 // tmp: >= scan_tmp_elems(n_cap) int64 slots, zero on first use (`fresh`
 // zeroes it here); every scan leaves it zeroed again.
-template <typename TIn>
-void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
-               cudaStream_t st, bool fresh = false) {
+template <typename Load>
+void scan_excl_fn(Load ld, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
+                  cudaStream_t st, bool fresh = false) {
   const int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
   if (fresh) cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 2), st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
-  k_scan1<TIn><<<grid, SCAN_NT, 0, st>>>(in, n_dev, n_cap, out, (unsigned long long*)tmp);
+  k_scan1<Load><<<grid, SCAN_NT, 0, st>>>(ld, n_dev, n_cap, out, (unsigned long long*)tmp);
+}
+
+template <typename TIn>
+void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
+               cudaStream_t st, bool fresh = false) {
+  scan_excl_fn(LoadArr<TIn>{in}, out, n_dev, n_cap, tmp, st, fresh);
 }
 
 // ---------------------------------------------------------------------------
@@ -1545,11 +1559,6 @@ __global__ void __launch_bounds__(DIRECT_NT) k_node_shared(BatchDev B, LevelDev 
 // ---------------------------------------------------------------------------
 // Filter path, level l < d_sigma.
 
-__global__ void k_level_prep(BatchDev B, LevelDev L) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.nseg) return;
-  L.nb[i] = is_filter(L.seg_d[i], L.level) ? L.in.cnt[i] + 1 : 0;
-}
 
 // Clears the bucket counters of the live buckets only (B read on device).
 __global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
@@ -1584,25 +1593,38 @@ __device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa
 
 // Work items of the filter: L.run_item consecutive sampled indices of one run
 // (a multiple of CHUNK, chosen per level so that the grid has enough threads).
-
-__global__ void k_work_count(BatchDev B, LevelDev L) {
-  const int64_t beta = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (beta >= B.nblk) return;
-  const int j = find_base(B.blk_base, B.nsteps, beta);
-  const StepDev& s = B.steps[j];
-  const int64_t lb = beta - B.blk_base[j];
-  const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
-  const int64_t gs = B.seg_base[j] + li;
-  int64_t w = 0;
-  if (is_filter(L.seg_d[gs], L.level)) {
-    Blk b = load_blk(s, s.seg_lo + li, k);
-    int lf, fa, fb;
-    int64_t c[3];
-    run_shape(b, L.st, lf, fa, fb, c);
-    w = c[fa] * c[fb] * ((c[lf] + L.run_item - 1) / L.run_item);
+// Per-segment bucket counts nb and per-block work-item counts wcnt, computed
+// as scan loaders (fused into the scans that consume them: bucket bases,
+// work offsets) and stored for the later kernels.
+struct LoadNb {
+  LevelDev L;
+  __device__ __forceinline__ long long operator()(int64_t i) const {
+    const int64_t v = is_filter(L.seg_d[i], L.level) ? L.in.cnt[i] + 1 : 0;
+    L.nb[i] = v;
+    return v;
   }
-  L.wcnt[beta] = w;
-}
+};
+
+struct LoadWork {
+  BatchDev B;
+  LevelDev L;
+  __device__ __forceinline__ long long operator()(int64_t beta) const {
+    const int j = find_base(B.blk_base, B.nsteps, beta);
+    const StepDev& s = B.steps[j];
+    const int64_t lb = beta - B.blk_base[j];
+    const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
+    int64_t w = 0;
+    if (is_filter(L.seg_d[B.seg_base[j] + li], L.level)) {
+      Blk b = load_blk(s, s.seg_lo + li, k);
+      int lf, fa, fb;
+      int64_t c[3];
+      run_shape(b, L.st, lf, fa, fb, c);
+      w = c[fa] * c[fb] * ((c[lf] + L.run_item - 1) / L.run_item);
+    }
+    L.wcnt[beta] = w;
+    return w;
+  }
+};
 
 // K1: product + pre-filter, output-sensitive run walk.  A work item is a
 // range of one run (short-factor indices fixed, long factor sweeping: m
@@ -2751,12 +2773,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(2);
-        nl += 7;  // prep, scan, bucket_init, work_count, scan, filter, check_cand
-        k_level_prep<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L);
-        scan_excl<int64_t>(L.nb, L.bucket_base, nullptr, nloc, tmp, st);
+        nl += 5;  // scan(+nb), bucket_init, scan(+work counts), filter, check_cand
+        scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
         k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
-        k_work_count<<<grid_for(nbl, 256, 1 << 30), 256, 0, st>>>(s, L);
-        scan_excl<int64_t>(L.wcnt, L.wo, nullptr, nbl, tmp, st);
+        scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st);
         k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
         k_check_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)

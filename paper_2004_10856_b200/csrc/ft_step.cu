@@ -1058,19 +1058,18 @@ __host__ __device__ inline size_t np_smem(int rmax, int64_t ztn) {
          (size_t)NP_WORDS * NP_NT * 4;
 }
 
+// One row: generate its (<= WARP_DIRECT) tuples, sort 64-bit keys
+// (m << 9 | e) in registers (m < 3 * 2^40, R10) and gather t_xy and the block
+// by e (= the tuple id rel_k + x, R6).  Ties in m need no re-sort: the sweep
+// applies the exact equal-m group rule, which scans the whole group.
 template <int R>
 __device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, const int64_t* bo,
                                             const int64_t* ym, const int64_t* yt, int nblk, int n,
                                             int64_t* sm, int64_t* stxy, uint32_t* sidk) {
   const int lane = threadIdx.x & 31;
-  int64_t m[R], t[R];
-  uint64_t id[R];
+  uint64_t key[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    m[r] = INF;
-    t[r] = INF;
-    id[r] = ~0ull;
-  }
+  for (int r = 0; r < R; ++r) key[r] = ~0ull;
 #pragma unroll 1
   for (int r = 0; r < R && (r << 5) < n; ++r) {
     const int e = (r << 5) | lane;
@@ -1083,33 +1082,38 @@ __device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, co
       }
       const int x = e - pre[lo];
       const int64_t vm = __ldg(s.X.m + bo[lo] + x) + ym[lo];
-      const int64_t vt = __ldg(s.X.t + bo[lo] + x) + yt[lo];
-      // id = rel_k + x (|Y| = |Z| = 1, R6); k rides in bits 32.. (monotone in id)
-      const uint64_t vi = ((uint64_t)lo << 32) | (uint64_t)e;
+      stxy[e] = __ldg(s.X.t + bo[lo] + x) + yt[lo];  // staged by e
+      sidk[e] = (uint32_t)lo;
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (q == r) {
-          m[q] = vm;
-          t[q] = vt;
-          id[q] = vi;
-        }
+        if (q == r) key[q] = ((uint64_t)vm << 9) | (uint64_t)e;
     }
   }
-  warp_bitonic<R>(m, t, id);
+  __syncwarp();
+  warp_bitonic_keys<R>(key);
+  int64_t t[R];
+  uint32_t kb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
+    const int src = (int)(key[r] & 511u);
+    t[r] = e < n ? stxy[src] : INF;
+    kb[r] = e < n ? sidk[src] : 0u;
+  }
+  __syncwarp();  // all gathers before the sorted rows are written back
   bool tie = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    int64_t nm = __shfl_down_sync(0xffffffffu, m[r], 1);
-    const int64_t n0 = r + 1 < R ? __shfl_sync(0xffffffffu, m[r + 1 < R ? r + 1 : r], 0) : INF;
-    if (lane == 31) nm = n0;
+    uint64_t nk = __shfl_down_sync(0xffffffffu, key[r], 1);
+    const uint64_t n0 = r + 1 < R ? __shfl_sync(0xffffffffu, key[r + 1 < R ? r + 1 : r], 0) : ~0ull;
+    if (lane == 31) nk = n0;
     const int e = (r << 5) | lane;
-    const bool same_next = e + 1 < n && nm == m[r];
+    const bool same_next = e + 1 < n && (nk >> 9) == (key[r] >> 9);
     if (same_next) tie = true;
-    if (e < n)  {  // id | k << 16 | (last of its equal-m group) << 31
-      sm[e] = m[r];
+    if (e < n) {  // id | k << 16 | (last of its equal-m group) << 31
+      sm[e] = (int64_t)(key[r] >> 9);
       stxy[e] = t[r];
-      sidk[e] = (uint32_t)(id[r] & 0xffffu) | (uint32_t)((id[r] >> 32) << 16) |
-                (same_next ? 0u : 0x80000000u);
+      sidk[e] = (uint32_t)(key[r] & 511u) | (kb[r] << 16) | (same_next ? 0u : 0x80000000u);
     }
   }
   return __any_sync(0xffffffffu, tie);

@@ -2096,6 +2096,10 @@ __device__ __forceinline__ void cta_bucket_regs(const LevelDev& L, int64_t bkt, 
   __syncthreads();  // sh / x* reuse
 }
 
+template <int NT>
+__device__ void bucket_huge_one(const LevelDev& L, int64_t bkt, int64_t* sm, int64_t* stt, uint64_t* sid,
+                                long long* sh);
+
 __global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
   extern __shared__ int64_t dyn[];
   int64_t* sm = dyn;
@@ -2108,8 +2112,9 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
   for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
     const int64_t bkt = L.large_list[e];
     const int64_t c = L.boff[bkt + 1] - L.boff[bkt];
-    if (c > BUCKET_SMEM) {
-      if (threadIdx.x == 0) L.huge_list[atomicAdd(L.huge_n, 1ull)] = bkt;
+    if (c > BUCKET_SMEM) {  // huge: tiles + global merges in this CTA (rare)
+      bucket_huge_one<DIRECT_NT>(L, bkt, sm, stt, sid, sh);
+      __syncthreads();
       continue;
     }
     const int64_t base = L.boff[bkt];
@@ -2147,25 +2152,20 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
   }
 }
 
-// K2+K3 for huge buckets (> BUCKET_SMEM): one CTA; smem-sorted tiles, then
-// pairwise merges through the (dead) candidate arrays as scratch.
-__global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
-  extern __shared__ int64_t dyn[];
-  int64_t* sm = dyn;
-  int64_t* stt = sm + BUCKET_SMEM;
-  uint64_t* sid = (uint64_t*)(stt + BUCKET_SMEM);
-  __shared__ long long sh[33];
-  if (L.hdr->overflow) return;
-  const int64_t nh = *L.huge_n;
-  for (int64_t e = blockIdx.x; e < nh; e += gridDim.x) {
-    const int64_t bkt = L.huge_list[e];
+// K2+K3 for a huge bucket (> BUCKET_SMEM candidates), one CTA of NT threads
+// (called from k_bucket_large): smem-sorted tiles, then pairwise merges
+// through the (dead) candidate arrays as scratch, then Alg. 1 with carry.
+template <int NT>
+__device__ void bucket_huge_one(const LevelDev& L, int64_t bkt, int64_t* sm, int64_t* stt, uint64_t* sid,
+                                long long* sh) {
+  {
     const int64_t c = L.boff[bkt + 1] - L.boff[bkt];
     const int64_t base = L.boff[bkt];
     if (threadIdx.x == 0) atomicAdd(&L.hdr->huge, 1ull);
     // 1) sort tiles of BUCKET_SMEM
     for (int64_t t0 = 0; t0 < c; t0 += BUCKET_SMEM) {
       const int64_t n = min((int64_t)BUCKET_SMEM, c - t0);
-      for (int i = threadIdx.x; i < BUCKET_SMEM; i += 1024) {
+      for (int i = threadIdx.x; i < BUCKET_SMEM; i += NT) {
         if (i < n) {
           sm[i] = L.gm[base + t0 + i];
           stt[i] = L.gt[base + t0 + i];
@@ -2177,8 +2177,8 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
         }
       }
       __syncthreads();
-      bitonic_smem<1024>(sm, stt, sid, BUCKET_SMEM);
-      for (int i = threadIdx.x; i < n; i += 1024) {
+      bitonic_smem<NT>(sm, stt, sid, BUCKET_SMEM);
+      for (int i = threadIdx.x; i < n; i += NT) {
         L.gm[base + t0 + i] = sm[i];
         L.gt[base + t0 + i] = stt[i];
         L.gid[base + t0 + i] = sid[i];
@@ -2191,7 +2191,7 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
     int64_t *bm = L.cm + base, *bt = L.ct + base;
     uint64_t* bi = L.cid + base;
     for (int64_t wdt = BUCKET_SMEM; wdt < c; wdt <<= 1) {
-      for (int64_t i = threadIdx.x; i < c; i += 1024) {
+      for (int64_t i = threadIdx.x; i < c; i += NT) {
         const int64_t r0 = (i / (2 * wdt)) * 2 * wdt;
         const int64_t mid = min(r0 + wdt, c), r1 = min(r0 + 2 * wdt, c);
         const bool left = i < mid;
@@ -2214,7 +2214,7 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
       uint64_t* y = ai; ai = bi; bi = y;
     }
     if (am != L.gm + base) {
-      for (int64_t i = threadIdx.x; i < c; i += 1024) {
+      for (int64_t i = threadIdx.x; i < c; i += NT) {
         L.gm[base + i] = am[i];
         L.gt[base + i] = at[i];
         L.gid[base + i] = ai[i];
@@ -2223,16 +2223,16 @@ __global__ void __launch_bounds__(1024) k_bucket_huge(LevelDev L) {
     }
     // 3) Alg.1 sweep in chunks with carry
     long long carry = L.bcarry[bkt];
-    __shared__ long long s_carry;
-    for (int64_t c0 = 0; c0 < c; c0 += 1024) {
+    __shared__ long long s_carry_h;
+    for (int64_t c0 = 0; c0 < c; c0 += NT) {
       const int64_t i = c0 + threadIdx.x;
       const long long v = i < c ? L.gt[base + i] : INF;
-      long long ex = block_excl_min<1024>(v, sh);
+      long long ex = block_excl_min<NT>(v, sh);
       long long pv = ex < carry ? ex : carry;
       if (i < c) L.gflag[base + i] = v < pv ? 1 : 0;
-      if (threadIdx.x == 1023) s_carry = v < pv ? v : pv;
+      if (threadIdx.x == NT - 1) s_carry_h = v < pv ? v : pv;
       __syncthreads();
-      carry = s_carry;
+      carry = s_carry_h;
       __syncthreads();
     }
   }
@@ -2785,14 +2785,13 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         k_check_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
         mark(3);
-        nl += 6;  // scan, carry, scatter, 3 bucket sorts
+        nl += 5;  // scan, carry, scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
         k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L);
         k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
         k_bucket_small<<<148 * 8, 256, 0, st>>>(s, L);
         const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
         k_bucket_large<<<148 * 2, DIRECT_NT, lsm, st>>>(L);
-        k_bucket_huge<<<148, 1024, (size_t)BUCKET_SMEM * 3 * sizeof(int64_t), st>>>(L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
         mark(4);
         nl += 3;  // scan, compact, seg_out
@@ -2957,8 +2956,7 @@ cudaError_t StepRunner::configure() {
   cudaError_t e = cudaFuncSetAttribute(k_bucket_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)lsm);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_bucket_huge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)((size_t)BUCKET_SMEM * 3 * sizeof(int64_t)));
+  return cudaSuccess;
 }
 
 }  // namespace ftk

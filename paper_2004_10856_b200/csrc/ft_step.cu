@@ -1838,18 +1838,18 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
   }
 }
 
-__global__ void k_check_cand(LevelDev L, int64_t* ncand) {
-  unsigned long long c = *L.cand_cursor;
-  L.hdr->cand_total[L.level] = c;
-  if ((int64_t)c > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
-  *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
-}
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
 // (the running minimum v of Alg.1 entering each bucket).
-__global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L) {
+__global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L, int64_t* ncand) {
   __shared__ long long sh[33];
   __shared__ long long chunk_min;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // candidate total (after k_filter)
+    const unsigned long long c = *L.cand_cursor;
+    L.hdr->cand_total[L.level] = c;
+    if ((int64_t)c > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
+    *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
+  }
   if (L.hdr->overflow) return;
   const int64_t nloc = B.nseg;
   for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
@@ -2777,17 +2777,16 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(2);
-        nl += 5;  // scan(+nb), bucket_init, scan(+work counts), filter, check_cand
+        nl += 4;  // scan(+nb), bucket_init, scan(+work counts), filter
         scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
         k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
         scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st);
         k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
-        k_check_cand<<<1, 1, 0, st>>>(L, nc);
         // bucket offsets over B buckets (B on device)
         mark(3);
         nl += 5;  // scan, carry, scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
-        k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L);
+        k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L, nc);  // + candidate total
         k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
         k_bucket_small<<<148 * 8, 256, 0, st>>>(s, L);
         const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));

@@ -31,7 +31,6 @@ constexpr int64_t INF = INT64_MAX;
 constexpr int LMAX = 12;            // max sample level
 constexpr int C_DIRECT = 4096;      // max direct (single-CTA) segment capacity (dynamic smem)
 constexpr int WARP_DIRECT = 256;    // direct segments up to this size: one warp each (R <= 8)
-constexpr int WARP_DIRECT2 = 512;   // ... up to this size: one warp with R = 16 rows
 constexpr int NS_CAP = 2048;        // shared-order node path: tuples per (step, w) group
 constexpr int NS_MAXBLK = 128;      // ... and blocks (K_i)
 constexpr int SPECIAL_LEVEL = 60;   // seg_d of segments handled by the shared-order node path
@@ -145,8 +144,6 @@ struct LevelDev {
   int64_t* gflag;        // keep flags (0/1), scanned in place -> positions
   int64_t* large_list;
   unsigned long long* large_n;
-  int64_t* huge_list;
-  unsigned long long* huge_n;
   int64_t* scratch;      // global-memory sort scratch (huge buckets)
   int64_t scratch_cap;
   StepHdr* hdr;

@@ -810,7 +810,7 @@ __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&k)[R]) {
 }
 
 constexpr int WARP_BLK_CACHE = 64;
-constexpr size_t DW_SMEM = 8 * 2 * WARP_DIRECT * 8, DW16_SMEM = 4 * 2 * WARP_DIRECT2 * 8;  // t/id staging  // block descriptors cached per warp
+constexpr size_t DW_SMEM = 8 * 2 * WARP_DIRECT * 8;  // t/id staging of k_direct_warp  // block descriptors cached per warp
 
 template <int R>
 __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre,
@@ -973,24 +973,6 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
       L.out.id[d] = id[r];
     }
     off += __popc(bal);
-  }
-}
-
-// Segments of 257..512 tuples: R = 16 rows per warp (own kernel: more registers).
-__global__ void __launch_bounds__(128) k_direct_warp16(BatchDev B, LevelDev L) {
-  __shared__ int pre_all[4][WARP_DIRECT2 + 1];
-  __shared__ Blk blk_all[4][WARP_BLK_CACHE];
-  extern __shared__ int64_t dyn_dw16[];  // per warp: t[WARP_DIRECT2], id[WARP_DIRECT2]
-  const int wid = threadIdx.x >> 5;
-  const int64_t nw = (int64_t)gridDim.x * 4;
-  for (int64_t gs = (int64_t)blockIdx.x * 4 + wid; gs < B.nseg; gs += nw) {
-    if (L.seg_d[gs] != L.level) continue;
-    const int n = L.seg_n[gs];
-    if (n <= WARP_DIRECT || n > L.warp2) continue;
-    if (L.hdr->overflow) return;
-    warp_direct_seg<16>(B, L, gs, n, pre_all[wid], blk_all[wid], dyn_dw16 + wid * 2 * WARP_DIRECT2,
-                        (uint64_t*)(dyn_dw16 + wid * 2 * WARP_DIRECT2 + WARP_DIRECT2));
-    __syncwarp();
   }
 }
 
@@ -1571,7 +1553,6 @@ __global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
     L.hdr->bucket_total[L.level] = Bt0;
     if (Bt0 > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
     *L.large_n = 0;
-    *L.huge_n = 0;
     *L.cand_cursor = 0;
   }
   const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
@@ -2507,7 +2488,7 @@ void StepRunner::release() {
   Buf* all[] = {&seg_d, &seg_n, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
-                &cgb, &gm, &gt, &gid, &gflag, &large_list, &huge_list, &scan_tmp, &ncand,
+                &cgb, &gm, &gt, &gid, &gflag, &large_list, &scan_tmp, &ncand,
                 &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev};
   for (Buf* b : all) {
     if (b->p) cudaFree(b->p);
@@ -2690,7 +2671,6 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(gid, uint64_t, cand_cap);
       GROW(gflag, int64_t, cand_cap + 1);
       GROW(large_list, int64_t, bcap);
-      GROW(huge_list, int64_t, bcap);
       GROW(ncand, int64_t, 2);
     }
     const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
@@ -2718,7 +2698,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       std::memset(&L, 0, sizeof(L));
       L.level = l;
       L.st = level_shift(l, slog0, slog);
-      L.warp2 = warp16 ? WARP_DIRECT2 : WARP_DIRECT;
+      L.warp2 = WARP_DIRECT;
       L.fstats = fstats;
       {  // ~item_div work items per resident thread (148 SMs x 2048 threads)
         const int64_t tot = (int64_t)plan_copy[LMAX + 1 + l];
@@ -2745,10 +2725,6 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
             s, L, (const NodeGroup*)groups_dev.p);
       }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, DW_SMEM, st>>>(s, L);
-      if (warp16) {
-        k_direct_warp16<<<grid_for(nloc, 4, 148 * 8), 128, DW16_SMEM, st>>>(s, L);
-        ++nl;
-      }
       k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cdirect), st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
@@ -2772,8 +2748,6 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         L.gflag = (int64_t*)gflag.p;
         L.large_list = (int64_t*)large_list.p;
         L.large_n = cur + 3;
-        L.huge_list = (int64_t*)huge_list.p;
-        L.huge_n = cur + 4;
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(2);
@@ -2939,12 +2913,9 @@ cudaError_t StepRunner::configure() {
     if (e0 != cudaSuccess) return e0;
     e0 = cudaFuncSetAttribute(k_direct_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DW_SMEM);
     if (e0 != cudaSuccess) return e0;
-    e0 = cudaFuncSetAttribute(k_direct_warp16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DW16_SMEM);
-    if (e0 != cudaSuccess) return e0;
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
-  if (const char* e = getenv("FT_WARP16")) warp16 = atoi(e) != 0;
   if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(256, std::min(C_DIRECT, atoi(e)));
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -81,7 +81,6 @@ class StepRunner {
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
   int cdirect = 1024;                 // direct-path capacity (<= C_DIRECT)
-  bool warp16 = false;                // 257..512-tuple direct segments on one warp (R = 16; A/B: slower)
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int pack_grid = 148 * 4;             // CTAs of k_node_pack (each takes a contiguous pack range)
@@ -104,7 +103,7 @@ class StepRunner {
   Buf poolA_m, poolA_t, poolA_id, poolA_start, poolA_cnt;
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
-  Buf cm, ct, cid, cgb, gm, gt, gid, gflag, large_list, huge_list, scan_tmp, ncand, dst_off;
+  Buf cm, ct, cid, cgb, gm, gt, gid, gflag, large_list, scan_tmp, ncand, dst_off;
   Buf steps_dev, base_dev, pos, step_arr, groups_dev, packs_dev, big_dev;
   std::vector<int64_t> step_host;
   int64_t* step_host_p = nullptr;

@@ -77,7 +77,7 @@ struct ft_graph {
   int rank = 0, world = 1;
   bool loopback = false;  // world > 1 simulated on one GPU (tests)
   bool no_shared = false;  // FT_NO_SHARED=1 disables the shared-order node path (A/B tests)
-  double replicate_tau = 1e8;  // waves below this estimated cost (tuples) are replicated
+  double replicate_tau = 2e7;  // waves below this estimated cost (tuples) are replicated
   std::vector<int> set_edge;   // original edge index of each original edge set (-1 otherwise)
   ncclComm_t comm = nullptr;
   bool keep_all = false;

@@ -2572,7 +2572,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   s.nsteps = nsteps;
   s.slog = slog;
   s.slog0 = slog0;
-  s.cdirect = cdirect;
+  // waves of few segments (LDP: one per configuration) take a larger direct
+  // capacity: one filter level fewer per segment, and few CTAs sort in smem
+  // (A/B: a global 2048 helped C5's LDP waves but slowed C4's 6e4-segment
+  // node waves, 52 -> 58 ms)
+  const int cd = nloc <= small_wave_segs ? std::min(C_DIRECT, cdirect * 2) : cdirect;
+  s.cdirect = cd;
   s.nseg = nloc;
   s.nblk = nbl;
   batch = s;
@@ -2725,7 +2730,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
             s, L, (const NodeGroup*)groups_dev.p);
       }
       k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, DW_SMEM, st>>>(s, L);
-      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cdirect), st>>>(s, L);
+      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cd), st>>>(s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
         L.bucket_base = (int64_t*)bucket_base.p;
@@ -2917,6 +2922,7 @@ cudaError_t StepRunner::configure() {
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(256, std::min(C_DIRECT, atoi(e)));
+  if (const char* e = getenv("FT_SMALL_WAVE")) small_wave_segs = std::max(0, atoi(e));
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)direct_smem(C_DIRECT));

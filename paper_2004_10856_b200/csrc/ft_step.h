@@ -81,6 +81,7 @@ class StepRunner {
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
   int cdirect = 1024;                 // direct-path capacity (<= C_DIRECT)
+  int small_wave_segs = 4096;         // waves with <= this many segments: capacity 2 x cdirect (A/B: 4096 > 1024 > 0)
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int pack_grid = 148 * 4;             // CTAs of k_node_pack (each takes a contiguous pack range)

@@ -218,6 +218,70 @@ const char* ft_last_error(const ft_graph* g);
 /* Library version string, e.g. "ft-b200 0.1 sm_100a". */
 const char* ft_version(void);
 
+/* ---------------------------------------------------------------------------
+ * Edge-cost generation: the step before the FT path.
+ * Produces t_x(e_ij, s_i^k, s_j^p) of Eq. 2 (m(e,...) = 0) from
+ * the profile-interpolated communication time (reading R18) and
+ * tensor re-scheduling as a shortest path over tensor splits (R19).
+ * Standalone: no graph handle; all arrays are HOST memory, copied in/out by
+ * the call; the computation runs on the current CUDA device (FT_ECUDA
+ * without one).  Thread-safe (no global state besides the device).
+ * ------------------------------------------------------------------------- */
+#define FT_CG_MAX_MESH 6   /* mesh of up to 2^6 = 64 devices */
+#define FT_CG_MAX_P 46     /* profiled sizes 2^0 .. 2^P bytes, P <= 46 */
+#define FT_CG_MAX_DIMS 4   /* tensor rank */
+#define FT_CG_MAX_STATES 160 /* split states per tensor (shared-memory APSP) */
+
+/* Bandwidth profile: for a collective whose device group has
+ * 2^c members (c = 1..mesh_log2; the "device partitioning scheme"),
+ * bw[c][i] = measured bandwidth in bytes/s (> 0) at data size 2^i, i = 0..P,
+ * and latency_ns[c] >= 0.  Row c = 0 is unused (no partners, time 0). */
+typedef struct ft_comm_profile {
+  int32_t mesh_log2;                                  /* L: 2^L devices, 1..FT_CG_MAX_MESH */
+  int32_t P;                                          /* largest profiled size 2^P, 1..FT_CG_MAX_P */
+  int64_t latency_ns[FT_CG_MAX_MESH + 1];
+  int64_t bw[FT_CG_MAX_MESH + 1][FT_CG_MAX_P + 1];
+} ft_comm_profile;
+
+/* comm_time (R18), n queries: t_out[q] = time in integer ns to
+ * move bytes[q] per device in a collective over a group of 2^group_log2[q]
+ * devices.  0 if bytes == 0 or group_log2 == 0; else with 2^i <= b < 2^(i+1),
+ * bw = bw[c][i] + (bw[c][i+1]-bw[c][i])*(b-2^i)/2^i (C integer division;
+ * bw[c][P] when i == P) and t = latency_ns[c] + ceil(b*1e9 / bw).
+ * Errors: FT_EINVAL (bad profile, group_log2 outside 0..mesh_log2, negative
+ * bytes), FT_EOVERFLOW (bytes > 2^P: outside the profile). */
+int ft_comm_time(const ft_comm_profile* prof, int64_t n, const int64_t* bytes,
+                 const int32_t* group_log2, int64_t* t_out);
+
+/* Split states of a tensor (R19): a = (a_0..a_{D-1}), a_j >= 0,
+ * sum a_j <= mesh_log2, 2^a_j divides dims[j]; dim j is split over 2^a_j
+ * devices and the tensor is replicated over the remaining 2^(L - sum a).
+ * Index = rank in lexicographic order of a.  states_out[cap * ndims]
+ * (row-major, may be NULL when cap = 0); *n_out = number of states
+ * (two-call pattern, FT_ESIZE if cap too small).  Host only, no device. */
+int ft_split_states(int32_t ndims, const int64_t* dims, int32_t mesh_log2, int64_t cap,
+                    int32_t* states_out, int64_t* n_out);
+
+/* Re-scheduling edge costs (R19): for n_tensors tensors (tensor τ:
+ * ndims[τ] <= FT_CG_MAX_DIMS dims at dims[τ*FT_CG_MAX_DIMS + j] >= 1,
+ * elem_bytes[τ] >= 1, product < 2^P) the library builds the state graph
+ * whose edges are single collectives -- all-gather on one dim (group 2^c,
+ * each device receives shard*(2^c-1) bytes), local slice on one dim (time 0)
+ * and all-to-all moving a factor 2^c from dim i to dim j (group 2^c,
+ * shard - shard/2^c bytes) -- weighted by ft_comm_time, and solves all-pairs
+ * shortest paths on the GPU.  For n_q queries (tensor q_tensor[q], output
+ * split q_from[q], required input split q_to[q], state indices of
+ * ft_split_states):  t_out[q] = d(from, to) + d(to, from)  (forward
+ * re-scheduling plus the backward re-scheduling of the gradient, Eq. 2
+ * "both forward pass and backward pass").
+ * Errors: FT_EINVAL (bad tensor / query index / profile), FT_EOVERFLOW
+ * (tensor bytes > 2^P), FT_ESIZE (a tensor with > FT_CG_MAX_STATES states),
+ * FT_ECUDA. */
+int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
+                        const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
+                        const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,
+                        int64_t* t_out);
+
 #ifdef __cplusplus
 }
 #endif

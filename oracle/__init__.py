@@ -31,13 +31,13 @@ STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 
 
 def build(force: bool = False) -> str:
     """Compile liboracle_ft.so with g++ (plain -O2, no vectorisation tricks)."""
-    src = os.path.join(_HERE, "oracle_ft.cpp")
+    srcs = [os.path.join(_HERE, f) for f in ("oracle_ft.cpp", "oracle_costgen.cpp")]
     hdr = os.path.join(_HERE, "oracle_ft.h")
     if (not force and os.path.exists(LIB_PATH)
-            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(f) for f in srcs + [hdr])):
         return LIB_PATH
     subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-shared", "-fPIC", "-o",
-                           LIB_PATH, src, "-lpthread"])
+                           LIB_PATH, *srcs, "-lpthread"])
     return LIB_PATH
 
 
@@ -70,6 +70,11 @@ def lib():
         L.oft_last_error.restype = C.c_char_p
         L.oft_reduce.argtypes = [C.c_int64, P64, P64, PU64, P64, P64, PU64, P64]
         L.oft_segment_reduce.argtypes = [C.c_int32] + [P64] * 9 + [C.c_int64, P64, P64, PU64, P64]
+        L.ocg_comm_time.argtypes = [C.c_void_p, C.c_int64, P64, P32, P64]
+        L.ocg_split_states.argtypes = [C.c_int32, P64, C.c_int32, C.c_int64, P32, P64]
+        L.ocg_state_dist.argtypes = [C.c_void_p, C.c_int32, P64, C.c_int64, C.c_int64, P64, P64]
+        L.ocg_reschedule_costs.argtypes = [C.c_void_p, C.c_int32, P32, P64, P64, C.c_int64,
+                                           P32, P32, P32, P64]
         _lib = L
     return _lib
 
@@ -241,3 +246,81 @@ def segment_reduce(blocks):
         raise OracleError(rc, "segment_reduce")
     k = no.value
     return mo[:k], to[:k], io[:k]
+
+
+# ---------------------------------------------------------------------------
+# Edge-cost generation (oracle_costgen.cpp)
+# ---------------------------------------------------------------------------
+class _Profile(C.Structure):
+    _fields_ = [("L", C.c_int32), ("P", C.c_int32), ("lat", C.c_int64 * 7),
+                ("bw", (C.c_int64 * 47) * 7)]
+
+
+def _profile(prof) -> _Profile:
+    p = _Profile()
+    p.L, p.P = int(prof["L"]), int(prof["P"])
+    for c in range(7):
+        p.lat[c] = int(prof["lat"][c])
+        for i in range(47):
+            p.bw[c][i] = int(prof["bw"][c][i])
+    return p
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise OracleError(rc, what)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, what):
+        super().__init__(f"oracle {what}: error {code}")
+        self.code = code
+
+
+def comm_time(prof, nbytes, group_log2) -> np.ndarray:
+    """P:668-671 interpolated communication time in ns (R18)."""
+    b = np.ascontiguousarray(nbytes, np.int64)
+    g = np.ascontiguousarray(np.broadcast_to(np.asarray(group_log2, np.int32), b.shape), np.int32)
+    out = np.zeros(b.shape, np.int64)
+    p = _profile(prof)
+    _check(lib().ocg_comm_time(C.byref(p), b.size, _p(b, C.c_int64), _p(g, C.c_int32),
+                               _p(out, C.c_int64)), "comm_time")
+    return out
+
+
+def split_states(dims, L: int) -> np.ndarray:
+    """Split states (R19) of a tensor with shape `dims` on 2^L devices, [S, D] int32."""
+    d = np.ascontiguousarray(dims, np.int64)
+    n = C.c_int64(0)
+    rc = lib().ocg_split_states(d.size, _p(d, C.c_int64), L, 0, None, C.byref(n))
+    out = np.zeros((n.value, d.size), np.int32)
+    _check(lib().ocg_split_states(d.size, _p(d, C.c_int64), L, n.value, _p(out, C.c_int32),
+                                  C.byref(n)), "split_states")
+    return out
+
+
+def state_dist(prof, dims, elem_bytes: int) -> np.ndarray:
+    """All-pairs re-scheduling distances (Dijkstra), [S, S] int64."""
+    d = np.ascontiguousarray(dims, np.int64)
+    S = len(split_states(d, int(prof["L"])))
+    out = np.zeros((S, S), np.int64)
+    n = C.c_int64(0)
+    p = _profile(prof)
+    _check(lib().ocg_state_dist(C.byref(p), d.size, _p(d, C.c_int64), int(elem_bytes), S * S,
+                                _p(out, C.c_int64), C.byref(n)), "state_dist")
+    return out
+
+
+def reschedule_costs(prof, ndims, dims, elem_bytes, q_tensor, q_from, q_to) -> np.ndarray:
+    """t_x = d(from,to) + d(to,from) per query (Eq. 2 + P:860, R19)."""
+    nd = np.ascontiguousarray(ndims, np.int32)
+    dm = np.ascontiguousarray(dims, np.int64)
+    eb = np.ascontiguousarray(elem_bytes, np.int64)
+    qt, qf, qo = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_from, q_to))
+    out = np.zeros(qt.size, np.int64)
+    p = _profile(prof)
+    _check(lib().ocg_reschedule_costs(C.byref(p), nd.size, _p(nd, C.c_int32), _p(dm, C.c_int64),
+                                      _p(eb, C.c_int64), qt.size, _p(qt, C.c_int32),
+                                      _p(qf, C.c_int32), _p(qo, C.c_int32), _p(out, C.c_int64)),
+           "reschedule_costs")
+    return out

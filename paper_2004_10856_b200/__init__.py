@@ -53,6 +53,15 @@ class ft_step_stats(C.Structure):
                 ("compact_ms", C.c_float), ("host_ms", C.c_float), ("path", C.c_int64 * 4)]
 
 
+CG_MAX_MESH, CG_MAX_P, CG_MAX_DIMS = 6, 46, 4
+
+
+class ft_comm_profile(C.Structure):
+    _fields_ = [("mesh_log2", C.c_int32), ("P", C.c_int32),
+                ("latency_ns", C.c_int64 * (CG_MAX_MESH + 1)),
+                ("bw", (C.c_int64 * (CG_MAX_P + 1)) * (CG_MAX_MESH + 1))]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libft.so not built ({LIB_PATH}); run __graft_entry__.build()")
@@ -83,6 +92,10 @@ def _load():
     L.ft_last_error.restype = C.c_char_p
     L.ft_version.argtypes = []
     L.ft_version.restype = C.c_char_p
+    L.ft_comm_time.argtypes = [C.POINTER(ft_comm_profile), C.c_int64, P64, P32, P64]
+    L.ft_split_states.argtypes = [C.c_int32, P64, C.c_int32, C.c_int64, P32, P64]
+    L.ft_reschedule_costs.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64,
+                                      C.c_int64, P32, P32, P32, P64]
     return L
 
 
@@ -90,7 +103,8 @@ lib = _load()
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
            "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
-           "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version"]
+           "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version",
+           "ft_comm_time", "ft_split_states", "ft_reschedule_costs"]
 
 
 def _p(a, t):
@@ -288,3 +302,63 @@ def run_ft(w, **kw):
     g.eliminate(AUTO)
     m, t = g.frontier()
     return g, m, t
+
+
+# ---------------------------------------------------------------------------
+# Edge-cost generation (csrc/ft_costgen.cu)
+# ---------------------------------------------------------------------------
+def comm_profile(prof) -> ft_comm_profile:
+    """Pack {L, P, lat[7], bw[7][47]} into the C struct of include/ft.h."""
+    p = ft_comm_profile()
+    p.mesh_log2, p.P = int(prof["L"]), int(prof["P"])
+    lat = np.asarray(prof["lat"], np.int64)
+    bw = np.asarray(prof["bw"], np.int64)
+    for c in range(CG_MAX_MESH + 1):
+        p.latency_ns[c] = int(lat[c])
+        for i in range(CG_MAX_P + 1):
+            p.bw[c][i] = int(bw[c, i])
+    return p
+
+
+def _cg_check(rc: int, what: str):
+    if rc != OK:
+        raise FTError(rc, what)
+
+
+def comm_time(prof, nbytes, group_log2) -> np.ndarray:
+    """ft_comm_time: interpolated collective time in ns (R18), on the GPU."""
+    b = np.ascontiguousarray(nbytes, np.int64).ravel()
+    g = np.ascontiguousarray(np.broadcast_to(np.asarray(group_log2, np.int32), b.shape), np.int32)
+    out = np.zeros(b.shape, np.int64)
+    p = prof if isinstance(prof, ft_comm_profile) else comm_profile(prof)
+    _cg_check(lib.ft_comm_time(C.byref(p), b.size, _p(b, C.c_int64), _p(g, C.c_int32),
+                               _p(out, C.c_int64)), "ft_comm_time")
+    return out
+
+
+def split_states(dims, mesh_log2: int) -> np.ndarray:
+    """ft_split_states: split states (R19) of a tensor, [S, ndims] int32 (host)."""
+    d = np.ascontiguousarray(dims, np.int64)
+    n = C.c_int64(0)
+    rc = lib.ft_split_states(d.size, _p(d, C.c_int64), mesh_log2, 0, None, C.byref(n))
+    if rc not in (OK, ESIZE):
+        raise FTError(rc, "ft_split_states")
+    out = np.zeros((n.value, d.size), np.int32)
+    _cg_check(lib.ft_split_states(d.size, _p(d, C.c_int64), mesh_log2, n.value,
+                                  _p(out, C.c_int32), C.byref(n)), "ft_split_states")
+    return out
+
+
+def reschedule_costs(prof, ndims, dims, elem_bytes, q_tensor, q_from, q_to) -> np.ndarray:
+    """ft_reschedule_costs: t_x = d(from,to) + d(to,from) per query (Eq. 2, R19)."""
+    nd = np.ascontiguousarray(ndims, np.int32)
+    dm = np.ascontiguousarray(dims, np.int64).reshape(nd.size, CG_MAX_DIMS)
+    eb = np.ascontiguousarray(elem_bytes, np.int64)
+    qt, qf, qo = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_from, q_to))
+    out = np.zeros(qt.size, np.int64)
+    p = prof if isinstance(prof, ft_comm_profile) else comm_profile(prof)
+    _cg_check(lib.ft_reschedule_costs(C.byref(p), nd.size, _p(nd, C.c_int32), _p(dm, C.c_int64),
+                                      _p(eb, C.c_int64), qt.size, _p(qt, C.c_int32),
+                                      _p(qf, C.c_int32), _p(qo, C.c_int32), _p(out, C.c_int64)),
+              "ft_reschedule_costs")
+    return out

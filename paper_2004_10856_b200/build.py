@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libft.so")
-SOURCES = ["ft_step.cu", "ft_api.cu"]
+SOURCES = ["ft_step.cu", "ft_api.cu", "ft_costgen.cu"]
 HEADERS = ["ft_kernels.cuh", "ft_step.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

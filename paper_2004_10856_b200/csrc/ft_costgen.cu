@@ -1,0 +1,335 @@
+// ft_costgen.cu -- edge-cost generation on the GPU:
+// t_x(e, s_i^k, s_j^p) of Eq. 2 from the profile-interpolated
+// communication time (reading R18) and tensor re-scheduling as a
+// shortest path over tensor splits (R19).  C-ABI in include/ft.h.
+//
+// Kernels:
+//   k_cg_comm_time  grid-stride batch of comm_time queries (HBM streaming)
+//   k_cg_apsp       one CTA per tensor: build the state graph's weight matrix
+//                   in shared memory (one row per source state, moves generated
+//                   by the owning thread), then Floyd-Warshall in place in
+//                   shared memory (S <= 160: 200 KB of int64), store S x S.
+//   k_cg_gather     grid-stride: t_x[q] = d(from,to) + d(to,from).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ft.h"
+
+namespace {
+
+constexpr int64_t kInf = INT64_MAX / 4;
+constexpr int kApspThreads = 512;
+constexpr int kMaxCode = 7 * 7 * 7 * 7;  // (L+1)^D state codes, L <= 6, D <= 4
+
+struct TensorDesc {
+  int64_t total;     // bytes of the whole tensor
+  int64_t dist_off;  // offset of its S x S block in the distance buffer
+  int32_t state_off; // first row in the state table
+  int32_t n_states;
+  int32_t ndims;
+  int32_t pad;
+  int64_t dims[FT_CG_MAX_DIMS];
+};
+
+// comm_time (R18): 2^i <= b < 2^(i+1), linear interpolation of bw[c][i],
+// bw[c][i+1] in b (C division), then latency + ceil(b * 1e9 / bw).
+__device__ inline int64_t cg_time_dev(const ft_comm_profile& p, int64_t b, int c) {
+  if (b == 0 || c == 0) return 0;
+  const int i = 63 - __clzll(b);
+  __int128 bw = p.bw[c][i];
+  if (i < p.P) {
+    const int64_t lo = int64_t(1) << i;
+    bw += (__int128)(p.bw[c][i + 1] - p.bw[c][i]) * (b - lo) / lo;
+  }
+  const __int128 num = (__int128)b * 1000000000;
+  return p.latency_ns[c] + (int64_t)((num + bw - 1) / bw);
+}
+
+__global__ void k_cg_comm_time(const ft_comm_profile* __restrict__ prof, int64_t n,
+                               const int64_t* __restrict__ bytes, const int32_t* __restrict__ grp,
+                               int64_t* __restrict__ out) {
+  __shared__ ft_comm_profile p;
+  for (int i = threadIdx.x; i < (int)(sizeof(p) / 8); i += blockDim.x)
+    reinterpret_cast<int64_t*>(&p)[i] = reinterpret_cast<const int64_t*>(prof)[i];
+  __syncthreads();
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = cg_time_dev(p, bytes[q], grp[q]);
+}
+
+// One CTA per tensor.  States are packed one byte per dim (a_j <= 6) into
+// int32 codes; the lookup table maps the mixed-radix code sum a_j (L+1)^j to
+// the state index (-1 = invalid split).
+__global__ void __launch_bounds__(kApspThreads)
+k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict__ tens,
+          const int32_t* __restrict__ states, int64_t* __restrict__ dist) {
+  extern __shared__ int64_t smem[];
+  __shared__ ft_comm_profile p;
+  __shared__ int16_t lut[kMaxCode];
+  const TensorDesc td = tens[blockIdx.x];
+  const int S = td.n_states, D = td.ndims;
+  for (int i = threadIdx.x; i < (int)(sizeof(p) / 8); i += blockDim.x)
+    reinterpret_cast<int64_t*>(&p)[i] = reinterpret_cast<const int64_t*>(prof)[i];
+  const int L = prof->mesh_log2, R = L + 1;
+  int ncode = 1;
+  for (int j = 0; j < D; ++j) ncode *= R;
+  for (int i = threadIdx.x; i < ncode; i += blockDim.x) lut[i] = -1;
+  int64_t* d = smem;  // S x S
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) d[i] = (i / S == i % S) ? 0 : kInf;
+  __syncthreads();
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int32_t pk = states[td.state_off + s];
+    int code = 0, mul = 1;
+    for (int j = 0; j < D; ++j, mul *= R) code += ((pk >> (8 * j)) & 0xff) * mul;
+    lut[code] = (int16_t)s;
+  }
+  __syncthreads();
+  // Row s of the weight matrix: every single collective out of state s.
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int32_t pk = states[td.state_off + s];
+    int a[FT_CG_MAX_DIMS], pw[FT_CG_MAX_DIMS];
+    int used = 0, code = 0, mul = 1;
+    for (int j = 0; j < D; ++j, mul *= R) {
+      a[j] = (pk >> (8 * j)) & 0xff;
+      pw[j] = mul;
+      used += a[j];
+      code += a[j] * mul;
+    }
+    const int64_t shard = td.total >> used;
+    int64_t* row = d + (int64_t)s * S;
+    for (int j = 0; j < D; ++j) {
+      for (int c = 1; c <= a[j]; ++c) {  // all-gather on dim j, group 2^c
+        const int t = lut[code - c * pw[j]];
+        const int64_t w = cg_time_dev(p, shard * ((int64_t(1) << c) - 1), c);
+        if (w < row[t]) row[t] = w;
+      }
+      for (int c = 1; used + c <= L && a[j] + c <= L; ++c) {  // local slice
+        const int t = lut[code + c * pw[j]];
+        if (t >= 0) row[t] = 0;
+      }
+      for (int k = 0; k < D; ++k) {  // all-to-all: factor 2^c from dim j to dim k
+        if (k == j) continue;
+        for (int c = 1; c <= a[j] && a[k] + c <= L; ++c) {
+          const int t = lut[code - c * pw[j] + c * pw[k]];
+          if (t < 0) continue;
+          const int64_t w = cg_time_dev(p, shard - (shard >> c), c);
+          if (w < row[t]) row[t] = w;
+        }
+      }
+    }
+  }
+  // Floyd-Warshall in place: row k and column k do not change in round k
+  // (d[k][k] = 0), so the in-place update is race-free.
+  for (int k = 0; k < S; ++k) {
+    __syncthreads();
+    const int64_t* rk = d + (int64_t)k * S;
+    for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
+      const int i = e / S, j = e - i * S;
+      const int64_t v = d[(int64_t)i * S + k] + rk[j];
+      if (v < d[e]) d[e] = v;
+    }
+  }
+  __syncthreads();
+  int64_t* out = dist + td.dist_off;
+  for (int e = threadIdx.x; e < S * S; e += blockDim.x) out[e] = d[e];
+}
+
+__global__ void k_cg_gather(const TensorDesc* __restrict__ tens, const int64_t* __restrict__ dist,
+                            int64_t n, const int32_t* __restrict__ qt,
+                            const int32_t* __restrict__ qf, const int32_t* __restrict__ qo,
+                            int64_t* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int x = qt[q];
+    const int64_t S = tens[x].n_states, off = tens[x].dist_off;
+    const int64_t f = qf[q], t = qo[q];
+    out[q] = __ldg(dist + off + f * S + t) + __ldg(dist + off + t * S + f);
+  }
+}
+
+bool profile_valid(const ft_comm_profile* p) {
+  if (!p || p->mesh_log2 < 1 || p->mesh_log2 > FT_CG_MAX_MESH || p->P < 1 || p->P > FT_CG_MAX_P)
+    return false;
+  for (int c = 1; c <= p->mesh_log2; ++c) {
+    if (p->latency_ns[c] < 0) return false;
+    for (int i = 0; i <= p->P; ++i)
+      if (p->bw[c][i] <= 0) return false;
+  }
+  return true;
+}
+
+// Odometer enumeration of the split states in lexicographic order (a_0 most
+// significant).  Returns the packed codes (byte j = a_j).
+std::vector<int32_t> enum_states(int D, const int64_t* dims, int L) {
+  int amax[FT_CG_MAX_DIMS];
+  for (int j = 0; j < D; ++j) {
+    amax[j] = 0;
+    while (amax[j] < L && dims[j] % (int64_t(1) << (amax[j] + 1)) == 0) ++amax[j];
+  }
+  std::vector<int32_t> out;
+  int a[FT_CG_MAX_DIMS] = {0, 0, 0, 0};
+  for (;;) {
+    int sum = 0;
+    for (int j = 0; j < D; ++j) sum += a[j];
+    if (sum <= L) {
+      int32_t pk = 0;
+      for (int j = 0; j < D; ++j) pk |= a[j] << (8 * j);
+      out.push_back(pk);
+    }
+    int j = D - 1;  // increment the least significant digit first
+    while (j >= 0 && a[j] == amax[j]) a[j--] = 0;
+    if (j < 0) break;
+    ++a[j];
+  }
+  return out;
+}
+
+struct DevBufs {
+  std::vector<void*> ptrs;
+  ~DevBufs() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  cudaError_t alloc(T** p, size_t n) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, n ? n * sizeof(T) : 1);
+    if (e == cudaSuccess) ptrs.push_back(v);
+    *p = (T*)v;
+    return e;
+  }
+};
+
+#define CG_CHECK(x)                     \
+  do {                                  \
+    if ((x) != cudaSuccess) {           \
+      cudaGetLastError();               \
+      return FT_ECUDA;                  \
+    }                                   \
+  } while (0)
+
+int grid_for(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+}
+
+}  // namespace
+
+extern "C" int ft_comm_time(const ft_comm_profile* prof, int64_t n, const int64_t* bytes,
+                            const int32_t* group_log2, int64_t* t_out) {
+  if (!profile_valid(prof) || n < 0 || (n > 0 && (!bytes || !group_log2 || !t_out)))
+    return FT_EINVAL;
+  for (int64_t q = 0; q < n; ++q) {
+    if (bytes[q] < 0 || group_log2[q] < 0 || group_log2[q] > prof->mesh_log2) return FT_EINVAL;
+    if (bytes[q] > (int64_t(1) << prof->P)) return FT_EOVERFLOW;
+  }
+  if (n == 0) return FT_OK;
+  DevBufs B;
+  ft_comm_profile* dp;
+  int64_t *db, *dt;
+  int32_t* dg;
+  CG_CHECK(B.alloc(&dp, 1));
+  CG_CHECK(B.alloc(&db, n));
+  CG_CHECK(B.alloc(&dg, n));
+  CG_CHECK(B.alloc(&dt, n));
+  CG_CHECK(cudaMemcpy(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(db, bytes, n * 8, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dg, group_log2, n * 4, cudaMemcpyHostToDevice));
+  k_cg_comm_time<<<grid_for(n), 256>>>(dp, n, db, dg, dt);
+  CG_CHECK(cudaGetLastError());
+  CG_CHECK(cudaMemcpy(t_out, dt, n * 8, cudaMemcpyDeviceToHost));
+  return FT_OK;
+}
+
+extern "C" int ft_split_states(int32_t ndims, const int64_t* dims, int32_t mesh_log2, int64_t cap,
+                               int32_t* states_out, int64_t* n_out) {
+  if (ndims < 1 || ndims > FT_CG_MAX_DIMS || !dims || !n_out || mesh_log2 < 1 ||
+      mesh_log2 > FT_CG_MAX_MESH || cap < 0 || (cap > 0 && !states_out))
+    return FT_EINVAL;
+  for (int j = 0; j < ndims; ++j)
+    if (dims[j] < 1) return FT_EINVAL;
+  const std::vector<int32_t> st = enum_states(ndims, dims, mesh_log2);
+  *n_out = (int64_t)st.size();
+  if (cap < (int64_t)st.size()) return FT_ESIZE;
+  for (size_t s = 0; s < st.size(); ++s)
+    for (int j = 0; j < ndims; ++j) states_out[s * ndims + j] = (st[s] >> (8 * j)) & 0xff;
+  return FT_OK;
+}
+
+extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors,
+                                   const int32_t* ndims, const int64_t* dims,
+                                   const int64_t* elem_bytes, int64_t n_q, const int32_t* q_tensor,
+                                   const int32_t* q_from, const int32_t* q_to, int64_t* t_out) {
+  if (!profile_valid(prof) || n_tensors < 0 || n_q < 0 ||
+      (n_tensors > 0 && (!ndims || !dims || !elem_bytes)) ||
+      (n_q > 0 && (!q_tensor || !q_from || !q_to || !t_out)))
+    return FT_EINVAL;
+  const int64_t cap = int64_t(1) << prof->P;
+  std::vector<TensorDesc> td(n_tensors);
+  std::vector<int32_t> states;
+  int64_t dist_total = 0;
+  int max_s = 0;
+  for (int x = 0; x < n_tensors; ++x) {
+    TensorDesc& t = td[x];
+    std::memset(&t, 0, sizeof(t));
+    t.ndims = ndims[x];
+    if (t.ndims < 1 || t.ndims > FT_CG_MAX_DIMS || elem_bytes[x] < 1) return FT_EINVAL;
+    int64_t total = elem_bytes[x];
+    for (int j = 0; j < t.ndims; ++j) {
+      const int64_t dj = dims[(int64_t)x * FT_CG_MAX_DIMS + j];
+      if (dj < 1) return FT_EINVAL;
+      if (total > cap / dj) return FT_EOVERFLOW;
+      total *= dj;
+      t.dims[j] = dj;
+    }
+    t.total = total;
+    const std::vector<int32_t> st = enum_states(t.ndims, t.dims, prof->mesh_log2);
+    if ((int64_t)st.size() > FT_CG_MAX_STATES) return FT_ESIZE;
+    t.state_off = (int32_t)states.size();
+    t.n_states = (int32_t)st.size();
+    t.dist_off = dist_total;
+    dist_total += (int64_t)st.size() * st.size();
+    states.insert(states.end(), st.begin(), st.end());
+    if (t.n_states > max_s) max_s = t.n_states;
+  }
+  for (int64_t q = 0; q < n_q; ++q) {
+    const int32_t x = q_tensor[q];
+    if (x < 0 || x >= n_tensors || q_from[q] < 0 || q_from[q] >= td[x].n_states || q_to[q] < 0 ||
+        q_to[q] >= td[x].n_states)
+      return FT_EINVAL;
+  }
+  if (n_tensors == 0 || n_q == 0) return FT_OK;
+  DevBufs B;
+  ft_comm_profile* dp;
+  TensorDesc* dtd;
+  int32_t *dst, *dqt, *dqf, *dqo;
+  int64_t *dd, *dout;
+  CG_CHECK(B.alloc(&dp, 1));
+  CG_CHECK(B.alloc(&dtd, td.size()));
+  CG_CHECK(B.alloc(&dst, states.size()));
+  CG_CHECK(B.alloc(&dd, dist_total));
+  CG_CHECK(B.alloc(&dqt, n_q));
+  CG_CHECK(B.alloc(&dqf, n_q));
+  CG_CHECK(B.alloc(&dqo, n_q));
+  CG_CHECK(B.alloc(&dout, n_q));
+  CG_CHECK(cudaMemcpy(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dqt, q_tensor, n_q * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dqf, q_from, n_q * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dqo, q_to, n_q * 4, cudaMemcpyHostToDevice));
+  const size_t smem = (size_t)max_s * max_s * sizeof(int64_t);
+  CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_cg_apsp<<<n_tensors, kApspThreads, smem>>>(dp, dtd, dst, dd);
+  CG_CHECK(cudaGetLastError());
+  k_cg_gather<<<grid_for(n_q), 256>>>(dtd, dd, n_q, dqt, dqf, dqo, dout);
+  CG_CHECK(cudaGetLastError());
+  CG_CHECK(cudaMemcpy(t_out, dout, n_q * 8, cudaMemcpyDeviceToHost));
+  return FT_OK;
+}

@@ -1,0 +1,90 @@
+"""Measure edge-cost generation on one GPU.
+
+Workload "CG5": the edge-cost tables of the C5 graph (2,324 edges, K = 64
+configs per op -> 9.5 M (k, p) queries), one activation tensor per edge
+(D = 3 dims drawn by synth.comm.tensors), a 32-device mesh (L = 5), profile
+sizes 2^0..2^40.  Each op config k picks an output split and a required input
+split (seeded).  One step = one ft_reschedule_costs call through the C-ABI
+with HOST buffers (H2D of queries, the APSP + gather kernels, D2H of t_x), so
+the number is end-to-end; kernel shares come from the ncu launch list.
+Prints one JSON line; `--oracle` adds the CPU oracle timed on the same call.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from synth import comm, graphs as G  # noqa: E402
+
+
+def workload(seed=0, L=5):
+    w = G.c5(seed=seed)
+    n_e = w.n_edges
+    nd, dims, eb = comm.tensors(seed, n_e, L, max_ndims=3)
+    rng = np.random.default_rng(seed + 1)
+    return w, nd, dims, eb, rng
+
+
+def queries(w, ns, rng):
+    out_state = [None] * w.n_ops
+    in_state = [None] * w.n_ops
+    qt, qf, qo = [], [], []
+    for e, (s, d) in enumerate(zip(w.src, w.dst)):
+        S = ns[e]
+        ks, kd = int(w.n_cfgs[s]), int(w.n_cfgs[d])
+        f = rng.integers(0, S, ks)
+        t = rng.integers(0, S, kd)
+        F, T = np.meshgrid(f, t, indexing="ij")
+        qt.append(np.full(F.size, e, np.int32)); qf.append(F.ravel()); qo.append(T.ravel())
+    return tuple(np.concatenate(a).astype(np.int32) for a in (qt, qf, qo))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--L", type=int, default=5)
+    args = ap.parse_args()
+    import paper_2004_10856_b200 as ft
+    L = args.L
+    w, nd, dims, eb, rng = workload(0, L)
+    ns = [len(ft.split_states(dims[x, :nd[x]], L)) for x in range(len(nd))]
+    qt, qf, qo = queries(w, ns, rng)
+    prof = ft.comm_profile(comm.profile(0, L=L, P=40))
+    for _ in range(args.warmup):
+        out = ft.reschedule_costs(prof, nd, dims, eb, qt, qf, qo)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out = ft.reschedule_costs(prof, nd, dims, eb, qt, qf, qo)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.median(ts))
+    line = {"metric": "edge-cost queries/s (re-scheduling t_x, P:860)", "value": qt.size / (ms / 1e3),
+            "unit": "queries/s", "ms_per_step": ms, "ms_steps": [round(1e3 * t, 3) for t in ts],
+            "steps": args.steps, "warmup": args.warmup, "dtype": "int64", "data": "synthetic",
+            "timing": "host wall clock around the C-ABI call (H2D + kernels + D2H)",
+            "config": {"workload": "CG5: C5 edges x K^2 (2324 edges, K=64)", "tensors": int(len(nd)),
+                       "queries": int(qt.size), "mesh_log2": L, "states_total": int(sum(ns)),
+                       "max_states": int(max(ns)), "apsp_work": int(sum(s ** 3 for s in ns))},
+            "h2d_bytes_per_step": int(qt.size * 12 + dims.nbytes + nd.nbytes + eb.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes)}
+    if args.oracle:
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.reschedule_costs(comm.profile(0, L=L, P=40), nd, dims, eb, qt, qf, qo)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": qt.size / dt, "unit": "queries/s", "cores": 1,
+                                "kind": "oracle", "sample": f"the whole workload, {dt:.2f} s"}
+        line["parity"] = bool(np.array_equal(ref, out))
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

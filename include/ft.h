@@ -276,11 +276,23 @@ int ft_split_states(int32_t ndims, const int64_t* dims, int32_t mesh_log2, int64
  * "both forward pass and backward pass").
  * Errors: FT_EINVAL (bad tensor / query index / profile), FT_EOVERFLOW
  * (tensor bytes > 2^P), FT_ESIZE (a tensor with > FT_CG_MAX_STATES states),
- * FT_ECUDA. */
+ * FT_ECUDA.  Query indices are validated on the device (FT_EINVAL after
+ * the kernels; t_out is then unspecified).  Device buffers are pooled per
+ * device across calls (grow-only; calls on one device serialise). */
 int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
                         const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
                         const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,
                         int64_t* t_out);
+
+/* Same as ft_reschedule_costs, but q_tensor / q_from / q_to / t_out are
+ * DEVICE pointers (caller-owned, on the current device) and the kernels run
+ * on `stream` (cudaStream_t; NULL = legacy default stream).  The tensor
+ * descriptions and the profile stay HOST arrays.  Returns after the stream
+ * has completed the call's work. */
+int ft_reschedule_costs_dev(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
+                            const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
+                            const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,
+                            int64_t* t_out, void* stream);
 
 #ifdef __cplusplus
 }

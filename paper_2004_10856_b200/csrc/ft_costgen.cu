@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/ft.h"
@@ -22,7 +23,7 @@
 namespace {
 
 constexpr int64_t kInf = INT64_MAX / 4;
-constexpr int kApspThreads = 512;
+constexpr int kApspThreads = 256;
 constexpr int kMaxCode = 7 * 7 * 7 * 7;  // (L+1)^D state codes, L <= 6, D <= 4
 
 struct TensorDesc {
@@ -87,6 +88,19 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
     for (int j = 0; j < D; ++j, mul *= R) code += ((pk >> (8 * j)) & 0xff) * mul;
     lut[code] = (int16_t)s;
   }
+  // A move's time depends only on (sum a, c): shard = total >> sum a.  The
+  // 2 x (L+1) x L distinct comm times are computed once, one per thread.
+  __shared__ int64_t w_gather[FT_CG_MAX_MESH + 1][FT_CG_MAX_MESH + 1];
+  __shared__ int64_t w_a2a[FT_CG_MAX_MESH + 1][FT_CG_MAX_MESH + 1];
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * R * L; e += blockDim.x) {
+    const int kind = e / (R * L), u = (e / L) % R, c = e % L + 1;
+    const int64_t shard = td.total >> u;
+    if (kind == 0)
+      w_gather[u][c] = c <= u ? cg_time_dev(p, shard * ((int64_t(1) << c) - 1), c) : 0;
+    else
+      w_a2a[u][c] = c <= u ? cg_time_dev(p, shard - (shard >> c), c) : 0;
+  }
   __syncthreads();
   // Row s of the weight matrix: every single collective out of state s.
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -99,12 +113,11 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
       used += a[j];
       code += a[j] * mul;
     }
-    const int64_t shard = td.total >> used;
     int64_t* row = d + (int64_t)s * S;
     for (int j = 0; j < D; ++j) {
       for (int c = 1; c <= a[j]; ++c) {  // all-gather on dim j, group 2^c
         const int t = lut[code - c * pw[j]];
-        const int64_t w = cg_time_dev(p, shard * ((int64_t(1) << c) - 1), c);
+        const int64_t w = w_gather[used][c];
         if (w < row[t]) row[t] = w;
       }
       for (int c = 1; used + c <= L && a[j] + c <= L; ++c) {  // local slice
@@ -116,21 +129,79 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
         for (int c = 1; c <= a[j] && a[k] + c <= L; ++c) {
           const int t = lut[code - c * pw[j] + c * pw[k]];
           if (t < 0) continue;
-          const int64_t w = cg_time_dev(p, shard - (shard >> c), c);
+          const int64_t w = w_a2a[used][c];
           if (w < row[t]) row[t] = w;
         }
       }
     }
   }
-  // Floyd-Warshall in place: row k and column k do not change in round k
-  // (d[k][k] = 0), so the in-place update is race-free.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (S <= 64 && nwarp == 4) {
+    // Register-resident Floyd-Warshall (S <= 64, 4 warps): thread (warp w,
+    // lane l) owns d[w + 4r][l + 32c], r < 16, c < 2.  Round k publishes
+    // row k (its owner warp) and column k (lane k%32 of every warp) to
+    // double-buffered shared rows, one barrier per round; every thread then
+    // does 32 min-plus updates from 2 + 16 shared loads.
+    __syncthreads();
+    int64_t v[16][2];
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int i = warp + 4 * r, j = lane + 32 * c;
+        v[r][c] = (i < S && j < S) ? d[i * S + j] : kInf;
+      }
+    __shared__ int64_t rowbuf[2][64], colbuf[2][64];
+    for (int k = 0; k < S; ++k) {
+      const int b = k & 1;
+      if ((k & 3) == warp) {
+        const int r = k >> 2;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr)
+          if (rr == r) {
+            rowbuf[b][lane] = v[rr][0];
+            rowbuf[b][lane + 32] = v[rr][1];
+          }
+      }
+      if ((k & 31) == lane) {
+        const int c = k >> 5;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) colbuf[b][warp + 4 * r] = c ? v[r][1] : v[r][0];
+      }
+      __syncthreads();
+      const int64_t rk0 = rowbuf[b][lane], rk1 = rowbuf[b][lane + 32];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int64_t dik = colbuf[b][warp + 4 * r];
+        v[r][0] = min(v[r][0], dik + rk0);
+        v[r][1] = min(v[r][1], dik + rk1);
+      }
+    }
+    int64_t* out = dist + td.dist_off;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int i = warp + 4 * r, j = lane + 32 * c;
+        if (i < S && j < S) out[i * S + j] = v[r][c];
+      }
+    return;
+  }
+  // General case: Floyd-Warshall in place in shared memory: row k and column
+  // k do not change in round k (d[k][k] = 0), so the in-place update is
+  // race-free.  Lane -> column j
+  // (a warp reads 32 consecutive int64 of row k), warp -> row i (d[i][k] is a
+  // broadcast).
   for (int k = 0; k < S; ++k) {
     __syncthreads();
     const int64_t* rk = d + (int64_t)k * S;
-    for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
-      const int i = e / S, j = e - i * S;
-      const int64_t v = d[(int64_t)i * S + k] + rk[j];
-      if (v < d[e]) d[e] = v;
+    for (int i = warp; i < S; i += nwarp) {
+      int64_t* ri = d + (int64_t)i * S;
+      const int64_t dik = ri[k];
+      for (int j = lane; j < S; j += 32) {
+        const int64_t v = dik + rk[j];
+        if (v < ri[j]) ri[j] = v;
+      }
     }
   }
   __syncthreads();
@@ -138,16 +209,27 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
   for (int e = threadIdx.x; e < S * S; e += blockDim.x) out[e] = d[e];
 }
 
-__global__ void k_cg_gather(const TensorDesc* __restrict__ tens, const int64_t* __restrict__ dist,
-                            int64_t n, const int32_t* __restrict__ qt,
-                            const int32_t* __restrict__ qf, const int32_t* __restrict__ qo,
-                            int64_t* __restrict__ out) {
+__global__ void k_cg_gather(const TensorDesc* __restrict__ tens, int32_t n_tensors,
+                            const int64_t* __restrict__ dist, int64_t n,
+                            const int32_t* __restrict__ qt, const int32_t* __restrict__ qf,
+                            const int32_t* __restrict__ qo, int64_t* __restrict__ out,
+                            int32_t* __restrict__ bad) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const int x = qt[q];
+    const int x = __ldcs(qt + q);
+    const int64_t f = __ldcs(qf + q), t = __ldcs(qo + q);
+    if ((unsigned)x >= (unsigned)n_tensors) {  // invalid query: flag, write 0
+      *bad = 1;
+      __stcs(out + q, (int64_t)0);
+      continue;
+    }
     const int64_t S = tens[x].n_states, off = tens[x].dist_off;
-    const int64_t f = qf[q], t = qo[q];
-    out[q] = __ldg(dist + off + f * S + t) + __ldg(dist + off + t * S + f);
+    if ((uint64_t)f >= (uint64_t)S || (uint64_t)t >= (uint64_t)S) {
+      *bad = 1;
+      __stcs(out + q, (int64_t)0);
+      continue;
+    }
+    __stcs(out + q, __ldg(dist + off + f * S + t) + __ldg(dist + off + t * S + f));
   }
 }
 
@@ -202,6 +284,37 @@ struct DevBufs {
     return e;
   }
 };
+
+// Grow-only device buffers reused across calls (one pool per device; calls
+// on the same device serialise on its mutex).
+struct Pool {
+  std::mutex mu;
+  void* buf[8] = {};
+  size_t cap[8] = {};
+  cudaError_t get(int slot, size_t bytes, void** out) {
+    if (bytes > cap[slot]) {
+      const size_t want = std::max(bytes, cap[slot] * 3 / 2);
+      if (buf[slot]) cudaFree(buf[slot]);
+      buf[slot] = nullptr;
+      cap[slot] = 0;
+      cudaError_t e = cudaMalloc(&buf[slot], want);
+      if (e != cudaSuccess) return e;
+      cap[slot] = want;
+    }
+    *out = buf[slot];
+    return cudaSuccess;
+  }
+};
+
+Pool& pool_for_device() {
+  static std::mutex m;
+  static Pool* pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(m);
+  if (!pools[dev & 63]) pools[dev & 63] = new Pool();
+  return *pools[dev & 63];
+}
 
 #define CG_CHECK(x)                     \
   do {                                  \
@@ -262,22 +375,22 @@ extern "C" int ft_split_states(int32_t ndims, const int64_t* dims, int32_t mesh_
   return FT_OK;
 }
 
-extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors,
-                                   const int32_t* ndims, const int64_t* dims,
-                                   const int64_t* elem_bytes, int64_t n_q, const int32_t* q_tensor,
-                                   const int32_t* q_from, const int32_t* q_to, int64_t* t_out) {
-  if (!profile_valid(prof) || n_tensors < 0 || n_q < 0 ||
-      (n_tensors > 0 && (!ndims || !dims || !elem_bytes)) ||
-      (n_q > 0 && (!q_tensor || !q_from || !q_to || !t_out)))
+namespace {
+
+// Host-side part shared by both entry points: validate the tensors, enumerate
+// their split states, lay out the distance blocks.
+int plan_tensors(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
+                 const int64_t* dims, const int64_t* elem_bytes, std::vector<TensorDesc>& td,
+                 std::vector<int32_t>& states, int64_t& dist_total, int& max_s) {
+  if (!profile_valid(prof) || n_tensors < 0 || (n_tensors > 0 && (!ndims || !dims || !elem_bytes)))
     return FT_EINVAL;
   const int64_t cap = int64_t(1) << prof->P;
-  std::vector<TensorDesc> td(n_tensors);
-  std::vector<int32_t> states;
-  int64_t dist_total = 0;
-  int max_s = 0;
+  td.assign(n_tensors, TensorDesc{});
+  states.clear();
+  dist_total = 0;
+  max_s = 0;
   for (int x = 0; x < n_tensors; ++x) {
     TensorDesc& t = td[x];
-    std::memset(&t, 0, sizeof(t));
     t.ndims = ndims[x];
     if (t.ndims < 1 || t.ndims > FT_CG_MAX_DIMS || elem_bytes[x] < 1) return FT_EINVAL;
     int64_t total = elem_bytes[x];
@@ -298,38 +411,93 @@ extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensor
     states.insert(states.end(), st.begin(), st.end());
     if (t.n_states > max_s) max_s = t.n_states;
   }
-  for (int64_t q = 0; q < n_q; ++q) {
-    const int32_t x = q_tensor[q];
-    if (x < 0 || x >= n_tensors || q_from[q] < 0 || q_from[q] >= td[x].n_states || q_to[q] < 0 ||
-        q_to[q] >= td[x].n_states)
-      return FT_EINVAL;
-  }
-  if (n_tensors == 0 || n_q == 0) return FT_OK;
-  DevBufs B;
-  ft_comm_profile* dp;
-  TensorDesc* dtd;
-  int32_t *dst, *dqt, *dqf, *dqo;
-  int64_t *dd, *dout;
-  CG_CHECK(B.alloc(&dp, 1));
-  CG_CHECK(B.alloc(&dtd, td.size()));
-  CG_CHECK(B.alloc(&dst, states.size()));
-  CG_CHECK(B.alloc(&dd, dist_total));
-  CG_CHECK(B.alloc(&dqt, n_q));
-  CG_CHECK(B.alloc(&dqf, n_q));
-  CG_CHECK(B.alloc(&dqo, n_q));
-  CG_CHECK(B.alloc(&dout, n_q));
-  CG_CHECK(cudaMemcpy(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice));
-  CG_CHECK(cudaMemcpy(dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice));
-  CG_CHECK(cudaMemcpy(dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice));
-  CG_CHECK(cudaMemcpy(dqt, q_tensor, n_q * 4, cudaMemcpyHostToDevice));
-  CG_CHECK(cudaMemcpy(dqf, q_from, n_q * 4, cudaMemcpyHostToDevice));
-  CG_CHECK(cudaMemcpy(dqo, q_to, n_q * 4, cudaMemcpyHostToDevice));
+  return FT_OK;
+}
+
+// APSP + gather on `stream` with device query/output pointers; pool slots
+// 0..4 hold the profile, descriptors, states, distances and the error flag.
+int run_device(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDesc>& td,
+               const std::vector<int32_t>& states, int64_t dist_total, int max_s, int64_t n_q,
+               const int32_t* qt, const int32_t* qf, const int32_t* qo, int64_t* out,
+               cudaStream_t st) {
+  void *dp, *dtd, *dst, *dd, *dbad;
+  CG_CHECK(P.get(0, sizeof(*prof), &dp));
+  CG_CHECK(P.get(1, td.size() * sizeof(TensorDesc), &dtd));
+  CG_CHECK(P.get(2, states.size() * 4, &dst));
+  CG_CHECK(P.get(3, (size_t)dist_total * 8, &dd));
+  CG_CHECK(P.get(4, 4, &dbad));
+  CG_CHECK(cudaMemcpyAsync(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemsetAsync(dbad, 0, 4, st));
   const size_t smem = (size_t)max_s * max_s * sizeof(int64_t);
   CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_cg_apsp<<<n_tensors, kApspThreads, smem>>>(dp, dtd, dst, dd);
+  CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  // Small state graphs: 4 warps per tensor so more tensors are resident per SM.
+  const int threads = max_s <= 64 ? 128 : kApspThreads;
+  k_cg_apsp<<<(int)td.size(), threads, smem, st>>>((const ft_comm_profile*)dp,
+                                                       (const TensorDesc*)dtd, (const int32_t*)dst,
+                                                       (int64_t*)dd);
   CG_CHECK(cudaGetLastError());
-  k_cg_gather<<<grid_for(n_q), 256>>>(dtd, dd, n_q, dqt, dqf, dqo, dout);
+  k_cg_gather<<<grid_for(n_q), 256, 0, st>>>((const TensorDesc*)dtd, (int32_t)td.size(),
+                                             (const int64_t*)dd, n_q, qt, qf, qo, out,
+                                             (int32_t*)dbad);
   CG_CHECK(cudaGetLastError());
-  CG_CHECK(cudaMemcpy(t_out, dout, n_q * 8, cudaMemcpyDeviceToHost));
+  int32_t bad = 0;
+  CG_CHECK(cudaMemcpyAsync(&bad, dbad, 4, cudaMemcpyDeviceToHost, st));
+  CG_CHECK(cudaStreamSynchronize(st));
+  return bad ? FT_EINVAL : FT_OK;
+}
+
+}  // namespace
+
+extern "C" int ft_reschedule_costs_dev(const ft_comm_profile* prof, int32_t n_tensors,
+                                       const int32_t* ndims, const int64_t* dims,
+                                       const int64_t* elem_bytes, int64_t n_q,
+                                       const int32_t* q_tensor, const int32_t* q_from,
+                                       const int32_t* q_to, int64_t* t_out, void* stream) {
+  if (n_q < 0 || (n_q > 0 && (!q_tensor || !q_from || !q_to || !t_out))) return FT_EINVAL;
+  std::vector<TensorDesc> td;
+  std::vector<int32_t> states;
+  int64_t dist_total;
+  int max_s;
+  int rc = plan_tensors(prof, n_tensors, ndims, dims, elem_bytes, td, states, dist_total, max_s);
+  if (rc != FT_OK) return rc;
+  if (n_q == 0) return FT_OK;
+  if (n_tensors == 0) return FT_EINVAL;
+  Pool& P = pool_for_device();
+  std::lock_guard<std::mutex> lk(P.mu);
+  return run_device(P, prof, td, states, dist_total, max_s, n_q, q_tensor, q_from, q_to, t_out,
+                    (cudaStream_t)stream);
+}
+
+extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors,
+                                   const int32_t* ndims, const int64_t* dims,
+                                   const int64_t* elem_bytes, int64_t n_q, const int32_t* q_tensor,
+                                   const int32_t* q_from, const int32_t* q_to, int64_t* t_out) {
+  if (n_q < 0 || (n_q > 0 && (!q_tensor || !q_from || !q_to || !t_out))) return FT_EINVAL;
+  std::vector<TensorDesc> td;
+  std::vector<int32_t> states;
+  int64_t dist_total;
+  int max_s;
+  int rc = plan_tensors(prof, n_tensors, ndims, dims, elem_bytes, td, states, dist_total, max_s);
+  if (rc != FT_OK) return rc;
+  if (n_q == 0) return FT_OK;
+  if (n_tensors == 0) return FT_EINVAL;
+  Pool& P = pool_for_device();
+  std::lock_guard<std::mutex> lk(P.mu);
+  void *dq, *dout;
+  CG_CHECK(P.get(5, (size_t)n_q * 12, &dq));
+  CG_CHECK(P.get(6, (size_t)n_q * 8, &dout));
+  int32_t* dqt = (int32_t*)dq;
+  cudaStream_t st = cudaStreamPerThread;
+  CG_CHECK(cudaMemcpyAsync(dqt, q_tensor, n_q * 4, cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(dqt + n_q, q_from, n_q * 4, cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(dqt + 2 * n_q, q_to, n_q * 4, cudaMemcpyHostToDevice, st));
+  rc = run_device(P, prof, td, states, dist_total, max_s, n_q, dqt, dqt + n_q, dqt + 2 * n_q,
+                  (int64_t*)dout, st);
+  if (rc != FT_OK) return rc;
+  CG_CHECK(cudaMemcpyAsync(t_out, dout, n_q * 8, cudaMemcpyDeviceToHost, st));
+  CG_CHECK(cudaStreamSynchronize(st));
   return FT_OK;
 }

@@ -146,3 +146,26 @@ def test_generated_edge_costs_drive_ft(ft):
     g, m, t = ft.run_ft(w2)
     og, om, ot = oracle.run_ft(w2, threads=4)
     assert np.array_equal(m, om) and np.array_equal(t, ot)
+
+
+def test_reschedule_dev_pointers(ft):
+    """ft_reschedule_costs_dev: device queries/output on a torch stream."""
+    import torch
+    prof = comm.profile(6, L=4, P=40)
+    nd, dims, eb, ns = _tensor_set(6, 100, 4)
+    qt, qf, qo = comm.queries(6, ns, 123_457)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(a).to(dev) for a in (qt, qf, qo)]
+    out = torch.full((qt.size,), -1, dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    ft.reschedule_costs_dev(prof, nd, dims, eb, qt.size, d[0].data_ptr(), d[1].data_ptr(),
+                            d[2].data_ptr(), out.data_ptr(), s.cuda_stream)
+    want = oracle.reschedule_costs(prof, nd, dims, eb, qt, qf, qo)
+    assert np.array_equal(out.cpu().numpy(), want)
+    bad = d[1].clone()
+    bad[777] = 10_000                                   # out-of-range state, caught on device
+    with pytest.raises(ft.FTError) as e:
+        ft.reschedule_costs_dev(prof, nd, dims, eb, qt.size, d[0].data_ptr(), bad.data_ptr(),
+                                d[2].data_ptr(), out.data_ptr(), s.cuda_stream)
+    assert e.value.code == ft.EINVAL

@@ -209,28 +209,47 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
   for (int e = threadIdx.x; e < S * S; e += blockDim.x) out[e] = d[e];
 }
 
+__device__ __forceinline__ int64_t cg_one(const TensorDesc* __restrict__ tens, int32_t n_tensors,
+                                          const int64_t* __restrict__ dist, int x, int64_t f,
+                                          int64_t t, int32_t* bad) {
+  if ((unsigned)x >= (unsigned)n_tensors) {  // invalid query: flag, write 0
+    *bad = 1;
+    return 0;
+  }
+  const int64_t S = __ldg(&tens[x].n_states), off = __ldg(&tens[x].dist_off);
+  if ((uint64_t)f >= (uint64_t)S || (uint64_t)t >= (uint64_t)S) {
+    *bad = 1;
+    return 0;
+  }
+  return __ldg(dist + off + f * S + t) + __ldg(dist + off + t * S + f);
+}
+
+// Four queries per thread per iteration with 16-byte loads/stores when the
+// arrays are 16-byte aligned (independent loads in flight), scalar tail.
 __global__ void k_cg_gather(const TensorDesc* __restrict__ tens, int32_t n_tensors,
                             const int64_t* __restrict__ dist, int64_t n,
                             const int32_t* __restrict__ qt, const int32_t* __restrict__ qf,
                             const int32_t* __restrict__ qo, int64_t* __restrict__ out,
                             int32_t* __restrict__ bad) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int x = __ldcs(qt + q);
-    const int64_t f = __ldcs(qf + q), t = __ldcs(qo + q);
-    if ((unsigned)x >= (unsigned)n_tensors) {  // invalid query: flag, write 0
-      *bad = 1;
-      __stcs(out + q, (int64_t)0);
-      continue;
-    }
-    const int64_t S = tens[x].n_states, off = tens[x].dist_off;
-    if ((uint64_t)f >= (uint64_t)S || (uint64_t)t >= (uint64_t)S) {
-      *bad = 1;
-      __stcs(out + q, (int64_t)0);
-      continue;
-    }
-    __stcs(out + q, __ldg(dist + off + f * S + t) + __ldg(dist + off + t * S + f));
+  const bool vec = ((reinterpret_cast<uintptr_t>(qt) | reinterpret_cast<uintptr_t>(qf) |
+                     reinterpret_cast<uintptr_t>(qo) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = tid; v < n4; v += stride) {
+    const int4 x = reinterpret_cast<const int4*>(qt)[v];
+    const int4 f = reinterpret_cast<const int4*>(qf)[v];
+    const int4 t = reinterpret_cast<const int4*>(qo)[v];
+    longlong2 o0, o1;
+    o0.x = cg_one(tens, n_tensors, dist, x.x, f.x, t.x, bad);
+    o0.y = cg_one(tens, n_tensors, dist, x.y, f.y, t.y, bad);
+    o1.x = cg_one(tens, n_tensors, dist, x.z, f.z, t.z, bad);
+    o1.y = cg_one(tens, n_tensors, dist, x.w, f.w, t.w, bad);
+    reinterpret_cast<longlong2*>(out)[2 * v] = o0;
+    reinterpret_cast<longlong2*>(out)[2 * v + 1] = o1;
   }
+  for (int64_t q = n4 * 4 + tid; q < n; q += stride)
+    out[q] = cg_one(tens, n_tensors, dist, qt[q], qf[q], qo[q], bad);
 }
 
 bool profile_valid(const ft_comm_profile* p) {
@@ -439,7 +458,7 @@ int run_device(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDes
                                                        (const TensorDesc*)dtd, (const int32_t*)dst,
                                                        (int64_t*)dd);
   CG_CHECK(cudaGetLastError());
-  k_cg_gather<<<grid_for(n_q), 256, 0, st>>>((const TensorDesc*)dtd, (int32_t)td.size(),
+  k_cg_gather<<<grid_for((n_q + 3) / 4), 256, 0, st>>>((const TensorDesc*)dtd, (int32_t)td.size(),
                                              (const int64_t*)dd, n_q, qt, qf, qo, out,
                                              (int32_t*)dbad);
   CG_CHECK(cudaGetLastError());

@@ -408,6 +408,7 @@ int plan_tensors(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* 
   states.clear();
   dist_total = 0;
   max_s = 0;
+  std::vector<int64_t> memo(1 << 15, -1);
   for (int x = 0; x < n_tensors; ++x) {
     TensorDesc& t = td[x];
     t.ndims = ndims[x];
@@ -421,13 +422,24 @@ int plan_tensors(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* 
       t.dims[j] = dj;
     }
     t.total = total;
-    const std::vector<int32_t> st = enum_states(t.ndims, t.dims, prof->mesh_log2);
-    if ((int64_t)st.size() > FT_CG_MAX_STATES) return FT_ESIZE;
-    t.state_off = (int32_t)states.size();
-    t.n_states = (int32_t)st.size();
+    // The state set depends only on (ndims, min(L, 2-adic valuation of each
+    // dim)): tensors with the same signature share one run of state rows.
+    int key = t.ndims;
+    for (int j = 0; j < t.ndims; ++j) {
+      int v = 0;
+      while (v < prof->mesh_log2 && t.dims[j] % (int64_t(1) << (v + 1)) == 0) ++v;
+      key |= v << (3 + 3 * j);
+    }
+    if (memo[key] < 0) {
+      const std::vector<int32_t> st = enum_states(t.ndims, t.dims, prof->mesh_log2);
+      if ((int64_t)st.size() > FT_CG_MAX_STATES) return FT_ESIZE;
+      memo[key] = (int64_t)states.size() | ((int64_t)st.size() << 32);
+      states.insert(states.end(), st.begin(), st.end());
+    }
+    t.state_off = (int32_t)(memo[key] & 0xffffffff);
+    t.n_states = (int32_t)(memo[key] >> 32);
     t.dist_off = dist_total;
-    dist_total += (int64_t)st.size() * st.size();
-    states.insert(states.end(), st.begin(), st.end());
+    dist_total += (int64_t)t.n_states * t.n_states;
     if (t.n_states > max_s) max_s = t.n_states;
   }
   return FT_OK;

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int64_t kInf = INT64_MAX / 4;
 constexpr int kApspThreads = 256;
+constexpr int kRegWarps = 8;  // warps of the register-resident FW (S <= 64)
 constexpr int kMaxCode = 7 * 7 * 7 * 7;  // (L+1)^D state codes, L <= 6, D <= 4
 
 struct TensorDesc {
@@ -65,7 +66,7 @@ __global__ void k_cg_comm_time(const ft_comm_profile* __restrict__ prof, int64_t
 // One CTA per tensor.  States are packed one byte per dim (a_j <= 6) into
 // int32 codes; the lookup table maps the mixed-radix code sum a_j (L+1)^j to
 // the state index (-1 = invalid split).
-__global__ void __launch_bounds__(kApspThreads)
+__global__ void __launch_bounds__(kApspThreads, 3)
 k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict__ tens,
           const int32_t* __restrict__ states, int64_t* __restrict__ dist) {
   extern __shared__ int64_t smem[];
@@ -136,28 +137,29 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  if (S <= 64 && nwarp == 4) {
-    // Register-resident Floyd-Warshall (S <= 64, 4 warps): thread (warp w,
-    // lane l) owns d[w + 4r][l + 32c], r < 16, c < 2.  Round k publishes
+  if (S <= 64 && nwarp == kRegWarps) {
+    // Register-resident Floyd-Warshall (S <= 64): thread (warp w, lane l)
+    // owns d[w + kRegWarps*r][l + 32c], r < kRows, c < 2.  Round k publishes
     // row k (its owner warp) and column k (lane k%32 of every warp) to
     // double-buffered shared rows, one barrier per round; every thread then
-    // does 32 min-plus updates from 2 + 16 shared loads.
+    // does 2*kRows min-plus updates from 2 + kRows shared loads.
+    constexpr int kRows = 64 / kRegWarps;
     __syncthreads();
-    int64_t v[16][2];
+    int64_t v[kRows][2];
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < kRows; ++r)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int i = warp + 4 * r, j = lane + 32 * c;
+        const int i = warp + kRegWarps * r, j = lane + 32 * c;
         v[r][c] = (i < S && j < S) ? d[i * S + j] : kInf;
       }
     __shared__ int64_t rowbuf[2][64], colbuf[2][64];
     for (int k = 0; k < S; ++k) {
       const int b = k & 1;
-      if ((k & 3) == warp) {
-        const int r = k >> 2;
+      if ((k % kRegWarps) == warp) {
+        const int r = k / kRegWarps;
 #pragma unroll
-        for (int rr = 0; rr < 16; ++rr)
+        for (int rr = 0; rr < kRows; ++rr)
           if (rr == r) {
             rowbuf[b][lane] = v[rr][0];
             rowbuf[b][lane + 32] = v[rr][1];
@@ -166,23 +168,23 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
       if ((k & 31) == lane) {
         const int c = k >> 5;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) colbuf[b][warp + 4 * r] = c ? v[r][1] : v[r][0];
+        for (int r = 0; r < kRows; ++r) colbuf[b][warp + kRegWarps * r] = c ? v[r][1] : v[r][0];
       }
       __syncthreads();
       const int64_t rk0 = rowbuf[b][lane], rk1 = rowbuf[b][lane + 32];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int64_t dik = colbuf[b][warp + 4 * r];
+      for (int r = 0; r < kRows; ++r) {
+        const int64_t dik = colbuf[b][warp + kRegWarps * r];
         v[r][0] = min(v[r][0], dik + rk0);
         v[r][1] = min(v[r][1], dik + rk1);
       }
     }
     int64_t* out = dist + td.dist_off;
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < kRows; ++r)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int i = warp + 4 * r, j = lane + 32 * c;
+        const int i = warp + kRegWarps * r, j = lane + 32 * c;
         if (i < S && j < S) out[i * S + j] = v[r][c];
       }
     return;
@@ -464,8 +466,7 @@ int run_device(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDes
   const size_t smem = (size_t)max_s * max_s * sizeof(int64_t);
   CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  // Small state graphs: 4 warps per tensor so more tensors are resident per SM.
-  const int threads = max_s <= 64 ? 128 : kApspThreads;
+  const int threads = max_s <= 64 ? kRegWarps * 32 : kApspThreads;
   k_cg_apsp<<<(int)td.size(), threads, smem, st>>>((const ft_comm_profile*)dp,
                                                        (const TensorDesc*)dtd, (const int32_t*)dst,
                                                        (int64_t*)dd);

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/ft.h"
@@ -447,39 +448,102 @@ int plan_tensors(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* 
   return FT_OK;
 }
 
-// APSP + gather on `stream` with device query/output pointers; pool slots
-// 0..4 hold the profile, descriptors, states, distances and the error flag.
-int run_device(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDesc>& td,
-               const std::vector<int32_t>& states, int64_t dist_total, int max_s, int64_t n_q,
-               const int32_t* qt, const int32_t* qf, const int32_t* qo, int64_t* out,
-               cudaStream_t st) {
+// Device state of one call (pool slots 0..4: profile, descriptors, states,
+// distances, error flag).
+struct Launch {
   void *dp, *dtd, *dst, *dd, *dbad;
-  CG_CHECK(P.get(0, sizeof(*prof), &dp));
-  CG_CHECK(P.get(1, td.size() * sizeof(TensorDesc), &dtd));
-  CG_CHECK(P.get(2, states.size() * 4, &dst));
-  CG_CHECK(P.get(3, (size_t)dist_total * 8, &dd));
-  CG_CHECK(P.get(4, 4, &dbad));
-  CG_CHECK(cudaMemcpyAsync(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice, st));
-  CG_CHECK(cudaMemcpyAsync(dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice, st));
-  CG_CHECK(cudaMemcpyAsync(dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice, st));
-  CG_CHECK(cudaMemsetAsync(dbad, 0, 4, st));
+  int32_t n_tensors;
+};
+
+// Upload the plan and launch the APSP on `st`.
+int launch_apsp(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDesc>& td,
+                const std::vector<int32_t>& states, int64_t dist_total, int max_s, cudaStream_t st,
+                Launch& L) {
+  CG_CHECK(P.get(0, sizeof(*prof), &L.dp));
+  CG_CHECK(P.get(1, td.size() * sizeof(TensorDesc), &L.dtd));
+  CG_CHECK(P.get(2, states.size() * 4, &L.dst));
+  CG_CHECK(P.get(3, (size_t)dist_total * 8, &L.dd));
+  CG_CHECK(P.get(4, 4, &L.dbad));
+  L.n_tensors = (int32_t)td.size();
+  CG_CHECK(cudaMemcpyAsync(L.dp, prof, sizeof(*prof), cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(L.dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemcpyAsync(L.dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice, st));
+  CG_CHECK(cudaMemsetAsync(L.dbad, 0, 4, st));
   const size_t smem = (size_t)max_s * max_s * sizeof(int64_t);
   CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const int threads = max_s <= 64 ? kRegWarps * 32 : kApspThreads;
-  k_cg_apsp<<<(int)td.size(), threads, smem, st>>>((const ft_comm_profile*)dp,
-                                                       (const TensorDesc*)dtd, (const int32_t*)dst,
-                                                       (int64_t*)dd);
+  k_cg_apsp<<<(int)td.size(), threads, smem, st>>>((const ft_comm_profile*)L.dp,
+                                                   (const TensorDesc*)L.dtd,
+                                                   (const int32_t*)L.dst, (int64_t*)L.dd);
   CG_CHECK(cudaGetLastError());
-  k_cg_gather<<<grid_for((n_q + 3) / 4), 256, 0, st>>>((const TensorDesc*)dtd, (int32_t)td.size(),
-                                             (const int64_t*)dd, n_q, qt, qf, qo, out,
-                                             (int32_t*)dbad);
+  return FT_OK;
+}
+
+int launch_gather(const Launch& L, int64_t n, const int32_t* qt, const int32_t* qf,
+                  const int32_t* qo, int64_t* out, cudaStream_t st) {
+  k_cg_gather<<<grid_for((n + 3) / 4), 256, 0, st>>>((const TensorDesc*)L.dtd, L.n_tensors,
+                                                     (const int64_t*)L.dd, n, qt, qf, qo, out,
+                                                     (int32_t*)L.dbad);
   CG_CHECK(cudaGetLastError());
+  return FT_OK;
+}
+
+int finish(const Launch& L, cudaStream_t st) {
   int32_t bad = 0;
-  CG_CHECK(cudaMemcpyAsync(&bad, dbad, 4, cudaMemcpyDeviceToHost, st));
+  CG_CHECK(cudaMemcpyAsync(&bad, L.dbad, 4, cudaMemcpyDeviceToHost, st));
   CG_CHECK(cudaStreamSynchronize(st));
   return bad ? FT_EINVAL : FT_OK;
 }
+
+// Host copy split over up to 8 threads (pageable <-> pinned staging is bound
+// by one core's memcpy bandwidth otherwise).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const size_t parts = bytes < (size_t(1) << 21) ? 1 : hw;
+  if (parts == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + parts - 1) / parts;
+  for (size_t k = 1; k < parts; ++k) {
+    const size_t lo = k * per, n = lo < bytes ? std::min(per, bytes - lo) : 0;
+    if (n) th.emplace_back([=] { std::memcpy((char*)dst + lo, (const char*)src + lo, n); });
+  }
+  std::memcpy(dst, src, std::min(per, bytes));
+  for (auto& t : th) t.join();
+}
+
+// Pinned host staging for the host-buffer entry: two slots of kChunk queries
+// (inputs 12 B, output 8 B per query), grow-once, one set per process.
+constexpr int64_t kChunk = int64_t(1) << 20;
+struct Staging {
+  int32_t* in[2] = {nullptr, nullptr};
+  int64_t* out[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int dev = -1;
+  cudaError_t init(int device) {
+    if (dev == device) return cudaSuccess;
+    for (int b = 0; b < 2; ++b) {
+      if (in[b]) cudaFreeHost(in[b]);
+      if (out[b]) cudaFreeHost(out[b]);
+      if (ev[b]) cudaEventDestroy(ev[b]);
+      in[b] = nullptr;
+      out[b] = nullptr;
+      ev[b] = nullptr;
+    }
+    dev = -1;
+    for (int b = 0; b < 2; ++b) {
+      cudaError_t e = cudaMallocHost(&in[b], kChunk * 12);
+      if (e == cudaSuccess) e = cudaMallocHost(&out[b], kChunk * 8);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    dev = device;
+    return cudaSuccess;
+  }
+};
 
 }  // namespace
 
@@ -499,8 +563,13 @@ extern "C" int ft_reschedule_costs_dev(const ft_comm_profile* prof, int32_t n_te
   if (n_tensors == 0) return FT_EINVAL;
   Pool& P = pool_for_device();
   std::lock_guard<std::mutex> lk(P.mu);
-  return run_device(P, prof, td, states, dist_total, max_s, n_q, q_tensor, q_from, q_to, t_out,
-                    (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  Launch L;
+  rc = launch_apsp(P, prof, td, states, dist_total, max_s, st, L);
+  if (rc != FT_OK) return rc;
+  rc = launch_gather(L, n_q, q_tensor, q_from, q_to, t_out, st);
+  if (rc != FT_OK) return rc;
+  return finish(L, st);
 }
 
 extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors,
@@ -518,18 +587,49 @@ extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensor
   if (n_tensors == 0) return FT_EINVAL;
   Pool& P = pool_for_device();
   std::lock_guard<std::mutex> lk(P.mu);
+  int dev = 0;
+  CG_CHECK(cudaGetDevice(&dev));
+  static Staging stage_by_dev[64];
+  Staging& SG = stage_by_dev[dev & 63];
+  CG_CHECK(SG.init(dev));
   void *dq, *dout;
   CG_CHECK(P.get(5, (size_t)n_q * 12, &dq));
   CG_CHECK(P.get(6, (size_t)n_q * 8, &dout));
   int32_t* dqt = (int32_t*)dq;
+  int64_t* dO = (int64_t*)dout;
   cudaStream_t st = cudaStreamPerThread;
-  CG_CHECK(cudaMemcpyAsync(dqt, q_tensor, n_q * 4, cudaMemcpyHostToDevice, st));
-  CG_CHECK(cudaMemcpyAsync(dqt + n_q, q_from, n_q * 4, cudaMemcpyHostToDevice, st));
-  CG_CHECK(cudaMemcpyAsync(dqt + 2 * n_q, q_to, n_q * 4, cudaMemcpyHostToDevice, st));
-  rc = run_device(P, prof, td, states, dist_total, max_s, n_q, dqt, dqt + n_q, dqt + 2 * n_q,
-                  (int64_t*)dout, st);
+  Launch L;
+  // The APSP needs only the plan: it runs while the queries stream in.
+  rc = launch_apsp(P, prof, td, states, dist_total, max_s, st, L);
   if (rc != FT_OK) return rc;
-  CG_CHECK(cudaMemcpyAsync(t_out, dout, n_q * 8, cudaMemcpyDeviceToHost, st));
-  CG_CHECK(cudaStreamSynchronize(st));
+  // Chunk pipeline through pinned staging: host copies of chunk i overlap
+  // the DMA / gather of chunk i-1; results drain two chunks behind.
+  const int64_t nch = (n_q + kChunk - 1) / kChunk;
+  auto drain = [&](int64_t i) -> int {
+    const int b = (int)(i & 1);
+    const int64_t lo = i * kChunk, n = std::min(kChunk, n_q - lo);
+    CG_CHECK(cudaEventSynchronize(SG.ev[b]));
+    par_memcpy(t_out + lo, SG.out[b], n * 8);
+    return FT_OK;
+  };
+  for (int64_t i = 0; i < nch; ++i) {
+    const int b = (int)(i & 1);
+    if (i >= 2 && (rc = drain(i - 2)) != FT_OK) return rc;
+    const int64_t lo = i * kChunk, n = std::min(kChunk, n_q - lo);
+    int32_t* in = SG.in[b];
+    par_memcpy(in, q_tensor + lo, n * 4);
+    par_memcpy(in + n, q_from + lo, n * 4);
+    par_memcpy(in + 2 * n, q_to + lo, n * 4);
+    int32_t* d = dqt + 3 * lo;
+    CG_CHECK(cudaMemcpyAsync(d, in, n * 12, cudaMemcpyHostToDevice, st));
+    rc = launch_gather(L, n, d, d + n, d + 2 * n, dO + lo, st);
+    if (rc != FT_OK) return rc;
+    CG_CHECK(cudaMemcpyAsync(SG.out[b], dO + lo, n * 8, cudaMemcpyDeviceToHost, st));
+    CG_CHECK(cudaEventRecord(SG.ev[b], st));
+  }
+  for (int64_t i = std::max<int64_t>(0, nch - 2); i < nch; ++i)
+    if ((rc = drain(i)) != FT_OK) return rc;
+  rc = finish(L, st);
+  if (rc != FT_OK) return rc;
   return FT_OK;
 }

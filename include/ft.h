@@ -278,7 +278,9 @@ int ft_split_states(int32_t ndims, const int64_t* dims, int32_t mesh_log2, int64
  * (tensor bytes > 2^P), FT_ESIZE (a tensor with > FT_CG_MAX_STATES states),
  * FT_ECUDA.  Query indices are validated on the device (FT_EINVAL after
  * the kernels; t_out is then unspecified).  Device buffers are pooled per
- * device across calls (grow-only; calls on one device serialise). */
+ * device across calls (grow-only; calls on one device serialise).  Queries
+ * and results stream in chunks of 2^20 through library-owned pinned staging
+ * (2 x 20 MB per device), copied by up to 8 host threads. */
 int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
                         const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
                         const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,

@@ -73,6 +73,8 @@ def lib():
         L.ocg_comm_time.argtypes = [C.c_void_p, C.c_int64, P64, P32, P64]
         L.ocg_split_states.argtypes = [C.c_int32, P64, C.c_int32, C.c_int64, P32, P64]
         L.ocg_state_dist.argtypes = [C.c_void_p, C.c_int32, P64, C.c_int64, C.c_int64, P64, P64]
+        L.ocg_sync_costs.argtypes = [C.c_void_p, C.c_int32, P32, P64, P64, C.c_int64, P32, P32,
+                                     P64, P64]
         L.ocg_reschedule_costs.argtypes = [C.c_void_p, C.c_int32, P32, P64, P64, C.c_int64,
                                            P32, P32, P32, P64]
         _lib = L
@@ -324,3 +326,18 @@ def reschedule_costs(prof, ndims, dims, elem_bytes, q_tensor, q_from, q_to) -> n
                                       _p(qf, C.c_int32), _p(qo, C.c_int32), _p(out, C.c_int64)),
            "reschedule_costs")
     return out
+
+
+def sync_costs(prof, ndims, dims, elem_bytes, q_tensor, q_state):
+    """(m_p, t_s) of a parameter tensor in a split state (Eq. 1 + P:668-671, R20)."""
+    nd = np.ascontiguousarray(ndims, np.int32)
+    dm = np.ascontiguousarray(dims, np.int64)
+    eb = np.ascontiguousarray(elem_bytes, np.int64)
+    qt, qs = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_state))
+    m = np.zeros(qt.size, np.int64)
+    t = np.zeros(qt.size, np.int64)
+    p = _profile(prof)
+    _check(lib().ocg_sync_costs(C.byref(p), nd.size, _p(nd, C.c_int32), _p(dm, C.c_int64),
+                                _p(eb, C.c_int64), qt.size, _p(qt, C.c_int32), _p(qs, C.c_int32),
+                                _p(m, C.c_int64), _p(t, C.c_int64)), "sync_costs")
+    return m, t

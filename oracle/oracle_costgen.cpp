@@ -208,3 +208,42 @@ int ocg_reschedule_costs(const void* prof, int32_t n_tensors, const int32_t* ndi
 }
 
 }  // extern "C"
+
+// Gradient synchronisation cost of a parameter tensor (Eq. 1's m_p and t_s,
+// P:399-406 with the comm model of P:668-671; reading R20): in split state a
+// each device stores shard = total / 2^(sum a) bytes (m_p) and all-reduces
+// its gradient with the r = 2^(L - sum a) devices holding the same shard; a
+// ring all-reduce moves 2 * (shard - shard / r) bytes per device, timed by
+// comm_time over a group of r devices.  r = 1: t_s = 0.
+extern "C" int ocg_sync_costs(const void* prof, int32_t n_tensors, const int32_t* ndims,
+                              const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
+                              const int32_t* q_tensor, const int32_t* q_state, int64_t* m_out,
+                              int64_t* t_out) {
+  const Profile* p = (const Profile*)prof;
+  if (!profile_ok(p)) return -1;
+  for (int64_t q = 0; q < n_q; q++) {
+    int x = q_tensor[q];
+    if (x < 0 || x >= n_tensors) return -1;
+    int D = ndims[x];
+    const int64_t* dm = dims + (int64_t)x * MAXD;
+    if (D < 1 || D > MAXD || elem_bytes[x] < 1) return -1;
+    int64_t total = elem_bytes[x];
+    for (int j = 0; j < D; j++) {
+      if (dm[j] < 1) return -1;
+      if (total > ((int64_t(1) << p->P) / dm[j])) return -6;
+      total *= dm[j];
+    }
+    if (total > (int64_t(1) << (p->P - 1))) return -6;  // 2 * total must fit the profile
+    std::vector<std::vector<int>> S;
+    std::vector<int> cur(D, 0);
+    enum_states(D, dm, p->L, 0, 0, cur, S);
+    if (q_state[q] < 0 || q_state[q] >= (int)S.size()) return -1;
+    int used = 0;
+    for (int j = 0; j < D; j++) used += S[q_state[q]][j];
+    int64_t shard = total >> used;
+    int u = p->L - used;
+    m_out[q] = shard;
+    t_out[q] = comm_time(p, 2 * (shard - (shard >> u)), u);
+  }
+  return 0;
+}

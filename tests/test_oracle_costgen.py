@@ -209,3 +209,25 @@ def test_reschedule_costs_queries():
     assert np.all(t[qf == qo] == 0)
     with pytest.raises(oracle.OracleError):
         oracle.reschedule_costs(p, nd, dims, eb, qt[:1], np.array([999], np.int32), qo[:1])
+
+
+def test_sync_costs_pins():
+    # R20 (Eq. 1 m_p / t_s with P:668-671): SPEC S:231-233 examples -- fully
+    # replicated on n devices: m_p = full parameter bytes; no sync partners
+    # (fully split): t_s = 0 -- and the ring all-reduce volume by hand.
+    p = flat_profile(L=2, P=20, bw=10 ** 9, lat=5)
+    nd = np.array([1, 2], np.int32)
+    dims = np.array([[1024, 1, 1, 1], [32, 64, 1, 1]], np.int64)
+    eb = np.array([4, 2], np.int64)
+    S0 = [tuple(r) for r in oracle.split_states([1024], 2)]     # (0), (1), (2)
+    m, t = oracle.sync_costs(p, nd, dims, eb, [0, 0, 0], [S0.index((0,)), S0.index((1,)),
+                                                         S0.index((2,))])
+    assert m.tolist() == [4096, 2048, 1024]
+    # replicated over 4: 2*(4096 - 1024) = 6144 B at 1e9 B/s -> 6144 ns + 5
+    # split 2, replicated over 2: 2*(2048 - 1024) = 2048 B -> 2048 ns + 5
+    assert t.tolist() == [6149, 2053, 0]
+    S1 = [tuple(r) for r in oracle.split_states([32, 64], 2)]
+    m, t = oracle.sync_costs(p, nd, dims, eb, [1, 1], [S1.index((1, 1)), S1.index((0, 0))])
+    assert m.tolist() == [1024, 4096] and t[0] == 0 and t[1] == 6149
+    with pytest.raises(oracle.OracleError):          # 2 * total > 2^P
+        oracle.sync_costs(flat_profile(L=2, P=12, bw=10 ** 9), nd, dims, eb, [0], [0])

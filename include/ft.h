@@ -286,6 +286,21 @@ int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors, const in
                         const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,
                         int64_t* t_out);
 
+/* Gradient-synchronisation operator costs (Eq. 1: m_p and t_s;
+ * comm model P:668-671; reading R20): for n_q queries (parameter tensor
+ * q_tensor[q] described as in ft_reschedule_costs, split state q_state[q]
+ * of ft_split_states) each device stores shard = total / 2^(sum a) bytes,
+ * m_out[q] = shard, and all-reduces the gradient over the r = 2^(L - sum a)
+ * devices holding the same shard: t_out[q] = ft_comm_time of
+ * 2*(shard - shard/r) bytes (ring all-reduce volume) over a group of r
+ * (0 when r = 1).  Host arrays; runs on the current device.
+ * Errors: FT_EINVAL (bad tensor / state / profile), FT_EOVERFLOW
+ * (2 * tensor bytes > 2^P), FT_ESIZE (> FT_CG_MAX_STATES states), FT_ECUDA. */
+int ft_sync_costs(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
+                  const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
+                  const int32_t* q_tensor, const int32_t* q_state, int64_t* m_out,
+                  int64_t* t_out);
+
 /* Same as ft_reschedule_costs, but q_tensor / q_from / q_to / t_out are
  * DEVICE pointers (caller-owned, on the current device) and the kernels run
  * on `stream` (cudaStream_t; NULL = legacy default stream).  The tensor

@@ -96,6 +96,8 @@ def _load():
     L.ft_split_states.argtypes = [C.c_int32, P64, C.c_int32, C.c_int64, P32, P64]
     L.ft_reschedule_costs.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64,
                                       C.c_int64, P32, P32, P32, P64]
+    L.ft_sync_costs.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64, C.c_int64,
+                                P32, P32, P64, P64]
     L.ft_reschedule_costs_dev.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64,
                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]
@@ -107,7 +109,7 @@ SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edg
            "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version",
-           "ft_comm_time", "ft_split_states", "ft_reschedule_costs", "ft_reschedule_costs_dev"]
+           "ft_comm_time", "ft_split_states", "ft_reschedule_costs", "ft_reschedule_costs_dev", "ft_sync_costs"]
 
 
 def _p(a, t):
@@ -380,3 +382,18 @@ def reschedule_costs_dev(prof, ndims, dims, elem_bytes, n_q: int, q_tensor: int,
                                           C.c_void_p(q_tensor), C.c_void_p(q_from),
                                           C.c_void_p(q_to), C.c_void_p(t_out),
                                           C.c_void_p(stream)), "ft_reschedule_costs_dev")
+
+
+def sync_costs(prof, ndims, dims, elem_bytes, q_tensor, q_state):
+    """ft_sync_costs: (m_p, t_s) of a parameter tensor per split state (Eq. 1, R20)."""
+    nd = np.ascontiguousarray(ndims, np.int32)
+    dm = np.ascontiguousarray(dims, np.int64).reshape(nd.size, CG_MAX_DIMS)
+    eb = np.ascontiguousarray(elem_bytes, np.int64)
+    qt, qs = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_state))
+    m = np.zeros(qt.size, np.int64)
+    t = np.zeros(qt.size, np.int64)
+    p = prof if isinstance(prof, ft_comm_profile) else comm_profile(prof)
+    _cg_check(lib.ft_sync_costs(C.byref(p), nd.size, _p(nd, C.c_int32), _p(dm, C.c_int64),
+                                _p(eb, C.c_int64), qt.size, _p(qt, C.c_int32), _p(qs, C.c_int32),
+                                _p(m, C.c_int64), _p(t, C.c_int64)), "ft_sync_costs")
+    return m, t

@@ -255,6 +255,36 @@ __global__ void k_cg_gather(const TensorDesc* __restrict__ tens, int32_t n_tenso
     out[q] = cg_one(tens, n_tensors, dist, qt[q], qf[q], qo[q], bad);
 }
 
+// Gradient-sync op costs (R20): m_p = shard, t_s = comm time of the ring
+// all-reduce volume 2*(shard - shard/r) over r = 2^(L - sum a) replicas.
+__global__ void k_cg_sync(const ft_comm_profile* __restrict__ prof,
+                          const TensorDesc* __restrict__ tens, int32_t n_tensors,
+                          const int32_t* __restrict__ states, int64_t n,
+                          const int32_t* __restrict__ qt, const int32_t* __restrict__ qs,
+                          int64_t* __restrict__ m_out, int64_t* __restrict__ t_out,
+                          int32_t* __restrict__ bad) {
+  __shared__ ft_comm_profile p;
+  for (int i = threadIdx.x; i < (int)(sizeof(p) / 8); i += blockDim.x)
+    reinterpret_cast<int64_t*>(&p)[i] = reinterpret_cast<const int64_t*>(prof)[i];
+  __syncthreads();
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int x = qt[q], s = qs[q];
+    if ((unsigned)x >= (unsigned)n_tensors || (unsigned)s >= (unsigned)tens[x].n_states) {
+      *bad = 1;
+      m_out[q] = 0;
+      t_out[q] = 0;
+      continue;
+    }
+    const int32_t pk = states[tens[x].state_off + s];
+    const int used = (pk & 0xff) + ((pk >> 8) & 0xff) + ((pk >> 16) & 0xff) + ((pk >> 24) & 0xff);
+    const int64_t shard = tens[x].total >> used;
+    const int u = p.mesh_log2 - used;
+    m_out[q] = shard;
+    t_out[q] = cg_time_dev(p, 2 * (shard - (shard >> u)), u);
+  }
+}
+
 bool profile_valid(const ft_comm_profile* p) {
   if (!p || p->mesh_log2 < 1 || p->mesh_log2 > FT_CG_MAX_MESH || p->P < 1 || p->P > FT_CG_MAX_P)
     return false;
@@ -631,5 +661,49 @@ extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensor
     if ((rc = drain(i)) != FT_OK) return rc;
   rc = finish(L, st);
   if (rc != FT_OK) return rc;
+  return FT_OK;
+}
+
+extern "C" int ft_sync_costs(const ft_comm_profile* prof, int32_t n_tensors, const int32_t* ndims,
+                             const int64_t* dims, const int64_t* elem_bytes, int64_t n_q,
+                             const int32_t* q_tensor, const int32_t* q_state, int64_t* m_out,
+                             int64_t* t_out) {
+  if (n_q < 0 || (n_q > 0 && (!q_tensor || !q_state || !m_out || !t_out))) return FT_EINVAL;
+  std::vector<TensorDesc> td;
+  std::vector<int32_t> states;
+  int64_t dist_total;
+  int max_s;
+  int rc = plan_tensors(prof, n_tensors, ndims, dims, elem_bytes, td, states, dist_total, max_s);
+  if (rc != FT_OK) return rc;
+  for (const TensorDesc& t : td)
+    if (t.total > (int64_t(1) << (prof->P - 1))) return FT_EOVERFLOW;
+  if (n_q == 0) return FT_OK;
+  if (n_tensors == 0) return FT_EINVAL;
+  DevBufs B;
+  ft_comm_profile* dp;
+  TensorDesc* dtd;
+  int32_t *dst, *dq, *dbad;
+  int64_t *dm, *dt;
+  CG_CHECK(B.alloc(&dp, 1));
+  CG_CHECK(B.alloc(&dtd, td.size()));
+  CG_CHECK(B.alloc(&dst, states.size()));
+  CG_CHECK(B.alloc(&dq, 2 * n_q));
+  CG_CHECK(B.alloc(&dm, n_q));
+  CG_CHECK(B.alloc(&dt, n_q));
+  CG_CHECK(B.alloc(&dbad, 1));
+  CG_CHECK(cudaMemcpy(dp, prof, sizeof(*prof), cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dtd, td.data(), td.size() * sizeof(TensorDesc), cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dq, q_tensor, n_q * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemcpy(dq + n_q, q_state, n_q * 4, cudaMemcpyHostToDevice));
+  CG_CHECK(cudaMemset(dbad, 0, 4));
+  k_cg_sync<<<grid_for(n_q), 256>>>(dp, dtd, (int32_t)td.size(), dst, n_q, dq, dq + n_q, dm, dt,
+                                    dbad);
+  CG_CHECK(cudaGetLastError());
+  int32_t bad = 0;
+  CG_CHECK(cudaMemcpy(&bad, dbad, 4, cudaMemcpyDeviceToHost));
+  if (bad) return FT_EINVAL;
+  CG_CHECK(cudaMemcpy(m_out, dm, n_q * 8, cudaMemcpyDeviceToHost));
+  CG_CHECK(cudaMemcpy(t_out, dt, n_q * 8, cudaMemcpyDeviceToHost));
   return FT_OK;
 }

@@ -169,3 +169,17 @@ def test_reschedule_dev_pointers(ft):
         ft.reschedule_costs_dev(prof, nd, dims, eb, qt.size, d[0].data_ptr(), bad.data_ptr(),
                                 d[2].data_ptr(), out.data_ptr(), s.cuda_stream)
     assert e.value.code == ft.EINVAL
+
+
+@pytest.mark.parametrize("seed,L", [(0, 3), (1, 5), (2, 6)])
+def test_sync_costs_parity(ft, seed, L):
+    """ft_sync_costs (Eq. 1 m_p / t_s, R20) bit-exact vs the oracle."""
+    prof = comm.profile(seed, L=L, P=44)
+    nd, dims, eb, ns = _tensor_set(seed, 80, L, max_ndims=3)
+    qt, qs, _ = comm.queries(seed, ns, 60_000)
+    m, t = ft.sync_costs(prof, nd, dims, eb, qt, qs)
+    om, ot = oracle.sync_costs(prof, nd, dims, eb, qt, qs)
+    assert np.array_equal(m, om) and np.array_equal(t, ot)
+    with pytest.raises(ft.FTError) as e:
+        ft.sync_costs(prof, nd, dims, eb, qt[:1], np.array([10_000], np.int32))
+    assert e.value.code == ft.EINVAL

@@ -225,7 +225,8 @@ const char* ft_version(void);
  * tensor re-scheduling as a shortest path over tensor splits (R19).
  * Standalone: no graph handle; all arrays are HOST memory, copied in/out by
  * the call; the computation runs on the current CUDA device (FT_ECUDA
- * without one).  Thread-safe (no global state besides the device).
+ * without one).  Thread-safe: the per-device buffer pool and pinned staging
+ * (library-owned, kept for the process lifetime) are guarded by a mutex.
  * ------------------------------------------------------------------------- */
 #define FT_CG_MAX_MESH 6   /* mesh of up to 2^6 = 64 devices */
 #define FT_CG_MAX_P 46     /* profiled sizes 2^0 .. 2^P bytes, P <= 46 */

@@ -312,6 +312,13 @@ int ft_reschedule_costs_dev(const ft_comm_profile* prof, int32_t n_tensors, cons
                             const int32_t* q_tensor, const int32_t* q_from, const int32_t* q_to,
                             int64_t* t_out, void* stream);
 
+/* Measurement: ft_costgen_profile(1) makes every later ft_reschedule_costs_dev
+ * record CUDA events around its two kernels (on the call's stream);
+ * ft_costgen_last_times returns the last such call's APSP and gather kernel
+ * times in ms on the current device (0 before any profiled call). */
+int ft_costgen_profile(int32_t on);
+int ft_costgen_last_times(float* apsp_ms, float* gather_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,8 @@ def _load():
                                       C.c_int64, P32, P32, P32, P64]
     L.ft_sync_costs.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64, C.c_int64,
                                 P32, P32, P64, P64]
+    L.ft_costgen_profile.argtypes = [C.c_int32]
+    L.ft_costgen_last_times.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.ft_reschedule_costs_dev.argtypes = [C.POINTER(ft_comm_profile), C.c_int32, P32, P64, P64,
                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]
@@ -109,7 +111,8 @@ SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edg
            "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version",
-           "ft_comm_time", "ft_split_states", "ft_reschedule_costs", "ft_reschedule_costs_dev", "ft_sync_costs"]
+           "ft_comm_time", "ft_split_states", "ft_reschedule_costs", "ft_reschedule_costs_dev", "ft_sync_costs", "ft_costgen_profile",
+           "ft_costgen_last_times"]
 
 
 def _p(a, t):
@@ -397,3 +400,15 @@ def sync_costs(prof, ndims, dims, elem_bytes, q_tensor, q_state):
                                 _p(eb, C.c_int64), qt.size, _p(qt, C.c_int32), _p(qs, C.c_int32),
                                 _p(m, C.c_int64), _p(t, C.c_int64)), "ft_sync_costs")
     return m, t
+
+
+def costgen_profile(on: bool) -> None:
+    """ft_costgen_profile: CUDA-event timing of ft_reschedule_costs_dev's kernels."""
+    _cg_check(lib.ft_costgen_profile(1 if on else 0), "ft_costgen_profile")
+
+
+def costgen_last_times():
+    """ft_costgen_last_times -> (apsp_ms, gather_ms) of the last profiled device call."""
+    a, g = C.c_float(0), C.c_float(0)
+    _cg_check(lib.ft_costgen_last_times(C.byref(a), C.byref(g)), "ft_costgen_last_times")
+    return a.value, g.value

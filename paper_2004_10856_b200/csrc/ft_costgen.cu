@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -339,10 +340,14 @@ struct DevBufs {
 
 // Grow-only device buffers reused across calls (one pool per device; calls
 // on the same device serialise on its mutex).
+std::atomic<int> g_profile{0};  // ft_costgen_profile
+
 struct Pool {
   std::mutex mu;
   void* buf[8] = {};
   size_t cap[8] = {};
+  cudaEvent_t ev[4] = {};     // apsp begin/end, gather begin/end (profiling)
+  float last_ms[2] = {0, 0};  // last ft_reschedule_costs_dev: apsp, gather
   cudaError_t get(int slot, size_t bytes, void** out) {
     if (bytes > cap[slot]) {
       const size_t want = std::max(bytes, cap[slot] * 3 / 2);
@@ -594,12 +599,40 @@ extern "C" int ft_reschedule_costs_dev(const ft_comm_profile* prof, int32_t n_te
   Pool& P = pool_for_device();
   std::lock_guard<std::mutex> lk(P.mu);
   cudaStream_t st = (cudaStream_t)stream;
+  const bool prof_on = g_profile.load() != 0;
+  if (prof_on && !P.ev[0])
+    for (int i = 0; i < 4; ++i) CG_CHECK(cudaEventCreate(&P.ev[i]));
   Launch L;
+  if (prof_on) CG_CHECK(cudaEventRecord(P.ev[0], st));
   rc = launch_apsp(P, prof, td, states, dist_total, max_s, st, L);
   if (rc != FT_OK) return rc;
+  if (prof_on) {
+    CG_CHECK(cudaEventRecord(P.ev[1], st));
+    CG_CHECK(cudaEventRecord(P.ev[2], st));
+  }
   rc = launch_gather(L, n_q, q_tensor, q_from, q_to, t_out, st);
   if (rc != FT_OK) return rc;
-  return finish(L, st);
+  if (prof_on) CG_CHECK(cudaEventRecord(P.ev[3], st));
+  rc = finish(L, st);
+  if (rc == FT_OK && prof_on) {
+    CG_CHECK(cudaEventElapsedTime(&P.last_ms[0], P.ev[0], P.ev[1]));
+    CG_CHECK(cudaEventElapsedTime(&P.last_ms[1], P.ev[2], P.ev[3]));
+  }
+  return rc;
+}
+
+extern "C" int ft_costgen_profile(int32_t on) {
+  g_profile.store(on != 0);
+  return FT_OK;
+}
+
+extern "C" int ft_costgen_last_times(float* apsp_ms, float* gather_ms) {
+  if (!apsp_ms || !gather_ms) return FT_EINVAL;
+  Pool& P = pool_for_device();
+  std::lock_guard<std::mutex> lk(P.mu);
+  *apsp_ms = P.last_ms[0];
+  *gather_ms = P.last_ms[1];
+  return FT_OK;
 }
 
 extern "C" int ft_reschedule_costs(const ft_comm_profile* prof, int32_t n_tensors,

@@ -183,3 +183,23 @@ def test_sync_costs_parity(ft, seed, L):
     with pytest.raises(ft.FTError) as e:
         ft.sync_costs(prof, nd, dims, eb, qt[:1], np.array([10_000], np.int32))
     assert e.value.code == ft.EINVAL
+
+
+def test_costgen_profile_times(ft):
+    """ft_costgen_profile / ft_costgen_last_times report both kernels' times."""
+    import torch
+    prof = comm.profile(7, L=3, P=40)
+    nd, dims, eb, ns = _tensor_set(7, 30, 3)
+    qt, qf, qo = comm.queries(7, ns, 200_000)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(a).to(dev) for a in (qt, qf, qo)]
+    out = torch.empty(qt.size, dtype=torch.int64, device=dev)
+    ft.costgen_profile(True)
+    try:
+        ft.reschedule_costs_dev(prof, nd, dims, eb, qt.size, d[0].data_ptr(), d[1].data_ptr(),
+                                d[2].data_ptr(), out.data_ptr(), 0)
+        a, g = ft.costgen_last_times()
+    finally:
+        ft.costgen_profile(False)
+    assert a > 0 and g > 0
+    assert np.array_equal(out.cpu().numpy(), oracle.reschedule_costs(prof, nd, dims, eb, qt, qf, qo))

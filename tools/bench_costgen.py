@@ -47,7 +47,8 @@ def queries(w, ns, rng):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=300,
+                    help="timed calls (enough for nvidia-smi to sample clocks under load)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--L", type=int, default=5)
@@ -71,7 +72,11 @@ def main():
                                 d_qo.data_ptr(), d_out.data_ptr(), sp)
     for _ in range(args.warmup):
         dev_call()
-    dms = []
+    from bench import ClockSampler
+    ft.costgen_profile(True)
+    clk = ClockSampler(0)
+    clk.start()
+    dms, kern = [], []
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -80,7 +85,25 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         dms.append(e0.elapsed_time(e1))
+        kern.append(ft.costgen_last_times())
+    clocks = clk.stop()
+    ft.costgen_profile(False)
     dev_ms = float(np.median(dms))
+    apsp_ms = float(np.median([k[0] for k in kern]))
+    gather_ms = float(np.median([k[1] for k in kern]))
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    algo_bytes = 20 * qt.size
+    achieved = algo_bytes / (gather_ms * 1e-3) / 1e9
+    roof = {"kernel": "k_cg_gather", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": 165122816,
+            "traffic_source": "ncu --set full (r1_cg_gather6, CG5): dram__bytes_read 126.24 MB "
+                              "+ dram__bytes_write 38.88 MB per launch (profiles/r1_costgen.md)",
+            "bytes_per_unit": 20, "unit_desc": "queries (12 B indices read + 8 B t_x written)",
+            "units_per_step": int(qt.size), "kernel_ms_per_step": gather_ms,
+            "apsp_ms_per_step": apsp_ms, "share_of_step": gather_ms / dev_ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
     for _ in range(args.warmup):
         out = ft.reschedule_costs(prof, nd, dims, eb, qt, qf, qo)
     ts = []
@@ -92,15 +115,16 @@ def main():
     dev_ok = bool(torch.equal(d_out.cpu(), torch.from_numpy(out)))
     line = {"metric": "edge-cost queries/s (re-scheduling t_x, P:860)",
             "value": qt.size / (dev_ms / 1e3), "unit": "queries/s", "ms_per_step": dev_ms,
-            "ms_steps": [round(x, 4) for x in dms],
+            "ms_steps_first10": [round(x, 4) for x in dms[:10]],
             "timing": "CUDA events on the launching stream around ft_reschedule_costs_dev "
                       "(queries resident in HBM; APSP + gather + descriptor upload + sync)",
             "e2e": {"value": qt.size / (ms / 1e3), "unit": "queries/s", "ms_per_step": ms,
-                    "ms_steps": [round(1e3 * t, 3) for t in ts],
+                    "ms_steps_first10": [round(1e3 * t, 3) for t in ts[:10]],
                     "timing": "host wall clock around ft_reschedule_costs (HOST buffers: H2D + kernels + D2H)",
                     "h2d_bytes_per_step": int(qt.size * 12 + dims.nbytes + nd.nbytes + eb.nbytes),
                     "d2h_bytes_per_step": int(out.nbytes)},
-            "dev_equals_host_call": dev_ok,
+            "dev_equals_host_call": dev_ok, "roofline": roof, "clocks": clocks,
+            "gpu_launches": 2,
             "steps": args.steps, "warmup": args.warmup, "dtype": "int64", "data": "synthetic",
             "config": {"workload": "CG5: C5 edges x K^2 (2324 edges, K=64)", "tensors": int(len(nd)),
                        "queries": int(qt.size), "mesh_log2": L, "states_total": int(sum(ns)),

@@ -26,7 +26,8 @@ namespace {
 
 constexpr int64_t kInf = INT64_MAX / 4;
 constexpr int kApspThreads = 256;
-constexpr int kRegWarps = 8;  // warps of the register-resident FW (S <= 64)
+
+constexpr int kRegWarps = 8;  // warps of the register-resident FW
 constexpr int kMaxCode = 7 * 7 * 7 * 7;  // (L+1)^D state codes, L <= 6, D <= 4
 
 struct TensorDesc {
@@ -65,10 +66,72 @@ __global__ void k_cg_comm_time(const ft_comm_profile* __restrict__ prof, int64_t
     out[q] = cg_time_dev(p, bytes[q], grp[q]);
 }
 
+// Register-resident Floyd-Warshall for S <= 32*C (C = 2: S <= 64, C = 3:
+// S <= 96) with kRegWarps warps: thread (warp w, lane l) owns
+// d[w + kRegWarps*r][l + 32c], r < 32*C/kRegWarps, c < C.  Round k publishes
+// row k (its owner warp) and column k (lane k%32 of every warp) to
+// double-buffered shared rows, one barrier per round; every thread then does
+// rows*C min-plus updates from C + rows shared loads.  Writes the result.
+template <int C>
+__device__ __forceinline__ void fw_registers(const int64_t* __restrict__ d, int S,
+                                             int64_t* __restrict__ out, int warp, int lane) {
+  constexpr int kRows = 32 * C / kRegWarps;
+  __shared__ int64_t rowbuf[2][32 * C], colbuf[2][32 * C];
+  int64_t v[kRows][C];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int i = warp + kRegWarps * r, j = lane + 32 * c;
+      v[r][c] = (i < S && j < S) ? d[i * S + j] : kInf;
+    }
+  for (int k = 0; k < S; ++k) {
+    const int b = k & 1;
+    if ((k % kRegWarps) == warp) {
+      const int r = k / kRegWarps;
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr)
+        if (rr == r) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) rowbuf[b][lane + 32 * c] = v[rr][c];
+        }
+    }
+    if ((k & 31) == lane) {
+      const int cc = k >> 5;
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        int64_t x = v[r][0];
+#pragma unroll
+        for (int c = 1; c < C; ++c)
+          if (cc == c) x = v[r][c];
+        colbuf[b][warp + kRegWarps * r] = x;
+      }
+    }
+    __syncthreads();
+    int64_t rk[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) rk[c] = rowbuf[b][lane + 32 * c];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int64_t dik = colbuf[b][warp + kRegWarps * r];
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[r][c] = min(v[r][c], dik + rk[c]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int i = warp + kRegWarps * r, j = lane + 32 * c;
+      if (i < S && j < S) out[i * S + j] = v[r][c];
+    }
+}
+
 // One CTA per tensor.  States are packed one byte per dim (a_j <= 6) into
 // int32 codes; the lookup table maps the mixed-radix code sum a_j (L+1)^j to
 // the state index (-1 = invalid split).
-__global__ void __launch_bounds__(kApspThreads, 3)
+template <int C>
+__global__ void __launch_bounds__(kApspThreads, C == 2 ? 3 : 2)
 k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict__ tens,
           const int32_t* __restrict__ states, int64_t* __restrict__ dist) {
   extern __shared__ int64_t smem[];
@@ -139,56 +202,9 @@ k_cg_apsp(const ft_comm_profile* __restrict__ prof, const TensorDesc* __restrict
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  if (S <= 64 && nwarp == kRegWarps) {
-    // Register-resident Floyd-Warshall (S <= 64): thread (warp w, lane l)
-    // owns d[w + kRegWarps*r][l + 32c], r < kRows, c < 2.  Round k publishes
-    // row k (its owner warp) and column k (lane k%32 of every warp) to
-    // double-buffered shared rows, one barrier per round; every thread then
-    // does 2*kRows min-plus updates from 2 + kRows shared loads.
-    constexpr int kRows = 64 / kRegWarps;
-    __syncthreads();
-    int64_t v[kRows][2];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int i = warp + kRegWarps * r, j = lane + 32 * c;
-        v[r][c] = (i < S && j < S) ? d[i * S + j] : kInf;
-      }
-    __shared__ int64_t rowbuf[2][64], colbuf[2][64];
-    for (int k = 0; k < S; ++k) {
-      const int b = k & 1;
-      if ((k % kRegWarps) == warp) {
-        const int r = k / kRegWarps;
-#pragma unroll
-        for (int rr = 0; rr < kRows; ++rr)
-          if (rr == r) {
-            rowbuf[b][lane] = v[rr][0];
-            rowbuf[b][lane + 32] = v[rr][1];
-          }
-      }
-      if ((k & 31) == lane) {
-        const int c = k >> 5;
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) colbuf[b][warp + kRegWarps * r] = c ? v[r][1] : v[r][0];
-      }
-      __syncthreads();
-      const int64_t rk0 = rowbuf[b][lane], rk1 = rowbuf[b][lane + 32];
-#pragma unroll
-      for (int r = 0; r < kRows; ++r) {
-        const int64_t dik = colbuf[b][warp + kRegWarps * r];
-        v[r][0] = min(v[r][0], dik + rk0);
-        v[r][1] = min(v[r][1], dik + rk1);
-      }
-    }
-    int64_t* out = dist + td.dist_off;
-#pragma unroll
-    for (int r = 0; r < kRows; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int i = warp + kRegWarps * r, j = lane + 32 * c;
-        if (i < S && j < S) out[i * S + j] = v[r][c];
-      }
+  if (S <= 32 * C && nwarp == kRegWarps) {
+    __syncthreads();  // weight matrix complete
+    fw_registers<C>(d, S, dist + td.dist_off, warp, lane);
     return;
   }
   // General case: Floyd-Warshall in place in shared memory: row k and column
@@ -505,12 +521,14 @@ int launch_apsp(Pool& P, const ft_comm_profile* prof, const std::vector<TensorDe
   CG_CHECK(cudaMemcpyAsync(L.dst, states.data(), states.size() * 4, cudaMemcpyHostToDevice, st));
   CG_CHECK(cudaMemsetAsync(L.dbad, 0, 4, st));
   const size_t smem = (size_t)max_s * max_s * sizeof(int64_t);
-  CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CG_CHECK(cudaFuncSetAttribute(k_cg_apsp, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  const int threads = max_s <= 64 ? kRegWarps * 32 : kApspThreads;
-  k_cg_apsp<<<(int)td.size(), threads, smem, st>>>((const ft_comm_profile*)L.dp,
-                                                   (const TensorDesc*)L.dtd,
-                                                   (const int32_t*)L.dst, (int64_t*)L.dd);
+  // Register Floyd-Warshall with 2 columns per lane (S <= 64, 3 CTAs/SM) or
+  // 3 (S <= 96, 2 CTAs/SM); larger tensors use the shared-memory path.
+  auto kern = max_s <= 64 ? k_cg_apsp<2> : k_cg_apsp<3>;
+  CG_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CG_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  kern<<<(int)td.size(), kApspThreads, smem, st>>>((const ft_comm_profile*)L.dp,
+                                                  (const TensorDesc*)L.dtd,
+                                                  (const int32_t*)L.dst, (int64_t*)L.dd);
   CG_CHECK(cudaGetLastError());
   return FT_OK;
 }

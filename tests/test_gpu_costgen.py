@@ -203,3 +203,27 @@ def test_costgen_profile_times(ft):
         ft.costgen_profile(False)
     assert a > 0 and g > 0
     assert np.array_equal(out.cpu().numpy(), oracle.reschedule_costs(prof, nd, dims, eb, qt, qf, qo))
+
+
+@pytest.mark.parametrize("L", [5, 6])
+def test_costgen_fullsize_bench_workload(ft, L):
+    """Full-size parity at the bench configuration (tools/bench_costgen.py,
+    CG5: 9.52 M queries, the launch configuration it times), host-buffer and
+    device-pointer entries, every query against the oracle."""
+    import os
+    import sys
+    import torch
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import bench_costgen as B
+    w, nd, dims, eb, rng = B.workload(0, L)
+    ns = [len(ft.split_states(dims[x, :nd[x]], L)) for x in range(len(nd))]
+    qt, qf, qo = B.queries(w, ns, rng)
+    prof = comm.profile(0, L=L, P=40)
+    want = oracle.reschedule_costs(prof, nd, dims, eb, qt, qf, qo)
+    assert np.array_equal(ft.reschedule_costs(prof, nd, dims, eb, qt, qf, qo), want)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(a).to(dev) for a in (qt, qf, qo)]
+    out = torch.empty(qt.size, dtype=torch.int64, device=dev)
+    ft.reschedule_costs_dev(prof, nd, dims, eb, qt.size, d[0].data_ptr(), d[1].data_ptr(),
+                            d[2].data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(out.cpu().numpy(), want)

@@ -17,7 +17,10 @@ Pins derived from them (SURVEY 8(c) "Large graphs"):
   for every lambda = a/b >= 0 (the frontier contains a minimiser
   of every monotone objective).
 
-Lexicographic costs are carried as two int64 arrays (primary, secondary).
+Lexicographic costs are carried as two integer arrays (primary, secondary):
+int64 while the sum of every op's and edge's largest key provably stays below
+2^62, else numpy object arrays of Python ints (exact at any size: frontier
+sums reach 2^60 under R10, and b*t + a*m exceeds int64 there).
 """
 from __future__ import annotations
 
@@ -27,7 +30,7 @@ import numpy as np
 def _lexmin(P, S, axis):
     """Lexicographic min over ``axis`` of pairs (P, S)."""
     pmin = P.min(axis=axis, keepdims=True)
-    big = np.iinfo(np.int64).max
+    big = np.iinfo(np.int64).max if P.dtype == np.int64 else 1 << 200
     smin = np.where(P == pmin, S, big).min(axis=axis)
     return np.squeeze(pmin, axis=axis), smin
 
@@ -46,6 +49,12 @@ def solve(w, key):
         em = (np.zeros(K[s] * K[d], np.int64) if w.edge_m is None else w.edge_m[e].astype(np.int64))
         p, q = key(em, w.edge_t[e].astype(np.int64))
         edges[e] = (s, d, p.reshape(K[s], K[d]), q.reshape(K[s], K[d]))
+    # exact integer type: int64 only if no partial sum can reach 2^62
+    bound = sum(max(int(np.abs(a).max()), int(np.abs(b).max())) for a, b in op.values())
+    bound += sum(max(int(np.abs(p).max()), int(np.abs(q).max())) for _, _, p, q in edges.values())
+    if bound >= 1 << 62:
+        op = {i: (a.astype(object), b.astype(object)) for i, (a, b) in op.items()}
+        edges = {e: (s, d, p.astype(object), q.astype(object)) for e, (s, d, p, q) in edges.items()}
     alive = set(range(n))
     nid = w.n_edges
 
@@ -142,8 +151,11 @@ def min_time_endpoint(w):
 
 
 def weighted_optimum(w, a: int, b: int):
-    """min over strategies of b*t + a*m (int64; a, b small non-negative ints)."""
-    z = lambda m, t: (b * t + a * m, np.zeros_like(m))
+    """min over strategies of b*t + a*m (exact; a, b non-negative ints)."""
+    if max(a, b) < 1 << 20:  # per-entry keys fit int64 (costs < 2^40, R10); solve() widens sums
+        z = lambda m, t: (b * t + a * m, np.zeros_like(m))
+    else:
+        z = lambda m, t: (b * t.astype(object) + a * m.astype(object), np.zeros(len(m), np.int64))
     return solve(w, z)[0]
 
 

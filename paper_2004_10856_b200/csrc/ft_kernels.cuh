@@ -73,6 +73,7 @@ struct BatchDev {
   int slog;                 // sample stride at level l >= 1: 2^(slog0 + slog*(l-1))
   int slog0;
   int cdirect;              // direct-path capacity (<= C_DIRECT)
+  int kspan;                // single-key sorts pack (m - m_min) when it fits in kspan bits
   int64_t nseg;             // local segments over all steps
   int64_t nblk;             // local blocks over all steps
 };

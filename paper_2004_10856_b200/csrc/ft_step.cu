@@ -435,7 +435,7 @@ __device__ __forceinline__ void cta_bitonic_keys(uint64_t (&k)[R], uint64_t* xk)
 template <int R, typename Gen>
 __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int64_t* xt, uint64_t* xid,
                                                uint64_t* xk, long long* sh, const LevelDev& L,
-                                               int64_t gs, int64_t* s_start) {
+                                               int64_t gs, int64_t* s_start, int kspan) {
   constexpr int NW = DIRECT_NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eb = wid * 32 * R;
@@ -447,13 +447,13 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     t[r] = INF;
     id[r] = ~0ull;
   }
-  // Tuples are staged in x*; the sort runs on 64-bit keys (m << 10 | e)
-  // (m < 3 * 2^40 by R10, e < N <= 1024) and t, id are gathered by e.  The
-  // key order is the (m, t, id) order unless two tuples share m: then the
-  // staged tuples are re-sorted on the full key.
-  uint64_t k[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) k[r] = ~0ull;
+  // Tuples are staged in x*; the sort runs on 64-bit keys ((m - m0) << 10 | e)
+  // (m0 = the sample's least m, e < N <= 1024) and t, id are gathered by e.
+  // Frontier m grows with the eliminated subgraph (sums up to 2^60, R10), so
+  // the packing is used only when the sample's m span fits in kspan (<= 53)
+  // bits; otherwise, and when two tuples share m (the key order is then not
+  // the (m, t, id) order), the staged tuples are sorted on the full key.
+  long long lmin = INF, lmax = -1;
 #pragma unroll 1
   for (int r = 0; r < R; ++r) {
     const int e = eb + (r << 5) + lane;
@@ -464,32 +464,56 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
       xm[e] = vm;
       xt[e] = vt;
       xid[e] = vi;
-#pragma unroll
-      for (int q = 0; q < R; ++q)
-        if (q == r) k[q] = ((uint64_t)vm << 10) | (uint64_t)e;
+      lmin = vm < lmin ? vm : lmin;
+      lmax = vm > lmax ? vm : lmax;
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long a = __shfl_xor_sync(0xffffffffu, lmin, o), b = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmin = a < lmin ? a : lmin;
+    lmax = b > lmax ? b : lmax;
+  }
+  if (lane == 0) {
+    sh[wid] = lmin;
+    sh[NW + wid] = lmax;
+  }
   __syncthreads();
-  cta_bitonic_keys<R>(k, xk);
-  bool tie = false;
+  long long m0 = INF, m1 = -1;
+  for (int w = 0; w < NW; ++w) {
+    m0 = sh[w] < m0 ? sh[w] : m0;
+    m1 = sh[NW + w] > m1 ? sh[NW + w] : m1;
+  }
+  const bool wide = ((unsigned long long)(m1 - m0) >> kspan) != 0;
+  uint64_t k[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = eb + (r << 5) + lane;
-    if (e < n) {
-      const int src = (int)(k[r] & 1023u);
-      m[r] = (int64_t)(k[r] >> 10);
-      t[r] = xt[src];
-      id[r] = xid[src];
-    }
-    uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
-    const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
-    if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
-    if (e < n && prev != ~0ull && (prev >> 10) == (k[r] >> 10)) tie = true;
+    k[r] = e < n ? ((uint64_t)(xm[e] - m0) << 10) | (uint64_t)e : ~0ull;
   }
-  if (lane == 31) sh[wid] = (long long)(k[R - 1] >> 10);  // last m of the warp (INF-padded: huge)
-  __syncthreads();
-  if (wid > 0 && lane == 0 && eb < n && (long long)(k[0] >> 10) == sh[wid - 1]) tie = true;
-  if (__syncthreads_or(tie)) {  // equal m values: exact sort on (m, t, id)
+  __syncthreads();  // sh reuse
+  bool tie = false;
+  if (!wide) {
+    cta_bitonic_keys<R>(k, xk);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = eb + (r << 5) + lane;
+      if (e < n) {
+        const int src = (int)(k[r] & 1023u);
+        m[r] = (int64_t)(k[r] >> 10) + m0;
+        t[r] = xt[src];
+        id[r] = xid[src];
+      }
+      uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+      const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
+      if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
+      if (e < n && prev != ~0ull && (prev >> 10) == (k[r] >> 10)) tie = true;
+    }
+    if (lane == 31) sh[wid] = (long long)(k[R - 1] >> 10);  // last key m of the warp (padding: 2^54 - 1)
+    __syncthreads();
+    if (wid > 0 && lane == 0 && eb < n && (long long)(k[0] >> 10) == sh[wid - 1]) tie = true;
+  }
+  if (__syncthreads_or(tie || wide)) {  // exact sort on (m, t, id)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int e = eb + (r << 5) + lane;
@@ -672,8 +696,8 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_direct(BatchDev B, LevelDev L)
     };
     if ((N == 2 * DIRECT_NT || N == 4 * DIRECT_NT) && N <= B.cdirect) {
       uint64_t* xk = (uint64_t*)kf;  // kf + pre (>= 8 N bytes) are free after generation
-      if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start);
-      else cta_sort_sweep<4>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start);
+      if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
+      else cta_sort_sweep<4>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
       continue;
     }
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
@@ -856,9 +880,12 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
     make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
                samp_idx(jz, b.n[2], st), vm, vt, vi);
   };
-  // sort 64-bit keys (m << 9 | e), t and id staged in wt/wi (m < 3 * 2^40,
-  // R10); equal m values (detected after the sort) -> full (m, t, id) sort
+  // sort 64-bit keys ((m - m0) << 9 | e), m0 = the sample's least m, with t
+  // and id staged in wt/wi; a sample whose m span needs more than B.kspan
+  // bits (frontier m reaches 2^60, R10), or with equal m values (detected
+  // after the sort), takes the full (m, t, id) sort instead
   uint64_t k[R];
+  long long lmin = INF, lmax = -1;
 #pragma unroll
   for (int r = 0; r < R; ++r) k[r] = ~0ull;
 #pragma unroll 1
@@ -870,30 +897,46 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
       gen(e, vm, vt, vi);
       wt[e] = vt;
       wi[e] = vi;
+      lmin = vm < lmin ? vm : lmin;
+      lmax = vm > lmax ? vm : lmax;
 #pragma unroll
       for (int q2 = 0; q2 < R; ++q2)
-        if (q2 == r) k[q2] = ((uint64_t)vm << 9) | (uint64_t)e;
+        if (q2 == r) k[q2] = (uint64_t)vm;
     }
   }
-  __syncwarp();
-  warp_bitonic_keys<R>(k);
-  bool tie = false;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int e = (r << 5) | lane;
-    m[r] = INF;
-    t[r] = INF;
-    id[r] = ~0ull;
-    if (e < n) {
-      const int src = (int)(k[r] & 511u);
-      m[r] = (int64_t)(k[r] >> 9);
-      t[r] = wt[src];
-      id[r] = wi[src];
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long a = __shfl_xor_sync(0xffffffffu, lmin, o), b = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmin = a < lmin ? a : lmin;
+    lmax = b > lmax ? b : lmax;
+  }
+  const bool wide = ((unsigned long long)(lmax - lmin) >> B.kspan) != 0;
+  bool tie = wide;
+  __syncwarp();
+  if (!wide) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = (r << 5) | lane;
+      if (e < n) k[r] = ((k[r] - (uint64_t)lmin) << 9) | (uint64_t)e;
     }
-    uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
-    const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
-    if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
-    if (e < n && prev != ~0ull && (prev >> 9) == (k[r] >> 9)) tie = true;
+    warp_bitonic_keys<R>(k);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = (r << 5) | lane;
+      m[r] = INF;
+      t[r] = INF;
+      id[r] = ~0ull;
+      if (e < n) {
+        const int src = (int)(k[r] & 511u);
+        m[r] = (int64_t)(k[r] >> 9) + lmin;
+        t[r] = wt[src];
+        id[r] = wi[src];
+      }
+      uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+      const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
+      if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
+      if (e < n && prev != ~0ull && (prev >> 9) == (k[r] >> 9)) tie = true;
+    }
   }
   if (__any_sync(0xffffffffu, tie)) {
 #pragma unroll
@@ -1026,9 +1069,10 @@ __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) 
 // registers, t_z(k, p) is staged once per step in shared memory and reused
 // across the CTA's packs, and one thread per (w, p) runs Alg. 1 as a
 // sequential running min, recording keep bits; survivors are then written
-// warp-cooperatively (coalesced).  Rows with equal m values, more than
-// WARP_DIRECT tuples or an oversized t_z table go to k_node_shared (one CTA per
-// row, exact group rule for ties) through a device list.
+// warp-cooperatively (coalesced).  Rows with more than WARP_DIRECT tuples, an
+// m span wider than the packed keys hold, or an oversized t_z table go to
+// k_node_shared (one CTA per row, full int64 keys, exact group rule for ties)
+// through a device list.
 constexpr int NP_NT = 256;
 constexpr int NP_WORDS = WARP_DIRECT / 32;
 constexpr int NP_ROWS = 8;
@@ -1041,15 +1085,19 @@ __host__ __device__ inline size_t np_smem(int rmax, int64_t ztn) {
 }
 
 // One row: generate its (<= WARP_DIRECT) tuples, sort 64-bit keys
-// (m << 9 | e) in registers (m < 3 * 2^40, R10) and gather t_xy and the block
-// by e (= the tuple id rel_k + x, R6).  Ties in m need no re-sort: the sweep
-// applies the exact equal-m group rule, which scans the whole group.
+// ((m - m0) << 9 | e) in registers (m0 = the row's least m) and gather t_xy
+// and the block by e (= the tuple id rel_k + x, R6).  Ties in m need no
+// re-sort: the sweep applies the exact equal-m group rule, which scans the
+// whole group.  Returns bit 0: equal m values; bit 1: the row's m span needs
+// more than kspan bits (frontier m reaches 2^60, R10) -- the caller then
+// hands the row to k_node_shared, which sorts the full int64 m.
 template <int R>
-__device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, const int64_t* bo,
-                                            const int64_t* ym, const int64_t* yt, int nblk, int n,
-                                            int64_t* sm, int64_t* stxy, uint32_t* sidk) {
+__device__ __forceinline__ int np_row_sort(const StepDev& s, const int* pre, const int64_t* bo,
+                                           const int64_t* ym, const int64_t* yt, int nblk, int n,
+                                           int64_t* sm, int64_t* stxy, uint32_t* sidk, int kspan) {
   const int lane = threadIdx.x & 31;
   uint64_t key[R];
+  long long lmin = INF, lmax = -1;
 #pragma unroll
   for (int r = 0; r < R; ++r) key[r] = ~0ull;
 #pragma unroll 1
@@ -1066,10 +1114,24 @@ __device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, co
       const int64_t vm = __ldg(s.X.m + bo[lo] + x) + ym[lo];
       stxy[e] = __ldg(s.X.t + bo[lo] + x) + yt[lo];  // staged by e
       sidk[e] = (uint32_t)lo;
+      lmin = vm < lmin ? vm : lmin;
+      lmax = vm > lmax ? vm : lmax;
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (q == r) key[q] = ((uint64_t)vm << 9) | (uint64_t)e;
+        if (q == r) key[q] = (uint64_t)vm;
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long a = __shfl_xor_sync(0xffffffffu, lmin, o), b = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmin = a < lmin ? a : lmin;
+    lmax = b > lmax ? b : lmax;
+  }
+  if (((unsigned long long)(lmax - lmin) >> kspan) != 0) return 2;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = (r << 5) | lane;
+    if (e < n) key[r] = ((key[r] - (uint64_t)lmin) << 9) | (uint64_t)e;
   }
   __syncwarp();
   warp_bitonic_keys<R>(key);
@@ -1093,12 +1155,12 @@ __device__ __forceinline__ bool np_row_sort(const StepDev& s, const int* pre, co
     const bool same_next = e + 1 < n && (nk >> 9) == (key[r] >> 9);
     if (same_next) tie = true;
     if (e < n) {  // id | k << 16 | (last of its equal-m group) << 31
-      sm[e] = (int64_t)(key[r] >> 9);
+      sm[e] = (int64_t)(key[r] >> 9) + lmin;
       stxy[e] = t[r];
       sidk[e] = (uint32_t)(key[r] & 511u) | (kb[r] << 16) | (same_next ? 0u : 0x80000000u);
     }
   }
-  return __any_sync(0xffffffffu, tie);
+  return __any_sync(0xffffffffu, tie) ? 1 : 0;
 }
 
 __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, const NodeGroup* packs,
@@ -1178,15 +1240,16 @@ __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, 
           int64_t* rm = sm + r * WARP_DIRECT;
           int64_t* rt = stxy + r * WARP_DIRECT;
           uint32_t* ri = sidk + r * WARP_DIRECT;
-          bool tie;
-          if (n <= 32) tie = np_row_sort<1>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          else if (n <= 64) tie = np_row_sort<2>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          else if (n <= 128) tie = np_row_sort<4>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          else tie = np_row_sort<8>(s, pr, b, ym, yt, nblk, n, rm, rt, ri);
-          if (lane == 0) {
-            row_tie[r] = tie;
+          int rc;
+          if (n <= 32) rc = np_row_sort<1>(s, pr, b, ym, yt, nblk, n, rm, rt, ri, B.kspan);
+          else if (n <= 64) rc = np_row_sort<2>(s, pr, b, ym, yt, nblk, n, rm, rt, ri, B.kspan);
+          else if (n <= 128) rc = np_row_sort<4>(s, pr, b, ym, yt, nblk, n, rm, rt, ri, B.kspan);
+          else rc = np_row_sort<8>(s, pr, b, ym, yt, nblk, n, rm, rt, ri, B.kspan);
+          ok = rc != 2;  // wide m span: k_node_shared
+          if (lane == 0 && ok) {
+            row_tie[r] = rc != 0;
             atomicAdd(&L.hdr->ns_rows, 1ull);
-            if (tie) atomicAdd(&L.hdr->ns_tie, 1ull);
+            if (rc) atomicAdd(&L.hdr->ns_tie, 1ull);
           }
         }
         if (!ok) {  // large rows / tables: one CTA per row in k_node_shared
@@ -2572,6 +2635,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   s.nsteps = nsteps;
   s.slog = slog;
   s.slog0 = slog0;
+  {  // test hook: FT_KEY_SPAN_BITS < 53 forces the full-key sorts (read per wave)
+    const char* ks = getenv("FT_KEY_SPAN_BITS");
+    s.kspan = ks ? std::max(0, std::min(53, atoi(ks))) : 53;
+  }
   // waves of few segments (LDP: one per configuration) take a larger direct
   // capacity: one filter level fewer per segment, and few CTAs sort in smem
   // (A/B: a global 2048 helped C5's LDP waves but slowed C4's 6e4-segment

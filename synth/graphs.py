@@ -407,6 +407,45 @@ def c5(seed: int = 0, n_ops: int = 2000, K: int = 64, B: int = 32, Lmin: int = 4
                     {"B": B, "Lmin": Lmin, "Lmax": Lmax, "rho": rho, "seed": seed}).check()
 
 
+def big_chain(seed: int = 0, n_ops: int = 16384, K: int = 2, rho: float = 0.95,
+              span: int = 1 << 16) -> Workload:
+    """Wide-cost chain (R10 range test): o_0 -> ... -> o_{n-1}, K configs.
+    Every op and edge cost has m = 2^40 - 1 - span + floor(span u) (edge
+    memory included, R11) and t = floor(span (rho u + (1 - rho) w)), u, w ~
+    U[0,1) per entry: each input cost sits just below the 2^40 bound, so the
+    frontier m of an i-op prefix is about i 2^40 (2^55 at 16,384 ops) while
+    its spread stays small; rho keeps the frontiers bounded (as in C5).
+    Draw order: ops (u, w) by id, then edges (u, w) by id."""
+    rng = np.random.default_rng(seed)
+    base = float((1 << 40) - 1 - span)
+    op_m, op_t = [], []
+    for _ in range(n_ops):
+        u = rng.random(K)
+        w = rng.random(K)
+        op_m.append(_i64(base + np.floor(span * u)))
+        op_t.append(_i64(np.floor(span * (rho * u + (1.0 - rho) * w))))
+    edge_m, edge_t = [], []
+    for _ in range(n_ops - 1):
+        u = rng.random(K * K)
+        w = rng.random(K * K)
+        edge_m.append(_i64(base + np.floor(span * u)))
+        edge_t.append(_i64(np.floor(span * (rho * u + (1.0 - rho) * w))))
+    src = np.arange(n_ops - 1, dtype=np.int32)
+    return Workload(f"bigchain-n{n_ops}-K{K}", np.full(n_ops, K, np.int32), src, src + 1, op_m, op_t,
+                    edge_t, edge_m, None, {"rho": rho, "span": span, "seed": seed}).check()
+
+
+def scaled(w: Workload, bits: int = 40) -> Workload:
+    """The same graph with every cost multiplied by one integer factor so
+    that the largest cost is just below 2^bits (R10's bound at bits = 40)."""
+    mx = max([int(a.max()) for a in w.op_m + w.op_t + w.edge_t] +
+             [int(a.max()) for a in (w.edge_m or [])] + [1])
+    f = ((1 << bits) - 1) // mx
+    mul = lambda L: None if L is None else [_i64(a * f) for a in L]
+    return Workload(w.name + f"-x{f}", w.n_cfgs, w.src, w.dst, mul(w.op_m), mul(w.op_t),
+                    mul(w.edge_t), mul(w.edge_m), w.op_names, dict(w.meta, scale=f)).check()
+
+
 CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
 
 

@@ -380,3 +380,32 @@ def test_partition_invariance_new_kinds(ft, world):
         for s in range(len(a.stats())):
             for x, y in zip(a.step_output(s), b.step_output(s)):
                 assert np.array_equal(x, y), (w.name, s)
+
+
+# ---- R10 range: frontier m up to 2^60 (packed single-key sorts must stay exact)
+
+def test_big_chain_wide_costs(ft):
+    """16,384-op chain, K = 2, every op and edge cost (memory included) just
+    below 2^40: frontier m ~ 2^55, beyond what an unshifted (m << 10 | e) key
+    holds.  Every step bit-exact against the oracle."""
+    w = G.big_chain(n_ops=16384)
+    gg, st = compare(ft, w, strategies=48)
+    assert gg.frontier()[0][0] > 1 << 54
+
+
+def test_bert_2layers_scaled_to_2_40(ft):
+    """BERT-2L with every cost scaled just below 2^40 (R10's input bound)."""
+    compare(ft, G.scaled(G.c4(layers=2)), strategies=32)
+
+
+@pytest.mark.parametrize("bits", ["0", "12"])
+def test_full_key_sort_fallback(ft, monkeypatch, bits):
+    """FT_KEY_SPAN_BITS forces the full (m, t, id) sorts that take over when a
+    sample's m span does not fit the packed key: every step still exact, and
+    the shared-order node rows go to the full-key CTA kernel."""
+    monkeypatch.setenv("FT_KEY_SPAN_BITS", bits)
+    for w in (G.c3(), G.c4(layers=2), G.c5(n_ops=300, K=32, B=8, Lmin=3, Lmax=8),
+              G.scaled(G.random_sp(1003, n_ops=14, kmax=12, cost_hi=1 << 20))):
+        gg, st = compare(ft, w, strategies=16)
+        if w.name.startswith("C5"):
+            assert sum(s["path"]["shared_cta_rows"] for s in st) > 0  # rows handed to k_node_shared

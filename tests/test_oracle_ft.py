@@ -125,3 +125,30 @@ def test_thread_count_invariance():
         b = g4.step_output(s)
         for x, y in zip(a, b):
             assert (x == y).all()
+
+
+# ---- R10 range: costs just below 2^40, frontier m far beyond 2^40
+
+@pytest.mark.parametrize("seed", range(40))
+def test_scaled_costs_vs_bruteforce(seed):
+    """Tiny graphs with every cost scaled just below 2^40 (edge memory too):
+    brute force in Python ints (Eq. 3, Def. 1)."""
+    w = G.scaled(G.random_sp(seed, n_ops=2 + seed % 7, kmax=3, edge_mem=(seed % 3 == 0)))
+    if int(np.prod(w.n_cfgs.astype(np.int64))) > 100_000:
+        pytest.skip("too many strategies")
+    _check_vs_bruteforce(w)
+
+
+def test_big_chain_scalar_pins():
+    """Wide-cost chain (1,024 ops; m ~ 2^50): endpoints and supported points
+    by the scalar DPs in exact integers."""
+    w = G.big_chain(n_ops=1024)
+    g, m, t = oracle.run_ft(w, threads=4)
+    assert (np.diff(m) > 0).all() and (np.diff(t) < 0).all() and int(m[0]) > 1 << 49
+    assert (int(m[0]), int(t[0])) == sdp.min_memory_endpoint(w)
+    assert (int(m[-1]), int(t[-1])) == sdp.min_time_endpoint(w)
+    M, T = [int(x) for x in m], [int(x) for x in t]
+    for a, b in [(1, 4), (1, 1), (3, 1), (1 << 30, 1)]:
+        assert min(b * y + a * x for x, y in zip(M, T)) == sdp.weighted_optimum(w, a, b), (a, b)
+    for i in np.linspace(0, len(m) - 1, 6).astype(int):
+        assert bf.total_cost(w, g.strategy(int(i))) == (M[i], T[i])

@@ -26,7 +26,8 @@ LIB_PATH = os.path.join(_HERE, "liboracle_ft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -6, -7, -8
 NODE, EDGE, AUTO, AUTO_HEUR = 1, 2, 3, 4
-STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch"}
+STEP_NAMES = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch", 8: "compose",
+              9: "remap"}
 
 
 def build(force: bool = False) -> str:

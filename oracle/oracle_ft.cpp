@@ -81,7 +81,8 @@ struct Edge {
 }  // namespace
 
 struct oft_graph {
-  int n_ops = 0;
+  int n_ops = 0;       // operators so far: originals, then composites (R21)
+  int n_orig_ops = 0;  // operators of the input graph
   int n_orig_edges = 0;
   int threads = 1;
   std::vector<int> K;
@@ -92,7 +93,8 @@ struct oft_graph {
   std::vector<FSet> sets;        // sets[0] = unit {(0,0)}
   std::vector<Step> steps;
   std::vector<bool> op_cost_set, edge_cost_set;
-  std::vector<int> pos0;         // position in the original graph's topological order (R9)
+  std::vector<int> pos0;         // position in the live graph's topological order (R9, R21)
+  std::vector<std::pair<int, int>> comp;  // composite op (R21): (o_h, o_i), config w = s_h*K_i + s_i
   bool started = false;
   bool have_final = false;
   int final_mode = 0;  // 1 = LDP (Alg. 3), 2 = FT-Elimination
@@ -141,6 +143,26 @@ void block_segs(const Step& s, int64_t sigma, int64_t k, int64_t* sx, int64_t* s
       *sx = sigma;                                            // F(o_h, s_h)
       *sy = s.KC ? k * s.KA + sigma : sigma * s.KB + k;       // F(e, s_i, s_h) | F(e, s_h, s_i)
       *sz = k;                                                // F(o_i, s_i)
+      break;
+    }
+    case OFT_STEP_COMPOSE: {  // Eq.6 P:609-613 (R21): sigma = w = s_h*K_i + s_i, one block
+      const int64_t p = sigma / s.KB, k = sigma % s.KB;     // KA = K_h, KB = K_i
+      *sx = p;                                              // F(o_h, s_h^p)
+      *sy = k * s.KA + p;                                   // F(e_ih, s_i^k, s_h^p)
+      *sz = k;                                              // F(o_i, s_i^k)
+      break;
+    }
+    case OFT_STEP_REMAP: {  // R21: an edge of o_h or o_i re-indexed onto the composite o_v
+      // KA = K_y (the other endpoint), KB = K_i, KC = side | part << 1: side 0 =
+      // o_v is the new edge's source, 1 = its destination; part 0 = the old
+      // endpoint was o_h (its config is w / K_i), 1 = o_i (w % K_i)
+      const int64_t Kv = s.nseg / s.KA, side = s.KC & 1, part = s.KC >> 1;
+      const int64_t Kold = part ? s.KB : Kv / s.KB;
+      const int64_t w = side == 0 ? sigma / s.KA : sigma % Kv, y = side == 0 ? sigma % s.KA : sigma / Kv;
+      const int64_t c = part ? w % s.KB : w / s.KB;
+      *sx = side == 0 ? c * s.KA + y : y * Kold + c;
+      *sy = 0;
+      *sz = 0;
       break;
     }
     case OFT_STEP_PAIR:  // FT-Elimination P:628: k = s_1 * K_n + s_n over the 2-op graph
@@ -399,9 +421,148 @@ int do_branch(oft_graph* g, const Adj& a, int i) {
   return OFT_OK;
 }
 
+// Eq. 6 with composite configurations (reading R21): o_i feeds o_h
+// through the single edge e and keeps other edges, so nothing can be reduced
+// over s_i; o_i and o_h are replaced by one operator o_v whose configurations
+// are the pairs w = (s_h, s_i) (w = s_h * K_i + s_i):
+//   F(o_v, w) = reduce(F(o_h, s_h) (x) F(e, s_i, s_h) (x) F(o_i, s_i))
+// and every other edge of o_h or o_i is re-indexed onto o_v (F(e', w, .) =
+// F(e', s_h or s_i, .)).  The live graph's topological order is recomputed
+// (Kahn's algorithm, ready ops by (previous position, id); o_v takes o_h's).
+void reorder(oft_graph* g) {
+  Adj a = build_adj(g);
+  std::vector<int> indeg(g->n_ops, 0);
+  std::set<std::pair<int, int>> ready;
+  for (int i = 0; i < g->n_ops; ++i)
+    if (g->op_alive[i]) {
+      indeg[i] = (int)a.in[i].size();
+      if (indeg[i] == 0) ready.insert({g->pos0[i], i});
+    }
+  int pos = 0;
+  std::vector<int> np(g->n_ops, INT_MAX);
+  while (!ready.empty()) {
+    int u = ready.begin()->second;
+    ready.erase(ready.begin());
+    np[u] = pos++;
+    for (int e : a.out[u]) {
+      int d = g->edges[e].dst;
+      if (--indeg[d] == 0) ready.insert({g->pos0[d], d});
+    }
+  }
+  for (int i = 0; i < g->n_ops; ++i)
+    if (g->op_alive[i]) g->pos0[i] = np[i];
+}
+
+// Is there a path o_i -> ... -> o_h other than the direct edges?  (Merging
+// o_i into o_h would then close a cycle.)
+bool other_path(const oft_graph* g, const Adj& a, int i, int h) {
+  std::vector<char> seen(g->n_ops, 0);
+  std::vector<int> st;
+  for (int e : a.out[i])
+    if (g->edges[e].dst != h) st.push_back(g->edges[e].dst);
+  while (!st.empty()) {
+    int u = st.back();
+    st.pop_back();
+    if (u == h) return true;
+    if (seen[u]) continue;
+    seen[u] = 1;
+    for (int e : a.out[u]) st.push_back(g->edges[e].dst);
+  }
+  return false;
+}
+
+int do_compose(oft_graph* g, const Adj& a, int i, int h) {
+  int e = -1;
+  for (int x : a.in[h])
+    if (g->edges[x].src == i) e = x;
+  const int v = g->n_ops;
+  g->n_ops++;
+  g->K.push_back(g->K[h] * g->K[i]);
+  g->op_alive.push_back(true);
+  g->pos0.push_back(g->pos0[h]);
+  g->comp.resize(g->n_ops, {-1, -1});
+  g->comp[v] = {h, i};
+  Step s;
+  s.kind = OFT_STEP_COMPOSE;
+  s.X = g->op_set[h];
+  s.Y = g->edges[e].set;
+  s.Z = g->op_set[i];
+  s.KA = g->K[h];
+  s.KB = g->K[i];
+  s.nseg = g->K[v];
+  s.nblk = 1;
+  int rc = run_step(g, s);
+  if (rc) return rc;
+  g->op_set.push_back(g->steps.back().out);
+  g->sets[g->steps.back().out].a_op = v;
+  g->edges[e].alive = false;
+  // the other edges of o_h and o_i, ascending edge id
+  std::set<int> others;
+  for (int o : {h, i}) {
+    for (int x : a.in[o]) others.insert(x);
+    for (int x : a.out[o]) others.insert(x);
+  }
+  others.erase(e);
+  for (int x : others) {
+    const int src = g->edges[x].src, dst = g->edges[x].dst;
+    const int old = (src == h || src == i) ? src : dst;
+    const int y = old == src ? dst : src;
+    Step r;
+    r.kind = OFT_STEP_REMAP;
+    r.X = g->edges[x].set;
+    r.Y = 0;
+    r.Z = 0;
+    r.KA = g->K[y];
+    r.KB = g->K[i];
+    r.KC = (old == src ? 0 : 1) | (old == i ? 2 : 0);
+    r.nseg = (int64_t)g->K[v] * g->K[y];
+    r.nblk = 1;
+    if ((rc = run_step(g, r))) return rc;
+    const int so = g->steps.back().out;
+    const int ns = old == src ? v : y, nd = old == src ? y : v;
+    g->sets[so].a_op = ns;
+    g->sets[so].b_op = nd;
+    g->edges[x].alive = false;
+    new_edge(g, ns, nd, so);
+  }
+  g->op_alive[h] = false;
+  g->op_alive[i] = false;
+  reorder(g);
+  return OFT_OK;
+}
+
+// Composite branch elimination candidate (R21): the topologically first
+// operator o_h with >= 2 input operators that has an unmarked input o_i with
+// K_h * K_i <= 4096, no other path o_i -> o_h, and that is not a source
+// feeding >= 2 operators (a broadcast input like BERT's attention mask,
+// which P:618-620 leaves to heuristic elimination); among its inputs the one
+// with the smallest K_i (SPEC: "the input operator with the smaller config
+// space"), ties by topological position.  Returns (i, h) or (-1, -1).
+std::pair<int, int> compose_candidate(const oft_graph* g, const Adj& a, const std::vector<int>& topo,
+                                      const std::vector<bool>& marked) {
+  for (int h : topo) {
+    std::set<std::pair<int, int>> ins;  // (position, op)
+    for (int e : a.in[h]) ins.insert({g->pos0[g->edges[e].src], g->edges[e].src});
+    if (ins.size() < 2) continue;
+    int best = -1;
+    for (auto& pi : ins) {
+      const int i = pi.second;
+      if (marked[i] || (int64_t)g->K[h] * g->K[i] > 4096 || other_path(g, a, i, h)) continue;
+      if (a.in[i].empty()) {  // a source: not if it feeds several operators
+        std::set<int> outs;
+        for (int e : a.out[i]) outs.insert(g->edges[e].dst);
+        if (outs.size() >= 2) continue;
+      }
+      if (best < 0 || g->K[i] < g->K[best]) best = i;
+    }
+    if (best >= 0) return {best, h};
+  }
+  return {-1, -1};
+}
+
 int check_started(oft_graph* g) {
   if (g->started) return OFT_OK;
-  for (int i = 0; i < g->n_ops; ++i)
+  for (int i = 0; i < g->n_orig_ops; ++i)
     if (!g->op_cost_set[i]) return fail(g, OFT_ESTATE, "missing op costs");
   for (int e = 0; e < g->n_orig_edges; ++e)
     if (!g->edge_cost_set[e]) return fail(g, OFT_ESTATE, "missing edge costs");
@@ -416,7 +577,8 @@ bool node_eligible(const oft_graph* g, const Adj& a, int i, const std::vector<bo
 
 // FT_AUTO policy (R9; Alg. 2 lines 4-11): one elimination.
 // Returns 1 if something was eliminated, 0 if none applies, <0 on error.
-int auto_one(oft_graph* g) {
+// compose = false skips (e) (FT_AUTO_HEUR tries heuristic elimination first).
+int auto_one(oft_graph* g, bool compose) {
   Adj a = build_adj(g);
   auto topo = live_order(g);
   auto marked = marking(g, a, topo);  // Alg.2 line 5
@@ -461,7 +623,25 @@ int auto_one(oft_graph* g) {
       int rc = do_branch(g, a, i);
       return rc ? rc : 1;
     }
+  // (e) branch elimination with composite configurations (Eq. 6, R21)
+  if (!compose) return 0;
+  const auto ih = compose_candidate(g, a, topo, marked);
+  if (ih.first >= 0) {
+    int rc = do_compose(g, a, ih.first, ih.second);
+    return rc ? rc : 1;
+  }
   return 0;
+}
+
+// (e) alone: one composite branch elimination (R21), 1 = done, 0 = none.
+int compose_one(oft_graph* g) {
+  Adj a = build_adj(g);
+  auto topo = live_order(g);
+  auto marked = marking(g, a, topo);
+  const auto ih = compose_candidate(g, a, topo, marked);
+  if (ih.first < 0) return 0;
+  int rc = do_compose(g, a, ih.first, ih.second);
+  return rc ? rc : 1;
 }
 
 // Heuristic elimination (Eq. 7; lossy, opt-in): the unmarked
@@ -601,6 +781,11 @@ int assign(oft_graph* g, std::vector<int32_t>& cfg, int op, int64_t c) {
   if (op < 0) return OFT_OK;
   if (cfg[op] >= 0 && cfg[op] != c) return fail(g, OFT_EINTERNAL, "broken provenance: config conflict");
   cfg[op] = (int32_t)c;
+  if (op < (int)g->comp.size() && g->comp[op].first >= 0) {  // composite (R21): w = s_h * K_i + s_i
+    const int h = g->comp[op].first, i = g->comp[op].second;
+    int rc = assign(g, cfg, h, c / g->K[i]);
+    return rc ? rc : assign(g, cfg, i, c % g->K[i]);
+  }
   return OFT_OK;
 }
 
@@ -654,6 +839,8 @@ int oft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, cons
   oft_graph* g = new (std::nothrow) oft_graph();
   if (!g) return OFT_ENOMEM;
   g->n_ops = n_ops;
+  g->n_orig_ops = n_ops;
+  g->comp.assign(n_ops, {-1, -1});
   g->n_orig_edges = n_edges;
   g->threads = threads < 1 ? 1 : threads;
   g->K.assign(n_cfgs, n_cfgs + n_ops);
@@ -700,7 +887,7 @@ void oft_graph_destroy(oft_graph* g) { delete g; }
 int oft_set_op_costs(oft_graph* g, int32_t op, const int64_t* m, const int64_t* t) {
   if (!g) return OFT_EINVAL;
   if (g->started) return fail(g, OFT_ESTATE, "costs set after elimination began");
-  if (op < 0 || op >= g->n_ops || !m || !t) return fail(g, OFT_EINVAL, "bad op");
+  if (op < 0 || op >= g->n_orig_ops || !m || !t) return fail(g, OFT_EINVAL, "bad op");
   for (int k = 0; k < g->K[op]; ++k) {
     if (m[k] < 0 || t[k] < 0) return fail(g, OFT_EINVAL, "negative cost");
     if (m[k] >= (int64_t(1) << 40) || t[k] >= (int64_t(1) << 40)) return fail(g, OFT_EOVERFLOW, "cost >= 2^40");
@@ -754,8 +941,10 @@ int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* out_edge) {
     return do_edge(g, std::min(id, other), std::max(id, other), out_edge);
   }
   if (kind == OFT_AUTO || kind == OFT_AUTO_HEUR) {
+    // FT_AUTO: (a)-(e) until none applies.  FT_AUTO_HEUR (R17, R21): (a)-(d);
+    // if the graph is not linear, one heuristic elimination, else (e); repeat.
     for (;;) {
-      int r = auto_one(g);
+      int r = auto_one(g, kind == OFT_AUTO);
       if (r < 0) return r;
       if (r == 1) continue;
       if (kind == OFT_AUTO) break;
@@ -763,6 +952,9 @@ int oft_eliminate(oft_graph* g, int32_t kind, int32_t id, int32_t* out_edge) {
       if (chain_of(g, &ch, &ce) == OFT_OK) break;  // linear: LDP can run
       g->err.clear();
       r = heur_one(g);
+      if (r < 0) return r;
+      if (r == 1) continue;
+      r = compose_one(g);
       if (r < 0) return r;
       if (r == 0) break;
     }
@@ -821,9 +1013,9 @@ int oft_strategy(oft_graph* g, int64_t idx, int32_t* cfg_out) {
   std::vector<int32_t> cfg(g->n_ops, -1);
   int rc = visit(g, cfg, g->final_set, 0, idx);
   if (rc) return rc;
-  for (int i = 0; i < g->n_ops; ++i)
+  for (int i = 0; i < g->n_orig_ops; ++i)
     if (cfg[i] < 0) return fail(g, OFT_EINTERNAL, "broken provenance: op without config");
-  std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_ops);
+  std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_orig_ops);
   return OFT_OK;
 }
 

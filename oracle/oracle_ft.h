@@ -33,7 +33,9 @@ enum { OFT_OK = 0, OFT_EINVAL = -1, OFT_ESTATE = -2, OFT_EPRECOND = -3, OFT_ENOM
 enum { OFT_NODE = 1, OFT_EDGE = 2, OFT_AUTO = 3, OFT_AUTO_HEUR = 4 };
 /* step kinds reported by oft_step_info */
 enum { OFT_STEP_NODE = 1, OFT_STEP_EDGE = 2, OFT_STEP_FOLD = 3, OFT_STEP_LDP = 4,
-       OFT_STEP_FINAL = 5, OFT_STEP_PAIR = 6, OFT_STEP_BRANCH = 7 };
+       OFT_STEP_FINAL = 5, OFT_STEP_PAIR = 6, OFT_STEP_BRANCH = 7,
+       OFT_STEP_COMPOSE = 8 /* Eq. 6 composite configurations (R21) */,
+       OFT_STEP_REMAP = 9 /* an edge re-indexed onto a composite op (R21) */ };
 
 typedef struct oft_graph oft_graph;
 

@@ -499,6 +499,28 @@ def random_masked(seed: int, n_ops: int = 5, kmax: int = 3, mask_k: int = 2, fan
     return random_graph(len(K), edges, K, seed + 32452843, cost_hi=cost_hi, name=f"masked{seed}")
 
 
+def random_dag(seed: int, n_ops: int = 6, kmax: int = 3, p_edge: float = 0.4, cost_hi: int = 8,
+               edge_mem: bool = False) -> Workload:
+    """Small random DAG, in general NOT series-parallel (brute-force fixtures
+    for composite branch elimination, Eq. 6): ops 0..n-1 in topological id
+    order; every op v > 0 gets an input from a random u < v, every op
+    v < n-1 an output to a random later op, and every other pair u < v an
+    edge with probability ``p_edge``.  K ~ U{1..kmax}; costs U{0..cost_hi}."""
+    rng = np.random.default_rng(seed)
+    E = set()
+    for v in range(1, n_ops):
+        E.add((int(rng.integers(0, v)), v))
+    for u in range(n_ops - 1):
+        E.add((u, int(rng.integers(u + 1, n_ops))))
+    for u in range(n_ops):
+        for v in range(u + 1, n_ops):
+            if rng.random() < p_edge:
+                E.add((u, v))
+    K = [int(rng.integers(1, kmax + 1)) for _ in range(n_ops)]
+    return random_graph(n_ops, sorted(E), K, seed + 7919, cost_hi=cost_hi, edge_mem=edge_mem,
+                        name=f"dag-s{seed}")
+
+
 def random_sp(seed: int, n_ops: int = 6, kmax: int = 3, p_parallel: float = 0.35,
               p_mask: float = 0.3, cost_hi: int = 8, edge_mem: bool = False) -> Workload:
     """Small random two-terminal series-parallel DAG (brute-force fixtures).

@@ -38,9 +38,10 @@ def test_errors():
 
 
 def test_not_linear():
-    # the bridge DAG (non-series-parallel, every op of degree >= 2, K > 1):
-    # no node, edge, K=1-fold or branch elimination applies
-    w = G.random_graph(4, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], 2, 0)
+    # the bridge DAG (non-series-parallel, every op of degree >= 2) with K = 65:
+    # no node, edge, K=1-fold or leaf branch elimination applies, and a
+    # composite configuration space would exceed 4096 (R21) -> not linear
+    w = G.random_graph(4, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], 65, 0)
     g = oracle.load(w)
     g.eliminate()
     with pytest.raises(oracle.OracleError) as e:

@@ -58,3 +58,65 @@ def test_branch_sink_and_source_orientation():
     assert bf.check_frontier(m, t, ma, ta) == []
     for i in range(len(m)):
         assert bf.total_cost(w, g.strategy(i)) == (int(m[i]), int(t[i]))
+
+
+# ---- composite configurations (Eq. 6 with o_i keeping other edges, R21)
+
+BRIDGE = [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)]
+
+
+@pytest.mark.parametrize("K", [2, 3, [2, 3, 4, 2], [3, 4, 1, 2]])
+def test_bridge_dag_composite(K):
+    """The bridge DAG is not series-parallel: no node, edge, fold or leaf
+    branch elimination applies.  Merging o_1 into o_2 (composite configs
+    (s_2, s_1)) makes it a chain; the frontier equals brute force and every
+    unrolled strategy -- composites split back -- re-costs exactly."""
+    w = G.random_graph(4, BRIDGE, K, 3, cost_hi=40, edge_mem=True)
+    g, m, t, kinds = _run(w)
+    assert kinds.count("compose") == 1 and kinds.count("remap") == 4
+    ma, ta, _ = bf.enumerate_costs(w)
+    assert bf.check_frontier(m, t, ma, ta) == []
+    for i in range(len(m)):
+        assert bf.total_cost(w, g.strategy(i)) == (int(m[i]), int(t[i]))
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_dag_composite_brute_force(seed):
+    """Random (mostly non-series-parallel) DAGs: FT_AUTO with composite
+    branch elimination is exact -- Def. 1 against the enumeration, re-cost of
+    every strategy -- and FT-Elimination agrees with FT-LDP."""
+    w = G.random_dag(seed, n_ops=3 + seed % 6, kmax=3, p_edge=0.35, edge_mem=(seed % 4 == 0))
+    if int(np.prod([int(k) for k in w.n_cfgs], dtype=np.int64)) > 100_000:
+        pytest.skip("too many strategies for brute force")
+    g, m, t, kinds = _run(w)
+    ma, ta, _ = bf.enumerate_costs(w)
+    assert bf.check_frontier(m, t, ma, ta) == []
+    for i in range(len(m)):
+        assert bf.total_cost(w, g.strategy(i)) == (int(m[i]), int(t[i]))
+    _, m2, t2, _ = _run(w, algo="elim")
+    assert np.array_equal(m, m2) and np.array_equal(t, t2)
+
+
+def test_composite_used_on_most_random_dags():
+    used = 0
+    for seed in range(60):
+        w = G.random_dag(seed, n_ops=6, kmax=3, p_edge=0.35)
+        _, _, _, kinds = _run(w)
+        used += "compose" in kinds
+    assert used >= 20
+
+
+def test_composite_cap_and_cycle_guard():
+    """K_h * K_i > 4096 is refused (the graph stays non-linear: FT_EPRECOND);
+    an input o_i with another path to o_h is never merged into it (it would
+    close a cycle) -- here o_1 -> o_2 -> o_3 and o_1 -> o_3: o_2 is
+    node-eliminated first instead (series), so no composite is needed."""
+    w = G.random_graph(4, BRIDGE, 65, 0)
+    g = oracle.load(w)
+    g.eliminate()
+    with pytest.raises(oracle.OracleError):
+        g.frontier()
+    w = G.random_graph(4, [(0, 1), (1, 2), (2, 3), (1, 3), (0, 3)], 3, 1)
+    g, m, t, kinds = _run(w)
+    ma, ta, _ = bf.enumerate_costs(w)
+    assert bf.check_frontier(m, t, ma, ta) == []

@@ -56,15 +56,12 @@ def test_heuristic_restricted_brute_force(seed):
         pytest.skip("not linearisable by source heuristics")
     g, m, t = r
     mask = w.n_ops - 1
-    exact_only = oracle.load(w, 2)
-    exact_only.eliminate(oracle.AUTO)
-    try:  # FT_AUTO alone linearised it: no heuristic step, the result is exact
-        exact_only.frontier()
-        ma, ta, _ = bf.enumerate_costs(w)
-        assert bf.check_frontier(m, t, ma, ta) == []
+    # FT_AUTO_HEUR tries heuristic elimination before composite branch
+    # elimination (R17, R21): either the mask was fixed (then the result is
+    # exact on the restricted space) or no heuristic ran (then it is exact)
+    ma, ta, _ = bf.enumerate_costs(w)
+    if bf.check_frontier(m, t, ma, ta) == []:
         return
-    except oracle.OracleError:
-        pass
     om, ot = w.op_m[mask], w.op_t[mask]
     ks = min(range(len(om)), key=lambda k: (int(om[k]), int(ot[k]), k))
     wr = _restricted(w, mask, ks)

@@ -6,7 +6,7 @@ One "step" = one complete Frontier-Tracking search of the workload graph
 Alg. 2 of arXiv 2004.10856, with every step's Product / Union /
 Reduce in libft's sm_100a kernels.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5]
     python bench.py --impl reference ...      # CPU oracle arm (host cores)
 
 N > 1: launched by torchrun, one rank per GPU; each FT step's configuration
@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="C4", help="C1..C5 (BASELINE.json configs)")
+    ap.add_argument("--workload", default="C5", help="C1..C5 (BASELINE.json configs); default C5, the largest config (configs[4])")
     ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline budget")
@@ -179,8 +179,74 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 
+def spawn_ranks(args):
+    """--gpus N without a launcher: re-exec under torchrun, one rank per GPU
+    (the driver's own launch line), so the N-GPU path always runs."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def kernel_profile(workload):
+    """ncu counters of the dominant kernel for this workload (committed by
+    tools/ncu_round.sh -> profiles/r2_kernels.json): instructions and DRAM
+    bytes per search, per kernel."""
+    path = os.path.join(ROOT, "profiles", "r2_kernels.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    return d.get(workload)
+
+
+def roofline(dom_kernel, dom_ms, workload, tuples, ms_per_step, clocks, peaks):
+    """Roofline of the dominant kernel.  The FT path is integer compare/add
+    work on a PRUNED stream: k_filter proves most product tuples
+    dominated without touching DRAM, so its real bound is instruction issue /
+    latency, not HBM.  achieved = ncu-counted warp instructions of the kernel
+    per search (deterministic for a fixed workload; profiles/r2_kernels.json)
+    / its live CUDA-event time per search; peak = 148 SMs x 4 warp
+    instructions per clock (one issue per SMSP) x the SM clock measured under
+    load.  traffic = ncu DRAM bytes per search of that kernel.  The survey's
+    40 B/tuple materialised cost is reported separately, labelled."""
+    prof = kernel_profile(workload) or {}
+    k = prof.get("kernels", {}).get(dom_kernel)
+    sm_mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    peak = 148 * 4 * sm_mhz * 1e6 / 1e9  # G warp-instructions / s
+    achieved = traffic = None
+    src = None
+    if k and dom_ms > 0:
+        achieved = k["inst_per_search"] / (dom_ms / 1e3) / 1e9
+        traffic = k["dram_bytes_per_search"] / max(1, k["launches_per_search"])
+        src = (f"profiles/r2_kernels.json ({prof.get('source', 'ncu')}): {k['inst_per_search']:.4g} warp "
+               f"instructions, {k['dram_bytes_per_search'] / 1e6:.1f} MB DRAM over {k['launches_per_search']} "
+               f"launches per search; ncu sm__throughput {k.get('sm_throughput_pct', 0):.1f} %, "
+               f"issue active {k.get('issue_active_pct', 0):.1f} %")
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    mat = tuples * 40 / (ms_per_step / 1e3) / 1e9
+    return {"kernel": dom_kernel, "bound": "alu", "achieved": achieved, "peak": peak,
+            "unit": "G warp-instructions/s", "frac": achieved / peak if achieved else None,
+            "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, mean over the search)",
+            "source": src, "kernel_ms_per_step": dom_ms, "share_of_step": dom_ms / ms_per_step,
+            "peak_source": f"148 SM x 4 SMSP x 1 warp-inst/clk x {sm_mhz:.0f} MHz (clock under load)",
+            "materialised_equivalent": {
+                "bytes_per_tuple": 40, "GB_per_s": mat, "frac_of_hbm": mat / hbm, "hbm_peak_gbs": hbm,
+                "note": "SURVEY 8(d) expand->sort->scan->compact cost of the product tuples of one "
+                        "search / search time: what a materialising design would have to stream; "
+                        "not a DRAM utilisation"}}
+
+
+KERNEL_OF_GROUP = {"filter": "k_filter", "direct": "direct", "bucket": "bucket", "compact": "compact",
+                   "plan": "k_plan"}
+
+
 def main():
     args = parse()
+    if args.impl != "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     # exactly one JSON line on stdout: libraries (NCCL prints its version on
     # init) write to fd 1 too, so everything else goes to stderr
     out = os.fdopen(os.dup(1), "w")
@@ -195,6 +261,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dist = None
     comm = None
@@ -209,10 +278,11 @@ def main():
         comm = ft.nccl_comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()), local)
     w, cfg = workload_config(args.workload)
     cfg.update({"algo": ALGO[args.algo], "graphs_per_step": 1,
-                "parallelism": f"config-pair sharding x{world} + NCCL all-gather",
-                "l2_flush": not args.no_flush})
+                "parallelism": f"config-pair sharding x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                "l2_flush": "512 MiB memset between timed searches" if not args.no_flush else "none"})
     stream = torch.cuda.current_stream()
-    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm)
+    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm,
+              torch_alloc=True)
 
     def barrier():
         if dist is not None:
@@ -225,10 +295,17 @@ def main():
         if not args.no_flush:
             flush_buf.zero_()
 
-    def search(profile, keep=None):
+    def search(profile):
         g = ft.load(w, profile=profile, **kw)
         g.prepare()
         return g
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     # warm-up (module load, scratch growth, NCCL)
     for _ in range(args.warmup):
@@ -238,12 +315,13 @@ def main():
         g.close()
     torch.cuda.synchronize()
 
-    # timed region: inputs resident in HBM (ft_prepare before the events)
+    # timed region: inputs resident in HBM (ft_prepare before the events), no
+    # instrumentation (profile=0)
     clk = ClockSampler(local)
     clk.start()
-    ev_ms, stats_all, nfront = [], [], 0
+    ev_ms, nfront, st = [], 0, None
     for _ in range(args.steps):
-        g = search(True)
+        g = search(False)
         flush()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -255,24 +333,28 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ev_ms.append(e0.elapsed_time(e1))
-        stats_all.append(g.stats())
+        st = g.stats()
         nfront = len(m)
         g.close()
     clocks = clk.stop()
-    total_ms = sum(ev_ms)
-    st = stats_all[-1]
-    local_tuples = sum(s["tuples"] for s in st)
+    total_ms = max_over_ranks(sum(ev_ms))
+    # ft_step_stats.tuples counts every rank's segments (the per-segment
+    # counts are all-gathered with the survivors): the whole job's work
+    tuples = sum(s["tuples"] for s in st)
     launches = sum(s["launches"] for s in st)
-    groups = {k: sum(s[k + "_ms"] for s in st) for k in ("plan", "direct", "filter", "bucket", "compact")}
-    # ft_step_stats.tuples already counts every rank's segments (the per-segment
-    # counts are all-gathered with the survivors), so this is the whole job
-    tuples = local_tuples
-    if dist is not None:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
     value = tuples / (ms_per_step / 1e3)
+
+    # kernel-group split: one extra, instrumented search (CUDA events between
+    # kernel groups on the library stream), outside the timed region
+    flush()
+    barrier()
+    g = search(True)
+    g.eliminate()
+    g.frontier(algo=args.algo)
+    sp = g.stats()
+    g.close()
+    groups = {k: sum(s[k + "_ms"] for s in sp) for k in ("plan", "direct", "filter", "bucket", "compact")}
 
     # end-to-end through the public API with host buffers: the step's inputs
     # (concatenated Eq. 1 / Eq. 2 cost tables) sit in pinned host memory; the
@@ -304,57 +386,23 @@ def main():
         e2e_ms.append(e0.elapsed_time(e1))
         d2h = m.nbytes + t.nbytes
         g.close()
-    e2e_tot = sum(e2e_ms)
-    if dist is not None:
-        tt = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_tot = float(tt.item())
+    e2e_tot = max_over_ranks(sum(e2e_ms))
     e2e_value = tuples / (e2e_tot / args.steps / 1e3)
 
-    # roofline of the dominant kernel group on this rank
-    dom = max(groups, key=groups.get)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    cand = sum(s["candidates"] for s in st)
-    units = {"filter": (sum(s["filter_tuples"] for s in st), 40, "sampled product tuples streamed"),
-             "direct": (sum(s["direct_tuples"] for s in st), 40, "sampled product tuples sorted on chip"),
-             "bucket": (cand, 56, "pre-filter candidates sorted in place (24 B read + 24 B write + 8 B flag)"),
-             "compact": (cand, 24, "candidates scanned/compacted"),
-             "plan": (len(st), 0, "steps")}[dom]
-    n_units, bpu, what = units
-    # DRAM bytes of one launch of the dominant kernel from a committed ncu
-    # --set full capture (profiles/r1_traffic.json, tools/ncu_final.sh)
-    traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if dom == "filter" and os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        traffic = tj["traffic_bytes"]
-        traffic_src = (f"ncu --set full, {tj['launch']}: {tj['traffic_bytes']/1e6:.1f} MB DRAM in "
-                       f"{tj['duration_s']*1e3:.3f} ms; that wave streams {tj['wave_filter_tuples_all_levels']:.3e} "
-                       f"sampled tuples over all levels ({40 * tj['wave_filter_tuples_all_levels']/1e9:.1f} GB "
-                       f"at 40 B/tuple)")
-    gsec = groups[dom] / 1e3
-    achieved = n_units * bpu / gsec / 1e9 if gsec > 0 and bpu else None
-    roof = {"kernel": {"filter": "k_filter", "direct": "k_direct_warp+k_direct", "bucket":
-                       "k_bucket_small/large/huge+k_carry+k_scatter", "compact": "k_compact+scans",
-                       "plan": "k_plan"}[dom],
-            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
-            "traffic_source": traffic_src,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s",
-            "units_per_step": n_units, "bytes_per_unit": bpu, "unit_desc": what,
-            "kernel_ms_per_step": groups[dom], "share_of_step": groups[dom] / ms_per_step,
-            "yardstick": ("40 B/tuple = SURVEY 8(d) materialised expand->sort->scan->compact cost; the "
-                          "pruned kernel moves far fewer DRAM bytes (ncu traffic in profiles/), so "
-                          "frac > 1 means faster than that design's HBM ceiling")}
+    dom = max(groups, key=groups.get)
+    roof = roofline(KERNEL_OF_GROUP[dom], groups[dom], args.workload, tuples, ms_per_step, clocks, peaks)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": cfg, "search_ms": ms_per_step, "product_tuples_per_step": tuples,
+            "config": cfg, "search_ms": ms_per_step,
+            "search_ms_steps": [round(x, 3) for x in ev_ms], "product_tuples_per_step": tuples,
             "frontier_size": nfront, "ft_steps": len(st), "gpu_launches": launches * args.steps,
+            "waves": 1 + max(s["wave"] for s in st),
             "kernel_group_ms": {k: round(v, 3) for k, v in groups.items()},
+            "kernel_group_source": "one instrumented search after the timed region (profile=1)",
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot / args.steps,
                     "ms_steps": [round(x, 2) for x in e2e_ms]},
@@ -365,8 +413,13 @@ def main():
         tp, dt, _ = oracle_run(sw, threads, args.algo)
         line["cpu_baseline"] = {"value": tp / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "sample": sample + f"; {tp} product tuples in {dt:.2f} s"}
+        full = os.path.join(ROOT, "profiles", "r2_oracle_timing.json")
+        if os.path.exists(full):
+            line["cpu_baseline"]["full_protocol"] = {
+                "source": "profiles/r2_oracle_timing.json (tools/oracle_timing.py on a GPU-box host)",
+                "runs": json.load(open(full)).get("runs")}
     if args.details and rank == 0:
-        for s in st:
+        for s in sp:
             print(json.dumps(s), file=sys.stderr)
     if rank == 0:
         print_line(line)

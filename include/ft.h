@@ -25,7 +25,8 @@
  *  - Ownership: input arrays are copied before the call returns; output
  *    buffers are caller-allocated HOST memory; sizes use the two-call pattern
  *    (a too-small buffer returns FT_ESIZE with *n_out = required count).
- *    The handle owns all device memory.
+ *    The handle owns all device memory, allocated through ft_options.alloc /
+ *    .free when given (else cudaMallocAsync on the handle's stream).
  *  - Strong guarantee: on any error except FT_ECUDA / FT_EINTERNAL the graph
  *    is unchanged.  FT_ECUDA / FT_EINTERNAL poison the handle (every later
  *    call returns the same code).
@@ -62,9 +63,20 @@ enum { FT_NODE = 1, FT_EDGE = 2, FT_AUTO = 3, FT_AUTO_HEUR = 4 };
 /* Step kinds in ft_step_stats records. */
 enum { FT_STEP_NODE = 1, FT_STEP_EDGE = 2, FT_STEP_FOLD = 3, FT_STEP_LDP = 4, FT_STEP_FINAL = 5,
        FT_STEP_PAIR = 6 /* FT-Elimination's reduce over configuration pairs */,
-       FT_STEP_BRANCH = 7 /* branch elimination, Eq. 6 (merge a one-edge op into its neighbour) */ };
+       FT_STEP_BRANCH = 7 /* branch elimination, Eq. 6 (merge a one-edge op into its neighbour) */,
+       FT_STEP_COMPOSE = 8 /* branch elimination with composite configurations, Eq. 6 (R21) */,
+       FT_STEP_REMAP = 9 /* an edge re-indexed onto a composite operator (R21) */ };
 
 typedef struct ft_graph ft_graph; /* opaque, library-owned */
+
+/* Device-memory hooks (ft_options.alloc / .free, e.g. a
+ * framework's caching allocator).  alloc returns `bytes` of device memory on
+ * the graph's device, usable by work on `stream` (NULL = out of memory ->
+ * FT_ENOMEM); free is stream-ordered: work enqueued on `stream` before the
+ * call may still read p.  The library calls them with the device current,
+ * from the thread that called into it; `ctx` is passed through. */
+typedef void* (*ft_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*ft_free_fn)(void* p, void* stream, void* ctx);
 
 /* All fields optional; a zeroed struct (or NULL) selects defaults. */
 typedef struct {
@@ -76,7 +88,14 @@ typedef struct {
   int32_t profile;     /* != 0: CUDA events between kernel groups (ft_step_stats *_ms) */
   int32_t loopback;    /* != 0 with world > 1 and nccl_comm == NULL: every virtual rank's
                           shard runs in this process on one GPU (partition-invariance tests) */
-  int32_t reserved[5];
+  ft_alloc_fn alloc;   /* both NULL: cudaMallocAsync / cudaFreeAsync (stream-ordered pool) and a */
+  ft_free_fn free;     /*   process-wide per-device scratch; both set: EVERY device allocation of */
+  void* alloc_ctx;     /*   the handle, and the pipeline scratch shared by all live handles with the
+                            same (alloc, free, ctx) on the device, goes through them; everything is
+                            handed back by the time the last such handle is destroyed.  Exactly one
+                            of the two set: FT_EINVAL.  A NULL from alloc: FT_ENOMEM, and the handle
+                            is poisoned if the failure interrupted a search. */
+  int32_t reserved[4];
 } ft_options;
 
 /* Per-step statistics (ft_get_stats). */
@@ -99,7 +118,9 @@ typedef struct {
   int64_t direct_tuples; /* wave: sampled tuples sorted by the direct kernels (this rank) */
   float kernel_ms;       /* CUDA-event time of the step's kernels on this rank */
   float comm_ms;         /* all-gather time (world > 1) */
-  float plan_ms, direct_ms, filter_ms, bucket_ms, compact_ms; /* opt.profile only */
+  float plan_ms, direct_ms, filter_ms, bucket_ms, compact_ms; /* opt.profile only: k_plan; direct
+                            kernels (k_direct*, k_node_*); k_filter alone; bucket sorts + carry +
+                            scatter; scans and compaction */
   float host_ms;         /* opt.profile only: host readback + scratch sizing inside the step */
   int64_t path[4];       /* wave: kernel-path counters (this rank) -- shared-order node rows
                             reduced by the packed kernel, ... of them with equal m values,
@@ -146,14 +167,20 @@ int ft_set_edge_costs(ft_graph* g, int32_t edge, const int64_t* m, const int64_t
  *  FT_AUTO: id ignored; the deterministic policy of DESIGN.md R9 until no
  *           exact elimination applies: parallel edges (Eq. 5), node
  *           elimination (Eq. 4), the K=1 source fold (Eq. 7, exact for
- *           K=1), then branch elimination (Eq. 6: an unmarked op whose only
+ *           K=1), branch elimination (Eq. 6: an unmarked op whose only
  *           edge joins it to o_h is merged into o_h, reducing over its
- *           configurations -- reading R14).
- *  FT_AUTO_HEUR: FT_AUTO, then, while the graph is not linear and no exact
- *           elimination applies, one heuristic elimination (Eq. 7,
- *           P:618-622; lossy): the unmarked source op with the most
- *           out-edges is fixed to its least-memory configuration (ties:
- *           time, index) and folded into its consumers.
+ *           configurations -- reading R14), then branch elimination with
+ *           composite configurations (Eq. 6, R21: an unmarked input o_i of
+ *           an op o_h with >= 2 inputs, K_h*K_i <= 4096, becomes part of a
+ *           new operator o_v = (o_h, o_i) with K_h*K_i configurations; new
+ *           operator ids are n_ops, n_ops+1, ... in creation order; the
+ *           edges of o_h and o_i move to o_v).
+ *  FT_AUTO_HEUR: FT_AUTO without the composite step, then, while the graph
+ *           is not linear: one heuristic elimination (Eq. 7, P:618-622;
+ *           lossy) -- the unmarked source op with the most out-edges is
+ *           fixed to its least-memory configuration (ties: time, index) and
+ *           folded into its consumers -- or, if there is no such source, one
+ *           composite branch elimination; repeat.
  * New edge ids are n_edges, n_edges+1, ... in creation order (*new_edge,
  * nullable).  Errors: FT_EINVAL, FT_ESTATE, FT_EPRECOND, FT_ENOMEM, FT_ECUDA. */
 int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge);

@@ -27,7 +27,8 @@ LIB_PATH = os.path.join(_HERE, "libft.so")
 
 OK, EINVAL, ESTATE, EPRECOND, ENOMEM, ECUDA, EOVERFLOW, ESIZE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8
 NODE, EDGE, AUTO, AUTO_HEUR = 1, 2, 3, 4
-STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch"}
+STEP_KINDS = {1: "node", 2: "edge", 3: "fold", 4: "ldp", 5: "final", 6: "pair", 7: "branch", 8: "compose",
+              9: "remap"}
 
 
 class FTError(RuntimeError):
@@ -36,10 +37,15 @@ class FTError(RuntimeError):
         self.code = code
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
 class ft_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_comm", C.c_void_p), ("keep_all", C.c_int32),
-                ("profile", C.c_int32), ("loopback", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("profile", C.c_int32), ("loopback", C.c_int32), ("alloc", C.c_void_p),
+                ("free", C.c_void_p), ("alloc_ctx", C.c_void_p), ("reserved", C.c_int32 * 4)]
 
 
 class ft_step_stats(C.Structure):
@@ -107,6 +113,23 @@ def _load():
 
 
 lib = _load()
+TORCH_ALLOC_PATH = os.path.join(_HERE, "libft_torch_alloc.so")
+_torch_alloc = None
+
+
+def torch_allocator():
+    """(alloc, free) C function pointers backed by torch's CUDA caching
+    allocator (libft_torch_alloc.so, csrc/ft_torch_alloc.cpp) for
+    ft_options.alloc / .free: no Python on the allocation path."""
+    global _torch_alloc
+    if _torch_alloc is None:
+        import torch  # noqa: F401  (libc10_cuda must be loaded and initialised)
+        torch.cuda.init()
+        if not os.path.exists(TORCH_ALLOC_PATH):
+            raise ImportError(f"{TORCH_ALLOC_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(TORCH_ALLOC_PATH)
+        _torch_alloc = (L, C.cast(L.ft_torch_alloc, C.c_void_p).value, C.cast(L.ft_torch_free, C.c_void_p).value)
+    return _torch_alloc[1], _torch_alloc[2]
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
            "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
@@ -131,7 +154,10 @@ def shard_plan(weights, world: int) -> np.ndarray:
 class Graph:
     def __init__(self, n_cfgs, src, dst, device: int = 0, stream=None, rank: int = 0,
                  world: int = 1, nccl_comm=None, keep_all: bool = False, profile: bool = False,
-                 loopback: bool = False):
+                 loopback: bool = False, torch_alloc: bool = False, alloc=None):
+        """alloc: optional (alloc_fn, free_fn[, ctx]) raw C function pointers
+        (ints) for ft_options.alloc / .free; torch_alloc=True uses torch's
+        caching allocator (torch_allocator())."""
         K = np.ascontiguousarray(n_cfgs, dtype=np.int32)
         s = np.ascontiguousarray(src, dtype=np.int32)
         d = np.ascontiguousarray(dst, dtype=np.int32)
@@ -145,6 +171,12 @@ class Graph:
         opt.keep_all = 1 if keep_all else 0
         opt.profile = 1 if profile else 0
         opt.loopback = 1 if loopback else 0
+        if torch_alloc and alloc is None:
+            alloc = torch_allocator()
+        if alloc is not None:
+            opt.alloc = alloc[0]
+            opt.free = alloc[1]
+            opt.alloc_ctx = alloc[2] if len(alloc) > 2 else None
         h = C.c_void_p()
         rc = lib.ft_graph_create(self.n_ops, _p(K, C.c_int32), len(s), _p(s, C.c_int32),
                                  _p(d, C.c_int32), C.byref(opt), C.byref(h))
@@ -251,8 +283,8 @@ class Graph:
         rc = lib.ft_step_output(self.h, step, 0, None, None, None, None, C.byref(n))
         if rc not in (OK, ESIZE):
             self._chk(rc)
-        st = self.stats()[step]
-        so = np.empty(st["nseg"] + 1, np.int64)
+        _, par = self.step_inputs(step)  # params {kind, KA, KB, KC, nseg, nblk}
+        so = np.empty(int(par[4]) + 1, np.int64)
         m = np.empty(n.value, np.int64) if with_mt else None
         t = np.empty(n.value, np.int64) if with_mt else None
         bp = np.empty(n.value, np.uint64)
@@ -362,7 +394,11 @@ def reschedule_costs(prof, ndims, dims, elem_bytes, q_tensor, q_from, q_to) -> n
     nd = np.ascontiguousarray(ndims, np.int32)
     dm = np.ascontiguousarray(dims, np.int64).reshape(nd.size, CG_MAX_DIMS)
     eb = np.ascontiguousarray(elem_bytes, np.int64)
-    qt, qf, qo = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_from, q_to))
+    qt, qf, qo = (np.ascontiguousarray(a, np.int32).ravel() for a in (q_tensor, q_from, q_to))
+    if not qt.size == qf.size == qo.size:
+        raise ValueError(f"query arrays differ in length: {qt.size}, {qf.size}, {qo.size}")
+    if dm.shape[0] != eb.size:
+        raise ValueError("dims / elem_bytes do not match ndims")
     out = np.zeros(qt.size, np.int64)
     p = prof if isinstance(prof, ft_comm_profile) else comm_profile(prof)
     _cg_check(lib.ft_reschedule_costs(C.byref(p), nd.size, _p(nd, C.c_int32), _p(dm, C.c_int64),
@@ -392,7 +428,11 @@ def sync_costs(prof, ndims, dims, elem_bytes, q_tensor, q_state):
     nd = np.ascontiguousarray(ndims, np.int32)
     dm = np.ascontiguousarray(dims, np.int64).reshape(nd.size, CG_MAX_DIMS)
     eb = np.ascontiguousarray(elem_bytes, np.int64)
-    qt, qs = (np.ascontiguousarray(a, np.int32) for a in (q_tensor, q_state))
+    qt, qs = (np.ascontiguousarray(a, np.int32).ravel() for a in (q_tensor, q_state))
+    if qt.size != qs.size:
+        raise ValueError(f"query arrays differ in length: {qt.size}, {qs.size}")
+    if dm.shape[0] != eb.size:
+        raise ValueError("dims / elem_bytes do not match ndims")
     m = np.zeros(qt.size, np.int64)
     t = np.zeros(qt.size, np.int64)
     p = prof if isinstance(prof, ft_comm_profile) else comm_profile(prof)

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libft.so")
+TORCH_ALLOC_LIB = os.path.join(HERE, "libft_torch_alloc.so")
 SOURCES = ["ft_step.cu", "ft_api.cu", "ft_costgen.cu"]
 HEADERS = ["ft_kernels.cuh", "ft_step.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -50,7 +51,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    build_torch_alloc(force=True)
     return LIB
+
+
+def build_torch_alloc(force: bool = False) -> str:
+    """libft_torch_alloc.so: ft_options.alloc/.free backed by torch's CUDA
+    caching allocator (csrc/ft_torch_alloc.cpp; links libc10_cuda)."""
+    src = os.path.join(CSRC, "ft_torch_alloc.cpp")
+    if not force and os.path.exists(TORCH_ALLOC_LIB) and os.path.getmtime(TORCH_ALLOC_LIB) >= os.path.getmtime(src):
+        return TORCH_ALLOC_LIB
+    import torch
+    tdir = os.path.dirname(torch.__file__)
+    cuda_inc = os.path.join(os.path.dirname(os.path.dirname(nvcc())) if nvcc() != "nvcc" else "/usr/local/cuda",
+                            "include")
+    cmd = ["g++", "-std=c++17", "-O2", "-shared", "-fPIC", f"-I{os.path.join(tdir, 'include')}",
+           f"-I{cuda_inc}", "-o", TORCH_ALLOC_LIB, src, f"-L{os.path.join(tdir, 'lib')}", "-lc10_cuda",
+           "-lc10", f"-Wl,-rpath,{os.path.join(tdir, 'lib')}"]
+    subprocess.check_call(cmd)
+    return TORCH_ALLOC_LIB
 
 
 if __name__ == "__main__":

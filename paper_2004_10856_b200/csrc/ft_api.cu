@@ -81,8 +81,9 @@ struct ft_graph {
   std::vector<int> set_edge;   // original edge index of each original edge set (-1 otherwise)
   ncclComm_t comm = nullptr;
   bool keep_all = false;
-  int n_ops = 0, n_orig_edges = 0;
-  std::vector<int> K;
+  int n_ops = 0, n_orig_edges = 0;  // of the input graph; composite ops (R21) get ids n_ops, n_ops+1, ...
+  std::vector<int> K;                // per op (original and composite)
+  std::vector<std::pair<int, int>> comp;  // composite op (R21): (o_h, o_i), config w = s_h * K_i + s_i
   std::vector<char> op_alive;
   std::vector<int> op_set;
   std::vector<EdgeRec> edges;
@@ -111,7 +112,8 @@ struct ft_graph {
   std::vector<int64_t> final_m, final_t;
   int poisoned = 0;
   std::string err;
-  ftk::StepRunner* runner = nullptr;  // process-wide per device
+  ftk::StepRunner* runner = nullptr;  // process-wide per (device, allocator)
+  ftk::DevAlloc alloc;                // ft_options.alloc / .free, else cudaMallocAsync
   bool profile = false;
   int64_t* d_costs = nullptr;  // all original costs + iota offsets + unit (alloc_costs)
   std::vector<int64_t> op_off, e_off;  // concatenation offsets of op / edge costs
@@ -135,29 +137,51 @@ double now_ms() {
 
 namespace ftk {
 static std::mutex g_reg_mu;
-static std::map<int, StepRunner*> g_runners;
-static std::map<int, std::mutex*> g_mutexes;
-StepRunner* device_runner(int device) {
+static std::map<std::pair<int, DevAlloc>, StepRunner*> g_runners;
+StepRunner* device_runner(int device, const DevAlloc& a) {
   std::lock_guard<std::mutex> l(g_reg_mu);
-  auto it = g_runners.find(device);
-  if (it != g_runners.end()) return it->second;
+  const auto key = std::make_pair(device, a);
+  auto it = g_runners.find(key);
+  if (it != g_runners.end()) {
+    it->second->users++;
+    return it->second;
+  }
   StepRunner* r = new (std::nothrow) StepRunner();
   if (!r) return nullptr;
+  r->alloc = a;
   if (cudaSetDevice(device) != cudaSuccess || r->configure() != cudaSuccess) {
     delete r;
     return nullptr;
   }
-  g_runners[device] = r;
-  g_mutexes[device] = new std::mutex();
+  r->users = 1;
+  g_runners[key] = r;
   return r;
 }
-std::mutex& runner_mutex(int device) {
+void release_runner(int device, const DevAlloc& a) {
   std::lock_guard<std::mutex> l(g_reg_mu);
-  return *g_mutexes[device];
+  auto it = g_runners.find(std::make_pair(device, a));
+  if (it == g_runners.end() || --it->second->users > 0 || !a.hooked()) return;
+  it->second->release_device();  // scratch back through the hooks (host buffers stay)
 }
 }  // namespace ftk
 
 namespace {
+
+// Stream-ordered temporaries of one call, handed back on scope exit (also on
+// an error return).
+struct Temps {
+  const ftk::DevAlloc& A;
+  cudaStream_t st;
+  std::vector<void*> p;
+  ~Temps() {
+    for (void* q : p) A.put(q, st);
+  }
+  cudaError_t get(int64_t** out, size_t bytes) {
+    const cudaError_t e = A.get((void**)out, bytes, st);
+    if (e == cudaSuccess) p.push_back(*out);
+    return e;
+  }
+};
 
 int setf(ft_graph* g, int code, const std::string& m) {
   if (g) g->err = m;
@@ -165,9 +189,12 @@ int setf(ft_graph* g, int code, const std::string& m) {
 }
 
 int cuda_fail(ft_graph* g, cudaError_t e, const char* where) {
-  g->poisoned = FT_ECUDA;
+  // device memory exhausted (the allocator hook returned NULL, or the pool
+  // is empty) -> FT_ENOMEM; either poisons the handle (a wave was cut short)
+  const int code = e == cudaErrorMemoryAllocation ? FT_ENOMEM : FT_ECUDA;
+  g->poisoned = code;
   g->err = std::string(where) + ": " + cudaGetErrorString(e);
-  return FT_ECUDA;
+  return code;
 }
 
 #define CU(call, where)                                  \
@@ -299,7 +326,7 @@ int alloc_costs(ft_graph* g) {
   CU(cudaSetDevice(g->dev), "cudaSetDevice");
   // stream-ordered pool (release threshold: unlimited) -- a plain
   // cudaMalloc/cudaFree per graph showed ~100 ms driver stalls
-  CU(cudaMallocAsync((void**)&g->d_costs, sizeof(int64_t) * total, g->stream), "cudaMallocAsync(costs)");
+  CU(g->alloc.get((void**)&g->d_costs, sizeof(int64_t) * total, g->stream), "cudaMallocAsync(costs)");
   std::vector<int64_t> head(maxseg + 3);
   for (int64_t i = 0; i <= maxseg; ++i) head[i] = i;
   head[maxseg + 1] = 0;
@@ -371,8 +398,8 @@ void consume(ft_graph* g, int set) {
   s.mt_live = false;
   WaveBuf& w = g->waves[s.wave_buf];
   if (--w.live == 0 && !g->keep_all) {
-    cudaFreeAsync(w.m, g->stream);
-    cudaFreeAsync(w.t, g->stream);
+    g->alloc.put(w.m, g->stream);
+    g->alloc.put(w.t, g->stream);
     w.m = w.t = nullptr;
   }
 }
@@ -394,6 +421,16 @@ void host_block_segs(const StepRec& r, int64_t sg, int64_t k, int64_t& sx, int64
     sx = sg; sy = r.KC ? k * r.KA + sg : sg * r.KB + k; sz = k;
   } else if (r.kind == ftk::K_FOLD) {
     sx = sg; sy = r.KB * r.KA + sg; sz = r.KC;
+  } else if (r.kind == ftk::K_COMPOSE) {
+    const int64_t p = sg / r.KB, q = sg % r.KB;
+    sx = p; sy = q * r.KA + p; sz = q;
+  } else if (r.kind == ftk::K_REMAP) {
+    const int64_t Kv = r.nseg / r.KA, side = r.KC & 1, part = r.KC >> 1;
+    const int64_t Kold = part ? r.KB : Kv / r.KB;
+    const int64_t w = side == 0 ? sg / r.KA : sg % Kv, y = side == 0 ? sg % r.KA : sg / Kv;
+    const int64_t c = part ? w % r.KB : w / r.KB;
+    sx = side == 0 ? c * r.KA + y : y * Kold + c;
+    sy = 0; sz = 0;
   } else {
     sx = sg; sy = sg; sz = 0;
   }
@@ -548,7 +585,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   // counts are all-gathered on the device, every rank scans them into the
   // same arena offsets, gathers its own contiguous arena range and broadcasts it.
   if (world > 1 && !g->loopback) {
-    std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
+    std::lock_guard<std::mutex> lock(g->runner->mu);
     g->runner->profile = g->profile;
     std::vector<ftk::StepDev> sd = make_sd(lo[rank], lo[rank + 1]);
     const std::vector<ftk::NodeGroupH> grp = make_groups(sd);
@@ -556,24 +593,29 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     const double h1 = now_ms();
     cudaError_t ce = g->runner->run(sd, g->stream, &res, nullptr, &grp, true);
     if (ce == cudaErrorInvalidConfiguration)
-      return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
+      return setf(g, FT_EOVERFLOW, "step shape unsupported (a segment sample did not shrink to the direct path within the level plan)");
     if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
     const double h2 = now_ms();
     cudaEvent_t ca, cb;
     cudaEventCreate(&ca);
     cudaEventCreate(&cb);
     cudaEventRecord(ca, g->stream);
-    WaveBuf wb;
+    // the wave arena is registered before its buffers are allocated, so a
+    // failure part-way leaves nothing unowned (ft_graph_destroy frees it)
+    const int wi = (int)g->waves.size();
+    g->waves.emplace_back();
+    WaveBuf& wb = g->waves.back();
     int64_t *cntg = nullptr, *tupg = nullptr, *pos = nullptr, *sb = nullptr, *stats = nullptr,
             *tmp = nullptr;
+    Temps tmps{g->alloc, g->stream};
     const int64_t nloc = lo[rank + 1] - lo[rank];
-    CU(cudaMallocAsync((void**)&cntg, sizeof(int64_t) * std::max<int64_t>(NS, 1), g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&tupg, sizeof(int64_t) * std::max<int64_t>(NS, 1), g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&pos, sizeof(int64_t) * (NS + 1), g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&sb, sizeof(int64_t) * (ns + 1), g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&stats, sizeof(int64_t) * 3 * ns, g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&tmp, sizeof(int64_t) * ftk::scan_tmp_elems(NS + 1), g->stream), "alloc");
-    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+    CU(tmps.get(&cntg, sizeof(int64_t) * std::max<int64_t>(NS, 1)), "alloc");
+    CU(tmps.get(&tupg, sizeof(int64_t) * std::max<int64_t>(NS, 1)), "alloc");
+    CU(tmps.get(&pos, sizeof(int64_t) * (NS + 1)), "alloc");
+    CU(tmps.get(&sb, sizeof(int64_t) * (ns + 1)), "alloc");
+    CU(tmps.get(&stats, sizeof(int64_t) * 3 * ns), "alloc");
+    CU(tmps.get(&tmp, sizeof(int64_t) * ftk::scan_tmp_elems(NS + 1)), "alloc");
+    CU(g->alloc.get((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
     if (nloc > 0) {
       CU(cudaMemcpyAsync(cntg + lo[rank], res.dev_cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice,
                          g->stream), "counts");
@@ -600,9 +642,9 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     for (int q = 0; q < ns; ++q) sbeg[q + 1] = sbeg[q] + hstat[3 * q];
     const int64_t total = sbeg[ns];
     const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
-    CU(cudaMallocAsync((void**)&wb.m, nb, g->stream), "alloc frontier");
-    CU(cudaMallocAsync((void**)&wb.t, nb, g->stream), "alloc frontier");
-    CU(cudaMallocAsync((void**)&wb.bp, nb, g->stream), "alloc frontier");
+    CU(g->alloc.get((void**)&wb.m, nb, g->stream), "alloc frontier");
+    CU(g->alloc.get((void**)&wb.t, nb, g->stream), "alloc frontier");
+    CU(g->alloc.get((void**)&wb.bp, nb, g->stream), "alloc frontier");
     CU(ftk::gather_range(res.pool, pos, lo[rank], lo[rank + 1], posb[rank + 1] - posb[rank], wb.m, wb.t,
                          wb.bp, g->stream), "gather");
     nr = ncclGroupStart();
@@ -616,16 +658,13 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     if (nr == ncclSuccess) nr = ncclGroupEnd();
     if (nr != ncclSuccess) return nccl_fail(g, nr);
     cudaEventRecord(cb, g->stream);
-    for (int64_t* p : {cntg, tupg, pos, sb, stats, tmp}) cudaFreeAsync(p, g->stream);
     CU(cudaStreamSynchronize(g->stream), "wave sync");
     float comm_ms = 0;
     cudaEventElapsedTime(&comm_ms, ca, cb);
     cudaEventDestroy(ca);
     cudaEventDestroy(cb);
     const double h4 = now_ms();
-    const int wi = (int)g->waves.size();
     wb.live = ns;
-    g->waves.push_back(wb);
     for (int q = 0; q < ns; ++q) {
       StepRec& r = g->steps[ids[q]];
       FSet& o = g->sets[r.out];
@@ -674,7 +713,8 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     g->hp[4] += now_ms() - h4;
     return FT_OK;
   }
-  // real ranks run their own range; loopback runs every virtual rank here
+  // Single rank, a replicated wave (every rank computes all of it: no
+  // collective), or loopback (every virtual rank's shard runs here).
   std::vector<int> vr;
   if (g->loopback)
     for (int q = 0; q < g->world; ++q) vr.push_back(q);
@@ -682,13 +722,15 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     vr.push_back(rank);
   ftk::StepResult res, agg;
   const double h1 = now_ms();
-  std::lock_guard<std::mutex> lock(ftk::runner_mutex(g->dev));
+  std::lock_guard<std::mutex> lock(g->runner->mu);
   g->runner->profile = g->profile;
   // single rank (or replicated wave): offsets computed on the device straight into the arena
   const bool devoff = world == 1 && !g->loopback;
-  WaveBuf wb;
+  const int wi = (int)g->waves.size();
+  g->waves.emplace_back();  // registered first: see the multi-rank branch
+  WaveBuf& wb = g->waves.back();
   if (devoff)
-    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+    CU(g->alloc.get((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
   std::vector<int64_t> cnt(devoff ? 0 : NS, 0), tup(devoff ? 0 : NS, 0);
   std::vector<int64_t> stot(ns, 0), smax(ns, 0), stup(ns, 0);
   std::vector<ftk::StepDev> sd;
@@ -698,7 +740,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     const std::vector<ftk::NodeGroupH> grp = make_groups(sd);
     cudaError_t ce = g->runner->run(sd, g->stream, &res, devoff ? wb.off : nullptr, &grp);
     if (ce == cudaErrorInvalidConfiguration)
-      return setf(g, FT_EOVERFLOW, "step shape unsupported (more than 1024 union terms per segment)");
+      return setf(g, FT_EOVERFLOW, "step shape unsupported (a segment sample did not shrink to the direct path within the level plan)");
     if (ce != cudaSuccess) return cuda_fail(g, ce, "step pipeline");
     if (devoff) {
       for (int q = 0; q < ns; ++q) {
@@ -727,36 +769,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     agg.compact_ms += res.compact_ms;
     agg.host_ms += res.host_ms;
   }
-  float comm_ms = 0;
   const double h2 = now_ms();
-  cudaEvent_t ca = nullptr, cb = nullptr;
-  if (world > 1 && !g->loopback) {
-    cudaEventCreate(&ca);
-    cudaEventCreate(&cb);
-    cudaEventRecord(ca, g->stream);
-    int64_t* dc = nullptr;
-    CU(cudaMallocAsync((void**)&dc, sizeof(int64_t) * 2 * NS, g->stream), "alloc counts");
-    std::vector<int64_t> both(2 * NS);
-    for (int64_t i = 0; i < NS; ++i) {
-      both[2 * i] = cnt[i];
-      both[2 * i + 1] = tup[i];
-    }
-    CU(cudaMemcpyAsync(dc, both.data(), sizeof(int64_t) * 2 * NS, cudaMemcpyHostToDevice, g->stream), "counts");
-    ncclResult_t nr = ncclGroupStart();
-    for (int q = 0; q < world && nr == ncclSuccess; ++q)
-      if (lo[q + 1] > lo[q])
-        nr = ncclBroadcast(dc + 2 * lo[q], dc + 2 * lo[q], 2 * (lo[q + 1] - lo[q]), ncclInt64, q,
-                           g->comm, g->stream);
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
-    if (nr != ncclSuccess) return nccl_fail(g, nr);
-    CU(cudaMemcpyAsync(both.data(), dc, sizeof(int64_t) * 2 * NS, cudaMemcpyDeviceToHost, g->stream), "counts");
-    CU(cudaFreeAsync(dc, g->stream), "free");
-    CU(cudaStreamSynchronize(g->stream), "counts");
-    for (int64_t i = 0; i < NS; ++i) {
-      cnt[i] = both[2 * i];
-      tup[i] = both[2 * i + 1];
-    }
-  }
   // wave arena: step-major CSR
   std::vector<int64_t> hoff(devoff ? 0 : NS + ns, 0);  // per step: nseg+1 offsets (relative)
   std::vector<int64_t> sbeg(ns + 1, 0);                // survivor start of each step in the arena
@@ -777,11 +790,11 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
   }
   const int64_t total = sbeg[ns];
   const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
-  CU(cudaMallocAsync((void**)&wb.m, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&wb.t, nb, g->stream), "alloc frontier");
-  CU(cudaMallocAsync((void**)&wb.bp, nb, g->stream), "alloc frontier");
+  CU(g->alloc.get((void**)&wb.m, nb, g->stream), "alloc frontier");
+  CU(g->alloc.get((void**)&wb.t, nb, g->stream), "alloc frontier");
+  CU(g->alloc.get((void**)&wb.bp, nb, g->stream), "alloc frontier");
   if (!devoff) {
-    CU(cudaMallocAsync((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
+    CU(g->alloc.get((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
     CU(cudaMemcpyAsync(wb.off, hoff.data(), sizeof(int64_t) * (NS + ns), cudaMemcpyHostToDevice,
                        g->stream), "upload seg_off");
   }
@@ -805,36 +818,10 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     set_out(sv);
     CU(g->runner->gather(sv, res, g->stream), "gather");
   }
-  if (world > 1 && !g->loopback) {
-    // all-gather-v of survivors: rank q owns arena range [A(lo[q]), A(lo[q+1]))
-    auto arena_pos = [&](int64_t gseg) -> int64_t {  // arena offset of global segment gseg
-      int q = (int)(std::upper_bound(sbase.begin(), sbase.end(), gseg) - sbase.begin()) - 1;
-      if (q >= ns) return total;
-      return sbeg[q] + hoff[sbase[q] + q + (gseg - sbase[q])];
-    };
-    ncclResult_t nr = ncclGroupStart();
-    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
-      const int64_t a0 = arena_pos(lo[q]), a1 = arena_pos(lo[q + 1]);
-      if (a1 <= a0) continue;
-      nr = ncclBroadcast(wb.m + a0, wb.m + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(wb.t + a0, wb.t + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(wb.bp + a0, wb.bp + a0, a1 - a0, ncclUint64, q, g->comm, g->stream);
-    }
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
-    if (nr != ncclSuccess) return nccl_fail(g, nr);
-    cudaEventRecord(cb, g->stream);
-  }
   CU(cudaStreamSynchronize(g->stream), "wave sync");
   const double h4 = now_ms();
-  if (world > 1 && !g->loopback) {
-    cudaEventElapsedTime(&comm_ms, ca, cb);
-    cudaEventDestroy(ca);
-    cudaEventDestroy(cb);
-  }
   // bookkeeping: sets, stats, consumption
-  const int wi = (int)g->waves.size();
   wb.live = ns;
-  g->waves.push_back(wb);
   for (int q = 0; q < ns; ++q) {
     StepRec& r = g->steps[ids[q]];
     FSet& o = g->sets[r.out];
@@ -866,7 +853,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       st.direct_tuples = agg.direct_tuples;
       for (int u = 0; u < 4; ++u) st.path[u] = agg.path[u];
       st.kernel_ms = agg.kernel_ms;
-      st.comm_ms = comm_ms;
+      st.comm_ms = 0;  // no collective: one rank, a replicated wave, or loopback
       st.launches = agg.launches + (int64_t)vr.size();
       st.plan_ms = agg.plan_ms;
       st.direct_ms = agg.direct_ms;
@@ -1035,8 +1022,160 @@ int do_branch(ft_graph* g, int i) {
   return FT_OK;
 }
 
+// Re-derives the live graph's topological order after a composite merge
+// (R21): Kahn's algorithm, ready ops by (previous position, id); the
+// position-keyed candidate sets are rebuilt.
+void reorder(ft_graph* g) {
+  const int n = (int)g->K.size();
+  std::vector<int> indeg(n, 0);
+  std::set<std::pair<int, int>> ready;
+  for (int v = 0; v < n; ++v)
+    if (g->op_alive[v]) {
+      indeg[v] = (int)g->in_e[v].size();
+      if (indeg[v] == 0) ready.insert({g->pos0[v], v});
+    }
+  std::vector<int> order;
+  while (!ready.empty()) {
+    const int u = ready.begin()->second;
+    ready.erase(ready.begin());
+    order.push_back(u);
+    for (int e : g->out_e[u]) {
+      const int d = g->edges[e].dst;
+      if (--indeg[d] == 0) ready.insert({g->pos0[d], d});
+    }
+  }
+  for (size_t q = 0; q < order.size(); ++q) g->pos0[order[q]] = (int)q;
+  g->order0 = order;
+  g->live_ops.clear();
+  g->one_one.clear();
+  g->leaf.clear();
+  g->k1src.clear();
+  g->multi.clear();
+  for (int v : order) {
+    g->live_ops.insert({g->pos0[v], v});
+    refresh(g, v);
+  }
+  for (const auto& kv : g->pair_edges)
+    if (kv.second.size() >= 2) g->multi.insert({g->pos0[kv.first.first], g->pos0[kv.first.second]});
+}
+
+// A path o_i -> ... -> o_h other than the direct edges (merging o_i into
+// o_h would close a cycle).
+bool other_path(const ft_graph* g, int i, int h) {
+  std::vector<char> seen(g->K.size(), 0);
+  std::vector<int> st;
+  for (int e : g->out_e[i])
+    if (g->edges[e].dst != h) st.push_back(g->edges[e].dst);
+  while (!st.empty()) {
+    const int u = st.back();
+    st.pop_back();
+    if (u == h) return true;
+    if (seen[u]) continue;
+    seen[u] = 1;
+    for (int e : g->out_e[u]) st.push_back(g->edges[e].dst);
+  }
+  return false;
+}
+
+// Eq. 6 with composite configurations (reading R21): o_i feeds
+// o_h through the single edge e and keeps other edges, so nothing is reduced
+// over s_i; o_i and o_h become one operator o_v with configurations
+// w = (s_h, s_i) = s_h * K_i + s_i:
+//   F(o_v, w) = reduce(F(o_h, s_h) (x) F(e, s_i, s_h) (x) F(o_i, s_i))  (K_COMPOSE)
+// and every other edge of o_h or o_i is re-indexed onto o_v (K_REMAP).
+int do_compose(ft_graph* g, int i, int h) {
+  int e = -1;
+  for (int x : g->in_e[h])
+    if (g->edges[x].src == i) e = x;
+  const int v = (int)g->K.size();
+  const int Kv = g->K[h] * g->K[i];
+  g->K.push_back(Kv);
+  g->op_alive.push_back(1);
+  g->in_e.emplace_back();
+  g->out_e.emplace_back();
+  g->pos0.push_back(g->pos0[h]);
+  g->mark_stamp.push_back(0);
+  g->comp.push_back({h, i});
+  StepRec r;
+  r.kind = ftk::K_COMPOSE;
+  r.X = g->op_set[h];
+  r.Y = g->edges[e].set;
+  r.Z = g->op_set[i];
+  r.KA = g->K[h];
+  r.KB = g->K[i];
+  r.nseg = Kv;
+  r.nblk = 1;
+  const int out = schedule(g, r);
+  g->sets[out].a_op = v;
+  g->op_set.push_back(out);
+  std::set<int> others;  // the other edges of o_h and o_i, ascending id
+  for (int o : {h, i}) {
+    others.insert(g->in_e[o].begin(), g->in_e[o].end());
+    others.insert(g->out_e[o].begin(), g->out_e[o].end());
+  }
+  others.erase(e);
+  kill_edge(g, e);
+  for (int x : others) {
+    const int src = g->edges[x].src, dst = g->edges[x].dst;
+    const int old = (src == h || src == i) ? src : dst;
+    const int y = old == src ? dst : src;
+    StepRec q;
+    q.kind = ftk::K_REMAP;
+    q.X = g->edges[x].set;
+    q.Y = 0;
+    q.Z = 0;
+    q.KA = g->K[y];
+    q.KB = g->K[i];
+    q.KC = (old == src ? 0 : 1) | (old == i ? 2 : 0);
+    q.nseg = (int64_t)Kv * g->K[y];
+    q.nblk = 1;
+    const int so = schedule(g, q);
+    const int ns = old == src ? v : y, nd = old == src ? y : v;
+    g->sets[so].a_op = ns;
+    g->sets[so].b_op = nd;
+    kill_edge(g, x);
+    add_edge(g, ns, nd, so);
+  }
+  kill_op(g, h);
+  kill_op(g, i);
+  reorder(g);
+  return FT_OK;
+}
+
+// Composite candidate (R21): the topologically first operator o_h with >= 2
+// input operators that has an unmarked input o_i with K_h * K_i <= 4096, no
+// other path o_i -> o_h, and that is not a source feeding >= 2 operators (a
+// broadcast input like BERT's mask, left to heuristic elimination,
+// P:618-620); among its inputs the smallest K_i, ties by position.
+// Requires a fresh mark_backbone.  Returns 1 = merged, 0 = none.
+int compose_step(ft_graph* g) {
+  for (const auto& kv : g->live_ops) {
+    const int h = kv.second;
+    std::set<std::pair<int, int>> ins;
+    for (int e : g->in_e[h]) ins.insert({g->pos0[g->edges[e].src], g->edges[e].src});
+    if (ins.size() < 2) continue;
+    int best = -1;
+    for (const auto& pi : ins) {
+      const int i = pi.second;
+      if (g->mark_stamp[i] == g->stamp || (int64_t)g->K[h] * g->K[i] > 4096 || other_path(g, i, h)) continue;
+      if (g->in_e[i].empty()) {
+        std::set<int> outs;
+        for (int x : g->out_e[i]) outs.insert(g->edges[x].dst);
+        if (outs.size() >= 2) continue;
+      }
+      if (best < 0 || g->K[i] < g->K[best]) best = i;
+    }
+    if (best >= 0) {
+      int rc = do_compose(g, best, h);
+      return rc ? rc : 1;
+    }
+  }
+  return 0;
+}
+
 // One FT_AUTO elimination (R9).  1 = scheduled, 0 = none applies, <0 error.
-int auto_step(ft_graph* g) {
+// compose = false skips (e) (FT_AUTO_HEUR tries heuristic elimination first).
+int auto_step(ft_graph* g, bool compose) {
   mark_backbone(g);
   // (a) parallel edges: topologically first (src, dst), two lowest ids
   if (!g->multi.empty()) {
@@ -1065,7 +1204,8 @@ int auto_step(ft_graph* g) {
       int rc = do_branch(g, kv.second);
       return rc ? rc : 1;
     }
-  return 0;
+  // (e) branch elimination with composite configurations (Eq. 6, R21)
+  return compose ? compose_step(g) : 0;
 }
 
 // Heuristic elimination (Eq. 7; lossy, FT_AUTO_HEUR only): the
@@ -1104,7 +1244,7 @@ int heur_step(ft_graph* g) {
 // The live graph as a chain o_1 -> ... -> o_n (LDP / FT-Elimination precondition).
 int linear_chain(ft_graph* g, std::vector<int>& chain, std::vector<int>& ce) {
   int src = -1, live = 0;
-  for (int v = 0; v < g->n_ops; ++v) {
+  for (int v = 0; v < (int)g->K.size(); ++v) {
     if (!g->op_alive[v]) continue;
     ++live;
     if (g->in_e[v].empty()) {
@@ -1235,6 +1375,11 @@ int put_cfg(ft_graph* g, std::vector<int32_t>& cfg, int op, int64_t c) {
     return setf(g, FT_EINTERNAL, "broken provenance (conflicting configs)");
   }
   cfg[op] = (int32_t)c;
+  if (op < (int)g->comp.size() && g->comp[op].first >= 0) {  // composite (R21): w = s_h * K_i + s_i
+    const int h = g->comp[op].first, i = g->comp[op].second;
+    int rc = put_cfg(g, cfg, h, c / g->K[i]);
+    return rc ? rc : put_cfg(g, cfg, i, c % g->K[i]);
+  }
   return FT_OK;
 }
 
@@ -1329,6 +1474,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
   g->n_ops = n_ops;
   g->n_orig_edges = n_edges;
   g->K.assign(n_cfgs, n_cfgs + n_ops);
+  g->comp.assign(n_ops, {-1, -1});
   g->op_alive.assign(n_ops, 1);
   g->in_e.resize(n_ops);
   g->out_e.resize(n_ops);
@@ -1387,6 +1533,13 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
     g->keep_all = opt->keep_all != 0;
     g->profile = opt->profile != 0;
     g->stream = (cudaStream_t)opt->stream;
+    if ((opt->alloc == nullptr) != (opt->free == nullptr)) {
+      delete g;
+      return FT_EINVAL;  // allocator hooks come in pairs
+    }
+    g->alloc.alloc = opt->alloc;
+    g->alloc.free = opt->free;
+    g->alloc.ctx = opt->alloc_ctx;
   }
   if (opt && g->world > 1 && !g->comm && opt->loopback) g->loopback = true;
   g->no_shared = getenv("FT_NO_SHARED") != nullptr;
@@ -1406,7 +1559,7 @@ int ft_graph_create(int32_t n_ops, const int32_t* n_cfgs, int32_t n_edges, const
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    g->runner = ftk::device_runner(g->dev);
+    g->runner = ftk::device_runner(g->dev, g->alloc);
     e = g->runner ? cudaSuccess : cudaErrorMemoryAllocation;
   }
   if (e != cudaSuccess) {
@@ -1437,13 +1590,14 @@ void ft_graph_destroy(ft_graph* g) {
   }
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {
-    if (w.m) cudaFreeAsync(w.m, g->stream);
-    if (w.t) cudaFreeAsync(w.t, g->stream);
-    if (w.bp) cudaFreeAsync(w.bp, g->stream);
-    if (w.off) cudaFreeAsync(w.off, g->stream);
+    if (w.m) g->alloc.put(w.m, g->stream);
+    if (w.t) g->alloc.put(w.t, g->stream);
+    if (w.bp) g->alloc.put(w.bp, g->stream);
+    if (w.off) g->alloc.put(w.off, g->stream);
   }
-  if (g->d_costs) cudaFreeAsync(g->d_costs, g->stream);
+  if (g->d_costs) g->alloc.put(g->d_costs, g->stream);
   if (g->stream) cudaStreamSynchronize(g->stream);  // back to the pool (not the driver)
+  if (g->runner) ftk::release_runner(g->dev, g->alloc);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -1512,7 +1666,7 @@ int ft_set_costs_all(ft_graph* g, const int64_t* op_m, const int64_t* op_t, cons
   int32_t status = 0;
   std::vector<char> mz(g->n_orig_edges, 1);
   CU(ftk::validate_costs(base + g->c_opm, 2 * nop + 2 * ned, base + g->c_em, g->e_off, g->n_orig_edges,
-                         &status, mz.data(), g->stream), "validate costs");
+                         &status, mz.data(), g->stream, g->alloc), "validate costs");
   if (status & 1) return setf(g, FT_EINVAL, "negative cost");
   if (status & 2) return setf(g, FT_EOVERFLOW, "cost >= 2^40");
   for (int i = 0; i < g->n_ops; ++i) g->op_ok[i] = 1;
@@ -1532,7 +1686,7 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
     return setf(g, FT_EINVAL, "bad kind");
   if (g->have_final) return setf(g, FT_ESTATE, "frontier already computed");
   if (kind == FT_NODE) {
-    if (id < 0 || id >= g->n_ops || !g->op_alive[id]) return setf(g, FT_EINVAL, "bad operator");
+    if (id < 0 || id >= (int)g->K.size() || !g->op_alive[id]) return setf(g, FT_EINVAL, "bad operator");
     mark_backbone(g);
     if (g->mark_stamp[id] == g->stamp || g->in_e[id].size() != 1 || g->out_e[id].size() != 1)
       return setf(g, FT_EPRECOND, "node elimination needs an unmarked op with one in- and one out-edge");
@@ -1558,8 +1712,10 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
   int rc = start(g);
   if (rc) return rc;
   const double a0 = now_ms();
+  // FT_AUTO: (a)-(e) until none applies.  FT_AUTO_HEUR (R17, R21): (a)-(d);
+  // if the graph is not linear, one heuristic elimination, else (e); repeat.
   for (;;) {
-    int r = auto_step(g);
+    int r = auto_step(g, kind == FT_AUTO);
     if (r < 0) return r;
     if (r == 1) continue;
     if (kind != FT_AUTO_HEUR) break;
@@ -1567,6 +1723,10 @@ int ft_eliminate(ft_graph* g, int32_t kind, int32_t id, int32_t* new_edge) {
     if (linear_chain(g, ch, ce) == FT_OK) break;  // linear: LDP can run
     g->err.clear();
     r = heur_step(g);
+    if (r < 0) return r;
+    if (r == 1) continue;
+    mark_backbone(g);
+    r = compose_step(g);
     if (r < 0) return r;
     if (r == 0) break;
   }
@@ -1619,7 +1779,7 @@ int ft_strategy(ft_graph* g, int64_t tuple_idx, int32_t* cfg_out) {
   if (g->poisoned) return g->poisoned;
   if (!g->have_final) return setf(g, FT_ESTATE, "call ft_frontier first");
   if (tuple_idx < 0 || tuple_idx >= (int64_t)g->final_m.size()) return setf(g, FT_EINVAL, "bad tuple index");
-  std::vector<int32_t> cfg(g->n_ops, -1);
+  std::vector<int32_t> cfg(g->K.size(), -1);
   int rc = unroll(g, g->final_set, 0, tuple_idx, cfg);
   if (rc) return rc;
   for (int i = 0; i < g->n_ops; ++i)

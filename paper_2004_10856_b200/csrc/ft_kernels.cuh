@@ -39,7 +39,8 @@ constexpr int CHUNK = 16;           // run elements per filter work item
 constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
 constexpr int BMIN_FILL = 0x7F;     // memset byte: 0x7F7F..7F > any t (< 2^60)
 
-enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5, K_PAIR = 6, K_BRANCH = 7 };
+enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5, K_PAIR = 6, K_BRANCH = 7, K_COMPOSE = 8,
+       K_REMAP = 9 };
 
 // A frontier set on the device (CSR): segment s = [off[s], off[s+1]).
 struct FacSet {
@@ -204,6 +205,21 @@ __device__ __forceinline__ void block_factor_segs(const StepDev& s, int64_t sg, 
     sx = k;                          // F(e_1n, s_1, s_n)
     sy = s1;                         // F(o_1, s_1)
     sz = k - s1 * s.KB;              // F(o_n, s_n)
+  } else if (s.kind == K_COMPOSE) {  // Eq. 6 composite (R21): sigma = w = s_h*K_i + s_i, one block
+    const int64_t p = sg / s.KB, q = sg - p * s.KB;  // KA = K_h, KB = K_i
+    sx = p;                          // F(o_h, s_h)
+    sy = q * s.KA + p;               // F(e_ih, s_i, s_h)
+    sz = q;                          // F(o_i, s_i)
+  } else if (s.kind == K_REMAP) {  // R21: an edge of o_h / o_i re-indexed onto the composite o_v
+    // KA = K_y (other endpoint), KB = K_i, KC = side | part << 1 (side 0: o_v is
+    // the source; part 0: the old endpoint was o_h -> w / K_i, 1: o_i -> w % K_i)
+    const int64_t Kv = s.nseg / s.KA, side = s.KC & 1, part = s.KC >> 1;
+    const int64_t Kold = part ? s.KB : Kv / s.KB;
+    const int64_t w = side == 0 ? sg / s.KA : sg % Kv, y = side == 0 ? sg % s.KA : sg / Kv;
+    const int64_t c = part ? w % s.KB : w / s.KB;
+    sx = side == 0 ? c * s.KA + y : y * Kold + c;
+    sy = 0;
+    sz = 0;
   } else if (s.kind == K_FOLD) {   // Eq. 7, source fixed to k* = KB: X=o_j, Y=F(e,k*,p), Z=o_src(k*)|unit
     sx = sg;
     sy = s.KB * s.KA + sg;           // K=1 fold: KB = KC = 0 (R13)

@@ -2437,26 +2437,26 @@ __global__ void k_edge_mzero(const int64_t* em, const int64_t* e_off, int ne, ch
 
 cudaError_t validate_costs(const int64_t* d, int64_t n, const int64_t* em,
                            const std::vector<int64_t>& e_off, int ne, int32_t* status_host,
-                           char* mz_host, cudaStream_t st) {
+                           char* mz_host, cudaStream_t st, const DevAlloc& A) {
   int32_t* dstat = nullptr;
   int64_t* doff = nullptr;
   char* dmz = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&dstat, sizeof(int32_t) + 16, st);
+  cudaError_t e = A.get((void**)&dstat, sizeof(int32_t) + 16, st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(dstat, 0, sizeof(int32_t), st);
   if (n > 0) k_validate<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(d, n, dstat);
   if (ne > 0) {
-    if ((e = cudaMallocAsync((void**)&doff, sizeof(int64_t) * (ne + 1), st)) != cudaSuccess) return e;
-    if ((e = cudaMallocAsync((void**)&dmz, ne, st)) != cudaSuccess) return e;
+    if ((e = A.get((void**)&doff, sizeof(int64_t) * (ne + 1), st)) != cudaSuccess) return e;
+    if ((e = A.get((void**)&dmz, ne, st)) != cudaSuccess) return e;
     cudaMemcpyAsync(doff, e_off.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice, st);
     k_edge_mzero<<<std::min(ne, 148 * 8), 128, 0, st>>>(em, doff, ne, dmz);
     cudaMemcpyAsync(mz_host, dmz, ne, cudaMemcpyDeviceToHost, st);
   }
   cudaMemcpyAsync(status_host, dstat, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(dstat, st);
-  if (doff) cudaFreeAsync(doff, st);
-  if (dmz) cudaFreeAsync(dmz, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  A.put(dstat, st);
+  A.put(doff, st);
+  A.put(dmz, st);
   return cudaGetLastError();
 }
 
@@ -2522,25 +2522,25 @@ int64_t scan_tmp_elems(int64_t n) { return ntiles_cap_slot(n) + 8; }
 // ---------------------------------------------------------------------------
 // Host side
 
-// Grow-only scratch with geometric growth: reallocation (a device-wide sync)
-// happens O(log size) times per process, not per step.
-static cudaError_t grow_raw(void** p, size_t* have, size_t need) {
+// Grow-only scratch with geometric growth: reallocation happens O(log size)
+// times per process, not per step.  Callers have synchronised the stream
+// since the buffer's last use (every wave ends with a stream sync).
+static cudaError_t grow_raw(const DevAlloc& A, cudaStream_t st, void** p, size_t* have, size_t need) {
   if (need <= *have && *p) return cudaSuccess;
   size_t nb = std::max<size_t>({need, 2 * *have, (size_t)1 << 16});
   if (*p) {
-    cudaError_t e = cudaFree(*p);
-    if (e != cudaSuccess) return e;
+    A.put(*p, st, true);
     *p = nullptr;
     *have = 0;
   }
-  cudaError_t e = cudaMalloc(p, nb);
+  cudaError_t e = A.get(p, nb, st, true);
   if (e == cudaSuccess) *have = nb;
   return e;
 }
 
 #define GROW(buf, T, n)                                                         \
   do {                                                                          \
-    cudaError_t e__ = grow_raw((void**)&buf.p, &buf.bytes, sizeof(T) * (size_t)(n)); \
+    cudaError_t e__ = grow_raw(alloc, st, (void**)&buf.p, &buf.bytes, sizeof(T) * (size_t)(n)); \
     if (e__ != cudaSuccess) return e__;                                         \
   } while (0)
 
@@ -2548,16 +2548,7 @@ StepRunner::StepRunner() {}
 StepRunner::~StepRunner() { release(); }
 
 void StepRunner::release() {
-  Buf* all[] = {&seg_d, &seg_n, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
-                &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
-                &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
-                &cgb, &gm, &gt, &gid, &gflag, &large_list, &scan_tmp, &ncand,
-                &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev};
-  for (Buf* b : all) {
-    if (b->p) cudaFree(b->p);
-    b->p = nullptr;
-    b->bytes = 0;
-  }
+  release_device();
   if (hdr_host) cudaFreeHost(hdr_host);
   hdr_host = nullptr;
   if (cnt_host) cudaFreeHost(cnt_host);
@@ -2574,6 +2565,19 @@ void StepRunner::release() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   ev0 = ev1 = nullptr;
+}
+
+void StepRunner::release_device() {
+  Buf* all[] = {&seg_d, &seg_n, &blk_rel, &seg_tuples, &hdr, &poolA_m, &poolA_t, &poolA_id, &poolA_start,
+                &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
+                &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
+                &cgb, &gm, &gt, &gid, &gflag, &large_list, &scan_tmp, &ncand,
+                &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev, &packs_dev, &big_dev};
+  for (Buf* b : all) {
+    if (b->p) alloc.put(b->p, nullptr, true);
+    b->p = nullptr;
+    b->bytes = 0;
+  }
 }
 
 static int grid_for(int64_t n, int nt, int maxg) {
@@ -2822,11 +2826,12 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         L.large_n = cur + 3;
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
-        mark(2);
+        mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
         nl += 4;  // scan(+nb), bucket_init, scan(+work counts), filter
         scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
         k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
         scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st);
+        mark(2);  // filter_ms: k_filter alone
         k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
         // bucket offsets over B buckets (B on device)
         mark(3);

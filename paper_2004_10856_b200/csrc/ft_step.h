@@ -1,6 +1,7 @@
 // ft_step.h -- host interface of the per-step GPU pipeline (internal).
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -30,10 +31,43 @@ struct StepResult {
   Pool pool;                        // level-0 pool (device)
 };
 
-// Process-wide scratch + pipeline per CUDA device, shared by all graphs on
-// that device (lock held for a whole step; see ft_api.cu).
+// Device memory: the caller's hooks (ft_options.alloc / .free) when set, else
+// the stream-ordered pool (cudaMallocAsync) or, for grow-only scratch,
+// cudaMalloc.
+struct DevAlloc {
+  void* (*alloc)(size_t, void*, void*) = nullptr;
+  void (*free)(void*, void*, void*) = nullptr;
+  void* ctx = nullptr;
+  bool hooked() const { return alloc != nullptr; }
+  cudaError_t get(void** p, size_t bytes, cudaStream_t st, bool scratch = false) const {
+    if (alloc) {
+      *p = alloc(bytes ? bytes : 1, (void*)st, ctx);
+      return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
+    return scratch ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, st);
+  }
+  void put(void* p, cudaStream_t st, bool scratch = false) const {
+    if (!p) return;
+    if (free) free(p, (void*)st, ctx);
+    else if (scratch) cudaFree(p);
+    else cudaFreeAsync(p, st);
+  }
+  bool operator<(const DevAlloc& o) const {
+    if (alloc != o.alloc) return (uintptr_t)alloc < (uintptr_t)o.alloc;
+    if (free != o.free) return (uintptr_t)free < (uintptr_t)o.free;
+    return (uintptr_t)ctx < (uintptr_t)o.ctx;
+  }
+};
+
+// Process-wide scratch + pipeline per (CUDA device, allocator), shared by all
+// graphs with that pair (its mutex is held for a whole wave; see ft_api.cu).
 class StepRunner;
-StepRunner* device_runner(int device);
+StepRunner* device_runner(int device, const DevAlloc& a);
+// A graph is done with its runner: a hooked runner (caller allocator) hands its
+// device scratch back through the hooks when its last graph is destroyed (so
+// every hooked allocation is returned by then); the default runner keeps its
+// scratch for the process lifetime.
+void release_runner(int device, const DevAlloc& a);
 
 // One (step, w) row of a shared-order node elimination (k_node_shared).
 struct NodeGroup {
@@ -59,7 +93,7 @@ int64_t scan_tmp_elems(int64_t n);
 // per edge whether its memory costs are all zero.
 cudaError_t validate_costs(const int64_t* d, int64_t n, const int64_t* em,
                            const std::vector<int64_t>& e_off, int ne, int32_t* status_host,
-                           char* mz_host, cudaStream_t st);
+                           char* mz_host, cudaStream_t st, const DevAlloc& A);
 
 class StepRunner {
  public:
@@ -77,6 +111,7 @@ class StepRunner {
   // Gathers the level-0 pool into each step's CSR output (steps[j].out_*).
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
+  void release_device();  // device scratch only (hooked runners, last graph gone)
 
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
@@ -91,6 +126,9 @@ class StepRunner {
   unsigned long long fstat_acc[4] = {0, 0, 0, 0};
   unsigned long long bstat_acc[2][10] = {};
   bool profile = false;               // events between kernel groups
+  DevAlloc alloc;                     // scratch memory (set once at creation)
+  std::mutex mu;                      // held by a graph for a whole wave
+  int users = 0;                      // live graphs (device_runner / release_runner)
   int64_t cand_budget = 16 << 20;     // candidate capacity (grown on overflow)
   int64_t out_budget = 1 << 20;
   int64_t bucket_budget = 1 << 20;

@@ -49,3 +49,19 @@ def test_host_only_entry_points():
     assert b[0] == 0 and b[-1] == 8
     with pytest.raises(ft.FTError):
         ft.shard_plan(np.array([1, -1]), 2)
+
+
+def test_allocator_hooks_checked_before_device_use():
+    """ft_options.alloc / .free come in pairs (FT_EINVAL), checked on the host."""
+    import paper_2004_10856_b200 as ft
+    dummy = ft.ALLOC_FN(lambda n, s, c: None)
+    with pytest.raises(ft.FTError) as e:
+        ft.Graph([2, 2], [0], [1], alloc=(ctypes.cast(dummy, ctypes.c_void_p).value, None))
+    assert e.value.code == ft.EINVAL
+    assert ctypes.sizeof(ft.ft_options) == 88  # include/ft.h layout (x86-64)
+
+
+def test_torch_alloc_shim_exports():
+    import paper_2004_10856_b200 as ft
+    lib = ctypes.CDLL(ft.TORCH_ALLOC_PATH)
+    assert hasattr(lib, "ft_torch_alloc") and hasattr(lib, "ft_torch_free")

@@ -54,3 +54,16 @@ def test_reschedule_host_errors(ft):
     with pytest.raises(ft.FTError) as e:
         ft.comm_time(p20, [2 ** 20 + 1], 1)
     assert e.value.code == ft.EOVERFLOW
+
+
+def test_query_length_checked_in_binding(ft):
+    """Mismatched query arrays are rejected before any pointer crosses the ABI."""
+    prof = comm.profile(0, L=2, P=20)
+    nd, dims, eb = np.array([1], np.int32), np.array([[4, 1, 1, 1]]), np.array([2], np.int64)
+    z = np.zeros(3, np.int32)
+    with pytest.raises(ValueError):
+        ft.reschedule_costs(prof, nd, dims, eb, z, z[:2], z)
+    with pytest.raises(ValueError):
+        ft.sync_costs(prof, nd, dims, eb, z, z[:1])
+    with pytest.raises(ValueError):
+        ft.sync_costs(prof, nd, dims, np.array([2, 2], np.int64), z, z)

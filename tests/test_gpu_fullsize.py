@@ -132,3 +132,28 @@ def test_c5_full_sampled_segments(ft):
     checked = check_sampled_segments(g, w, sorted(sample))
     assert checked > 100
     final_pins(g, w, m, t)
+
+
+def test_c5_full_every_step(ft):
+    """C5 (configs[4], the bench workload) end to end against the oracle run
+    over the whole search on every host core: every step's (seg_off, m, t,
+    bp), the final frontier and 48 strategies bit-identical (node /
+    edge elimination and LDP preserve the exact frontier)."""
+    import os
+    w = G.c5()
+    og = oracle.load(w, threads=len(os.sched_getaffinity(0)))
+    og.eliminate()
+    om, ot = og.frontier()
+    g = ft.load(w, keep_all=True)
+    g.eliminate()
+    gm, gt = g.frontier()
+    st = g.stats()
+    assert og.num_steps() == len(st)
+    for s in range(len(st)):
+        info = og.step_info(s)
+        assert info["tuples"] == st[s]["tuples"], s
+        for name, x, y in zip(("seg_off", "m", "t", "bp"), og.step_output(s), g.step_output(s)):
+            assert np.array_equal(x, y), (s, info["kind"], name)
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+    for i in np.linspace(0, len(om) - 1, 48).astype(int):
+        assert np.array_equal(og.strategy(int(i)), g.strategy(int(i)))

@@ -409,3 +409,42 @@ def test_full_key_sort_fallback(ft, monkeypatch, bits):
         gg, st = compare(ft, w, strategies=16)
         if w.name.startswith("C5"):
             assert sum(s["path"]["shared_cta_rows"] for s in st) > 0  # rows handed to k_node_shared
+
+
+# ---- branch elimination with composite configurations (Eq. 6, R21)
+
+def test_bridge_and_random_dags_composite(ft):
+    """Non-series-parallel DAGs linearised by composite branch elimination:
+    every step (compose, remap, ...) bit-exact against the oracle, composite
+    configurations split back in every strategy."""
+    n = 0
+    for K in (2, 3, [2, 3, 4, 2], [3, 4, 1, 2], 40):
+        w = G.random_graph(4, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], K, 3, cost_hi=1 << 20, edge_mem=True)
+        gg, st = compare(ft, w)
+        n += any(s["kind"] == "compose" for s in st)
+    for seed in range(120):
+        w = G.random_dag(seed, n_ops=3 + seed % 9, kmax=4 + seed % 5, p_edge=0.35,
+                         cost_hi=1 << (4 + seed % 20), edge_mem=(seed % 4 == 0))
+        gg, st = compare(ft, w, strategies=8)
+        n += any(s["kind"] == "compose" for s in st)
+    assert n >= 60
+
+
+def test_composite_loopback_and_elimination(ft):
+    """Composite graphs sharded over virtual ranks, and FT-Elimination on them."""
+    for seed in (5, 17, 29):
+        w = G.random_dag(seed, n_ops=10, kmax=6, p_edge=0.3, cost_hi=1 << 16)
+        a = ft.load(w, keep_all=True)
+        a.eliminate()
+        am, at = a.frontier()
+        b = ft.load(w, keep_all=True, world=3, loopback=True)
+        b.eliminate()
+        bm, bt = b.frontier()
+        assert np.array_equal(am, bm) and np.array_equal(at, bt)
+        c = ft.load(w)
+        c.eliminate()
+        cm, ct = c.frontier(algo="elim")
+        og = oracle.load(w, 4)
+        og.eliminate()
+        om, ot = og.frontier(algo="elim")
+        assert np.array_equal(cm, om) and np.array_equal(ct, ot) and np.array_equal(cm, am)

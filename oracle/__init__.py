@@ -37,7 +37,7 @@ def build(force: bool = False) -> str:
     if (not force and os.path.exists(LIB_PATH)
             and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(f) for f in srcs + [hdr])):
         return LIB_PATH
-    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-shared", "-fPIC", "-o",
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-Wall", "-shared", "-fPIC", "-o",
                            LIB_PATH, *srcs, "-lpthread"])
     return LIB_PATH
 
@@ -63,6 +63,7 @@ def lib():
         L.oft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
         L.oft_query_mini_time.argtypes = [C.c_void_p, C.c_int64, P64]
         L.oft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
+        L.oft_set_heuristic.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64]
         L.oft_num_steps.argtypes = [C.c_void_p]
         L.oft_num_steps.restype = C.c_int64
         L.oft_step_info.argtypes = [C.c_void_p, C.c_int64, P64]
@@ -150,6 +151,12 @@ class Graph:
         t = np.empty(n.value, np.int64)
         self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
+
+    def set_heuristic(self, policy="min_memory", alpha=(1, 2)):
+        """Heuristic-elimination rule: "min_memory" (R17) or "weighted"
+        alpha*m/M + (1-alpha)*t/T, alpha = num/den (R22, P:622)."""
+        pol = {"min_memory": 0, "weighted": 1}[policy]
+        return self._chk(self._L.oft_set_heuristic(self.h, pol, int(alpha[0]), int(alpha[1])))
 
     def mini_time(self, memory_limit):
         """SS4.1 mini-time: index of the fastest frontier tuple with m <= limit, or -1."""

@@ -99,6 +99,8 @@ struct oft_graph {
   bool have_final = false;
   int final_mode = 0;  // 1 = LDP (Alg. 3), 2 = FT-Elimination
   int final_set = -1;
+  int heur_policy = 0;                 // R17 least memory, 1 = weighted (R22)
+  int64_t heur_num = 1, heur_den = 2;  // alpha of the weighted rule
   std::string err;
 };
 
@@ -662,9 +664,39 @@ int heur_one(oft_graph* g) {
   if (best < 0) return 0;
   const FSet& S = g->sets[g->op_set[best]];
   int64_t ks = 0;
-  for (int64_t k = 1; k < (int64_t)S.seg.size(); ++k) {
-    const Tup &x = S.seg[k][0], &y = S.seg[ks][0];
-    if (x.m < y.m || (x.m == y.m && x.t < y.t)) ks = k;
+  if (g->heur_policy == 0) {
+    for (int64_t k = 1; k < (int64_t)S.seg.size(); ++k) {
+      const Tup &x = S.seg[k][0], &y = S.seg[ks][0];
+      if (x.m < y.m || (x.m == y.m && x.t < y.t)) ks = k;
+    }
+  } else {
+    // R22 ("a weighted combination of different objectives"): every
+    // tuple x of F(o_i, k) scores alpha * m_x / M + (1 - alpha) * t_x / T in
+    // IEEE double (M, T = largest m, t over F(o_i, .), at least 1; each
+    // operation rounded separately); the config of the least score wins,
+    // ties by (m, t) of its tuple, then k.
+    int64_t M = 1, T = 1;
+    for (const auto& f : S.seg)
+      for (const Tup& x : f) {
+        M = std::max(M, x.m);
+        T = std::max(T, x.t);
+      }
+    const double al = (double)g->heur_num / (double)g->heur_den;
+    bool have = false;
+    double bs = 0;
+    int64_t bm = 0, bt = 0;
+    for (int64_t k = 0; k < (int64_t)S.seg.size(); ++k)
+      for (const Tup& x : S.seg[k]) {
+        const double dm = (double)x.m / (double)M, dt = (double)x.t / (double)T;
+        const double sc = al * dm + (1.0 - al) * dt;
+        if (!have || sc < bs || (sc == bs && (x.m < bm || (x.m == bm && x.t < bt)))) {
+          have = true;
+          bs = sc;
+          bm = x.m;
+          bt = x.t;
+          ks = k;
+        }
+      }
   }
   int rc = do_fold(g, a, best, topo, ks);
   return rc ? rc : 1;
@@ -1016,6 +1048,18 @@ int oft_strategy(oft_graph* g, int64_t idx, int32_t* cfg_out) {
   for (int i = 0; i < g->n_orig_ops; ++i)
     if (cfg[i] < 0) return fail(g, OFT_EINTERNAL, "broken provenance: op without config");
   std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_orig_ops);
+  return OFT_OK;
+}
+
+int oft_set_heuristic(oft_graph* g, int32_t policy, int64_t alpha_num, int64_t alpha_den) {
+  if (!g || (policy != 0 && policy != 1)) return OFT_EINVAL;
+  if (policy == 1 && (alpha_den < 1 || alpha_num < 0 || alpha_num > alpha_den))
+    return fail(g, OFT_EINVAL, "alpha must be in [0, 1]");
+  g->heur_policy = policy;
+  if (policy == 1) {
+    g->heur_num = alpha_num;
+    g->heur_den = alpha_den;
+  }
   return OFT_OK;
 }
 

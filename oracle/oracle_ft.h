@@ -67,6 +67,10 @@ int oft_frontier_elim(oft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out,
  * tuple with m <= memory_limit (the last such tuple: m ascending, t strictly
  * descending), or -1 if none (infeasible).  Requires a computed frontier. */
 int oft_query_mini_time(oft_graph* g, int64_t memory_limit, int64_t* idx_out);
+/* Heuristic-elimination configuration rule (R17): policy 0 = least
+ * memory (default), 1 = weighted combination alpha*m/M + (1-alpha)*t/T with
+ * alpha = num/den (reading R22). */
+int oft_set_heuristic(oft_graph* g, int32_t policy, int64_t alpha_num, int64_t alpha_den);
 /* Unrolled strategy (config per original op) of final-frontier tuple idx. */
 int oft_strategy(oft_graph* g, int64_t tuple_idx, int32_t* cfg_out);
 int64_t oft_num_steps(const oft_graph* g);

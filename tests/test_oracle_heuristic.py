@@ -101,3 +101,94 @@ def test_heuristic_off_by_default():
     g.eliminate(oracle.AUTO_HEUR)
     m, t = g.frontier()
     assert len(m) > 0
+
+
+def _weighted_choice(w, op, alpha):
+    """R22's rule written out from the cost tables (IEEE double, each
+    operation rounded once -- Python floats): least alpha*m/M + (1-alpha)*t/T."""
+    m = [int(x) for x in w.op_m[op]]
+    t = [int(x) for x in w.op_t[op]]
+    M, T = max(1, max(m)), max(1, max(t))
+    al = alpha[0] / alpha[1]
+    key = lambda k: (al * (m[k] / M) + (1.0 - al) * (t[k] / T), m[k], t[k], k)
+    return min(range(len(m)), key=key)
+
+
+@pytest.mark.parametrize("alpha", [(1, 2), (1, 4), (3, 4), (0, 1), (1, 1)])
+@pytest.mark.parametrize("seed", range(24))
+def test_weighted_heuristic_restricted_brute_force(seed, alpha):
+    """P:622 "a weighted combination of different objectives" (reading R22):
+    exact on the restricted problem with the mask fixed to the rule's pick."""
+    w = G.random_masked(seed, n_ops=3 + seed % 4, kmax=3, mask_k=2 + seed % 3, fanout=2 + seed % 2,
+                        cost_hi=40)
+    g = oracle.load(w, 2)
+    g.set_heuristic("weighted", alpha)
+    g.eliminate(oracle.AUTO_HEUR)
+    try:
+        m, t = g.frontier()
+    except oracle.OracleError:
+        pytest.skip("not linearisable")
+    ma, ta, _ = bf.enumerate_costs(w)
+    if bf.check_frontier(m, t, ma, ta) == []:
+        return  # no heuristic step was needed
+    mask = w.n_ops - 1
+    ks = _weighted_choice(w, mask, alpha)
+    ma, ta, _ = bf.enumerate_costs(_restricted(w, mask, ks))
+    assert bf.check_frontier(m, t, ma, ta) == []
+    for i in range(len(m)):
+        s = g.strategy(i)
+        assert s[mask] == ks and bf.total_cost(w, s) == (int(m[i]), int(t[i]))
+
+
+def test_weighted_alpha_one_is_least_memory():
+    """alpha = 1 scores m/M: the same pick as the least-memory rule (ties by t)."""
+    for seed in range(30):
+        w = G.random_masked(seed, n_ops=5, kmax=3, mask_k=4, fanout=3, cost_hi=40)
+        res = []
+        for pol in ("min_memory", "weighted"):
+            g = oracle.load(w, 2)
+            g.set_heuristic(pol, (1, 1))
+            g.eliminate(oracle.AUTO_HEUR)
+            try:
+                res.append(g.frontier())
+            except oracle.OracleError:
+                res.append(None)
+        if res[0] is not None:
+            assert all(np.array_equal(a, b) for a, b in zip(res[0], res[1]))
+
+
+def test_set_heuristic_errors():
+    w = G.random_masked(0)
+    g = oracle.load(w)
+    for bad in ((2, 1), (-1, 2), (1, 0)):
+        with pytest.raises(oracle.OracleError):
+            g.set_heuristic("weighted", bad)
+
+
+def quality(policy, alpha=(1, 2), n=50):
+    """S:603 acceptance criterion 3 on n shared-input fixtures: every returned
+    tuple is feasible (re-costs exactly) and the output is mutually
+    non-dominated; returns the mean fraction of oracle (exact, brute-force)
+    frontier points that the heuristic output weakly dominates."""
+    fr = []
+    for seed in range(n):
+        w = G.random_masked(1000 + seed, n_ops=4 + seed % 3, kmax=3, mask_k=3, fanout=3, cost_hi=40)
+        g = oracle.load(w, 2)
+        g.set_heuristic(policy, alpha)
+        g.eliminate(oracle.AUTO_HEUR)
+        try:
+            m, t = g.frontier()
+        except oracle.OracleError:
+            continue
+        for i in range(len(m)):
+            assert bf.total_cost(w, g.strategy(i)) == (int(m[i]), int(t[i]))
+        assert (np.diff(m) > 0).all() and (np.diff(t) < 0).all()
+        ex = bf.brute_force(w)
+        fr.append(sum(bool(((m <= a) & (t <= b)).any()) for a, b in ex) / len(ex))
+    return float(np.mean(fr)), len(fr)
+
+
+def test_heuristic_quality_s603():
+    for pol in ("min_memory", "weighted"):
+        q, n = quality(pol)
+        assert n >= 40 and 0.0 < q <= 1.0, (pol, q, n)

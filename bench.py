@@ -281,8 +281,7 @@ def main():
                 "parallelism": f"config-pair sharding x{world} + NCCL all-gather" if world > 1 else "single GPU",
                 "l2_flush": "512 MiB memset between timed searches" if not args.no_flush else "none"})
     stream = torch.cuda.current_stream()
-    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm,
-              torch_alloc=True)
+    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_comm=comm)
 
     def barrier():
         if dist is not None:

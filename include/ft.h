@@ -201,6 +201,19 @@ int ft_frontier(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_
  * returns FT_ESTATE, and vice versa.  FT_EPRECOND if not a chain. */
 int ft_frontier_elim(ft_graph* g, int64_t cap, int64_t* m_out, int64_t* t_out, int64_t* n_out);
 
+/* Configuration rule of heuristic elimination (FT_AUTO_HEUR; Eq. 7,
+ * "minimizing the memory consumption of o_i or a weighted
+ * combination of different objectives"):
+ *  FT_HEUR_MIN_MEMORY (default): the config whose least-memory tuple of
+ *    F(o_i, k) has the least m, ties by t, then k (reading R17);
+ *  FT_HEUR_WEIGHTED: every tuple x of F(o_i, k) scores
+ *    alpha*m_x/M + (1-alpha)*t_x/T with alpha = alpha_num/alpha_den in [0, 1]
+ *    and M, T the largest m, t over F(o_i, .) (at least 1), evaluated in IEEE
+ *    double (reading R22); least score wins, ties by (m, t), then k.
+ * Errors: FT_EINVAL (policy, alpha outside [0, 1] or alpha_den < 1). */
+enum { FT_HEUR_MIN_MEMORY = 0, FT_HEUR_WEIGHTED = 1 };
+int ft_set_heuristic(ft_graph* g, int32_t policy, int64_t alpha_num, int64_t alpha_den);
+
 /* Mini-time query (SS4.1: "minimizes the per-iteration time while
  * satisfying the memory constraint"): *idx_out = index of the smallest-time
  * final-frontier tuple with m <= memory_limit -- binary search on the

@@ -84,6 +84,7 @@ def _load():
     L.ft_frontier_elim.argtypes = [C.c_void_p, C.c_int64, P64, P64, P64]
     L.ft_query_mini_time.argtypes = [C.c_void_p, C.c_int64, P64]
     L.ft_strategy.argtypes = [C.c_void_p, C.c_int64, P32]
+    L.ft_set_heuristic.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64]
     L.ft_get_stats.argtypes = [C.c_void_p, C.POINTER(ft_step_stats), C.c_int64, P64]
     L.ft_step_output.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P64, P64, P64, PU64, P64]
     L.ft_shard_plan.argtypes = [C.c_int64, P64, C.c_int32, P64]
@@ -131,7 +132,7 @@ def torch_allocator():
         _torch_alloc = (L, C.cast(L.ft_torch_alloc, C.c_void_p).value, C.cast(L.ft_torch_free, C.c_void_p).value)
     return _torch_alloc[1], _torch_alloc[2]
 SYMBOLS = ["ft_graph_create", "ft_graph_destroy", "ft_set_op_costs", "ft_set_edge_costs",
-           "ft_eliminate", "ft_frontier", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
+           "ft_eliminate", "ft_frontier", "ft_set_heuristic", "ft_frontier_elim", "ft_query_mini_time", "ft_strategy", "ft_get_stats", "ft_step_output",
            "ft_prepare", "ft_set_costs_all", "ft_step_inputs", "ft_shard_plan", "ft_nccl_unique_id",
            "ft_nccl_comm_init", "ft_nccl_comm_destroy", "ft_last_error", "ft_version",
            "ft_comm_time", "ft_split_states", "ft_reschedule_costs", "ft_reschedule_costs_dev", "ft_sync_costs", "ft_costgen_profile",
@@ -245,6 +246,12 @@ class Graph:
         t = np.empty(n.value, np.int64)
         self._chk(fn(self.h, n.value, _p(m, C.c_int64), _p(t, C.c_int64), C.byref(n)))
         return m, t
+
+    def set_heuristic(self, policy: str = "min_memory", alpha=(1, 2)):
+        """ft_set_heuristic: "min_memory" (R17) or "weighted" alpha*m/M +
+        (1-alpha)*t/T with alpha = num/den (R22, P:622)."""
+        pol = {"min_memory": 0, "weighted": 1}[policy]
+        self._chk(lib.ft_set_heuristic(self.h, pol, int(alpha[0]), int(alpha[1])))
 
     def mini_time(self, memory_limit: int) -> int:
         """SS4.1 mini-time: index of the fastest frontier tuple with m <= limit, or -1."""

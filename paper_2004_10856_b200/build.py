@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
         return LIB
     inc, lib = _nccl_dirs()
-    cmd = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-shared",
+    cmd = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared",
            "-cudart", "static", f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", "-o", LIB, *srcs,
            f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}"]
     if verbose:

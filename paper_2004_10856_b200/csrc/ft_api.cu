@@ -109,6 +109,8 @@ struct ft_graph {
   bool started = false, have_final = false;
   int final_mode = 0;  // 1 = LDP (Alg. 3), 2 = FT-Elimination
   int final_set = -1;
+  int heur_policy = 0;                 // FT_HEUR_MIN_MEMORY (R17) | FT_HEUR_WEIGHTED (R22)
+  int64_t heur_num = 1, heur_den = 2;  // alpha of the weighted rule
   std::vector<int64_t> final_m, final_t;
   int poisoned = 0;
   std::string err;
@@ -1233,9 +1235,37 @@ int heur_step(ft_graph* g) {
   CU(cudaMemcpy(hm.data(), S.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
   CU(cudaMemcpy(ht.data(), S.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
   int64_t ks = 0;
-  for (int64_t k = 1; k < S.nseg; ++k) {
-    const int64_t a = S.off[k], b = S.off[ks];
-    if (hm[a] < hm[b] || (hm[a] == hm[b] && ht[a] < ht[b])) ks = k;
+  if (g->heur_policy == 0) {
+    for (int64_t k = 1; k < S.nseg; ++k) {
+      const int64_t a = S.off[k], b = S.off[ks];
+      if (hm[a] < hm[b] || (hm[a] == hm[b] && ht[a] < ht[b])) ks = k;
+    }
+  } else {
+    // R22 (weighted combination): score alpha*m/M + (1-alpha)*t/T per
+    // tuple in IEEE double (M, T = largest m, t over F(o_i, .), >= 1; each
+    // operation rounded separately, no contraction); least score wins, ties
+    // by (m, t), then k
+    int64_t M = 1, T = 1;
+    for (int64_t q = 0; q < n; ++q) {
+      M = std::max(M, hm[q]);
+      T = std::max(T, ht[q]);
+    }
+    const double al = (double)g->heur_num / (double)g->heur_den;
+    bool have = false;
+    double bs = 0;
+    int64_t bm = 0, bt = 0;
+    for (int64_t k = 0; k < S.nseg; ++k)
+      for (int64_t q = S.off[k]; q < S.off[k + 1]; ++q) {
+        const double dm = (double)hm[q] / (double)M, dt = (double)ht[q] / (double)T;
+        const double sc = al * dm + (1.0 - al) * dt;
+        if (!have || sc < bs || (sc == bs && (hm[q] < bm || (hm[q] == bm && ht[q] < bt)))) {
+          have = true;
+          bs = sc;
+          bm = hm[q];
+          bt = ht[q];
+          ks = k;
+        }
+      }
   }
   rc = do_fold(g, best, ks);
   return rc ? rc : 1;
@@ -1788,6 +1818,20 @@ int ft_strategy(ft_graph* g, int64_t tuple_idx, int32_t* cfg_out) {
       return setf(g, FT_EINTERNAL, "broken provenance (operator without config)");
     }
   std::memcpy(cfg_out, cfg.data(), sizeof(int32_t) * g->n_ops);
+  return FT_OK;
+}
+
+int ft_set_heuristic(ft_graph* g, int32_t policy, int64_t alpha_num, int64_t alpha_den) {
+  if (!g) return FT_EINVAL;
+  if (g->poisoned) return g->poisoned;
+  if (policy != FT_HEUR_MIN_MEMORY && policy != FT_HEUR_WEIGHTED) return setf(g, FT_EINVAL, "bad policy");
+  if (policy == FT_HEUR_WEIGHTED && (alpha_den < 1 || alpha_num < 0 || alpha_num > alpha_den))
+    return setf(g, FT_EINVAL, "alpha must be in [0, 1]");
+  g->heur_policy = policy;
+  if (policy == FT_HEUR_WEIGHTED) {
+    g->heur_num = alpha_num;
+    g->heur_den = alpha_den;
+  }
   return FT_OK;
 }
 

@@ -157,3 +157,31 @@ def test_c5_full_every_step(ft):
     assert np.array_equal(om, gm) and np.array_equal(ot, gt)
     for i in np.linspace(0, len(om) - 1, 48).astype(int):
         assert np.array_equal(og.strategy(int(i)), g.strategy(int(i)))
+
+
+@pytest.mark.parametrize("policy,layers", [("min_memory", 24), ("weighted", 6)])
+def test_c4_full_k36_mask_heuristic(ft, policy, layers):
+    """BERT-large (C4; all 24 layers for the default rule) with a K = 36
+    attention mask: only heuristic elimination linearises it.
+    Every step bit-exact against the oracle under both configuration rules
+    (R17, R22)."""
+    import os
+    import paper_2004_10856_b200 as ftm
+    w = G.c4(mask_k1=False, layers=layers)
+    og = oracle.load(w, threads=len(os.sched_getaffinity(0)))
+    og.set_heuristic(policy)
+    og.eliminate(oracle.AUTO_HEUR)
+    om, ot = og.frontier()
+    g = ft.load(w, keep_all=True)
+    g.set_heuristic(policy)
+    g.eliminate(ftm.AUTO_HEUR)
+    gm, gt = g.frontier()
+    st = g.stats()
+    assert og.num_steps() == len(st)
+    assert sum(s["kind"] == "fold" for s in st) == layers  # one heuristic elimination, one fold per consumer
+    for s in range(len(st)):
+        for x, y in zip(og.step_output(s), g.step_output(s)):
+            assert np.array_equal(x, y), s
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+    for i in np.linspace(0, len(om) - 1, 24).astype(int):
+        assert np.array_equal(og.strategy(int(i)), g.strategy(int(i)))

@@ -266,28 +266,67 @@ __global__ void __launch_bounds__(256) k_plan(BatchDev B, int32_t* seg_d, int32_
   if (cached)
     for (int i = threadIdx.x; i <= B.nsteps; i += blockDim.x) s_base[i] = B.seg_base[i];
   __syncthreads();
+  // Warps take 32 consecutive segments: each lane first tries the
+  // shared-order node shortcut for its own segment (one thread suffices:
+  // n = X.off[(w+1)K_i] - X.off[w K_i]), then the warp plans the remaining
+  // segments one at a time (plan_seg, lanes over blocks).
+  const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wglob = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int j = 0;
   int64_t sb = 0, se = -1;
-  for (int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gs < B.nseg; gs += nwarps) {
-    if (gs < sb || gs >= se) {
-      if (cached) {
-        int lo = 0, hi = B.nsteps;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_base[mid] <= gs) lo = mid;
-          else hi = mid;
+  unsigned long long my_tuples = 0;
+  // cw segments per warp pass: 32 when segments are plentiful (node waves,
+  // ~1e6 segments), 1 when few (LDP waves: every warp plans its own)
+  int64_t cw = B.nseg / nwarps;
+  cw = cw < 1 ? 1 : (cw > 32 ? 32 : cw);
+  for (int64_t g0 = wglob * cw; g0 < B.nseg; g0 += nwarps * cw) {
+    const int64_t gs = lane < cw ? g0 + lane : B.nseg;
+    bool done = false;
+    if (gs < B.nseg) {
+      if (gs < sb || gs >= se) {
+        if (cached) {
+          int lo = 0, hi = B.nsteps;
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_base[mid] <= gs) lo = mid;
+            else hi = mid;
+          }
+          j = lo;
+          sb = s_base[j];
+          se = s_base[j + 1];
+        } else {
+          j = find_base(B.seg_base, B.nsteps, gs);
+          sb = B.seg_base[j];
+          se = B.seg_base[j + 1];
         }
-        j = lo;
-        sb = s_base[j];
-        se = s_base[j + 1];
-      } else {
-        j = find_base(B.seg_base, B.nsteps, gs);
-        sb = B.seg_base[j];
-        se = B.seg_base[j + 1];
+      }
+      const StepDev& s = B.steps[j];
+      if (s.node_shared && s.nblk <= NS_MAXBLK && s.KB == s.nblk) {
+        const int64_t w = (s.seg_lo + (gs - sb)) / s.KC;
+        const int64_t rel = s.X.off[(w + 1) * s.KB] - s.X.off[w * s.KB];
+        if (rel <= NS_CAP) {
+          seg_d[gs] = SPECIAL_LEVEL;
+          seg_n[gs] = (int32_t)rel;
+          seg_tuples[gs] = rel;
+          my_tuples += (unsigned long long)rel;
+          done = true;
+        }
       }
     }
-    plan_seg(B, gs, j, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+    unsigned todo = __ballot_sync(0xffffffffu, gs < B.nseg && !done);  // lanes >= cw: gs = nseg
+    while (todo) {
+      const int b = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int jb = __shfl_sync(0xffffffffu, j, b);
+      plan_seg(B, g0 + b, jb, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_tuples += __shfl_xor_sync(0xffffffffu, my_tuples, o);
+  if (lane == 0 && my_tuples) {
+    atomicAdd(&sh_tuples, my_tuples);
+    atomicAdd(&sh_direct[0], my_tuples);  // level-0 pool capacity
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -383,6 +422,21 @@ __device__ __forceinline__ void cta_bitonic_regs(int64_t (&m)[R], int64_t (&t)[R
   }
 }
 
+template <int R, int JR>
+__device__ __forceinline__ void cta_keys_rows(uint64_t (&k)[R], int kk, int eb) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r & JR) continue;
+    const int r2 = r | JR;
+    if (r2 >= R) continue;
+    const bool up = ((eb | (r << 5)) & kk) == 0;
+    const uint64_t a = k[r], b = k[r2];
+    const bool sw = up ? (b < a) : (a < b);
+    k[r] = sw ? b : a;
+    k[r2] = sw ? a : b;
+  }
+}
+
 // Register-blocked CTA bitonic on single 64-bit keys (same layout as
 // cta_bitonic_regs); xk: N keys of shared memory for the cross-warp stages.
 template <int R>
@@ -406,19 +460,10 @@ __device__ __forceinline__ void cta_bitonic_keys(uint64_t (&k)[R], uint64_t* xk)
           k[r] = (lower == up) ? (pk < k[r] ? pk : k[r]) : (pk > k[r] ? pk : k[r]);
         }
         __syncthreads();
-      } else if (j >= 32) {
+      } else if (j >= 32) {  // rows r, r | jr of this thread (compile-time distances)
         const int jr = j >> 5;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (r & jr) continue;  // jr is a power of two < R
-          const int r2 = r | jr;
-          if (r2 >= R) continue;
-          const bool up = ((eb | (r << 5)) & kk) == 0;
-          const uint64_t a = k[r], b = k[r2];
-          const bool sw = up ? (b < a) : (a < b);
-          k[r] = sw ? b : a;
-          k[r2] = sw ? a : b;
-        }
+        if (jr == 1) cta_keys_rows<R, 1>(k, kk, eb);
+        else if (R >= 4 && jr == 2) cta_keys_rows<R, (R >= 4 ? 2 : 1)>(k, kk, eb);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -800,6 +845,24 @@ __device__ __forceinline__ void warp_bitonic(int64_t (&m)[R], int64_t (&t)[R], u
 }
 
 // Warp bitonic on single 64-bit keys, R rows of 32 (element e = r*32 + lane).
+// Row exchanges (j >= 32) take the row distance as a template parameter so
+// that every register-array index is a compile-time constant (a runtime
+// index would put the array in local memory).
+template <int R, int JR>
+__device__ __forceinline__ void warp_keys_rows(uint64_t (&k)[R], int kk) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r & JR) continue;
+    const int r2 = r | JR;
+    if (r2 >= R) continue;
+    const bool up = ((r << 5) & kk) == 0;
+    const uint64_t a = k[r], b = k[r2];
+    const bool sw = up ? (b < a) : (a < b);
+    k[r] = sw ? b : a;
+    k[r2] = sw ? a : b;
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&k)[R]) {
   const int lane = threadIdx.x & 31;
@@ -809,17 +872,10 @@ __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&k)[R]) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
       if (j >= 32) {
         const int jr = j >> 5;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (r & jr) continue;
-          const int r2 = r | jr;
-          if (r2 >= R) continue;
-          const bool up = ((r << 5) & kk) == 0;
-          const uint64_t a = k[r], b = k[r2];
-          const bool sw = up ? (b < a) : (a < b);
-          k[r] = sw ? b : a;
-          k[r2] = sw ? a : b;
-        }
+        if (jr == 1) warp_keys_rows<R, 1>(k, kk);
+        else if (R >= 4 && jr == 2) warp_keys_rows<R, (R >= 4 ? 2 : 1)>(k, kk);
+        else if (R >= 8 && jr == 4) warp_keys_rows<R, (R >= 8 ? 4 : 1)>(k, kk);
+        else if (R >= 16) warp_keys_rows<R, (R >= 16 ? 8 : 1)>(k, kk);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -835,6 +891,116 @@ __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&k)[R]) {
 
 constexpr int WARP_BLK_CACHE = 64;
 constexpr size_t DW_SMEM = 8 * 2 * WARP_DIRECT * 8;  // t/id staging of k_direct_warp  // block descriptors cached per warp
+
+// Alg. 1 sweep over R rows of 32 sorted elements (element e = r*32 + lane,
+// t[r] in order; padding t = INF) and ballot compaction into the level pool;
+// out(r, d) writes element (r, lane) to pool slot d.
+template <int R, typename Out>
+__device__ __forceinline__ void warp_sweep_write(const LevelDev& L, int64_t gs, int n, const int64_t (&t)[R],
+                                                 Out out) {
+  const int lane = threadIdx.x & 31;
+  long long carry = INF;
+  unsigned keep = 0;  // bit r: element (r, lane) kept
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long inc = warp_incl_min(t[r]);
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = INF;
+    const long long v = ex < carry ? ex : carry;
+    const bool k = ((r << 5) | lane) < n && t[r] < v;
+    keep |= (unsigned)k << r;
+    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
+    carry = rowmin < carry ? rowmin : carry;
+    cnt += __popc(__ballot_sync(0xffffffffu, k));
+  }
+  int64_t base = 0;
+  if (lane == 0) {
+    unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
+    if ((int64_t)(st0 + cnt) > L.out.cap) {
+      atomicExch(&L.hdr->overflow, 1ull);
+      base = -1;
+    } else {
+      base = (int64_t)st0;
+    }
+    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)cnt);
+    L.out.start[gs] = base;
+    L.out.cnt[gs] = cnt;
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (base < 0) return;
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool k = (keep >> r) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, k);
+    if (k) out(r, base + off + __popc(bal & ((1u << lane) - 1u)));
+    off += __popc(bal);
+  }
+}
+
+// Exact (m, t, id) warp bitonic over R rows of 32 elements that carry only
+// (m, e): t and id of element e are staged in wt / wi and read only when two
+// m values are equal (padding: m = INF, ordered by e).  Register footprint:
+// R x (64 + 32) bits, so the full-key sort does not spill.
+template <int R>
+__device__ __forceinline__ bool pair_lt(int64_t ma, int ea, int64_t mb, int eb, const int64_t* wt,
+                                        const uint64_t* wi) {
+  if (ma != mb) return ma < mb;
+  if (ma == INF) return ea < eb;
+  const int64_t ta = wt[ea], tb = wt[eb];
+  if (ta != tb) return ta < tb;
+  return wi[ea] < wi[eb];
+}
+
+template <int R, int JR>
+__device__ __forceinline__ void warp_pairs_rows(int64_t (&m)[R], int (&e)[R], int kk, const int64_t* wt,
+                                                const uint64_t* wi) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r & JR) continue;
+    const int r2 = r | JR;
+    if (r2 >= R) continue;
+    const bool up = ((r << 5) & kk) == 0;
+    const bool sw = up ? pair_lt<R>(m[r2], e[r2], m[r], e[r], wt, wi)
+                       : pair_lt<R>(m[r], e[r], m[r2], e[r2], wt, wi);
+    if (sw) {
+      const int64_t a = m[r]; m[r] = m[r2]; m[r2] = a;
+      const int b = e[r]; e[r] = e[r2]; e[r2] = b;
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_bitonic_pairs(int64_t (&m)[R], int (&e)[R], const int64_t* wt,
+                                                   const uint64_t* wi) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int kk = 2; kk <= R * 32; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+        if (jr == 1) warp_pairs_rows<R, 1>(m, e, kk, wt, wi);
+        else if (R >= 4 && jr == 2) warp_pairs_rows<R, (R >= 4 ? 2 : 1)>(m, e, kk, wt, wi);
+        else if (R >= 8 && jr == 4) warp_pairs_rows<R, (R >= 8 ? 4 : 1)>(m, e, kk, wt, wi);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t pm = __shfl_xor_sync(0xffffffffu, m[r], j);
+          const int pe = __shfl_xor_sync(0xffffffffu, e[r], j);
+          const int x = (r << 5) | lane;
+          const bool up = (x & kk) == 0, lower = (x & j) == 0;
+          const bool p_lt = pair_lt<R>(pm, pe, m[r], e[r], wt, wi);
+          if ((lower == up) ? p_lt : !p_lt) {
+            m[r] = pm;
+            e[r] = pe;
+          }
+        }
+      }
+    }
+  }
+}
 
 template <int R>
 __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs, int n, int* wpre,
@@ -863,9 +1029,8 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
   }
   if (lane == 0) wpre[0] = 0;
   __syncwarp();
-  int64_t m[R], t[R];
-  uint64_t id[R];
   // tuple e of the sample (block: largest lo with wpre[lo] <= e)
+  const StepDev* sp = &s;
   auto gen = [&](int e, int64_t& vm, int64_t& vt, uint64_t& vi) {
     int lo = 0, hi = nblk;
     while (hi - lo > 1) {
@@ -873,17 +1038,19 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
       if (wpre[mid] <= e) lo = mid;
       else hi = mid;
     }
-    const Blk b = lo < WARP_BLK_CACHE ? wblk[lo] : load_blk(s, sg, lo);
+    const Blk b = lo < WARP_BLK_CACHE ? wblk[lo] : load_blk(*sp, sg, lo);
     const int rr = e - wpre[lo];
     const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
     const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
-    make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
+    make_tuple(*sp, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
                samp_idx(jz, b.n[2], st), vm, vt, vi);
   };
-  // sort 64-bit keys ((m - m0) << 9 | e), m0 = the sample's least m, with t
-  // and id staged in wt/wi; a sample whose m span needs more than B.kspan
-  // bits (frontier m reaches 2^60, R10), or with equal m values (detected
-  // after the sort), takes the full (m, t, id) sort instead
+  // Sort 64-bit keys ((m - m0) << 9 | e), m0 = the sample's least m, with t
+  // and id staged in wt/wi by e; after the sort an element carries (m, e).
+  // A sample whose m span needs more than B.kspan bits (frontier m reaches
+  // 2^60, R10), or with equal m values (detected after the sort: the key
+  // order is then not the (m, t, id) order), is (re)sorted exactly on (m, e)
+  // pairs with t / id looked up by e on equal m (warp_bitonic_pairs).
   uint64_t k[R];
   long long lmin = INF, lmax = -1;
 #pragma unroll
@@ -911,8 +1078,10 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
     lmax = b > lmax ? b : lmax;
   }
   const bool wide = ((unsigned long long)(lmax - lmin) >> B.kspan) != 0;
-  bool tie = wide;
   __syncwarp();
+  int64_t m[R];
+  int ix[R];
+  bool tie = false;
   if (!wide) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -923,100 +1092,34 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int e = (r << 5) | lane;
-      m[r] = INF;
-      t[r] = INF;
-      id[r] = ~0ull;
-      if (e < n) {
-        const int src = (int)(k[r] & 511u);
-        m[r] = (int64_t)(k[r] >> 9) + lmin;
-        t[r] = wt[src];
-        id[r] = wi[src];
-      }
       uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
       const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
       if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
       if (e < n && prev != ~0ull && (prev >> 9) == (k[r] >> 9)) tie = true;
+      m[r] = e < n ? (int64_t)(k[r] >> 9) + lmin : INF;
+      ix[r] = e < n ? (int)(k[r] & 511u) : e;
     }
-  }
-  if (__any_sync(0xffffffffu, tie)) {
+  } else {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      m[r] = INF;
-      t[r] = INF;
-      id[r] = ~0ull;
+      const int e = (r << 5) | lane;
+      m[r] = e < n ? (int64_t)k[r] : INF;
+      ix[r] = e;
     }
-#pragma unroll 1
-  for (int r = 0; r < R && (r << 5) < n; ++r) {
-    const int e = (r << 5) | lane;
-    if (e < n) {
-      int lo = 0, hi = nblk;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (wpre[mid] <= e) lo = mid;
-        else hi = mid;
+  }
+  if (__any_sync(0xffffffffu, tie || wide)) warp_bitonic_pairs<R>(m, ix, wt, wi);  // exact (m, t, id)
+  int64_t t[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) t[r] = ((r << 5) | lane) < n ? wt[ix[r]] : INF;
+  warp_sweep_write<R>(L, gs, n, t, [&](int r, int64_t d) {
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (q == r) {
+        L.out.m[d] = m[q];
+        L.out.t[d] = t[q];
+        L.out.id[d] = wi[ix[q]];
       }
-      const Blk b = lo < WARP_BLK_CACHE ? wblk[lo] : load_blk(s, sg, lo);
-      const int rr = e - wpre[lo];
-      const int cy = (int)samp_cnt(b.n[1], st), cz = (int)samp_cnt(b.n[2], st);
-      const int jz = rr % cz, q = rr / cz, jy = q % cy, jx = q / cy;
-      int64_t vm, vt;
-      uint64_t vi;
-      make_tuple(s, b, rel[lo], samp_idx(jx, b.n[0], st), samp_idx(jy, b.n[1], st),
-                 samp_idx(jz, b.n[2], st), vm, vt, vi);
-#pragma unroll
-      for (int q2 = 0; q2 < R; ++q2)
-        if (q2 == r) {
-          m[q2] = vm;
-          t[q2] = vt;
-          id[q2] = vi;
-        }
-    }
-  }
-    __syncwarp();
-    warp_bitonic<R>(m, t, id);
-  }
-  // Alg. 1 sweep in e order: keep iff t < min of all earlier t
-  long long carry = INF;
-  bool keep[R];
-  int cnt = 0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const long long inc = warp_incl_min(t[r]);
-    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) ex = INF;
-    const long long v = ex < carry ? ex : carry;
-    keep[r] = ((r << 5) | lane) < n && t[r] < v;
-    const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
-    carry = rowmin < carry ? rowmin : carry;
-    cnt += __popc(__ballot_sync(0xffffffffu, keep[r]));
-  }
-  int64_t base = 0;
-  if (lane == 0) {
-    unsigned long long st0 = atomicAdd(L.out.cursor, (unsigned long long)cnt);
-    if ((int64_t)(st0 + cnt) > L.out.cap) {
-      atomicExch(&L.hdr->overflow, 1ull);
-      base = -1;
-    } else {
-      base = (int64_t)st0;
-    }
-    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)cnt);
-    L.out.start[gs] = base;
-    L.out.cnt[gs] = cnt;
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (base < 0) return;
-  int off = 0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
-    if (keep[r]) {
-      const int64_t d = base + off + __popc(bal & ((1u << lane) - 1u));
-      L.out.m[d] = m[r];
-      L.out.t[d] = t[r];
-      L.out.id[d] = id[r];
-    }
-    off += __popc(bal);
-  }
+  });
 }
 
 __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) {
@@ -1627,16 +1730,18 @@ __global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
 }
 
 // Long factor = the one with most sampled indices; runs = product of the other two.
-__device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa, int& fb,
-                                          int64_t* c) {
-  c[0] = samp_cnt(b.n[0], st);
-  c[1] = samp_cnt(b.n[1], st);
-  c[2] = samp_cnt(b.n[2], st);
+__device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa, int& fb, int64_t& cL,
+                                          int64_t& cA, int64_t& cB) {
+  // scalars and selects only: an indexed local array would live in local memory
+  const int64_t c0 = samp_cnt(b.n[0], st), c1 = samp_cnt(b.n[1], st), c2 = samp_cnt(b.n[2], st);
   lf = 0;
-  if (c[1] > c[lf]) lf = 1;
-  if (c[2] > c[lf]) lf = 2;
+  if (c1 > c0) lf = 1;
+  if (c2 > (lf == 1 ? c1 : c0)) lf = 2;
   fa = lf == 0 ? 1 : 0;
   fb = lf == 2 ? 1 : 2;
+  cL = lf == 0 ? c0 : (lf == 1 ? c1 : c2);
+  cA = fa == 0 ? c0 : c1;
+  cB = fb == 2 ? c2 : c1;
 }
 
 // Work items of the filter: L.run_item consecutive sampled indices of one run
@@ -1665,9 +1770,9 @@ struct LoadWork {
     if (is_filter(L.seg_d[B.seg_base[j] + li], L.level)) {
       Blk b = load_blk(s, s.seg_lo + li, k);
       int lf, fa, fb;
-      int64_t c[3];
-      run_shape(b, L.st, lf, fa, fb, c);
-      w = c[fa] * c[fb] * ((c[lf] + L.run_item - 1) / L.run_item);
+      int64_t cL, cA, cB;
+      run_shape(b, L.st, lf, fa, fb, cL, cA, cB);
+      w = cA * cB * ((cL + L.run_item - 1) / L.run_item);
     }
     L.wcnt[beta] = w;
     return w;
@@ -1725,8 +1830,8 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     const Blk b = load_blk(s, s.seg_lo + li0, k);
     const int64_t rel = L.blk_rel[beta];
     int lf, fa, fb;
-    int64_t c[3];
-    run_shape(b, sh, lf, fa, fb, c);
+    int64_t cL, cA, cB;
+    run_shape(b, sh, lf, fa, fb, cL, cA, cB);
     // factor pointers without dynamic register-array indexing
     const int64_t* const fm[3] = {s.X.m, s.Y.m, s.Z.m};
     const int64_t* const ft[3] = {s.X.t, s.Y.t, s.Z.t};
@@ -1736,8 +1841,6 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     const int64_t nA = fa == 0 ? b.n[0] : b.n[1];
     const int64_t oB = fb == 2 ? b.o[2] : b.o[1];
     const int64_t nB = fb == 2 ? b.n[2] : b.n[1];
-    const int64_t cL = lf == 0 ? c[0] : (lf == 1 ? c[1] : c[2]);
-    const int64_t cB = fb == 2 ? c[2] : c[1];
     const int64_t RI = L.run_item;
     const int64_t nch = (cL + RI - 1) / RI;
     int64_t run, ch, ja, jb;
@@ -2525,9 +2628,13 @@ int64_t scan_tmp_elems(int64_t n) { return ntiles_cap_slot(n) + 8; }
 // Grow-only scratch with geometric growth: reallocation happens O(log size)
 // times per process, not per step.  Callers have synchronised the stream
 // since the buffer's last use (every wave ends with a stream sync).
-static cudaError_t grow_raw(const DevAlloc& A, cudaStream_t st, void** p, size_t* have, size_t need) {
+static cudaError_t grow_raw(const DevAlloc& A, cudaStream_t st, void** p, size_t* have, size_t need,
+                            size_t hw) {
   if (need <= *have && *p) return cudaSuccess;
-  size_t nb = std::max<size_t>({need, 2 * *have, (size_t)1 << 16});
+  // after a release (hooked runners hand their scratch back when their last
+  // graph goes), the first growth goes straight to the previous capacity:
+  // one allocation of a size a caching allocator has seen before
+  size_t nb = std::max<size_t>({need, 2 * *have, (size_t)1 << 16, hw});
   if (*p) {
     A.put(*p, st, true);
     *p = nullptr;
@@ -2540,7 +2647,7 @@ static cudaError_t grow_raw(const DevAlloc& A, cudaStream_t st, void** p, size_t
 
 #define GROW(buf, T, n)                                                         \
   do {                                                                          \
-    cudaError_t e__ = grow_raw(alloc, st, (void**)&buf.p, &buf.bytes, sizeof(T) * (size_t)(n)); \
+    cudaError_t e__ = grow_raw(alloc, st, (void**)&buf.p, &buf.bytes, sizeof(T) * (size_t)(n), buf.hw); \
     if (e__ != cudaSuccess) return e__;                                         \
   } while (0)
 
@@ -2576,6 +2683,7 @@ void StepRunner::release_device() {
   for (Buf* b : all) {
     if (b->p) alloc.put(b->p, nullptr, true);
     b->p = nullptr;
+    b->hw = std::max(b->hw, b->bytes);
     b->bytes = 0;
   }
 }

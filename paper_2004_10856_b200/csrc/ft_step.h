@@ -137,6 +137,7 @@ class StepRunner {
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
+    size_t hw = 0;  // capacity before the last release_device: re-grown in one step
   };
   Buf seg_d, seg_n, blk_rel, seg_tuples, hdr;
   Buf poolA_m, poolA_t, poolA_id, poolA_start, poolA_cnt;

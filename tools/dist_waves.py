@@ -33,13 +33,26 @@ for it in range(3):
     wall = (time.perf_counter() - t0) * 1e3
     st = g.stats()
     g.close()
+waves = {}
+for s in st:
+    waves.setdefault(s["wave"], s)
+ids = sorted(waves)
+# per-rank kernel / comm / host time of every wave -> rank 0 (imbalance)
+loc = torch.tensor([[waves[w]["kernel_ms"], waves[w]["comm_ms"], waves[w]["host_ms"]] for w in ids],
+                   dtype=torch.float64, device="cuda")
+allr = [torch.zeros_like(loc) for _ in range(world)]
+dist.all_gather(allr, loc)
 if rank == 0:
-    waves = {}
-    for s in st:
-        waves.setdefault(s["wave"], s)
-    tk = sum(s["kernel_ms"] for s in waves.values())
-    tc = sum(s["comm_ms"] for s in waves.values())
-    print(f"{name} N={world} wall {wall:.1f} ms, sum kernel {tk:.1f} ms, sum comm {tc:.1f} ms, waves {len(waves)}")
-    for wv, s in sorted(waves.items(), key=lambda x: -(x[1]["kernel_ms"] + x[1]["comm_ms"]))[:12]:
-        print(f"  wave {wv:3d} {s['kind']:5s} nseg {s['nseg']:8d} kernel {s['kernel_ms']:.3f} comm {s['comm_ms']:.3f}"
-              f" host {s['host_ms']:.3f} launches {s['launches']}")
+    A = torch.stack(allr).cpu().numpy()  # [rank, wave, 3]
+    tk = A[:, :, 0].max(0).sum()
+    tc = A[:, :, 1].max(0).sum()
+    print(f"{name} N={world} wall {wall:.1f} ms, sum over waves of max-rank kernel {tk:.1f} ms, "
+          f"comm {tc:.1f} ms, waves {len(ids)}; mean-rank kernel {A[:, :, 0].mean(0).sum():.1f} ms")
+    order = sorted(range(len(ids)), key=lambda i: -A[:, i, 0].max())
+    for i in order[:16]:
+        s = waves[ids[i]]
+        ks = " ".join(f"{x:.3f}" for x in A[:, i, 0])
+        print(f"  wave {ids[i]:3d} {s['kind']:5s} nseg {s['nseg']:8d} kernel/rank [{ks}] comm {A[:, i, 1].max():.3f}"
+              f" launches {s['launches']}")
+ft.nccl_comm_destroy(comm)
+dist.destroy_process_group()

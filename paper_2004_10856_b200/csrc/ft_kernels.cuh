@@ -146,6 +146,8 @@ struct LevelDev {
   int64_t* gflag;        // keep flags (0/1), scanned in place -> positions
   int64_t* large_list;
   unsigned long long* large_n;
+  int32_t* whint;        // [hcap] block of filter item 32c (k_filter warp starts)
+  int64_t hcap;
   int64_t* scratch;      // global-memory sort scratch (huge buckets)
   int64_t scratch_cap;
   StepHdr* hdr;

@@ -45,9 +45,15 @@ struct LoadArr {
   __device__ __forceinline__ long long operator()(int64_t i) const { return (long long)p[i]; }
 };
 
-template <typename Load>
+// Optional per-element epilogue of the scan: post(i, exclusive prefix, value).
+struct NoPost {
+  __device__ __forceinline__ void operator()(int64_t, long long, long long) const {}
+};
+
+template <typename Load, typename Post = NoPost>
 __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev, int64_t n_host,
-                                                   int64_t* out, unsigned long long* state) {
+                                                   int64_t* out, unsigned long long* state,
+                                                   Post post = Post()) {
   __shared__ long long sh[33];
   __shared__ int64_t s_tile;
   __shared__ long long s_pre;
@@ -103,7 +109,10 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
     ex += s_pre;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-      if (base + i < n) out[base + i] = ex;
+      if (base + i < n) {
+        out[base + i] = ex;
+        post(base + i, ex, v[i]);
+      }
       ex += v[i];
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
@@ -125,13 +134,13 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
 
 // tmp: >= scan_tmp_elems(n_cap) int64 slots, zero on first use (`fresh`
 // zeroes it here); every scan leaves it zeroed again.
-template <typename Load>
+template <typename Load, typename Post = NoPost>
 void scan_excl_fn(Load ld, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tmp,
-                  cudaStream_t st, bool fresh = false) {
+                  cudaStream_t st, bool fresh = false, Post post = Post()) {
   const int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
   if (fresh) cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 2), st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
-  k_scan1<Load><<<grid, SCAN_NT, 0, st>>>(ld, n_dev, n_cap, out, (unsigned long long*)tmp);
+  k_scan1<Load, Post><<<grid, SCAN_NT, 0, st>>>(ld, n_dev, n_cap, out, (unsigned long long*)tmp, post);
 }
 
 template <typename TIn>
@@ -1779,6 +1788,18 @@ struct LoadWork {
   }
 };
 
+// Epilogue of the work-offset scan: block beta covers filter items
+// [wo[beta], wo[beta] + count); record it as the block of every item c*32
+// (a warp's first item) in that range, so k_filter finds a warp's blocks
+// with two loads instead of two binary searches over all blocks.
+struct PostHint {
+  int32_t* hint;
+  int64_t hcap;
+  __device__ __forceinline__ void operator()(int64_t beta, long long ex, long long v) const {
+    for (long long c = (ex + 31) >> 5; c < hcap && (c << 5) < ex + v; ++c) hint[c] = (int32_t)beta;
+  }
+};
+
 // K1: product + pre-filter, output-sensitive run walk.  A work item is a
 // range of one run (short-factor indices fixed, long factor sweeping: m
 // strictly ascending, t strictly descending).  For element x let g be the
@@ -1787,7 +1808,7 @@ struct LoadWork {
 // later element with t >= t_g (their m exceeds m_g), so the walk jumps to
 // the first element with t < t_g (binary search on t).  Otherwise x is a
 // candidate: emitted with bucket = #G points with m <= m_x.
-__global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
+__device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L) {
   namespace cg = cooperative_groups;
   if (L.hdr->overflow) return;
   const int64_t nbl = B.nblk;
@@ -1798,24 +1819,33 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
   for (int64_t wbase = (int64_t)blockIdx.x * blockDim.x; wbase < W; wbase += gstride) {
     const int64_t w0 = wbase + (threadIdx.x & ~31);  // first item of this warp
     if (w0 >= W) break;
-    // blocks of the warp's first and last items (two full binary searches per
-    // warp), then a bounded binary search per lane
-    int64_t lo = 0;
-    if (lane == 0 || lane == 31) {
-      const int64_t x = lane == 0 ? w0 : min(w0 + 31, W - 1);
-      int64_t hi = nbl;  // largest beta with wo[beta] <= x
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (L.wo[mid] <= x) lo = mid;
-        else hi = mid;
+    // blocks of the warp's items: hint[w0/32] holds the block of item w0 and
+    // hint[w0/32 + 1] that of item w0 + 32 (the scan's epilogue, PostHint);
+    // beyond the hint table, two full binary searches per warp.  Then a
+    // bounded binary search per lane.
+    const int64_t c0 = w0 >> 5;
+    int64_t blo, bhi;  // wo[blo] <= w0 + lane < wo[bhi]
+    if (c0 + 1 < L.hcap) {
+      blo = L.whint[c0];
+      bhi = w0 + 32 < W ? (int64_t)L.whint[c0 + 1] + 1 : nbl;
+    } else {
+      int64_t lo = 0;
+      if (lane == 0 || lane == 31) {
+        const int64_t x = lane == 0 ? w0 : min(w0 + 31, W - 1);
+        int64_t hi = nbl;  // largest beta with wo[beta] <= x
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (L.wo[mid] <= x) lo = mid;
+          else hi = mid;
+        }
       }
+      blo = __shfl_sync(0xffffffffu, lo, 0);
+      bhi = __shfl_sync(0xffffffffu, lo, 31) + 1;
     }
-    const int64_t blo = __shfl_sync(0xffffffffu, lo, 0);
-    const int64_t bhi = __shfl_sync(0xffffffffu, lo, 31);
     const int64_t w = w0 + lane;
     if (w >= W) continue;
-    lo = blo;
-    int64_t hi = bhi + 1;  // wo[lo] <= w < wo[hi]
+    int64_t lo = blo;
+    int64_t hi = bhi;  // wo[lo] <= w < wo[hi]
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
       if (L.wo[mid] <= w) lo = mid;
@@ -1946,12 +1976,23 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
         continue;
       }
       c_elem += je - jj;
-      // element-level test of the chunk: p = #G points with m <= m_x
+      // element-level test of the chunk: p = #G points with m <= m_x; the
+      // run elements are loaded 4 at a time ahead of the (dependent) G walk
       int64_t p = q;
-      for (int64_t j = jj; j < je; ++j) {
-        const int64_t il = samp_idx(j, nL, sh);
-        const int64_t m = ms + __ldg(Lm + il);
-        const int64_t t = ts + __ldg(Lt + il);
+      for (int64_t j4 = jj; j4 < je; j4 += 4) {
+      int64_t em[4], et[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t iu = samp_idx(min(j4 + u, je - 1), nL, sh);
+        em[u] = __ldg(Lm + iu);
+        et[u] = __ldg(Lt + iu);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j4 + u >= je) break;
+        const int64_t il = samp_idx(j4 + u, nL, sh);
+        const int64_t m = ms + em[u];
+        const int64_t t = ts + et[u];
         while (p < g && Gm[p] <= m) ++p;
         if (p > 0 && (Gt[p - 1] < t || (Gt[p - 1] == t && Gm[p - 1] < m))) continue;
         int64_t x, y, z;
@@ -1974,6 +2015,7 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
           L.cgb[idx] = gb;
         }
       }
+      }
       jj = je;
     }
     if (L.fstats) {
@@ -1984,6 +2026,11 @@ __global__ void __launch_bounds__(256) k_filter(BatchDev B, LevelDev L) {
     }
   }
 }
+
+// Two register budgets for the same body (A/B: FT_FILTER_REGS=64 selects the
+// 64-register variant, 8 CTAs of 128 threads per SM; default 80 registers).
+__global__ void __launch_bounds__(128, 6) k_filter(BatchDev B, LevelDev L) { filter_body(B, L); }
+__global__ void __launch_bounds__(128, 8) k_filter64(BatchDev B, LevelDev L) { filter_body(B, L); }
 
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
@@ -2679,7 +2726,7 @@ void StepRunner::release_device() {
                 &poolA_cnt, &poolB_m, &poolB_t, &poolB_id, &poolB_start, &poolB_cnt, &cursors,
                 &nb, &bucket_base, &wcnt, &wo, &bcount, &bmin, &boff, &bcarry, &cm, &ct, &cid,
                 &cgb, &gm, &gt, &gid, &gflag, &large_list, &scan_tmp, &ncand,
-                &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev, &packs_dev, &big_dev};
+                &dst_off, &steps_dev, &base_dev, &pos, &step_arr, &groups_dev, &packs_dev, &big_dev, &whint};
   for (Buf* b : all) {
     if (b->p) alloc.put(b->p, nullptr, true);
     b->p = nullptr;
@@ -2818,6 +2865,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     plan_copy[l] = hdr_host->direct_samp[l];
     plan_copy[LMAX + 1 + l] = hdr_host->filter_samp[l];
   }
+  // warp-start hints of the filter items (PostHint): W <= the level's sample
+  // (an item holds >= 1 sampled element), capped at 4 M entries (16 MB);
+  // warps beyond it search
+  const int64_t hcap = nbl < ((int64_t)1 << 31) ? std::min<int64_t>(need_filter / 32 + 2, 1 << 22) : 0;
   for (int attempt = 0;; ++attempt) {
     const int64_t cand_cap = std::min<int64_t>(need_filter, cand_budget);
     need_out = 0;
@@ -2855,6 +2906,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(gid, uint64_t, cand_cap);
       GROW(gflag, int64_t, cand_cap + 1);
       GROW(large_list, int64_t, bcap);
+      GROW(whint, int32_t, hcap);
       GROW(ncand, int64_t, 2);
     }
     const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
@@ -2932,15 +2984,18 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         L.gflag = (int64_t*)gflag.p;
         L.large_list = (int64_t*)large_list.p;
         L.large_n = cur + 3;
+        L.whint = (int32_t*)whint.p;
+        L.hcap = hcap;
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
         nl += 4;  // scan(+nb), bucket_init, scan(+work counts), filter
         scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
         k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
-        scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st);
+        scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st, false, PostHint{L.whint, L.hcap});
         mark(2);  // filter_ms: k_filter alone
-        k_filter<<<filter_grid, filter_nt, 0, st>>>(s, L);
+        if (filter_regs64) k_filter64<<<filter_grid, 128, 0, st>>>(s, L);
+        else k_filter<<<filter_grid, 128, 0, st>>>(s, L);
         // bucket offsets over B buckets (B on device)
         mark(3);
         nl += 5;  // scan, carry, scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
@@ -3084,8 +3139,8 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
   if (const char* e = getenv("FT_PACK_GRID")) pack_grid = std::max(1, atoi(e));  // tests: packs per CTA
-  if (const char* e = getenv("FT_FILTER_NT")) filter_nt = std::max(32, std::min(256, atoi(e) / 32 * 32));
-  filter_grid = 148 * 128 * (256 / filter_nt);
+  filter_regs64 = getenv("FT_FILTER_REGS") && atoi(getenv("FT_FILTER_REGS")) == 64;
+  filter_grid = 148 * 256;
   if (const char* e = getenv("FT_FILTER_GRID")) filter_grid = std::max(148, atoi(e));
   if (const char* e = getenv("FT_ITEM_MAX")) item_max = std::max(16, atoi(e));
   if (const char* e = getenv("FT_ITEM_DIV")) item_div = std::max(1, atoi(e));

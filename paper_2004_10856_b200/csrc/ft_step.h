@@ -120,7 +120,7 @@ class StepRunner {
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int pack_grid = 148 * 4;             // CTAs of k_node_pack (each takes a contiguous pack range)
-  int filter_nt = 128;                 // threads per k_filter CTA (A/B: 128 >= 256 > 64)
+  bool filter_regs64 = false;          // k_filter64 (64 registers) instead of k_filter (80)
   int item_max = 512;                 // filter work item: max sampled run elements
   int item_div = 4;                   // ... and target items per resident thread
   unsigned long long fstat_acc[4] = {0, 0, 0, 0};
@@ -144,7 +144,7 @@ class StepRunner {
   Buf poolB_m, poolB_t, poolB_id, poolB_start, poolB_cnt;
   Buf cursors, nb, bucket_base, wcnt, wo, bcount, bmin, boff, bcarry;
   Buf cm, ct, cid, cgb, gm, gt, gid, gflag, large_list, scan_tmp, ncand, dst_off;
-  Buf steps_dev, base_dev, pos, step_arr, groups_dev, packs_dev, big_dev;
+  Buf steps_dev, base_dev, pos, step_arr, groups_dev, packs_dev, big_dev, whint;
   std::vector<int64_t> step_host;
   int64_t* step_host_p = nullptr;
   std::vector<int64_t> h_base;

@@ -531,11 +531,36 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
       return (double)g->steps[S.step].st.survivors / (double)std::max<int64_t>(S.nseg, 1);
     };
     std::vector<int64_t> w(NS, 1);
-    for (int q = 0; q < ns; ++q) {
-      const StepRec& r = g->steps[ids[q]];
-      const double e = (double)r.nblk * mean_sz(r.X) * mean_sz(r.Y) * mean_sz(r.Z);
-      const int64_t wi = std::max<int64_t>(1, (int64_t)std::min(e, 4e18 / (double)std::max<int64_t>(NS, 1)));
-      for (int64_t sg = 0; sg < r.nseg; ++sg) w[sbase[q] + sg] = wi;
+    int64_t blocks = 0;
+    for (int q = 0; q < ns; ++q) blocks += g->steps[ids[q]].nseg * g->steps[ids[q]].nblk;
+    if (ns <= 8 && blocks <= (1 << 22)) {
+      // few steps (LDP waves, the big ones): exact product tuples per segment
+      // from the (replicated) input offsets -- segment costs differ by
+      // several x within a step, and the slowest rank sets the wave's time
+      for (int q = 0; q < ns; ++q) {
+        const StepRec& r = g->steps[ids[q]];
+        int rc;
+        if ((rc = ensure_off(g, r.X)) || (rc = ensure_off(g, r.Y)) || (rc = ensure_off(g, r.Z))) return rc;
+        const FSet &X = g->sets[r.X], &Y = g->sets[r.Y], &Z = g->sets[r.Z];
+        const double cap = 4e18 / (double)std::max<int64_t>(NS, 1);
+        for (int64_t sg = 0; sg < r.nseg; ++sg) {
+          double e = 0;
+          for (int64_t k = 0; k < r.nblk; ++k) {
+            int64_t sx, sy, sz;
+            host_block_segs(r, sg, k, sx, sy, sz);
+            e += (double)(X.off[sx + 1] - X.off[sx]) * (double)(Y.off[sy + 1] - Y.off[sy]) *
+                 (double)(Z.off[sz + 1] - Z.off[sz]);
+          }
+          w[sbase[q] + sg] = std::max<int64_t>(1, (int64_t)std::min(e, cap));
+        }
+      }
+    } else {
+      for (int q = 0; q < ns; ++q) {
+        const StepRec& r = g->steps[ids[q]];
+        const double e = (double)r.nblk * mean_sz(r.X) * mean_sz(r.Y) * mean_sz(r.Z);
+        const int64_t wi = std::max<int64_t>(1, (int64_t)std::min(e, 4e18 / (double)std::max<int64_t>(NS, 1)));
+        for (int64_t sg = 0; sg < r.nseg; ++sg) w[sbase[q] + sg] = wi;
+      }
     }
     ft_shard_plan(NS, w.data(), world, lo.data());
   }
@@ -607,33 +632,39 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     const int wi = (int)g->waves.size();
     g->waves.emplace_back();
     WaveBuf& wb = g->waves.back();
+    // Exchange by two all-gathers: (1) every rank's per-segment
+    // {survivor counts, product tuples}, padded to the largest rank range;
+    // every rank scans them into the same arena offsets; (2) every rank's
+    // survivors, staged contiguously and padded to the largest rank total,
+    // then unpacked into the arena (one collective each instead of one
+    // broadcast per root and array).
     int64_t *cntg = nullptr, *tupg = nullptr, *pos = nullptr, *sb = nullptr, *stats = nullptr,
-            *tmp = nullptr;
+            *tmp = nullptr, *hloc = nullptr, *hall = nullptr, *lod = nullptr, *posd = nullptr;
     Temps tmps{g->alloc, g->stream};
     const int64_t nloc = lo[rank + 1] - lo[rank];
+    int64_t maxloc = 1;
+    for (int q = 0; q < world; ++q) maxloc = std::max<int64_t>(maxloc, lo[q + 1] - lo[q]);
     CU(tmps.get(&cntg, sizeof(int64_t) * std::max<int64_t>(NS, 1)), "alloc");
     CU(tmps.get(&tupg, sizeof(int64_t) * std::max<int64_t>(NS, 1)), "alloc");
     CU(tmps.get(&pos, sizeof(int64_t) * (NS + 1)), "alloc");
     CU(tmps.get(&sb, sizeof(int64_t) * (ns + 1)), "alloc");
     CU(tmps.get(&stats, sizeof(int64_t) * 3 * ns), "alloc");
     CU(tmps.get(&tmp, sizeof(int64_t) * ftk::scan_tmp_elems(NS + 1)), "alloc");
+    CU(tmps.get(&hloc, sizeof(int64_t) * 2 * maxloc), "alloc");
+    CU(tmps.get(&hall, sizeof(int64_t) * 2 * maxloc * world), "alloc");
+    CU(tmps.get(&lod, sizeof(int64_t) * 2 * (world + 1)), "alloc");
+    posd = lod + world + 1;
     CU(g->alloc.get((void**)&wb.off, sizeof(int64_t) * (NS + ns), g->stream), "alloc frontier");
     if (nloc > 0) {
-      CU(cudaMemcpyAsync(cntg + lo[rank], res.dev_cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice,
-                         g->stream), "counts");
-      CU(cudaMemcpyAsync(tupg + lo[rank], res.dev_tup, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice,
-                         g->stream), "counts");
+      CU(cudaMemcpyAsync(hloc, res.dev_cnt, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice, g->stream), "counts");
+      CU(cudaMemcpyAsync(hloc + maxloc, res.dev_tup, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice, g->stream),
+         "counts");
     }
-    ncclResult_t nr = ncclGroupStart();
-    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
-      const int64_t n = lo[q + 1] - lo[q];
-      if (n <= 0) continue;
-      nr = ncclBroadcast(cntg + lo[q], cntg + lo[q], n, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(tupg + lo[q], tupg + lo[q], n, ncclInt64, q, g->comm, g->stream);
-    }
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
-    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    CU(cudaMemcpyAsync(lod, lo.data(), sizeof(int64_t) * (world + 1), cudaMemcpyHostToDevice, g->stream), "lo");
     CU(cudaMemcpyAsync(sb, sbase.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, g->stream), "sbase");
+    ncclResult_t nr = ncclAllGather(hloc, hall, 2 * maxloc, ncclInt64, g->comm, g->stream);
+    if (nr != ncclSuccess) return nccl_fail(g, nr);
+    CU(ftk::unpack_counts(hall, maxloc, lod, world, NS, cntg, tupg, g->stream), "unpack counts");
     CU(ftk::wave_offsets(cntg, tupg, NS, ns, sb, pos, wb.off, stats, tmp, g->stream), "wave offsets");
     std::vector<int64_t> hstat(3 * ns), posb(world + 1);
     CU(cudaMemcpyAsync(hstat.data(), stats, sizeof(int64_t) * 3 * ns, cudaMemcpyDeviceToHost, g->stream), "stats");
@@ -643,22 +674,25 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     std::vector<int64_t> sbeg(ns + 1, 0);
     for (int q = 0; q < ns; ++q) sbeg[q + 1] = sbeg[q] + hstat[3 * q];
     const int64_t total = sbeg[ns];
+    int64_t maxn = 1;
+    for (int q = 0; q < world; ++q) maxn = std::max<int64_t>(maxn, posb[q + 1] - posb[q]);
     const size_t nb = sizeof(int64_t) * std::max<int64_t>(total, 1);
     CU(g->alloc.get((void**)&wb.m, nb, g->stream), "alloc frontier");
     CU(g->alloc.get((void**)&wb.t, nb, g->stream), "alloc frontier");
     CU(g->alloc.get((void**)&wb.bp, nb, g->stream), "alloc frontier");
-    CU(ftk::gather_range(res.pool, pos, lo[rank], lo[rank + 1], posb[rank + 1] - posb[rank], wb.m, wb.t,
-                         wb.bp, g->stream), "gather");
-    nr = ncclGroupStart();
-    for (int q = 0; q < world && nr == ncclSuccess; ++q) {
-      const int64_t a0 = posb[q], a1 = posb[q + 1];
-      if (a1 <= a0) continue;
-      nr = ncclBroadcast(wb.m + a0, wb.m + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(wb.t + a0, wb.t + a0, a1 - a0, ncclInt64, q, g->comm, g->stream);
-      if (nr == ncclSuccess) nr = ncclBroadcast(wb.bp + a0, wb.bp + a0, a1 - a0, ncclUint64, q, g->comm, g->stream);
-    }
-    if (nr == ncclSuccess) nr = ncclGroupEnd();
+    int64_t *sloc = nullptr, *sall = nullptr;
+    CU(tmps.get(&sloc, sizeof(int64_t) * 3 * maxn), "alloc");
+    CU(tmps.get(&sall, sizeof(int64_t) * 3 * maxn * world), "alloc");
+    // this rank's survivors -> staging {m[maxn], t[maxn], bp[maxn]} (positions
+    // relative to its arena start posb[rank])
+    CU(ftk::gather_range(res.pool, pos, lo[rank], lo[rank + 1], posb[rank + 1] - posb[rank],
+                         sloc - posb[rank], sloc + maxn - posb[rank],
+                         (uint64_t*)(sloc + 2 * maxn) - posb[rank], g->stream), "gather");
+    CU(cudaMemcpyAsync(posd, posb.data(), sizeof(int64_t) * (world + 1), cudaMemcpyHostToDevice, g->stream),
+       "posb");
+    nr = ncclAllGather(sloc, sall, 3 * maxn, ncclInt64, g->comm, g->stream);
     if (nr != ncclSuccess) return nccl_fail(g, nr);
+    CU(ftk::unpack_data(sall, maxn, posd, world, maxn, wb.m, wb.t, wb.bp, g->stream), "unpack survivors");
     cudaEventRecord(cb, g->stream);
     CU(cudaStreamSynchronize(g->stream), "wave sync");
     float comm_ms = 0;

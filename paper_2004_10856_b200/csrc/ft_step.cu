@@ -2035,16 +2035,23 @@ __global__ void __launch_bounds__(128, 8) k_filter64(BatchDev B, LevelDev L) { f
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
 // (the running minimum v of Alg.1 entering each bucket).
-__global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L, int64_t* ncand) {
+// After the bucket-offset scan: (1) the carry of every bucket = exclusive
+// prefix-min of the bucket minima within its segment (Alg. 1's running
+// minimum v entering the bucket), one CTA per segment; (2) every candidate
+// moved into its bucket (grid-stride; a slot inside the bucket is taken by
+// handing the bucket's count back down -- the order inside a bucket is
+// irrelevant, buckets are sorted by (m, t, id) next).  One launch.
+__global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, int64_t* ncand) {
   __shared__ long long sh[33];
   __shared__ long long chunk_min;
+  const unsigned long long cc = *(volatile unsigned long long*)L.cand_cursor;  // final: k_filter is done
+  const int64_t n = (int64_t)cc < L.cand_cap ? (int64_t)cc : L.cand_cap;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // candidate total (after k_filter)
-    const unsigned long long c = *L.cand_cursor;
-    L.hdr->cand_total[L.level] = c;
-    if ((int64_t)c > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
-    *ncand = (int64_t)c < L.cand_cap ? (int64_t)c : L.cand_cap;
+    L.hdr->cand_total[L.level] = cc;
+    if ((int64_t)cc > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
+    *ncand = n;
   }
-  if (L.hdr->overflow) return;
+  if ((int64_t)cc > L.cand_cap || L.hdr->overflow) return;
   const int64_t nloc = B.nseg;
   for (int64_t li = blockIdx.x; li < nloc; li += gridDim.x) {
     if (!is_filter(L.seg_d[li], L.level)) continue;
@@ -2061,15 +2068,8 @@ __global__ void __launch_bounds__(256) k_carry(BatchDev B, LevelDev L, int64_t* 
       __syncthreads();
     }
   }
-}
-
-__global__ void k_scatter(LevelDev L, const int64_t* ncand) {
-  if (L.hdr->overflow) return;
-  const int64_t n = *ncand;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    // slot inside the bucket: the count is handed back down (order inside a
-    // bucket is irrelevant, buckets are sorted by (m, t, id) next)
     const int64_t gb = L.cgb[i];
     const int64_t d = L.boff[gb] + (int64_t)(atomicSub(L.bcount + gb, 1u) - 1u);
     L.gm[d] = L.cm[i];
@@ -2077,7 +2077,6 @@ __global__ void k_scatter(LevelDev L, const int64_t* ncand) {
     L.gid[d] = L.cid[i];
   }
 }
-
 
 // K2+K3 for buckets of <= WARP_DIRECT candidates: one warp per bucket,
 // register bitonic sort by shuffles (R rows of 32), Alg.1 sweep with the
@@ -2435,11 +2434,27 @@ __device__ void bucket_huge_one(const LevelDev& L, int64_t bkt, int64_t* sm, int
 // Survivors of the filter path go to the level pool at the fixed offset
 // `base` = this level's direct-sample total (the direct kernels' outputs,
 // reserved by cursor atomics, never exceed it; the pool holds both).
-__global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand, int64_t base) {
-  if (L.hdr->overflow) return;
+// Survivors of the filter path go to the level pool at the fixed offset
+// `base` = this level's direct-sample total (the direct kernels' outputs,
+// reserved by cursor atomics, never exceed it; the pool holds both), and
+// every filter segment's pool range is recorded (one launch).
+__global__ void k_compact(BatchDev B, LevelDev L, const int64_t* gpos, const int64_t* ncand, int64_t base) {
   const int64_t n = *ncand;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gstride = (int64_t)gridDim.x * blockDim.x;
+  if (g0 == 0) {
+    const int64_t tot = gpos[n];
+    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
+    if (base + tot > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+  }
+  for (int64_t li = g0; li < B.nseg; li += gstride) {
+    if (!is_filter(L.seg_d[li], L.level)) continue;
+    const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
+    const int64_t lo = L.boff[b0], hi = L.boff[b1];
+    L.out.start[li] = base + gpos[lo];
+    L.out.cnt[li] = gpos[hi] - gpos[lo];
+  }
+  if (L.hdr->overflow) return;
+  for (int64_t i = g0; i < n; i += gstride) {
     if (gpos[i + 1] != gpos[i] && base + gpos[i] < L.out.cap) {
       const int64_t d = base + gpos[i];
       L.out.m[d] = L.gm[i];
@@ -2447,22 +2462,6 @@ __global__ void k_compact(LevelDev L, const int64_t* gpos, const int64_t* ncand,
       L.out.id[d] = L.gid[i];
     }
   }
-}
-
-__global__ void k_seg_out(BatchDev B, LevelDev L, const int64_t* gpos, const int64_t* ncand,
-                          int64_t base) {
-  const int64_t nloc = B.nseg;
-  const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (li == 0) {
-    const int64_t tot = gpos[*ncand];
-    atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
-    if (base + tot > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
-  }
-  if (li >= nloc || !is_filter(L.seg_d[li], L.level)) return;
-  const int64_t b0 = L.bucket_base[li], b1 = b0 + L.nb[li];
-  const int64_t lo = L.boff[b0], hi = L.boff[b1];
-  L.out.start[li] = base + gpos[lo];
-  L.out.cnt[li] = gpos[hi] - gpos[lo];
 }
 
 // Final gather of the level-0 pool into every step's CSR output set (one
@@ -2668,6 +2667,49 @@ cudaError_t gather_range(const Pool& P, const int64_t* pos, int64_t lo, int64_t 
 }
 
 int64_t scan_tmp_elems(int64_t n) { return ntiles_cap_slot(n) + 8; }
+
+// Multi-rank exchange by all-gathers: rank q's block of the
+// gathered buffer holds its segments' {counts[maxloc], tuples[maxloc]}; wave
+// segment gs of rank q (lo[q] <= gs < lo[q+1]) is local segment gs - lo[q].
+__global__ void k_unpack_counts(const int64_t* all, int64_t maxloc, const int64_t* lo, int world, int64_t NS,
+                                int64_t* cnt, int64_t* tup) {
+  for (int64_t gs = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gs < NS;
+       gs += (int64_t)gridDim.x * blockDim.x) {
+    int q = 0;
+    while (q + 1 < world && lo[q + 1] <= gs) ++q;
+    const int64_t* blk = all + (int64_t)q * 2 * maxloc;
+    cnt[gs] = blk[gs - lo[q]];
+    tup[gs] = blk[maxloc + gs - lo[q]];
+  }
+}
+
+// Rank q's staged survivors {m[cap], t[cap], bp[cap]} (gathered) -> the wave
+// arena at [posb[q], posb[q+1]) (blockIdx.y = q).
+__global__ void k_unpack_data(const int64_t* all, int64_t cap, const int64_t* posb, int64_t* om, int64_t* ot,
+                              uint64_t* obp) {
+  const int q = blockIdx.y;
+  const int64_t a0 = posb[q], n = posb[q + 1] - a0;
+  const int64_t* blk = all + (int64_t)q * 3 * cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    om[a0 + i] = blk[i];
+    ot[a0 + i] = blk[cap + i];
+    obp[a0 + i] = (uint64_t)blk[2 * cap + i];
+  }
+}
+
+cudaError_t unpack_counts(const int64_t* all, int64_t maxloc, const int64_t* lo_dev, int world, int64_t NS,
+                          int64_t* cnt, int64_t* tup, cudaStream_t st) {
+  if (NS <= 0) return cudaSuccess;
+  k_unpack_counts<<<grid_for(NS, 256, 148 * 8), 256, 0, st>>>(all, maxloc, lo_dev, world, NS, cnt, tup);
+  return cudaGetLastError();
+}
+
+cudaError_t unpack_data(const int64_t* all, int64_t cap, const int64_t* posb_dev, int world, int64_t maxn,
+                        int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st) {
+  if (maxn <= 0) return cudaSuccess;
+  k_unpack_data<<<dim3(grid_for(maxn, 256, 148 * 4), world), 256, 0, st>>>(all, cap, posb_dev, om, ot, obp);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -2998,21 +3040,19 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         else k_filter<<<filter_grid, 128, 0, st>>>(s, L);
         // bucket offsets over B buckets (B on device)
         mark(3);
-        nl += 5;  // scan, carry, scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
+        nl += 4;  // scan, carry+scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
-        k_carry<<<grid_for(nloc, 1, 148 * 8), 256, 0, st>>>(s, L, nc);  // + candidate total
-        k_scatter<<<148 * 8, 256, 0, st>>>(L, nc);
+        k_carry_scatter<<<148 * 8, 256, 0, st>>>(s, L, nc);  // + candidate total
         k_bucket_small<<<148 * 8, 256, 0, st>>>(s, L);
         const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
         k_bucket_large<<<148 * 2, DIRECT_NT, lsm, st>>>(L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
         mark(4);
-        nl += 3;  // scan, compact, seg_out
+        nl += 2;  // scan, compact (+ segment ranges)
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
         scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
         const int64_t cbase = (int64_t)plan_copy[l];  // direct outputs of level l stay below
-        k_compact<<<148 * 8, 256, 0, st>>>(L, gpos, nc, cbase);
-        k_seg_out<<<grid_for(nloc, 128, 1 << 30), 128, 0, st>>>(s, L, gpos, nc, cbase);
+        k_compact<<<148 * 8, 256, 0, st>>>(s, L, gpos, nc, cbase);
       }
     }
     mark(-1);

@@ -88,6 +88,12 @@ cudaError_t wave_offsets(const int64_t* cnt, const int64_t* tup, int64_t NS, int
 cudaError_t gather_range(const Pool& P, const int64_t* pos, int64_t lo, int64_t hi, int64_t nout,
                          int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st);
 int64_t scan_tmp_elems(int64_t n);
+// All-gather exchange helpers: gathered per-rank count blocks
+// -> per-segment counts / tuples; gathered per-rank survivor blocks -> arena.
+cudaError_t unpack_counts(const int64_t* all, int64_t maxloc, const int64_t* lo_dev, int world, int64_t NS,
+                          int64_t* cnt, int64_t* tup, cudaStream_t st);
+cudaError_t unpack_data(const int64_t* all, int64_t cap, const int64_t* posb_dev, int world, int64_t maxn,
+                        int64_t* om, int64_t* ot, uint64_t* obp, cudaStream_t st);
 
 // Validates costs on the device (bit 0: negative, bit 1: >= 2^40) and reports
 // per edge whether its memory costs are all zero.

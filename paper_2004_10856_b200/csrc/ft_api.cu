@@ -444,6 +444,13 @@ int nccl_fail(ft_graph* g, ncclResult_t nr) {
   return FT_ECUDA;
 }
 
+// Device -> host copy ordered after the handle's stream (its work may still be
+// in flight: waves do not end with a host sync), then wait for it.
+cudaError_t d2h(ft_graph* g, void* dst, const void* src, size_t bytes) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g->stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(g->stream);
+}
+
 // Host copy of a set's seg_off (single-rank step outputs keep it on the device
 // until needed).
 int ensure_off(ft_graph* g, int set) {
@@ -455,8 +462,7 @@ int ensure_off(ft_graph* g, int set) {
     S.off_ok = true;
     return FT_OK;
   }
-  CU(cudaMemcpy(S.off.data(), S.d_off, sizeof(int64_t) * (S.nseg + 1), cudaMemcpyDeviceToHost),
-     "seg_off d2h");
+  CU(d2h(g, S.off.data(), S.d_off, sizeof(int64_t) * (S.nseg + 1)), "seg_off d2h");
   S.off_ok = true;
   return FT_OK;
 }
@@ -695,6 +701,7 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     CU(ftk::unpack_data(sall, maxn, posd, world, maxn, wb.m, wb.t, wb.bp, g->stream), "unpack survivors");
     cudaEventRecord(cb, g->stream);
     CU(cudaStreamSynchronize(g->stream), "wave sync");
+    g->runner->fence(g->stream);
     float comm_ms = 0;
     cudaEventElapsedTime(&comm_ms, ca, cb);
     cudaEventDestroy(ca);
@@ -854,7 +861,11 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     set_out(sv);
     CU(g->runner->gather(sv, res, g->stream), "gather");
   }
-  CU(cudaStreamSynchronize(g->stream), "wave sync");
+  // no host sync: the next wave's work is ordered behind this one on the
+  // stream, and the host needs nothing from the gather (the runner's fence
+  // orders other streams that use the same scratch)
+  g->runner->fence(g->stream);
+  CU(cudaGetLastError(), "wave");
   const double h4 = now_ms();
   // bookkeeping: sets, stats, consumption
   wb.live = ns;
@@ -1266,8 +1277,8 @@ int heur_step(ft_graph* g) {
   const FSet& S = g->sets[set];
   const int64_t n = S.off[S.nseg];
   std::vector<int64_t> hm(n), ht(n);
-  CU(cudaMemcpy(hm.data(), S.d_m, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
-  CU(cudaMemcpy(ht.data(), S.d_t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+  CU(d2h(g, hm.data(), S.d_m, sizeof(int64_t) * n), "d2h");
+  CU(d2h(g, ht.data(), S.d_t, sizeof(int64_t) * n), "d2h");
   int64_t ks = 0;
   if (g->heur_policy == 0) {
     for (int64_t k = 1; k < S.nseg; ++k) {
@@ -1419,14 +1430,13 @@ int fetch_bp(ft_graph* g, FSet& s) {
   if (s.h_bp_ok) return FT_OK;
   if (!s.off_ok) {
     s.off.resize(s.nseg + 1);
-    CU(cudaMemcpy(s.off.data(), s.d_off, sizeof(int64_t) * (s.nseg + 1), cudaMemcpyDeviceToHost),
-       "seg_off d2h");
+    CU(d2h(g, s.off.data(), s.d_off, sizeof(int64_t) * (s.nseg + 1)), "seg_off d2h");
     s.off_ok = true;
   }
   int64_t n = s.off[s.nseg];
   s.h_bp.resize(n);
   if (n) {
-    CU(cudaMemcpy(s.h_bp.data(), s.d_bp, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost), "bp d2h");
+    CU(d2h(g, s.h_bp.data(), s.d_bp, sizeof(uint64_t) * n), "bp d2h");
   }
   s.h_bp_ok = true;
   return FT_OK;

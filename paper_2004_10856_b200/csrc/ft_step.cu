@@ -411,6 +411,7 @@ __device__ __forceinline__ void cta_bitonic_regs(int64_t (&m)[R], int64_t (&t)[R
         const int jr = j >> 5;
         if (jr == 1) cta_rows_xchg<R, 1>(m, t, id, k, eb);
         else if (R >= 4 && jr == 2) cta_rows_xchg<R, (R >= 4 ? 2 : 1)>(m, t, id, k, eb);
+        else if (R >= 8 && jr == 4) cta_rows_xchg<R, (R >= 8 ? 4 : 1)>(m, t, id, k, eb);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -473,6 +474,7 @@ __device__ __forceinline__ void cta_bitonic_keys(uint64_t (&k)[R], uint64_t* xk)
         const int jr = j >> 5;
         if (jr == 1) cta_keys_rows<R, 1>(k, kk, eb);
         else if (R >= 4 && jr == 2) cta_keys_rows<R, (R >= 4 ? 2 : 1)>(k, kk, eb);
+        else if (R >= 8 && jr == 4) cta_keys_rows<R, (R >= 8 ? 4 : 1)>(k, kk, eb);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -491,6 +493,8 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
                                                uint64_t* xk, long long* sh, const LevelDev& L,
                                                int64_t gs, int64_t* s_start, int kspan) {
   constexpr int NW = DIRECT_NT / 32;
+  constexpr int EB = R >= 8 ? 11 : 10;  // bits of the element index e < N = 32 R NW
+  constexpr uint64_t EM = (1ull << EB) - 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eb = wid * 32 * R;
   int64_t m[R], t[R];
@@ -501,8 +505,8 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     t[r] = INF;
     id[r] = ~0ull;
   }
-  // Tuples are staged in x*; the sort runs on 64-bit keys ((m - m0) << 10 | e)
-  // (m0 = the sample's least m, e < N <= 1024) and t, id are gathered by e.
+  // Tuples are staged in x*; the sort runs on 64-bit keys ((m - m0) << EB | e)
+  // (m0 = the sample's least m, e < N <= 2048) and t, id are gathered by e.
   // Frontier m grows with the eliminated subgraph (sums up to 2^60, R10), so
   // the packing is used only when the sample's m span fits in kspan (<= 53)
   // bits; otherwise, and when two tuples share m (the key order is then not
@@ -538,12 +542,12 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     m0 = sh[w] < m0 ? sh[w] : m0;
     m1 = sh[NW + w] > m1 ? sh[NW + w] : m1;
   }
-  const bool wide = ((unsigned long long)(m1 - m0) >> kspan) != 0;
+  const bool wide = ((unsigned long long)(m1 - m0) >> (kspan < 63 - EB ? kspan : 63 - EB)) != 0;
   uint64_t k[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = eb + (r << 5) + lane;
-    k[r] = e < n ? ((uint64_t)(xm[e] - m0) << 10) | (uint64_t)e : ~0ull;
+    k[r] = e < n ? ((uint64_t)(xm[e] - m0) << EB) | (uint64_t)e : ~0ull;
   }
   __syncthreads();  // sh reuse
   bool tie = false;
@@ -553,19 +557,19 @@ __device__ __forceinline__ void cta_sort_sweep(int n, Gen& gen, int64_t* xm, int
     for (int r = 0; r < R; ++r) {
       const int e = eb + (r << 5) + lane;
       if (e < n) {
-        const int src = (int)(k[r] & 1023u);
-        m[r] = (int64_t)(k[r] >> 10) + m0;
+        const int src = (int)(k[r] & EM);
+        m[r] = (int64_t)(k[r] >> EB) + m0;
         t[r] = xt[src];
         id[r] = xid[src];
       }
       uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
       const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
       if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
-      if (e < n && prev != ~0ull && (prev >> 10) == (k[r] >> 10)) tie = true;
+      if (e < n && prev != ~0ull && (prev >> EB) == (k[r] >> EB)) tie = true;
     }
-    if (lane == 31) sh[wid] = (long long)(k[R - 1] >> 10);  // last key m of the warp (padding: 2^54 - 1)
+    if (lane == 31) sh[wid] = (long long)(k[R - 1] >> EB);  // last key m of the warp (padding: all ones)
     __syncthreads();
-    if (wid > 0 && lane == 0 && eb < n && (long long)(k[0] >> 10) == sh[wid - 1]) tie = true;
+    if (wid > 0 && lane == 0 && eb < n && (long long)(k[0] >> EB) == sh[wid - 1]) tie = true;
   }
   if (__syncthreads_or(tie || wide)) {  // exact sort on (m, t, id)
 #pragma unroll
@@ -748,10 +752,11 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_direct(BatchDev B, LevelDev L)
                     z = samp_idx(jz, b.n[2], st);
       make_tuple(s, b, rel[k], x, y, z, om, ot, oid);
     };
-    if ((N == 2 * DIRECT_NT || N == 4 * DIRECT_NT) && N <= B.cdirect) {
+    if ((N == 2 * DIRECT_NT || N == 4 * DIRECT_NT || N == 8 * DIRECT_NT) && N <= B.cdirect) {
       uint64_t* xk = (uint64_t*)kf;  // kf + pre (>= 8 N bytes) are free after generation
       if (N == 2 * DIRECT_NT) cta_sort_sweep<2>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
-      else cta_sort_sweep<4>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
+      else if (N == 4 * DIRECT_NT) cta_sort_sweep<4>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
+      else cta_sort_sweep<8>(n, gen, sm, stt, sid, xk, sh, L, gs, &s_start, B.kspan);
       continue;
     }
     for (int i = threadIdx.x; i < N; i += DIRECT_NT) {
@@ -1721,23 +1726,6 @@ __global__ void __launch_bounds__(DIRECT_NT) k_node_shared(BatchDev B, LevelDev 
 // Filter path, level l < d_sigma.
 
 
-// Clears the bucket counters of the live buckets only (B read on device).
-__global__ void k_bucket_init(BatchDev Bt, LevelDev L) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // bucket totals, list/cursor resets
-    const int64_t Bt0 = L.bucket_base[Bt.nseg];
-    L.hdr->bucket_total[L.level] = Bt0;
-    if (Bt0 > L.bcap) atomicExch(&L.hdr->overflow, 1ull);
-    *L.large_n = 0;
-    *L.cand_cursor = 0;
-  }
-  const int64_t B = min(L.bucket_base[Bt.nseg], L.bcap);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    L.bcount[i] = 0;
-    L.bmin[i] = INF;
-  }
-}
-
 // Long factor = the one with most sampled indices; runs = product of the other two.
 __device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa, int& fb, int64_t& cL,
                                           int64_t& cA, int64_t& cB) {
@@ -1808,9 +1796,15 @@ struct PostHint {
 // later element with t >= t_g (their m exceeds m_g), so the walk jumps to
 // the first element with t < t_g (binary search on t).  Otherwise x is a
 // candidate: emitted with bucket = #G points with m <= m_x.
+constexpr int EPRE = 2;  // run elements loaded ahead in k_filter's element test (4: spills at 80 regs)
+
 __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L) {
   namespace cg = cooperative_groups;
   if (L.hdr->overflow) return;
+  if (L.bucket_base[B.nseg] > L.bcap) {  // more buckets than scratch: grow and retry
+    atomicExch(&L.hdr->overflow, 1ull);
+    return;
+  }
   const int64_t nbl = B.nblk;
   const int64_t W = L.wo[nbl];
   const int sh = L.st;
@@ -1913,7 +1907,16 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       const int64_t je = min(jj + CHUNK, j1);
       const int64_t mf = ms + __ldg(Lm + samp_idx(jj, nL, sh));
       const int64_t tl = ts + __ldg(Lt + samp_idx(je - 1, nL, sh));
-      if (q < g && Gm[q] < mf) {  // gallop + binary search to lower_bound(mf)
+      if (q < g && Gm[q] < mf) {  // lower_bound(mf) in G, starting at q
+        {  // short advances are the common case: probe q+1..q+4 with independent loads
+          const int64_t v1 = q + 1 < g ? Gm[q + 1] : INF, v2 = q + 2 < g ? Gm[q + 2] : INF;
+          const int64_t v3 = q + 3 < g ? Gm[q + 3] : INF, v4 = q + 4 < g ? Gm[q + 4] : INF;
+          if (v1 >= mf) { q += 1; goto g_done; }
+          if (v2 >= mf) { q += 2; goto g_done; }
+          if (v3 >= mf) { q += 3; goto g_done; }
+          if (v4 >= mf) { q += 4; goto g_done; }
+          q += 4;  // Gm[q] < mf still: interpolation / gallop from here
+        }
         if (g - q > 16) {
           // one interpolation probe between Gm[q] and Gm[g-1] (G's m values are
           // spread over the segment's range); the gallop then starts there
@@ -1977,24 +1980,35 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       }
       c_elem += je - jj;
       // element-level test of the chunk: p = #G points with m <= m_x; the
-      // run elements are loaded 4 at a time ahead of the (dependent) G walk
+      // run elements are loaded EPRE at a time ahead of the (dependent) G walk
       int64_t p = q;
-      for (int64_t j4 = jj; j4 < je; j4 += 4) {
-      int64_t em[4], et[4];
+      // G[p] and G[p-1] kept in registers: consecutive run elements mostly
+      // share p, so the walk and the dominance test reload only when p moves
+      int64_t gmp = p < g ? Gm[p] : INF;
+      int64_t gmq = p > 0 ? Gm[p - 1] : 0, gtq = p > 0 ? Gt[p - 1] : INF;
+      for (int64_t j4 = jj; j4 < je; j4 += EPRE) {
+      int64_t em[EPRE], et[EPRE];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < EPRE; ++u) {
         const int64_t iu = samp_idx(min(j4 + u, je - 1), nL, sh);
         em[u] = __ldg(Lm + iu);
         et[u] = __ldg(Lt + iu);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < EPRE; ++u) {
         if (j4 + u >= je) break;
         const int64_t il = samp_idx(j4 + u, nL, sh);
         const int64_t m = ms + em[u];
         const int64_t t = ts + et[u];
-        while (p < g && Gm[p] <= m) ++p;
-        if (p > 0 && (Gt[p - 1] < t || (Gt[p - 1] == t && Gm[p - 1] < m))) continue;
+        if (gmp <= m) {
+          do {
+            gmq = gmp;
+            ++p;
+            gmp = p < g ? Gm[p] : INF;
+          } while (gmp <= m);
+          gtq = Gt[p - 1];
+        }
+        if (p > 0 && (gtq < t || (gtq == t && gmq < m))) continue;
         int64_t x, y, z;
         if (lf == 0) { x = il; y = ia; z = ib; }
         else if (lf == 1) { x = ia; y = il; z = ib; }
@@ -2041,13 +2055,17 @@ __global__ void __launch_bounds__(128, 8) k_filter64(BatchDev B, LevelDev L) { f
 // moved into its bucket (grid-stride; a slot inside the bucket is taken by
 // handing the bucket's count back down -- the order inside a bucket is
 // irrelevant, buckets are sorted by (m, t, id) next).  One launch.
+__constant__ unsigned char kBminFill[8] = {BMIN_FILL, BMIN_FILL, BMIN_FILL, BMIN_FILL,
+                                           BMIN_FILL, BMIN_FILL, BMIN_FILL, BMIN_FILL};
+
 __global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, int64_t* ncand) {
   __shared__ long long sh[33];
   __shared__ long long chunk_min;
   const unsigned long long cc = *(volatile unsigned long long*)L.cand_cursor;  // final: k_filter is done
   const int64_t n = (int64_t)cc < L.cand_cap ? (int64_t)cc : L.cand_cap;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // candidate total (after k_filter)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // candidate and bucket totals (after k_filter)
     L.hdr->cand_total[L.level] = cc;
+    L.hdr->bucket_total[L.level] = L.bucket_base[B.nseg];
     if ((int64_t)cc > L.cand_cap) atomicExch(&L.hdr->overflow, 1ull);
     *ncand = n;
   }
@@ -2061,7 +2079,10 @@ __global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, i
       const int64_t i = c0 + threadIdx.x;
       const long long v = i < nb ? L.bmin[b0 + i] : INF;
       const long long ex = block_excl_min<256>(v, sh);
-      if (i < nb) L.bcarry[b0 + i] = ex < carry ? ex : carry;
+      if (i < nb) {
+        L.bcarry[b0 + i] = ex < carry ? ex : carry;
+        L.bmin[b0 + i] = *(const long long*)kBminFill;  // back to the reset state
+      }
       if (threadIdx.x == 255) chunk_min = v < ex ? v : ex;
       __syncthreads();
       carry = chunk_min < carry ? chunk_min : carry;
@@ -2445,6 +2466,8 @@ __global__ void k_compact(BatchDev B, LevelDev L, const int64_t* gpos, const int
     const int64_t tot = gpos[n];
     atomicAdd(&L.hdr->out_total[L.level], (unsigned long long)tot);
     if (base + tot > L.out.cap) atomicExch(&L.hdr->overflow, 1ull);
+    *L.cand_cursor = 0;  // ready for the next filter level
+    *L.large_n = 0;
   }
   for (int64_t li = g0; li < B.nseg; li += gstride) {
     if (!is_filter(L.seg_d[li], L.level)) continue;
@@ -2761,6 +2784,8 @@ void StepRunner::release() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   ev0 = ev1 = nullptr;
+  if (fence_ev) cudaEventDestroy(fence_ev);
+  fence_ev = nullptr;
 }
 
 void StepRunner::release_device() {
@@ -2788,6 +2813,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
                             int64_t* dev_off, const std::vector<NodeGroupH>* groups, bool keep_dev) {
   int64_t nl = 0;  // kernel launches
   int pgroup[64];
+  if (fence_ev && fence_st != st) cudaStreamWaitEvent(st, fence_ev, 0);  // scratch last used on another stream
   npev = 0;
   auto mark = [&](int group) {  // group of the interval that starts here
     if (!profile || npev >= 64) return;
@@ -2930,13 +2956,21 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     GROW(poolB_start, int64_t, nloc);
     GROW(poolB_cnt, int64_t, nloc);
     GROW(cursors, unsigned long long, 8);
+    cudaMemsetAsync(cursors.p, 0, sizeof(unsigned long long) * 8, st);  // cand / large cursors (k_compact resets them per level)
     if (D > 0) {
       GROW(nb, int64_t, nloc);
       GROW(bucket_base, int64_t, nloc + 1);
       GROW(wcnt, int64_t, std::max<int64_t>(nbl, 1));
       GROW(wo, int64_t, nbl + 1);
-      GROW(bcount, unsigned int, bcap);
-      GROW(bmin, long long, bcap);
+      {  // bucket counters / minima live in their reset state between levels
+         // (k_carry_scatter hands every count back to 0 and every minimum to
+         // INF); fresh or retried scratch is reset here
+        const size_t ob = bcount.bytes, om = bmin.bytes;
+        GROW(bcount, unsigned int, bcap);
+        GROW(bmin, long long, bcap);
+        if (bcount.bytes != ob || attempt > 0) cudaMemsetAsync(bcount.p, 0, bcount.bytes, st);
+        if (bmin.bytes != om || attempt > 0) cudaMemsetAsync(bmin.p, BMIN_FILL, bmin.bytes, st);
+      }
       GROW(boff, int64_t, bcap + 1);
       GROW(bcarry, long long, bcap);
       GROW(cm, int64_t, cand_cap);
@@ -3031,9 +3065,8 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
-        nl += 4;  // scan(+nb), bucket_init, scan(+work counts), filter
+        nl += 3;  // scan(+nb), scan(+work counts), filter
         scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
-        k_bucket_init<<<grid_for(bcap, 256, 148 * 8), 256, 0, st>>>(s, L);
         scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st, false, PostHint{L.whint, L.hcap});
         mark(2);  // filter_ms: k_filter alone
         if (filter_regs64) k_filter64<<<filter_grid, 128, 0, st>>>(s, L);

@@ -118,6 +118,13 @@ class StepRunner {
   cudaError_t gather(const std::vector<StepDev>& steps, const StepResult& r, cudaStream_t st);
   void release();
   void release_device();  // device scratch only (hooked runners, last graph gone)
+  // Marks the end of a wave's use of the scratch on stream st; the next run()
+  // on another stream waits for it (waves do not end with a host sync).
+  void fence(cudaStream_t st) {
+    if (!fence_ev) cudaEventCreateWithFlags(&fence_ev, cudaEventDisableTiming);
+    cudaEventRecord(fence_ev, st);
+    fence_st = st;
+  }
 
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
@@ -159,6 +166,8 @@ class StepRunner {
   int64_t* cnt_host = nullptr;
   int64_t cnt_host_n = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t fence_ev = nullptr;
+  cudaStream_t fence_st = nullptr;
   cudaEvent_t pev[64] = {};
   int npev = 0;
 };

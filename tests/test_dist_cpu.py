@@ -2,8 +2,9 @@
 
 Covers the N>1 path's host side: the shard plan (ft_shard_plan, the C++
 function libft uses to split a wave's segments over ranks) and the
-all-gather-v protocol of DESIGN.md 8 (per-rank counts broadcast by each root,
-then each rank's contiguous CSR slice broadcast into final positions).  The
+exchange protocol of DESIGN.md 8 (an all-gather of every rank's per-segment
+counts padded to the largest rank range, then an all-gather of every rank's
+survivors staged as padded {m, t, bp} blocks, unpacked into the CSR arena).  The
 frontier payload is the oracle's step output for C3, so the reassembled
 sets must equal the single-process result bit for bit, for any partition."""
 import os
@@ -51,28 +52,31 @@ def _worker(rank, world, port, q):
             assert all(torch.equal(x, allb[0]) for x in allb)
             assert b[0] == 0 and b[-1] == nseg and np.all(np.diff(b) >= 0)
             lo, hi = int(b[rank]), int(b[rank + 1])
-            # phase 1: counts (each root broadcasts its segments' counts)
-            counts = torch.zeros(nseg, dtype=torch.int64)
-            counts[lo:hi] = torch.from_numpy(cnt[lo:hi].astype(np.int64))
-            for r in range(world):
-                a0, a1 = int(b[r]), int(b[r + 1])
-                if a1 > a0:
-                    part = counts[a0:a1].clone()
-                    dist.broadcast(part, src=r)
-                    counts[a0:a1] = part
-            off = np.concatenate([[0], np.cumsum(counts.numpy())])
+            # phase 1: all-gather of every rank's per-segment
+            # counts, padded to the largest rank range; unpack by rank range
+            maxloc = max(1, max(int(b[r + 1] - b[r]) for r in range(world)))
+            mine = torch.zeros(maxloc, dtype=torch.int64)
+            mine[:hi - lo] = torch.from_numpy(cnt[lo:hi].astype(np.int64))
+            blocks = [torch.zeros(maxloc, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(blocks, mine)
+            counts = np.concatenate([blocks[r][:int(b[r + 1] - b[r])].numpy() for r in range(world)])
+            off = np.concatenate([[0], np.cumsum(counts)])
             assert np.array_equal(off, seg_off)
-            # phase 2: payload, each root's contiguous CSR slice into final positions
+            # phase 2: every rank's survivors staged as {m, t, bp} blocks padded
+            # to the largest rank total, all-gathered, unpacked at off[b[r]]
+            tot = [int(off[b[r + 1]] - off[b[r]]) for r in range(world)]
+            maxn = max(1, max(tot))
+            a0, a1 = int(off[lo]), int(off[hi])
+            st = torch.zeros((3, maxn), dtype=torch.int64)
+            st[0, :a1 - a0] = torch.from_numpy(m[a0:a1])
+            st[1, :a1 - a0] = torch.from_numpy(t[a0:a1])
+            st[2, :a1 - a0] = torch.from_numpy(bp[a0:a1].astype(np.int64))
+            allst = [torch.zeros((3, maxn), dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(allst, st)
             out = torch.zeros((3, int(off[-1])), dtype=torch.int64)
-            out[0, off[lo]:off[hi]] = torch.from_numpy(m[off[lo]:off[hi]])
-            out[1, off[lo]:off[hi]] = torch.from_numpy(t[off[lo]:off[hi]])
-            out[2, off[lo]:off[hi]] = torch.from_numpy(bp[off[lo]:off[hi]].astype(np.int64))
             for r in range(world):
-                a0, a1 = int(off[b[r]]), int(off[b[r + 1]])
-                if a1 > a0:
-                    part = out[:, a0:a1].contiguous()
-                    dist.broadcast(part, src=r)
-                    out[:, a0:a1] = part
+                o = int(off[b[r]])
+                out[:, o:o + tot[r]] = allst[r][:, :tot[r]]
             assert np.array_equal(out[0].numpy(), m) and np.array_equal(out[1].numpy(), t)
             assert np.array_equal(out[2].numpy().astype(np.uint64), bp)
             checked += 1

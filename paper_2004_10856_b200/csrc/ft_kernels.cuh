@@ -270,6 +270,13 @@ __device__ __forceinline__ int64_t samp_idx(int64_t j, int64_t n, int sh) {
   return j < c0 ? (j << sh) : n - 1;
 }
 
+// 32-bit variant for indices inside one factor segment (a segment frontier
+// holds < 2^31 tuples); the stride 2^sh itself may exceed 2^31.
+__device__ __forceinline__ int samp_idx32(int j, int n, int sh) {
+  const int64_t c0 = ((int64_t)n + ((int64_t)1 << sh) - 1) >> sh;
+  return j < c0 ? (int)((int64_t)j << sh) : n - 1;
+}
+
 __device__ __forceinline__ const int64_t* fac_m(const StepDev& s, int f) {
   return f == 0 ? s.X.m : (f == 1 ? s.Y.m : s.Z.m);
 }

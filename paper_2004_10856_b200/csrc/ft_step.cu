@@ -8,6 +8,7 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 
 #include "ft_kernels.cuh"
 #include "ft_step.h"
@@ -1860,7 +1861,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     const int64_t* const fm[3] = {s.X.m, s.Y.m, s.Z.m};
     const int64_t* const ft[3] = {s.X.t, s.Y.t, s.Z.t};
     const int64_t oL = lf == 0 ? b.o[0] : (lf == 1 ? b.o[1] : b.o[2]);
-    const int64_t nL = lf == 0 ? b.n[0] : (lf == 1 ? b.n[1] : b.n[2]);
+    const int nL = (int)(lf == 0 ? b.n[0] : (lf == 1 ? b.n[1] : b.n[2]));
     const int64_t oA = fa == 0 ? b.o[0] : b.o[1];
     const int64_t nA = fa == 0 ? b.n[0] : b.n[1];
     const int64_t oB = fb == 2 ? b.o[2] : b.o[1];
@@ -1881,7 +1882,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       ja = run / cB;
       jb = run - ja * cB;
     }
-    const int64_t ia = samp_idx(ja, nA, sh), ib = samp_idx(jb, nB, sh);
+    const int ia = (int)samp_idx(ja, nA, sh), ib = (int)samp_idx(jb, nB, sh);
     const int64_t* Am = fa == 0 ? fm[0] : fm[1];
     const int64_t* At = fa == 0 ? ft[0] : ft[1];
     const int64_t* Bm = fb == 2 ? fm[2] : fm[1];
@@ -1891,22 +1892,22 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     const int64_t ms = __ldg(Am + oA + ia) + __ldg(Bm + oB + ib);
     const int64_t ts = __ldg(At + oA + ia) + __ldg(Bt + oB + ib);
     // (x, y, z) index of the tuple for the id (R6): the long factor varies
-    const int64_t ny = b.n[1], nz = b.n[2];
-    const int64_t j0 = ch * RI, j1 = min(j0 + RI, cL);
+    const int ny = (int)b.n[1], nz = (int)b.n[2];
+    const int j0 = (int)(ch * RI), j1 = (int)min(ch * RI + RI, cL);
     const int64_t* Gm = L.in.m + L.in.start[li];
     const int64_t* Gt = L.in.t + L.in.start[li];
-    const int64_t g = L.in.cnt[li];
+    const int g = (int)L.in.cnt[li];
     const int64_t bb = L.bucket_base[li];
     const int64_t gml = g > 0 ? Gm[g - 1] : INF;  // largest G m (interpolation)
     // q: #G points with m < m of the current chunk start (galloping lower bound)
-    int64_t q = 0;
-    int64_t jj = j0;
-    unsigned long long c_tests = 0, c_skip = 0, c_elem = 0;
+    int q = 0;
+    int jj = j0;
+    unsigned c_tests = 0, c_skip = 0, c_elem = 0;
     while (jj < j1) {
       ++c_tests;
-      const int64_t je = min(jj + CHUNK, j1);
-      const int64_t mf = ms + __ldg(Lm + samp_idx(jj, nL, sh));
-      const int64_t tl = ts + __ldg(Lt + samp_idx(je - 1, nL, sh));
+      const int je = min(jj + CHUNK, j1);
+      const int64_t mf = ms + __ldg(Lm + samp_idx32(jj, nL, sh));
+      const int64_t tl = ts + __ldg(Lt + samp_idx32(je - 1, nL, sh));
       if (q < g && Gm[q] < mf) {  // lower_bound(mf) in G, starting at q
         {  // short advances are the common case: probe q+1..q+4 with independent loads
           const int64_t v1 = q + 1 < g ? Gm[q + 1] : INF, v2 = q + 2 < g ? Gm[q + 2] : INF;
@@ -1925,17 +1926,17 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
             q = g;
             goto g_done;
           }
-          int64_t e = q + (int64_t)((double)(mf - mq) / (double)(gml - mq) * (double)(g - 1 - q));
+          int e = q + (int)((double)(mf - mq) / (double)(gml - mq) * (double)(g - 1 - q));
           e = e <= q ? q + 1 : (e > g - 1 ? g - 1 : e);
           if (Gm[e] < mf) {
             q = e;
           } else {  // lower bound in (q, e]: gallop down from e
-            int64_t stp = 1;
+            int stp = 1;
             while (e - stp > q && Gm[e - stp] >= mf) stp <<= 1;
-            int64_t a0 = e - stp < q ? q + 1 : e - stp + 1, a1 = e - (stp >> 1);
+            int a0 = e - stp < q ? q + 1 : e - stp + 1, a1 = e - (stp >> 1);
             // Gm[a1] >= mf (or a1 == e), lower bound in [a0, a1]
             while (a0 < a1) {
-              const int64_t mid = (a0 + a1) >> 1;
+              const int mid = (a0 + a1) >> 1;
               if (Gm[mid] < mf) a0 = mid + 1;
               else a1 = mid;
             }
@@ -1943,11 +1944,11 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
             goto g_done;
           }
         }
-        int64_t step = 1;
+        int step = 1;
         while (q + step < g && Gm[q + step] < mf) step <<= 1;
-        int64_t a0 = q + (step >> 1) + 1, a1 = min(q + step, g);
+        int a0 = q + (step >> 1) + 1, a1 = min(q + step, g);
         while (a0 < a1) {
-          const int64_t mid = (a0 + a1) >> 1;
+          const int mid = (a0 + a1) >> 1;
           if (Gm[mid] < mf) a0 = mid + 1;
           else a1 = mid;
         }
@@ -1958,20 +1959,20 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
         // G[q-1] (m < mf) strictly dominates the whole chunk and every later
         // element with t >= its t: gallop along the run to the first t below it.
         const int64_t tg = Gt[q - 1];
-        if (ts + __ldg(Lt + samp_idx(j1 - 1, nL, sh)) >= tg) {  // common: the rest of the item
+        if (ts + __ldg(Lt + samp_idx32(j1 - 1, nL, sh)) >= tg) {  // common: the rest of the item
           c_skip += j1 - jj;
           jj = j1;
           continue;
         }
-        int64_t step = 1, last = je - 1;  // t(last) >= tg
-        while (last + step < j1 && ts + __ldg(Lt + samp_idx(last + step, nL, sh)) >= tg) {
+        int step = 1, last = je - 1;  // t(last) >= tg
+        while (last + step < j1 && ts + __ldg(Lt + samp_idx32(last + step, nL, sh)) >= tg) {
           last += step;
           step <<= 1;
         }
-        int64_t a0 = last + 1, a1 = min(last + step, j1);  // first index with t < tg in [a0, a1]
+        int a0 = last + 1, a1 = min(last + step, j1);  // first index with t < tg in [a0, a1]
         while (a0 < a1) {
-          const int64_t mid = (a0 + a1) >> 1;
-          if (ts + __ldg(Lt + samp_idx(mid, nL, sh)) >= tg) a0 = mid + 1;
+          const int mid = (a0 + a1) >> 1;
+          if (ts + __ldg(Lt + samp_idx32(mid, nL, sh)) >= tg) a0 = mid + 1;
           else a1 = mid;
         }
         c_skip += a0 - jj;
@@ -1981,54 +1982,70 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       c_elem += je - jj;
       // element-level test of the chunk: p = #G points with m <= m_x; the
       // run elements are loaded EPRE at a time ahead of the (dependent) G walk
-      int64_t p = q;
+      int p = q;
       // G[p] and G[p-1] kept in registers: consecutive run elements mostly
       // share p, so the walk and the dominance test reload only when p moves
       int64_t gmp = p < g ? Gm[p] : INF;
       int64_t gmq = p > 0 ? Gm[p - 1] : 0, gtq = p > 0 ? Gt[p - 1] : INF;
-      for (int64_t j4 = jj; j4 < je; j4 += EPRE) {
-      int64_t em[EPRE], et[EPRE];
+      unsigned surv = 0;  // bit j - jj: run element j is a candidate
+      for (int j4 = jj; j4 < je; j4 += EPRE) {
+        int64_t em[EPRE], et[EPRE];
 #pragma unroll
-      for (int u = 0; u < EPRE; ++u) {
-        const int64_t iu = samp_idx(min(j4 + u, je - 1), nL, sh);
-        em[u] = __ldg(Lm + iu);
-        et[u] = __ldg(Lt + iu);
-      }
-#pragma unroll
-      for (int u = 0; u < EPRE; ++u) {
-        if (j4 + u >= je) break;
-        const int64_t il = samp_idx(j4 + u, nL, sh);
-        const int64_t m = ms + em[u];
-        const int64_t t = ts + et[u];
-        if (gmp <= m) {
-          do {
-            gmq = gmp;
-            ++p;
-            gmp = p < g ? Gm[p] : INF;
-          } while (gmp <= m);
-          gtq = Gt[p - 1];
+        for (int u = 0; u < EPRE; ++u) {
+          const int iu = samp_idx32(min(j4 + u, je - 1), nL, sh);
+          em[u] = __ldg(Lm + iu);
+          et[u] = __ldg(Lt + iu);
         }
-        if (p > 0 && (gtq < t || (gtq == t && gmq < m))) continue;
-        int64_t x, y, z;
-        if (lf == 0) { x = il; y = ia; z = ib; }
-        else if (lf == 1) { x = ia; y = il; z = ib; }
-        else { x = ia; y = ib; z = il; }
-        const uint64_t id = (uint64_t)(rel + (x * ny + y) * nz + z);
-        const int64_t gb = bb + p;
+#pragma unroll
+        for (int u = 0; u < EPRE; ++u) {
+          if (j4 + u >= je) break;
+          const int64_t m = ms + em[u];
+          const int64_t t = ts + et[u];
+          if (gmp <= m) {
+            do {
+              gmq = gmp;
+              ++p;
+              gmp = p < g ? Gm[p] : INF;
+            } while (gmp <= m);
+            gtq = Gt[p - 1];
+          }
+          if (!(p > 0 && (gtq < t || (gtq == t && gmq < m)))) surv |= 1u << (j4 + u - jj);
+        }
+      }
+      if (surv) {
+        // one slot reservation per chunk for the coalesced threads (instead of
+        // one per candidate), then the candidates are re-derived (L1 hits)
         cg::coalesced_group grp = cg::coalesced_threads();
+        const unsigned nsv = __popc(surv);
+        const unsigned off = cg::exclusive_scan(grp, nsv);
+        const unsigned tot = grp.shfl(off + nsv, grp.size() - 1);
         unsigned long long base = 0;
-        if (grp.thread_rank() == 0) base = atomicAdd(L.cand_cursor, (unsigned long long)grp.size());
-        base = grp.shfl(base, 0);
-        const unsigned long long idx = base + grp.thread_rank();
-        if ((int64_t)idx < L.cand_cap) {
-          atomicAdd(L.bcount + gb, 1u);  // no return value: slots are taken in k_scatter
-          atomicMin(L.bmin + gb, (long long)t);
-          L.cm[idx] = m;
-          L.ct[idx] = t;
-          L.cid[idx] = id;
-          L.cgb[idx] = gb;
+        if (grp.thread_rank() == 0) base = atomicAdd(L.cand_cursor, (unsigned long long)tot);
+        base = grp.shfl(base, 0) + off;
+        int pp = q;
+        while (surv) {
+          const int b = __ffs(surv) - 1;
+          surv &= surv - 1;
+          const int il = samp_idx32(jj + b, nL, sh);
+          const int64_t m = ms + __ldg(Lm + il);
+          const int64_t t = ts + __ldg(Lt + il);
+          while (pp < g && Gm[pp] <= m) ++pp;
+          int64_t x, y, z;  // (x, y, z) in 64 bits for the id
+          if (lf == 0) { x = il; y = ia; z = ib; }
+          else if (lf == 1) { x = ia; y = il; z = ib; }
+          else { x = ia; y = ib; z = il; }
+          const uint64_t id = (uint64_t)(rel + (x * ny + y) * nz + z);
+          const int64_t gb = bb + pp;
+          const unsigned long long idx = base++;
+          if ((int64_t)idx < L.cand_cap) {
+            atomicAdd(L.bcount + gb, 1u);  // no return value: slots are taken in k_carry_scatter
+            atomicMin(L.bmin + gb, (long long)t);
+            L.cm[idx] = m;
+            L.ct[idx] = t;
+            L.cid[idx] = id;
+            L.cgb[idx] = gb;
+          }
         }
-      }
       }
       jj = je;
     }
@@ -2089,13 +2106,27 @@ __global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, i
       __syncthreads();
     }
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t gb = L.cgb[i];
-    const int64_t d = L.boff[gb] + (int64_t)(atomicSub(L.bcount + gb, 1u) - 1u);
-    L.gm[d] = L.cm[i];
-    L.gt[d] = L.ct[i];
-    L.gid[d] = L.cid[i];
+  // consecutive candidates mostly share a bucket (k_filter emits a chunk's
+  // candidates contiguously): lanes with equal buckets take their slots with
+  // one atomic (warp-aggregated), the leader handing out ranks
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += gstride) {
+    const int64_t i = i0 + lane;
+    const bool act = i < n;
+    const int64_t gb = act ? L.cgb[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, gb);
+    const int leader = __ffs(peers) - 1;
+    unsigned top = 0;
+    if (act && lane == leader) top = atomicSub(L.bcount + gb, (unsigned)__popc(peers));
+    top = __shfl_sync(0xffffffffu, top, leader);
+    if (act) {
+      const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+      const int64_t d = L.boff[gb] + (int64_t)(top - 1u - rank);
+      L.gm[d] = L.cm[i];
+      L.gt[d] = L.ct[i];
+      L.gid[d] = L.cid[i];
+    }
   }
 }
 

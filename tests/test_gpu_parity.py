@@ -491,3 +491,24 @@ def test_weighted_heuristic(ft, alpha):
             assert np.array_equal(og.strategy(i), g.strategy(i))
         n += 1
     assert n > 6
+
+
+def test_composite_max_k_and_heur_fallback(ft):
+    """Composite configurations at the library's bound (K_h * K_i = 4096:
+    4,096-configuration operator, wide segments downstream), and FT_AUTO_HEUR
+    falling back to a composite when no source can be fixed (R21)."""
+    bridge = [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)]
+    w = G.random_graph(4, bridge, [3, 64, 64, 5], 7, cost_hi=1 << 30)
+    gg, st = compare(ft, w, strategies=16)
+    assert any(s["kind"] == "compose" and s["nseg"] == 4096 for s in st)
+    w = G.random_graph(5, bridge + [(3, 4)], [2, 3, 4, 3, 2], 11, cost_hi=1 << 16)
+    og = oracle.load(w, 4)
+    og.eliminate(oracle.AUTO_HEUR)
+    om, ot = og.frontier()
+    g = ft.load(w, keep_all=True)
+    g.eliminate(ft.AUTO_HEUR)
+    gm, gt = g.frontier()
+    assert np.array_equal(om, gm) and np.array_equal(ot, gt)
+    assert any(s["kind"] == "compose" for s in g.stats())
+    for i in range(len(om)):
+        assert np.array_equal(og.strategy(i), g.strategy(i))

@@ -99,6 +99,7 @@ struct ft_graph {
   std::set<std::pair<int, int>> multi;      // (pos0 src, pos0 dst) with >= 2 live edges
   std::vector<int> mark_stamp;
   int stamp = 0;
+  bool mark_dirty = true;  // the marking must be recomputed (see note_change)
   std::vector<FSet> sets;
   std::vector<StepRec> steps;
   std::vector<int> pending;       // scheduled, not yet executed steps
@@ -243,8 +244,20 @@ void refresh(ft_graph* g, int v) {
   if (g->in_e[v].size() + g->out_e[v].size() == 1) g->leaf.insert(key);
 }
 
+// The marking depends only on the first live operator and on the out-edges
+// of marked operators, so it is recomputed only after a change that touches
+// a marked operator or the first one (the policy runs O(n) eliminations;
+// re-walking the backbone after each one cost ~1 us per step on C5).
+inline void note_change(ft_graph* g, int v) {
+  if (g->mark_dirty || g->mark_stamp.empty()) return;
+  if (g->mark_stamp[v] == g->stamp || (!g->live_ops.empty() && g->live_ops.begin()->second == v))
+    g->mark_dirty = true;
+}
+
 void kill_edge(ft_graph* g, int e) {
   const int u = g->edges[e].src, v = g->edges[e].dst;
+  note_change(g, u);
+  note_change(g, v);
   g->edges[e].alive = false;
   g->out_e[u].erase(e);
   g->in_e[v].erase(e);
@@ -257,6 +270,10 @@ void kill_edge(ft_graph* g, int e) {
 }
 
 int add_edge(ft_graph* g, int s, int d, int set) {
+  if (!g->pos0.empty()) {
+    note_change(g, s);
+    note_change(g, d);
+  }
   g->edges.push_back(EdgeRec{s, d, true, set});
   int e = (int)g->edges.size() - 1;
   g->out_e[s].insert(e);
@@ -272,6 +289,7 @@ int add_edge(ft_graph* g, int s, int d, int set) {
 }
 
 void kill_op(ft_graph* g, int v) {
+  note_change(g, v);
   g->op_alive[v] = 0;
   refresh(g, v);
 }
@@ -280,6 +298,8 @@ void kill_op(ft_graph* g, int v) {
 // marked op has exactly one downstream op, that op.  Marked ops get the
 // current stamp.
 void mark_backbone(ft_graph* g) {
+  if (!g->mark_dirty) return;  // unchanged since the last walk
+  g->mark_dirty = false;
   ++g->stamp;
   if (g->live_ops.empty()) return;
   int v = g->live_ops.begin()->second;
@@ -1093,6 +1113,7 @@ void reorder(ft_graph* g) {
   }
   for (size_t q = 0; q < order.size(); ++q) g->pos0[order[q]] = (int)q;
   g->order0 = order;
+  g->mark_dirty = true;
   g->live_ops.clear();
   g->one_one.clear();
   g->leaf.clear();

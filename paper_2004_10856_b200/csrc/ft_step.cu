@@ -155,11 +155,13 @@ void scan_excl(const TIn* in, int64_t* out, const int64_t* n_dev, int64_t n_cap,
 // segment (ids, R6), sample sizes per level, the level at which the segment
 // is small enough for the direct path.
 
+constexpr int PLAN_BLK_CACHE = 128;  // factor sizes of a segment's blocks cached per warp (k_plan)
+
 __device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, int32_t* seg_d, int32_t* seg_n,
                                          int64_t* blk_rel, int64_t* seg_tuples, StepHdr* hdr,
                                          unsigned long long& sh_D, unsigned long long& sh_tuples,
                                          unsigned long long* sh_filter,
-                                         unsigned long long* sh_direct) {
+                                         unsigned long long* sh_direct, int (*wn)[3]) {
   // one warp per local output segment (gs, of step j); lanes stride over its blocks
   const int lane = threadIdx.x & 31;
   const StepDev& s = B.steps[j];
@@ -190,6 +192,11 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, i
     if (k < s.nblk) {
       const Blk b = load_blk(s, sg, k);
       nk = b.n[0] * b.n[1] * b.n[2];
+      if (k < PLAN_BLK_CACHE) {  // the level loop below reuses the factor sizes
+        wn[k][0] = (int)min(b.n[0], (int64_t)INT32_MAX);
+        wn[k][1] = (int)min(b.n[1], (int64_t)INT32_MAX);
+        wn[k][2] = (int)min(b.n[2], (int64_t)INT32_MAX);
+      }
     }
     const int64_t inc = warp_incl_sum<long long>(nk);
     if (k < s.nblk) rel_out[k] = rel + inc - nk;
@@ -219,9 +226,20 @@ __device__ __forceinline__ void plan_seg(const BatchDev& B, int64_t gs, int j, i
     if (l > 0) {
       const int sh = level_shift(l, B.slog0, B.slog);
       unsigned long long loc = 0;
+      __syncwarp();
       for (int64_t k = lane; k < s.nblk; k += 32) {
-        const Blk b = load_blk(s, sg, k);
-        loc += (unsigned long long)(samp_cnt(b.n[0], sh) * samp_cnt(b.n[1], sh) * samp_cnt(b.n[2], sh));
+        int64_t n0, n1, n2;
+        if (k < PLAN_BLK_CACHE) {
+          n0 = wn[k][0];
+          n1 = wn[k][1];
+          n2 = wn[k][2];
+        } else {
+          const Blk b = load_blk(s, sg, k);
+          n0 = b.n[0];
+          n1 = b.n[1];
+          n2 = b.n[2];
+        }
+        loc += (unsigned long long)(samp_cnt(n0, sh) * samp_cnt(n1, sh) * samp_cnt(n2, sh));
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
@@ -261,6 +279,7 @@ __global__ void __launch_bounds__(256) k_plan(BatchDev B, int32_t* seg_d, int32_
                                               StepHdr* hdr) {
   __shared__ unsigned long long sh_D, sh_tuples, sh_filter[LMAX + 1], sh_direct[LMAX + 1];
   __shared__ int64_t s_base[PLAN_BASE_CAP + 1];
+  __shared__ int s_wn[8][PLAN_BLK_CACHE][3];  // per warp (256 threads)
   if (threadIdx.x == 0) {
     sh_D = 0;
     sh_tuples = 0;
@@ -329,7 +348,9 @@ __global__ void __launch_bounds__(256) k_plan(BatchDev B, int32_t* seg_d, int32_
       const int b = __ffs(todo) - 1;
       todo &= todo - 1;
       const int jb = __shfl_sync(0xffffffffu, j, b);
-      plan_seg(B, g0 + b, jb, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct);
+      plan_seg(B, g0 + b, jb, seg_d, seg_n, blk_rel, seg_tuples, hdr, sh_D, sh_tuples, sh_filter, sh_direct,
+               s_wn[threadIdx.x >> 5]);
+      __syncwarp();  // s_wn reuse by the next segment
     }
   }
 #pragma unroll

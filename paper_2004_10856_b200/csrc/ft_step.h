@@ -132,7 +132,7 @@ class StepRunner {
   int small_wave_segs = 4096;         // waves with <= this many segments: capacity 2 x cdirect (A/B: 4096 > 1024 > 0)
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
-  int pack_grid = 148 * 4;             // CTAs of k_node_pack (each takes a contiguous pack range)
+  int pack_grid = 148 * 6;             // CTAs of k_node_pack (each takes a contiguous pack range; A/B: 888 > 592 > 444 > 296 on C5)
   bool filter_regs64 = false;          // k_filter64 (64 registers) instead of k_filter (80)
   int item_max = 512;                 // filter work item: max sampled run elements
   int item_div = 4;                   // ... and target items per resident thread

@@ -15,6 +15,11 @@
 
 namespace ftk {
 
+#ifndef DW_GEN_UNROLL
+#define DW_GEN_UNROLL 1  // k_direct_warp: rows generated per unrolled step (A/B builds)
+#endif
+constexpr int kDwGenUnroll = DW_GEN_UNROLL;
+
 // ---------------------------------------------------------------------------
 // Generic exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, n]; n read
 // from *n_dev when given (device-resident counts), else n_host.
@@ -1091,8 +1096,11 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
   long long lmin = INF, lmax = -1;
 #pragma unroll
   for (int r = 0; r < R; ++r) k[r] = ~0ull;
-#pragma unroll 1
-  for (int r = 0; r < R && (r << 5) < n; ++r) {
+  // rows generated DW_GEN_UNROLL at a time, so that the factor loads of
+  // several rows are in flight together (each row is a chain of dependent
+  // loads: block search, offsets, factor values)
+#pragma unroll kDwGenUnroll
+  for (int r = 0; r < R; ++r) {
     const int e = (r << 5) | lane;
     if (e < n) {
       int64_t vm, vt;

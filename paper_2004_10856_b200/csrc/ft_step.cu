@@ -138,6 +138,103 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
   }
 }
 
+// Two independent exclusive scans of host-sized arrays in ONE launch (the
+// per-level bucket-count and work-item scans): tiles [0, tA) belong to A,
+// [tA, tA + tB) to B, each with its own decoupled look-back chain; state =
+// [tA + tB tile states][tile counter][done counter], left zeroed.
+template <typename LoadA, typename LoadB, typename PostB>
+__global__ void __launch_bounds__(SCAN_NT) k_scan2(LoadA lda, int64_t nA, int64_t* outA, LoadB ldb, int64_t nB,
+                                                   int64_t* outB, unsigned long long* state, PostB postb) {
+  __shared__ long long sh[33];
+  __shared__ int64_t s_tile;
+  __shared__ long long s_pre;
+  const int64_t tA = (nA + SCAN_TILE - 1) / SCAN_TILE, tB = (nB + SCAN_TILE - 1) / SCAN_TILE;
+  unsigned long long* ctr = state + tA + tB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (tA == 0) outA[0] = 0;
+    if (tB == 0) outB[0] = 0;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ctr, 1ull);
+    __syncthreads();
+    const int64_t gt = s_tile;
+    if (gt >= tA + tB) break;
+    const bool isA = gt < tA;
+    const int64_t tile = isA ? gt : gt - tA, n = isA ? nA : nB, ntiles = isA ? tA : tB;
+    unsigned long long* st = isA ? state : state + tA;
+    int64_t* out = isA ? outA : outB;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    long long v[SCAN_ITEMS];
+    long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      v[i] = base + i < n ? (isA ? lda(base + i) : ldb(base + i)) : 0;
+      sum += v[i];
+    }
+    long long tot;
+    long long ex = block_excl_sum<SCAN_NT>(sum, sh, &tot);
+    if (wid == 0) {
+      long long pre = 0;
+      if (tile == 0) {
+        if (lane == 0) atomicExch(st + tile, SC_PREF | (unsigned long long)tot);
+      } else {
+        if (lane == 0) atomicExch(st + tile, SC_AGG | (unsigned long long)tot);
+        int64_t p = tile - 1;
+        for (;;) {
+          const int64_t q = p - lane;
+          const unsigned long long x = q >= 0 ? *(volatile unsigned long long*)(st + q) : SC_PREF;
+          const unsigned long long fl = x & ~SC_VAL;
+          const unsigned pref = __ballot_sync(0xffffffffu, fl == SC_PREF);
+          const unsigned ready = __ballot_sync(0xffffffffu, fl != 0);
+          const int fp = pref ? __ffs(pref) - 1 : 32;
+          const unsigned need = fp == 32 ? 0xffffffffu : (fp == 31 ? 0xffffffffu : ((2u << fp) - 1u));
+          if ((ready & need) != need) continue;
+          long long c = lane <= fp ? (long long)(x & SC_VAL) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+          pre += c;
+          if (fp < 32) break;
+          p -= 32;
+        }
+        if (lane == 0) atomicExch(st + tile, SC_PREF | (unsigned long long)(pre + tot));
+      }
+      if (lane == 0) s_pre = pre;
+    }
+    __syncthreads();
+    ex += s_pre;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      if (base + i < n) {
+        out[base + i] = ex;
+        if (!isA) postb(base + i, ex, v[i]);
+      }
+      ex += v[i];
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
+    __syncthreads();
+  }
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    for (int64_t i = threadIdx.x; i < tA + tB; i += SCAN_NT) state[i] = 0;
+    if (threadIdx.x == 0) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+template <typename LoadA, typename LoadB, typename PostB>
+void scan2_excl_fn(LoadA lda, int64_t nA, int64_t* outA, LoadB ldb, int64_t nB, int64_t* outB, int64_t* tmp,
+                   cudaStream_t st, PostB postb) {
+  const int64_t tiles = (nA + SCAN_TILE - 1) / SCAN_TILE + (nB + SCAN_TILE - 1) / SCAN_TILE;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
+  k_scan2<LoadA, LoadB, PostB><<<grid, SCAN_NT, 0, st>>>(lda, nA, outA, ldb, nB, outB,
+                                                          (unsigned long long*)tmp, postb);
+}
+
 // tmp: >= scan_tmp_elems(n_cap) int64 slots, zero on first use (`fresh`
 // zeroes it here); every scan leaves it zeroed again.
 template <typename Load, typename Post = NoPost>
@@ -2930,7 +3027,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   // capacity: one filter level fewer per segment, and few CTAs sort in smem
   // (A/B: a global 2048 helped C5's LDP waves but slowed C4's 6e4-segment
   // node waves, 52 -> 58 ms)
-  const int cd = nloc <= small_wave_segs ? std::min(C_DIRECT, cdirect * 2) : cdirect;
+  const int cd = nloc <= small_wave_segs ? std::min(C_DIRECT, cdirect_small) : cdirect;
   s.cdirect = cd;
   s.nseg = nloc;
   s.nblk = nbl;
@@ -3045,7 +3142,8 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(whint, int32_t, hcap);
       GROW(ncand, int64_t, 2);
     }
-    const int64_t scan_n = std::max<int64_t>({nloc + 1, nbl + 1, bcap + 1, cand_cap + 1});
+    // scan scratch: the largest single scan, or the bucket-count + work-item pair
+    const int64_t scan_n = std::max<int64_t>({nloc + nbl + 2 * SCAN_TILE, bcap + 1, cand_cap + 1});
     {  // scan scratch: zeroed when (re)allocated -- compare the capacity, not the
        // address (a larger allocation can come back at the same address); scans
        // leave it zeroed
@@ -3125,9 +3223,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
-        nl += 3;  // scan(+nb), scan(+work counts), filter
-        scan_excl_fn(LoadNb{L}, L.bucket_base, nullptr, nloc, tmp, st);
-        scan_excl_fn(LoadWork{s, L}, L.wo, nullptr, nbl, tmp, st, false, PostHint{L.whint, L.hcap});
+        nl += 2;  // scan(+nb) and scan(+work counts) in one launch, filter
+        scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadWork{s, L}, nbl, L.wo, tmp, st,
+                      PostHint{L.whint, L.hcap});
         mark(2);  // filter_ms: k_filter alone
         if (filter_regs64) k_filter64<<<filter_grid, 128, 0, st>>>(s, L);
         else k_filter<<<filter_grid, 128, 0, st>>>(s, L);
@@ -3289,8 +3387,16 @@ cudaError_t StepRunner::configure() {
   }
   if (const char* e = getenv("FT_SLOG")) slog = std::max(1, std::min(6, atoi(e)));
   if (const char* e = getenv("FT_SLOG0")) slog0 = std::max(1, std::min(6, atoi(e)));
-  if (const char* e = getenv("FT_CDIRECT")) cdirect = std::max(256, std::min(C_DIRECT, atoi(e)));
+  // direct capacities are powers of two: a sample of n tuples is sorted as
+  // the next power of two N >= n, which must fit the capacity
+  auto pow2_floor = [](int v) {
+    int p = 256;
+    while (p * 2 <= v) p *= 2;
+    return p;
+  };
+  if (const char* e = getenv("FT_CDIRECT")) cdirect = pow2_floor(std::min(C_DIRECT, atoi(e)));
   if (const char* e = getenv("FT_SMALL_WAVE")) small_wave_segs = std::max(0, atoi(e));
+  if (const char* e = getenv("FT_CDIRECT_SMALL")) cdirect_small = pow2_floor(std::min(C_DIRECT, atoi(e)));
   {
     cudaError_t e0 = cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)direct_smem(C_DIRECT));

@@ -128,8 +128,10 @@ class StepRunner {
 
   int slog = 4;                       // sample stride x16 per level beyond level 1
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
-  int cdirect = 1024;                 // direct-path capacity (<= C_DIRECT)
-  int small_wave_segs = 4096;         // waves with <= this many segments: capacity 2 x cdirect (A/B: 4096 > 1024 > 0)
+  int cdirect = 512;                  // direct-path capacity of large waves (power of 2 <= C_DIRECT;
+                                      // A/B: 512 beats 1024 on C4 by 1 ms, C5 equal)
+  int small_wave_segs = 4096;         // waves with <= this many segments: capacity cdirect_small (A/B: 4096 > 1024 > 0)
+  int cdirect_small = 2048;           // direct capacity of waves of <= small_wave_segs segments
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
   int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
   int pack_grid = 148 * 6;             // CTAs of k_node_pack (each takes a contiguous pack range; A/B: 888 > 592 > 444 > 296 on C5)

@@ -57,68 +57,78 @@ def solve(w, key):
         edges = {e: (s, d, p.astype(object), q.astype(object)) for e, (s, d, p, q) in edges.items()}
     alive = set(range(n))
     nid = w.n_edges
+    # live adjacency kept incrementally (a worklist of operators and parallel
+    # pairs to revisit); the scalar (min, +) optimum does not depend on the
+    # order in which series / parallel / fold reductions are applied
+    ins = {i: set() for i in range(n)}
+    outs = {i: set() for i in range(n)}
+    pairs = {}
 
-    def adj():
-        ins = {i: [] for i in alive}
-        outs = {i: [] for i in alive}
-        for e, (s, d, _, _) in edges.items():
-            outs[s].append(e)
-            ins[d].append(e)
-        return ins, outs
+    def link(e, s, d):
+        outs[s].add(e)
+        ins[d].add(e)
+        pairs.setdefault((s, d), set()).add(e)
 
-    changed = True
-    while changed:
-        changed = False
-        # parallel edges
-        by_pair = {}
-        for e, (s, d, _, _) in sorted(edges.items()):
-            by_pair.setdefault((s, d), []).append(e)
-        for (s, d), es in by_pair.items():
+    def unlink(e):
+        s, d, _, _ = edges.pop(e)
+        outs[s].discard(e)
+        ins[d].discard(e)
+        ps = pairs[(s, d)]
+        ps.discard(e)
+        if not ps:
+            del pairs[(s, d)]
+
+    for e, (s, d, _, _) in edges.items():
+        link(e, s, d)
+    work_pairs = {k for k, v in pairs.items() if len(v) > 1}
+    work_ops = set(range(n))
+    while work_pairs or work_ops:
+        if work_pairs:  # parallel edges: C = C1 + C2 (+ ...)
+            s, d = work_pairs.pop()
+            es = sorted(pairs.get((s, d), ()))
             if len(es) > 1:
                 P = sum(edges[e][2] for e in es)
                 Q = sum(edges[e][3] for e in es)
                 for e in es:
-                    del edges[e]
+                    unlink(e)
                 edges[nid] = (s, d, P, Q)
+                link(nid, s, d)
                 nid += 1
-                changed = True
-        if changed:
+                work_ops.update((s, d))
             continue
-        ins, outs = adj()
-        # series: any 1-in-1-out op
-        for i in sorted(alive):
-            if len(ins[i]) == 1 and len(outs[i]) == 1:
-                h, _, A, Ab = edges[ins[i][0]]
-                _, j, B, Bb = edges[outs[i][0]]
-                P = A[:, :, None] + op[i][0][None, :, None] + B[None, :, :]
-                Q = Ab[:, :, None] + op[i][1][None, :, None] + Bb[None, :, :]
-                Pm, Qm = _lexmin(P, Q, 1)
-                del edges[ins[i][0]], edges[outs[i][0]]
-                alive.discard(i)
-                edges[nid] = (h, j, Pm, Qm)
-                nid += 1
-                changed = True
-                break
-        if changed:
+        i = work_ops.pop()
+        if i not in alive:
             continue
-        # fold K=1 sources
-        for i in sorted(alive):
-            if K[i] == 1 and not ins[i] and outs[i]:
-                first = True
-                for e in sorted(outs[i]):
-                    _, j, A, Ab = edges[e]
-                    p = op[j][0] + A[0]
-                    q = op[j][1] + Ab[0]
-                    if first:
-                        p = p + op[i][0][0]
-                        q = q + op[i][1][0]
-                        first = False
-                    op[j] = (p, q)
-                    del edges[e]
-                alive.discard(i)
-                changed = True
-                break
-    ins, outs = adj()
+        if len(ins[i]) == 1 and len(outs[i]) == 1:  # series: min over the middle config
+            ei, eo = next(iter(ins[i])), next(iter(outs[i]))
+            h, _, A, Ab = edges[ei]
+            _, j, Bm, Bb = edges[eo]
+            P = A[:, :, None] + op[i][0][None, :, None] + Bm[None, :, :]
+            Q = Ab[:, :, None] + op[i][1][None, :, None] + Bb[None, :, :]
+            Pm, Qm = _lexmin(P, Q, 1)
+            unlink(ei)
+            unlink(eo)
+            alive.discard(i)
+            edges[nid] = (h, j, Pm, Qm)
+            link(nid, h, j)
+            if len(pairs[(h, j)]) > 1:
+                work_pairs.add((h, j))
+            nid += 1
+            work_ops.update((h, j))
+        elif K[i] == 1 and not ins[i] and outs[i]:  # fold a K=1 source
+            first = True
+            for e in sorted(outs[i]):
+                _, j, A, Ab = edges[e]
+                p = op[j][0] + A[0]
+                q = op[j][1] + Ab[0]
+                if first:
+                    p = p + op[i][0][0]
+                    q = q + op[i][1][0]
+                    first = False
+                op[j] = (p, q)
+                unlink(e)
+                work_ops.add(j)
+            alive.discard(i)
     srcs = [i for i in alive if not ins[i]]
     assert len(srcs) == 1, "scalar DP: graph is not series-parallel reducible"
     cur = srcs[0]
@@ -126,7 +136,7 @@ def solve(w, key):
     seen = 1
     while outs[cur]:
         assert len(outs[cur]) == 1
-        _, j, A, Ab = edges[outs[cur][0]]
+        _, j, A, Ab = edges[next(iter(outs[cur]))]
         P = vP[:, None] + A
         Q = vQ[:, None] + Ab
         pm, qm = _lexmin(P, Q, 0)

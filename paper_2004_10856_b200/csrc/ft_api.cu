@@ -100,6 +100,7 @@ struct ft_graph {
   std::vector<int> mark_stamp;
   int stamp = 0;
   bool mark_dirty = true;  // the marking must be recomputed (see note_change)
+  std::vector<uint8_t> cand;  // refresh(): membership bits of one_one (1), k1src (2), leaf (4)
   std::vector<FSet> sets;
   std::vector<StepRec> steps;
   std::vector<int> pending;       // scheduled, not yet executed steps
@@ -230,18 +231,37 @@ std::vector<int> topo_order(const ft_graph* g) {
   return order;
 }
 
+// Keeps op v's membership of the policy's candidate sets (one_one, k1src,
+// leaf; keyed by topological position) current; touches the ordered sets only
+// when a membership changes (cand[v] caches it: most edge updates leave it).
 void refresh(ft_graph* g, int v) {
   const std::pair<int, int> key{g->pos0[v], v};
-  g->one_one.erase(key);
-  g->k1src.erase(key);
-  g->leaf.erase(key);
-  if (!g->op_alive[v]) {
+  if ((int)g->cand.size() <= v) g->cand.resize(v + 1, 0);
+  const uint8_t have = g->cand[v];
+  uint8_t want = 0;
+  if (g->op_alive[v]) {
+    const size_t ni = g->in_e[v].size(), no = g->out_e[v].size();
+    if (ni == 1 && no == 1) want |= 1;
+    if (g->K[v] == 1 && ni == 0 && no > 0) want |= 2;
+    if (ni + no == 1) want |= 4;
+  } else {
     g->live_ops.erase(key);
-    return;
   }
-  if (g->in_e[v].size() == 1 && g->out_e[v].size() == 1) g->one_one.insert(key);
-  if (g->K[v] == 1 && g->in_e[v].empty() && !g->out_e[v].empty()) g->k1src.insert(key);
-  if (g->in_e[v].size() + g->out_e[v].size() == 1) g->leaf.insert(key);
+  if (want == have) return;
+  const uint8_t diff = want ^ have;
+  if (diff & 1) {
+    if (want & 1) g->one_one.insert(key);
+    else g->one_one.erase(key);
+  }
+  if (diff & 2) {
+    if (want & 2) g->k1src.insert(key);
+    else g->k1src.erase(key);
+  }
+  if (diff & 4) {
+    if (want & 4) g->leaf.insert(key);
+    else g->leaf.erase(key);
+  }
+  g->cand[v] = want;
 }
 
 // The marking depends only on the first live operator and on the out-edges
@@ -1119,6 +1139,7 @@ void reorder(ft_graph* g) {
   g->leaf.clear();
   g->k1src.clear();
   g->multi.clear();
+  std::fill(g->cand.begin(), g->cand.end(), 0);
   for (int v : order) {
     g->live_ops.insert({g->pos0[v], v});
     refresh(g, v);

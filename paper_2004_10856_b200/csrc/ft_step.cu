@@ -1903,17 +1903,26 @@ struct LoadWork {
   }
 };
 
-// Epilogue of the work-offset scan: block beta covers filter items
-// [wo[beta], wo[beta] + count); record it as the block of every item c*32
-// (a warp's first item) in that range, so k_filter finds a warp's blocks
-// with two loads instead of two binary searches over all blocks.
-struct PostHint {
-  int32_t* hint;
-  int64_t hcap;
-  __device__ __forceinline__ void operator()(int64_t beta, long long ex, long long v) const {
-    for (long long c = (ex + 31) >> 5; c < hcap && (c << 5) < ex + v; ++c) hint[c] = (int32_t)beta;
+// Warp-start block hints for k_filter: hint[c] = the block of filter item
+// 32c (largest beta with wo[beta] <= 32c), one thread per hint, so that a
+// k_filter warp finds its items' blocks with two loads instead of two binary
+// searches over all blocks at the head of its dependent-load chain.  (Written
+// first in the work-offset scan's epilogue: serial per block, ~30 us per
+// LDP level.)
+__global__ void __launch_bounds__(256) k_hints(BatchDev B, LevelDev L) {
+  const int64_t nbl = B.nblk, W = L.wo[nbl];
+  const int64_t nh = min((W + 31) >> 5, L.hcap);
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nh; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = c << 5;
+    int64_t lo = 0, hi = nbl;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (L.wo[mid] <= x) lo = mid;
+      else hi = mid;
+    }
+    L.whint[c] = (int32_t)lo;
   }
-};
+}
 
 // K1: product + pre-filter, output-sensitive run walk.  A work item is a
 // range of one run (short-factor indices fixed, long factor sweeping: m
@@ -1941,7 +1950,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     const int64_t w0 = wbase + (threadIdx.x & ~31);  // first item of this warp
     if (w0 >= W) break;
     // blocks of the warp's items: hint[w0/32] holds the block of item w0 and
-    // hint[w0/32 + 1] that of item w0 + 32 (the scan's epilogue, PostHint);
+    // hint[w0/32 + 1] that of item w0 + 32 (k_hints);
     // beyond the hint table, two full binary searches per warp.  Then a
     // bounded binary search per lane.
     const int64_t c0 = w0 >> 5;
@@ -3090,7 +3099,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     plan_copy[l] = hdr_host->direct_samp[l];
     plan_copy[LMAX + 1 + l] = hdr_host->filter_samp[l];
   }
-  // warp-start hints of the filter items (PostHint): W <= the level's sample
+  // warp-start hints of the filter items (k_hints): W <= the level's sample
   // (an item holds >= 1 sampled element), capped at 4 M entries (16 MB);
   // warps beyond it search
   const int64_t hcap = nbl < ((int64_t)1 << 31) ? std::min<int64_t>(need_filter / 32 + 2, 1 << 22) : 0;
@@ -3224,8 +3233,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
         nl += 2;  // scan(+nb) and scan(+work counts) in one launch, filter
-        scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadWork{s, L}, nbl, L.wo, tmp, st,
-                      PostHint{L.whint, L.hcap});
+        scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadWork{s, L}, nbl, L.wo, tmp, st, NoPost());
+        ++nl;
+        k_hints<<<148 * 4, 256, 0, st>>>(s, L);
         mark(2);  // filter_ms: k_filter alone
         if (filter_regs64) k_filter64<<<filter_grid, 128, 0, st>>>(s, L);
         else k_filter<<<filter_grid, 128, 0, st>>>(s, L);

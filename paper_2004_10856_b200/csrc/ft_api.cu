@@ -101,6 +101,11 @@ struct ft_graph {
   int stamp = 0;
   bool mark_dirty = true;  // the marking must be recomputed (see note_change)
   std::vector<uint8_t> cand;  // refresh(): membership bits of one_one (1), k1src (2), leaf (4)
+  struct CommEv {
+    int step;
+    cudaEvent_t a, b;
+  };
+  std::vector<CommEv> comm_ev;  // exchange events of sharded waves (read by ft_get_stats)
   std::vector<FSet> sets;
   std::vector<StepRec> steps;
   std::vector<int> pending;       // scheduled, not yet executed steps
@@ -740,12 +745,12 @@ int exec_wave(ft_graph* g, const std::vector<int>& ids) {
     if (nr != ncclSuccess) return nccl_fail(g, nr);
     CU(ftk::unpack_data(sall, maxn, posd, world, maxn, wb.m, wb.t, wb.bp, g->stream), "unpack survivors");
     cudaEventRecord(cb, g->stream);
-    CU(cudaStreamSynchronize(g->stream), "wave sync");
+    // no host sync at the end of the wave (the next one is stream-ordered);
+    // the exchange time is read from the events when stats are requested
     g->runner->fence(g->stream);
-    float comm_ms = 0;
-    cudaEventElapsedTime(&comm_ms, ca, cb);
-    cudaEventDestroy(ca);
-    cudaEventDestroy(cb);
+    CU(cudaGetLastError(), "wave");
+    const float comm_ms = 0;
+    g->comm_ev.push_back({ids[0], ca, cb});
     const double h4 = now_ms();
     wb.live = ns;
     for (int q = 0; q < ns; ++q) {
@@ -1713,6 +1718,10 @@ void ft_graph_destroy(ft_graph* g) {
   }
   if (g->d_costs) g->alloc.put(g->d_costs, g->stream);
   if (g->stream) cudaStreamSynchronize(g->stream);  // back to the pool (not the driver)
+  for (auto& ev : g->comm_ev) {
+    cudaEventDestroy(ev.a);
+    cudaEventDestroy(ev.b);
+  }
   if (g->runner) ftk::release_runner(g->dev, g->alloc);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -1988,6 +1997,12 @@ int ft_get_stats(const ft_graph* g, ft_step_stats* buf, int64_t cap, int64_t* n_
   if (cap < *n_out) return FT_ESIZE;
   for (size_t i = 0; i < g->steps.size(); ++i)
     if (buf) buf[i] = g->steps[i].st;
+  if (buf)
+    for (const auto& ev : g->comm_ev) {  // exchange time of each sharded wave (first step)
+      float ms = 0;
+      if (cudaEventSynchronize(ev.b) == cudaSuccess && cudaEventElapsedTime(&ms, ev.a, ev.b) == cudaSuccess)
+        buf[ev.step].comm_ms = ms;
+    }
   return FT_OK;
 }
 

@@ -39,6 +39,18 @@ constexpr int CHUNK = 16;           // run elements per filter work item
 constexpr int BUCKET_SMEM = 4096;   // largest bucket sorted in shared memory
 constexpr int BMIN_FILL = 0x7F;     // memset byte: 0x7F7F..7F > any t (< 2^60)
 
+// Programmatic dependent launch (PDL): the pipeline's kernels are launched
+// with programmatic stream serialisation, so a kernel's CTAs are dispatched
+// while its predecessor still runs.  Every such kernel opens with this: wait
+// until the predecessor grid has completed and its writes are visible (before
+// ANY global access -- reads of its outputs and writes of its inputs alike),
+// then let the successor launch.  Without the launch attribute both are no-ops.
+#define FT_PDL_ENTRY()                                          \
+  do {                                                          \
+    asm volatile("griddepcontrol.wait;" ::: "memory");          \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
 enum { K_NODE = 1, K_EDGE = 2, K_FOLD = 3, K_LDP = 4, K_FINAL = 5, K_PAIR = 6, K_BRANCH = 7, K_COMPOSE = 8,
        K_REMAP = 9 };
 

@@ -20,6 +20,30 @@ namespace ftk {
 #endif
 constexpr int kDwGenUnroll = DW_GEN_UNROLL;
 
+// Launches of the per-level pipeline: with programmatic stream serialisation
+// (FT_PDL_ENTRY in every kernel launched here) unless FT_PDL=0.
+static bool g_pdl = true;
+
+template <typename... KArgs, typename... Args>
+static inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args... args) {
+  if (!g_pdl) {
+    k<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // ---------------------------------------------------------------------------
 // Generic exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, n]; n read
 // from *n_dev when given (device-resident counts), else n_host.
@@ -60,6 +84,7 @@ template <typename Load, typename Post = NoPost>
 __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev, int64_t n_host,
                                                    int64_t* out, unsigned long long* state,
                                                    Post post = Post()) {
+  FT_PDL_ENTRY();
   __shared__ long long sh[33];
   __shared__ int64_t s_tile;
   __shared__ long long s_pre;
@@ -145,6 +170,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
 template <typename LoadA, typename LoadB, typename PostB>
 __global__ void __launch_bounds__(SCAN_NT) k_scan2(LoadA lda, int64_t nA, int64_t* outA, LoadB ldb, int64_t nB,
                                                    int64_t* outB, unsigned long long* state, PostB postb) {
+  FT_PDL_ENTRY();
   __shared__ long long sh[33];
   __shared__ int64_t s_tile;
   __shared__ long long s_pre;
@@ -231,7 +257,7 @@ void scan2_excl_fn(LoadA lda, int64_t nA, int64_t* outA, LoadB ldb, int64_t nB, 
                    cudaStream_t st, PostB postb) {
   const int64_t tiles = (nA + SCAN_TILE - 1) / SCAN_TILE + (nB + SCAN_TILE - 1) / SCAN_TILE;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
-  k_scan2<LoadA, LoadB, PostB><<<grid, SCAN_NT, 0, st>>>(lda, nA, outA, ldb, nB, outB,
+  launch(k_scan2<LoadA, LoadB, PostB>, dim3(grid), dim3(SCAN_NT), 0, st, lda, nA, outA, ldb, nB, outB,
                                                           (unsigned long long*)tmp, postb);
 }
 
@@ -243,7 +269,8 @@ void scan_excl_fn(Load ld, int64_t* out, const int64_t* n_dev, int64_t n_cap, in
   const int64_t tiles = (n_cap + SCAN_TILE - 1) / SCAN_TILE;
   if (fresh) cudaMemsetAsync(tmp, 0, sizeof(int64_t) * (size_t)(ntiles_cap_slot(n_cap) + 2), st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 4));
-  k_scan1<Load, Post><<<grid, SCAN_NT, 0, st>>>(ld, n_dev, n_cap, out, (unsigned long long*)tmp, post);
+  launch(k_scan1<Load, Post>, dim3(grid), dim3(SCAN_NT), 0, st, ld, n_dev, n_cap, out, (unsigned long long*)tmp,
+         post);
 }
 
 template <typename TIn>
@@ -379,6 +406,7 @@ constexpr int PLAN_BASE_CAP = 2048;  // step bases cached in shared memory by k_
 __global__ void __launch_bounds__(256) k_plan(BatchDev B, int32_t* seg_d, int32_t* seg_n,
                                               int64_t* blk_rel, int64_t* seg_tuples,
                                               StepHdr* hdr) {
+  FT_PDL_ENTRY();
   __shared__ unsigned long long sh_D, sh_tuples, sh_filter[LMAX + 1], sh_direct[LMAX + 1];
   __shared__ int64_t s_base[PLAN_BASE_CAP + 1];
   __shared__ int s_wn[8][PLAN_BLK_CACHE][3];  // per warp (256 threads)
@@ -771,6 +799,7 @@ constexpr int DIRECT_MAXBLK = 128;  // per-block info cached in smem up to this 
 static size_t direct_smem(int cap) { return (size_t)cap * (3 * 8 + 4 + 4) + 8; }
 
 __global__ void __launch_bounds__(DIRECT_NT, 3) k_direct(BatchDev B, LevelDev L) {
+  FT_PDL_ENTRY();
   extern __shared__ int64_t dyn_direct[];  // capacity B.cdirect (runtime)
   int64_t* sm = dyn_direct;
   int64_t* stt = sm + B.cdirect;
@@ -1264,6 +1293,7 @@ __device__ void warp_direct_seg(const BatchDev& B, const LevelDev& L, int64_t gs
 }
 
 __global__ void __launch_bounds__(256, 3) k_direct_warp(BatchDev B, LevelDev L) {
+  FT_PDL_ENTRY();
   __shared__ int pre_all[8][WARP_DIRECT + 1];
   __shared__ Blk blk_all[8][WARP_BLK_CACHE];
   extern __shared__ int64_t dyn_dw[];  // per warp: t[WARP_DIRECT], id[WARP_DIRECT]
@@ -1410,6 +1440,7 @@ __device__ __forceinline__ int np_row_sort(const StepDev& s, const int* pre, con
 __global__ void __launch_bounds__(NP_NT, 3) k_node_pack(BatchDev B, LevelDev L, const NodeGroup* packs,
                                                      int npacks, int rmax, int64_t ztn,
                                                      NodeGroup* big) {
+  FT_PDL_ENTRY();
   extern __shared__ int64_t dyn_np[];
   int64_t* ztab = dyn_np;                                        // [ztn] t_z(k, p) at k*tpr+pl
   int64_t* sm = ztab + ztn;                                      // [rmax][WARP_DIRECT]
@@ -1617,6 +1648,7 @@ static_assert(sizeof(NodeGroup) == sizeof(NodeGroupH), "NodeGroup layout");
 
 __global__ void __launch_bounds__(DIRECT_NT) k_node_shared(BatchDev B, LevelDev L,
                                                            const NodeGroup* groups) {
+  FT_PDL_ENTRY();
   const int ngroups = (int)L.hdr->ns_big;  // rows k_node_pack handed over
   extern __shared__ int64_t dyn_ns[];
   int64_t* sm = dyn_ns;                            // [NS_CAP] m (sorted by (m, id))
@@ -1910,6 +1942,7 @@ struct LoadWork {
 // first in the work-offset scan's epilogue: serial per block, ~30 us per
 // LDP level.)
 __global__ void __launch_bounds__(256) k_hints(BatchDev B, LevelDev L) {
+  FT_PDL_ENTRY();
   const int64_t nbl = B.nblk, W = L.wo[nbl];
   const int64_t nh = min((W + 31) >> 5, L.hcap);
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nh; c += (int64_t)gridDim.x * blockDim.x) {
@@ -2195,8 +2228,8 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
 
 // Two register budgets for the same body (A/B: FT_FILTER_REGS=64 selects the
 // 64-register variant, 8 CTAs of 128 threads per SM; default 80 registers).
-__global__ void __launch_bounds__(128, 6) k_filter(BatchDev B, LevelDev L) { filter_body(B, L); }
-__global__ void __launch_bounds__(128, 8) k_filter64(BatchDev B, LevelDev L) { filter_body(B, L); }
+__global__ void __launch_bounds__(128, 6) k_filter(BatchDev B, LevelDev L) { FT_PDL_ENTRY(); filter_body(B, L); }
+__global__ void __launch_bounds__(128, 8) k_filter64(BatchDev B, LevelDev L) { FT_PDL_ENTRY(); filter_body(B, L); }
 
 
 // Carry per bucket: exclusive prefix-min of bucket minima within the segment
@@ -2211,6 +2244,7 @@ __constant__ unsigned char kBminFill[8] = {BMIN_FILL, BMIN_FILL, BMIN_FILL, BMIN
                                            BMIN_FILL, BMIN_FILL, BMIN_FILL, BMIN_FILL};
 
 __global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, int64_t* ncand) {
+  FT_PDL_ENTRY();
   __shared__ long long sh[33];
   __shared__ long long chunk_min;
   const unsigned long long cc = *(volatile unsigned long long*)L.cand_cursor;  // final: k_filter is done
@@ -2373,6 +2407,7 @@ __device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int6
 }
 
 __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L) {
+  FT_PDL_ENTRY();
   if (L.hdr->overflow) return;
   __shared__ int slist_all[8][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2481,6 +2516,7 @@ __device__ void bucket_huge_one(const LevelDev& L, int64_t bkt, int64_t* sm, int
                                 long long* sh);
 
 __global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
+  FT_PDL_ENTRY();
   extern __shared__ int64_t dyn[];
   int64_t* sm = dyn;
   int64_t* stt = sm + BUCKET_SMEM;
@@ -2626,6 +2662,7 @@ __device__ void bucket_huge_one(const LevelDev& L, int64_t bkt, int64_t* sm, int
 // reserved by cursor atomics, never exceed it; the pool holds both), and
 // every filter segment's pool range is recorded (one launch).
 __global__ void k_compact(BatchDev B, LevelDev L, const int64_t* gpos, const int64_t* ncand, int64_t base) {
+  FT_PDL_ENTRY();
   const int64_t n = *ncand;
   const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gstride = (int64_t)gridDim.x * blockDim.x;
   if (g0 == 0) {
@@ -2656,6 +2693,7 @@ __global__ void k_compact(BatchDev B, LevelDev L, const int64_t* gpos, const int
 // Final gather of the level-0 pool into every step's CSR output set (one
 // warp per segment).
 __global__ void __launch_bounds__(256) k_gather(BatchDev B, Pool P) {
+  FT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gs < B.nseg; gs += nw) {
@@ -2677,6 +2715,7 @@ __global__ void __launch_bounds__(256) k_gather(BatchDev B, Pool P) {
 // for the tile's segment range, then a short search per element.
 __global__ void __launch_bounds__(256) k_gather_flat(BatchDev B, Pool P, const int64_t* pos,
                                                      int64_t* om, int64_t* ot, uint64_t* obp) {
+  FT_PDL_ENTRY();
   __shared__ int64_t seg_lo_s, seg_hi_s;
   const int64_t total = pos[B.nseg];
   const int64_t ntiles = (total + 2047) / 2048;
@@ -2717,6 +2756,7 @@ __global__ void __launch_bounds__(256) k_gather_flat(BatchDev B, Pool P, const i
 // entries start at seg_base[j] + j) and per-step totals / max / tuples.
 __global__ void k_wave_off(BatchDev B, const int64_t* cnt, const int64_t* seg_tuples,
                            const int64_t* pos, int64_t* off, int64_t* step_arr) {
+  FT_PDL_ENTRY();
   const int64_t gs = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gs >= B.nseg) return;
   const int j = find_base(B.seg_base, B.nsteps, gs);
@@ -3082,7 +3122,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
   mark(0);
   cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
   ++nl;
-  k_plan<<<grid_for(nloc * 32, 256, 148 * 8), 256, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
+  launch(k_plan, dim3(grid_for(nloc * 32, 256, 148 * 8)), dim3(256), 0, st, s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                             (int64_t*)blk_rel.p,
                                                             (int64_t*)seg_tuples.p, H);
   cudaMemcpyAsync(hdr_host, H, sizeof(StepHdr), cudaMemcpyDeviceToHost, st);
@@ -3121,8 +3161,10 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     GROW(poolA_cnt, int64_t, nloc);
     GROW(poolB_start, int64_t, nloc);
     GROW(poolB_cnt, int64_t, nloc);
-    GROW(cursors, unsigned long long, 8);
-    cudaMemsetAsync(cursors.p, 0, sizeof(unsigned long long) * 8, st);  // cand / large cursors (k_compact resets them per level)
+    // [0..8): cand / large cursors (k_compact resets them per level); [8 + l]:
+    // the output cursor of level l (no memset between a wave's kernels: PDL)
+    GROW(cursors, unsigned long long, 8 + LMAX + 1);
+    cudaMemsetAsync(cursors.p, 0, sizeof(unsigned long long) * (8 + LMAX + 1), st);
     if (D > 0) {
       GROW(nb, int64_t, nloc);
       GROW(bucket_base, int64_t, nloc + 1);
@@ -3163,7 +3205,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
     unsigned long long* cur = (unsigned long long*)cursors.p;
     if (attempt > 0) {
       cudaMemsetAsync(H, 0, sizeof(StepHdr), st);
-      k_plan<<<grid_for(nloc * 32, 256, 148 * 8), 256, 0, st>>>(s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
+      launch(k_plan, dim3(grid_for(nloc * 32, 256, 148 * 8)), dim3(256), 0, st, s, (int32_t*)seg_d.p, (int32_t*)seg_n.p,
                                                                 (int64_t*)blk_rel.p,
                                                                 (int64_t*)seg_tuples.p, H);
     }
@@ -3191,20 +3233,20 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       L.in = pools[(l + 1) & 1];
       L.out = pools[l & 1];
       L.hdr = H;
-      cudaMemsetAsync(L.out.cursor, 0, sizeof(unsigned long long), st);
+      L.out.cursor = cur + 8 + l;
       mark(1);
       nl += 2;
       if (l == 0 && ngroups) {
         ++nl;
         ++nl;
         const int npk = (int)packs.size();
-        k_node_pack<<<std::min(npk, pack_grid), NP_NT, np_smem(np_rmax, np_ztn), st>>>(
+        launch(k_node_pack, dim3(std::min(npk, pack_grid)), dim3(NP_NT), np_smem(np_rmax, np_ztn), st, 
             s, L, (const NodeGroup*)packs_dev.p, npk, np_rmax, np_ztn, (NodeGroup*)groups_dev.p);
-        k_node_shared<<<std::min(ngroups, 148 * 2), DIRECT_NT, NS_SMEM, st>>>(
+        launch(k_node_shared, dim3(std::min(ngroups, 148 * 2)), dim3(DIRECT_NT), NS_SMEM, st, 
             s, L, (const NodeGroup*)groups_dev.p);
       }
-      k_direct_warp<<<grid_for(nloc, 8, 148 * 8), 256, DW_SMEM, st>>>(s, L);
-      k_direct<<<grid_for(nloc, 1, 148 * 8), DIRECT_NT, direct_smem(cd), st>>>(s, L);
+      launch(k_direct_warp, dim3(grid_for(nloc, 8, 148 * 8)), dim3(256), DW_SMEM, st, s, L);
+      launch(k_direct, dim3(grid_for(nloc, 1, 148 * 8)), dim3(DIRECT_NT), direct_smem(cd), st, s, L);
       if (l < D) {
         L.nb = (int64_t*)nb.p;
         L.bucket_base = (int64_t*)bucket_base.p;
@@ -3235,25 +3277,25 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         nl += 2;  // scan(+nb) and scan(+work counts) in one launch, filter
         scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadWork{s, L}, nbl, L.wo, tmp, st, NoPost());
         ++nl;
-        k_hints<<<148 * 4, 256, 0, st>>>(s, L);
+        launch(k_hints, dim3(148 * 4), dim3(256), 0, st, s, L);
         mark(2);  // filter_ms: k_filter alone
-        if (filter_regs64) k_filter64<<<filter_grid, 128, 0, st>>>(s, L);
-        else k_filter<<<filter_grid, 128, 0, st>>>(s, L);
+        if (filter_regs64) launch(k_filter64, dim3(filter_grid), dim3(128), 0, st, s, L);
+        else launch(k_filter, dim3(filter_grid), dim3(128), 0, st, s, L);
         // bucket offsets over B buckets (B on device)
         mark(3);
         nl += 4;  // scan, carry+scatter, 2 bucket sorts (huge buckets inside k_bucket_large)
         scan_excl<unsigned int>(L.bcount, L.boff, L.bucket_base + nloc, bcap, tmp, st);
-        k_carry_scatter<<<148 * 8, 256, 0, st>>>(s, L, nc);  // + candidate total
-        k_bucket_small<<<148 * 8, 256, 0, st>>>(s, L);
+        launch(k_carry_scatter, dim3(148 * 8), dim3(256), 0, st, s, L, nc);  // + candidate total
+        launch(k_bucket_small, dim3(148 * 8), dim3(256), 0, st, s, L);
         const size_t lsm = (size_t)BUCKET_SMEM * (3 * sizeof(int64_t) + sizeof(int));
-        k_bucket_large<<<148 * 2, DIRECT_NT, lsm, st>>>(L);
+        launch(k_bucket_large, dim3(148 * 2), dim3(DIRECT_NT), lsm, st, L);
         // positions of survivors: scan flags in place into gpos (reuse cgb as gpos)
         mark(4);
         nl += 2;  // scan, compact (+ segment ranges)
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
         scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
         const int64_t cbase = (int64_t)plan_copy[l];  // direct outputs of level l stay below
-        k_compact<<<148 * 8, 256, 0, st>>>(s, L, gpos, nc, cbase);
+        launch(k_compact, dim3(148 * 8), dim3(256), 0, st, s, L, gpos, nc, cbase);
       }
     }
     mark(-1);
@@ -3274,7 +3316,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       }
       scan_excl<int64_t>(pools[0].cnt, (int64_t*)pos.p, nullptr, nloc, (int64_t*)scan_tmp.p, st);
       cudaMemsetAsync(step_arr.p, 0, sizeof(int64_t) * 3 * nsteps, st);
-      k_wave_off<<<grid_for(nloc, 256, 1 << 30), 256, 0, st>>>(s, pools[0].cnt, (int64_t*)seg_tuples.p,
+      launch(k_wave_off, dim3(grid_for(nloc, 256, 1 << 30)), dim3(256), 0, st, s, pools[0].cnt, (int64_t*)seg_tuples.p,
                                                                (int64_t*)pos.p, dev_off,
                                                                (int64_t*)step_arr.p);
       nl += 2;  // scan, wave_off
@@ -3366,19 +3408,20 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
                                cudaStream_t st) {
   if (r.nloc == 0) return cudaSuccess;
   if (r.step_stats) {  // device-offset mode: arena is contiguous in pos order
-    k_gather_flat<<<grid_for(r.total, 2048, 148 * 16), 256, 0, st>>>(
+    launch(k_gather_flat, dim3(grid_for(r.total, 2048, 148 * 16)), dim3(256), 0, st, 
         batch, r.pool, (const int64_t*)pos.p, steps[0].out_m, steps[0].out_t, steps[0].out_bp);
     return cudaGetLastError();
   }
   // the output pointers changed: refresh the step array (same batch layout)
   cudaMemcpyAsync(steps_dev.p, steps.data(), sizeof(StepDev) * steps.size(), cudaMemcpyHostToDevice,
                   st);
-  k_gather<<<grid_for(r.nloc, 8, 148 * 16), 256, 0, st>>>(batch, r.pool);
+  launch(k_gather, dim3(grid_for(r.nloc, 8, 148 * 16)), dim3(256), 0, st, batch, r.pool);
   return cudaGetLastError();
 }
 
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
+  if (const char* e = getenv("FT_PDL")) g_pdl = atoi(e) != 0;
   if (const char* e = getenv("FT_PACK_GRID")) pack_grid = std::max(1, atoi(e));  // tests: packs per CTA
   filter_regs64 = getenv("FT_FILTER_REGS") && atoi(getenv("FT_FILTER_REGS")) == 64;
   filter_grid = 148 * 256;

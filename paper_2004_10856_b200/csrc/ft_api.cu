@@ -1700,14 +1700,17 @@ void ft_graph_destroy(ft_graph* g) {
             "bookkeeping %.2f wave-assign %.2f policy %.2f\n",
             (long long)g->nwaves, g->hp[0], g->hp[1], g->hp[2], g->hp[3], g->hp[4], g->hp[5], g->hp[6]);
   if (getenv("FT_FILTER_STATS") && g->runner)
-    fprintf(stderr, "[libft filter] items %llu chunk_tests %llu skipped_elems %llu tested_elems %llu\n",
+    fprintf(stderr, "[libft filter] items %llu chunk_tests %llu skipped_elems %llu tested_elems %llu "
+            "G_points %llu one_block_warps %llu warps %llu gallops %llu\n",
             g->runner->fstat_acc[0], g->runner->fstat_acc[1], g->runner->fstat_acc[2],
-            g->runner->fstat_acc[3]);
+            g->runner->fstat_acc[3], g->runner->fstat_acc[4], g->runner->fstat_acc[5],
+            g->runner->fstat_acc[6], g->runner->fstat_acc[7]);
   if (getenv("FT_FILTER_STATS") && g->runner) {
     fprintf(stderr, "[libft buckets] size-class: count/candidates 1 | 2-4 | 5-8 | 9-16 | 17-32 | 33-64 | 65-128 | 129-256 | <=4096 | >4096\n ");
     for (int q = 0; q < 10; ++q)
       fprintf(stderr, " %llu/%llu", g->runner->bstat_acc[0][q], g->runner->bstat_acc[1][q]);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "\n[libft buckets] key-sort fallbacks to (m, t, id): lane groups %llu, warps %llu\n",
+            g->runner->bfall_acc[0], g->runner->bfall_acc[1]);
   }
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& w : g->waves) {

@@ -104,9 +104,12 @@ struct StepHdr {
   unsigned long long bucket_total[LMAX + 1];  // buckets per level
   unsigned long long huge;                    // buckets sorted by the global-memory path
   unsigned long long bstat[2][10];            // bucket count / candidates by size class (stats)
-  unsigned long long fstat[4];                // filter work counters (FT_FILTER_STATS): work
+  unsigned long long bfall[2];                // key-sorted bucket sorts redone on (m, t, id): lane groups, warps (stats)
+  unsigned long long fstat[8];                // filter work counters (FT_FILTER_STATS): work
                                               // items, chunk tests, skipped chunks' elements,
-                                              // elements tested one by one
+                                              // elements tested one by one; G points over items,
+                                              // warp passes with all 32 items in one block, warp
+                                              // passes, chunk tests past the 4-point G probe
   unsigned long long ns_big;                  // rows handed from k_node_pack to k_node_shared
   unsigned long long ns_rows;                 // rows reduced by k_node_pack
   unsigned long long ns_tie;                  // ... of which with equal m values (group rule)
@@ -155,7 +158,7 @@ struct LevelDev {
   int64_t* gm;           // grouped (bucket-ordered) candidates
   int64_t* gt;
   uint64_t* gid;
-  int64_t* gflag;        // keep flags (0/1), scanned in place -> positions
+  uint8_t* gflag;        // keep flags (0/1), scanned -> positions
   int64_t* large_list;
   unsigned long long* large_n;
   int32_t* whint;        // [hcap] block of filter item 32c (k_filter warp starts)

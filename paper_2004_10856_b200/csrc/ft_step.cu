@@ -69,10 +69,18 @@ __device__ __forceinline__ bool is_filter(int32_t d, int level) {
 
 // Element loaders for the scan: a plain array, or a functor that computes
 // the element (and stores it for later kernels) while the scan reads it.
+// load(): the thread's N elements (0 past n); keep(): stores the loader
+// makes for later kernels, issued after the tile's loads.
 template <typename T>
 struct LoadArr {
   const T* p;
-  __device__ __forceinline__ long long operator()(int64_t i) const { return (long long)p[i]; }
+  template <int N>
+  __device__ __forceinline__ void load(int64_t base, int64_t n, long long (&v)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = base + i < n ? (long long)p[base + i] : 0;
+  }
+  template <int N>
+  __device__ __forceinline__ void keep(int64_t, int64_t, const long long (&)[N]) const {}
 };
 
 // Optional per-element epilogue of the scan: post(i, exclusive prefix, value).
@@ -100,12 +108,10 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
     if (tile >= ntiles) break;
     const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     long long v[SCAN_ITEMS];
+    ld.load(base, n, v);
     long long sum = 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-      v[i] = base + i < n ? ld(base + i) : 0;
-      sum += v[i];
-    }
+    for (int i = 0; i < SCAN_ITEMS; ++i) sum += v[i];
     long long tot;
     long long ex = block_excl_sum<SCAN_NT>(sum, sh, &tot);
     if (wid == 0) {
@@ -146,6 +152,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan1(Load ld, const int64_t* n_dev
       }
       ex += v[i];
     }
+    ld.keep(base, n, v);
     if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
     __syncthreads();  // s_tile / s_pre reuse
   }
@@ -192,12 +199,11 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan2(LoadA lda, int64_t nA, int64_
     int64_t* out = isA ? outA : outB;
     const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     long long v[SCAN_ITEMS];
+    if (isA) lda.load(base, n, v);
+    else ldb.load(base, n, v);
     long long sum = 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-      v[i] = base + i < n ? (isA ? lda(base + i) : ldb(base + i)) : 0;
-      sum += v[i];
-    }
+    for (int i = 0; i < SCAN_ITEMS; ++i) sum += v[i];
     long long tot;
     long long ex = block_excl_sum<SCAN_NT>(sum, sh, &tot);
     if (wid == 0) {
@@ -237,6 +243,8 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan2(LoadA lda, int64_t nA, int64_
       }
       ex += v[i];
     }
+    if (isA) lda.keep(base, n, v);
+    else ldb.keep(base, n, v);
     if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_pre + tot;
     __syncthreads();
   }
@@ -1907,31 +1915,79 @@ __device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa
 // work offsets) and stored for the later kernels.
 struct LoadNb {
   LevelDev L;
-  __device__ __forceinline__ long long operator()(int64_t i) const {
-    const int64_t v = is_filter(L.seg_d[i], L.level) ? L.in.cnt[i] + 1 : 0;
-    L.nb[i] = v;
-    return v;
+  template <int N>
+  __device__ __forceinline__ void load(int64_t base, int64_t n, long long (&v)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      v[i] = base + i < n && is_filter(L.seg_d[base + i], L.level) ? L.in.cnt[base + i] + 1 : 0;
+  }
+  template <int N>
+  __device__ __forceinline__ void keep(int64_t base, int64_t n, const long long (&v)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (base + i < n) L.nb[base + i] = v[i];
   }
 };
 
+// A thread's N consecutive blocks: when they belong to one step (the common
+// case) one binary search for the step and straight-line, independent loads
+// per block (the N load chains overlap; a loop per block would serialise
+// them), stores deferred to keep().
 struct LoadWork {
   BatchDev B;
   LevelDev L;
-  __device__ __forceinline__ long long operator()(int64_t beta) const {
-    const int j = find_base(B.blk_base, B.nsteps, beta);
-    const StepDev& s = B.steps[j];
-    const int64_t lb = beta - B.blk_base[j];
-    const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
-    int64_t w = 0;
-    if (is_filter(L.seg_d[B.seg_base[j] + li], L.level)) {
-      Blk b = load_blk(s, s.seg_lo + li, k);
-      int lf, fa, fb;
-      int64_t cL, cA, cB;
-      run_shape(b, L.st, lf, fa, fb, cL, cA, cB);
-      w = cA * cB * ((cL + L.run_item - 1) / L.run_item);
+  __device__ __forceinline__ long long work(const StepDev& s, int64_t sg, int64_t k, bool filt) const {
+    const Blk b = load_blk(s, sg, k);
+    int lf, fa, fb;
+    int64_t cL, cA, cB;
+    run_shape(b, L.st, lf, fa, fb, cL, cA, cB);
+    return filt ? cA * cB * ((cL + L.run_item - 1) / L.run_item) : 0;
+  }
+  template <int N>
+  __device__ __forceinline__ void load(int64_t base, int64_t n, long long (&v)[N]) const {
+    if (base >= n) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = 0;
+      return;
     }
-    L.wcnt[beta] = w;
-    return w;
+    const int64_t last = min(base + (int64_t)N, n) - 1;
+    const int j = find_base(B.blk_base, B.nsteps, base);
+    if (last < __ldg(B.blk_base + j + 1)) {  // one step
+      const StepDev& s = B.steps[j];
+      const int64_t nblk = s.nblk, b0 = __ldg(B.blk_base + j), sb = __ldg(B.seg_base + j), slo = s.seg_lo;
+      const bool small = ((last - b0) >> 31) == 0 && (nblk >> 31) == 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int64_t lb = min(base + i, last) - b0;
+        int64_t li;
+        if (small) li = (unsigned)lb / (unsigned)nblk;
+        else li = lb / nblk;
+        const int64_t k = lb - li * nblk;
+        const bool filt = is_filter(L.seg_d[sb + li], L.level);
+        const long long w = work(s, slo + li, k, filt);
+        v[i] = base + i <= last ? w : 0;
+      }
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int64_t beta = base + i;
+      if (beta > last) {
+        v[i] = 0;
+        continue;
+      }
+      const int jj = find_base(B.blk_base, B.nsteps, beta);
+      const StepDev& s = B.steps[jj];
+      const int64_t lb = beta - B.blk_base[jj];
+      const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
+      v[i] = work(s, s.seg_lo + li, k, is_filter(L.seg_d[B.seg_base[jj] + li], L.level));
+    }
+  }
+  template <int N>
+  __device__ __forceinline__ void keep(int64_t base, int64_t n, const long long (&v)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (base + i < n) L.wcnt[base + i] = v[i];
   }
 };
 
@@ -2006,6 +2062,13 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       bhi = __shfl_sync(0xffffffffu, lo, 31) + 1;
     }
     const int64_t w = w0 + lane;
+    if (L.fstats) {  // warp passes, and those whose items all lie in one block
+      const unsigned act = __ballot_sync(0xffffffffu, w < W);
+      if (lane == 0) {
+        atomicAdd(&L.hdr->fstat[6], 1ull);
+        if (bhi - blo <= 1 && act == 0xffffffffu) atomicAdd(&L.hdr->fstat[5], 1ull);
+      }
+    }
     if (w >= W) continue;
     int64_t lo = blo;
     int64_t hi = bhi;  // wo[lo] <= w < wo[hi]
@@ -2070,7 +2133,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     // q: #G points with m < m of the current chunk start (galloping lower bound)
     int q = 0;
     int jj = j0;
-    unsigned c_tests = 0, c_skip = 0, c_elem = 0;
+    unsigned c_tests = 0, c_skip = 0, c_elem = 0, c_gallop = 0;
     while (jj < j1) {
       ++c_tests;
       const int je = min(jj + CHUNK, j1);
@@ -2086,6 +2149,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
           if (v4 >= mf) { q += 4; goto g_done; }
           q += 4;  // Gm[q] < mf still: interpolation / gallop from here
         }
+        ++c_gallop;
         if (g - q > 16) {
           // one interpolation probe between Gm[q] and Gm[g-1] (G's m values are
           // spread over the segment's range); the gallop then starts there
@@ -2222,6 +2286,8 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       atomicAdd(&L.hdr->fstat[1], c_tests);
       atomicAdd(&L.hdr->fstat[2], c_skip);
       atomicAdd(&L.hdr->fstat[3], c_elem);
+      atomicAdd(&L.hdr->fstat[4], (unsigned long long)g);
+      atomicAdd(&L.hdr->fstat[7], (unsigned long long)c_gallop);
     }
   }
 }
@@ -2299,28 +2365,66 @@ __global__ void __launch_bounds__(256) k_carry_scatter(BatchDev B, LevelDev L, i
   }
 }
 
-// K2+K3 for buckets of <= WARP_DIRECT candidates: one warp per bucket,
+// K2+K3 for buckets of 33..WARP_DIRECT candidates: one warp per bucket,
 // register bitonic sort by shuffles (R rows of 32), Alg.1 sweep with the
-// bucket's carry.  Larger buckets go to the CTA kernels.
+// bucket's carry.  The sort runs on single 64-bit keys (m << 8 | e) when
+// every m fits in B.kspan bits (<= 55) and the bucket's m values are distinct
+// (then the key order is the (m, t, id) order, R1/R3/R6); otherwise on the
+// full (m, t, id) triple.  Only kept elements are written back (k_compact
+// reads nothing else); larger buckets go to the CTA kernels.
 template <int R>
-__device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int64_t c, int64_t base) {
+__device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int64_t c, int64_t base, int kspan) {
   const int lane = threadIdx.x & 31;
-  int64_t m[R], t[R];
-  uint64_t id[R];
+  const int sb = kspan < 55 ? kspan : 55;
+  uint64_t k[R];
+  bool fits = true;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = (r << 5) | lane;
+    k[r] = ~0ull;
     if (e < c) {
-      m[r] = L.gm[base + e];
-      t[r] = L.gt[base + e];
-      id[r] = L.gid[base + e];
-    } else {
-      m[r] = INF;
-      t[r] = INF;
-      id[r] = ~0ull;
+      const uint64_t v = (uint64_t)L.gm[base + e];
+      fits = fits && (v >> sb) == 0;
+      k[r] = (v << 8) | (uint64_t)e;
     }
   }
-  warp_bitonic<R>(m, t, id);
+  bool keyed = __all_sync(0xffffffffu, fits);
+  if (keyed) {
+    warp_bitonic_keys<R>(k);
+    bool tie = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = (r << 5) | lane;
+      uint64_t prev = __shfl_up_sync(0xffffffffu, k[r], 1);
+      const uint64_t rowlast = __shfl_sync(0xffffffffu, k[r > 0 ? r - 1 : 0], 31);
+      if (lane == 0) prev = r > 0 ? rowlast : ~0ull;
+      if (e < c && prev != ~0ull && (prev >> 8) == (k[r] >> 8)) tie = true;
+    }
+    keyed = !__any_sync(0xffffffffu, tie);
+  }
+  int64_t m[R], t[R];
+  uint64_t id[R];
+  if (keyed) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = (r << 5) | lane;
+      const int ix = (int)(k[r] & 255u);
+      m[r] = e < c ? (int64_t)(k[r] >> 8) : INF;
+      t[r] = e < c ? L.gt[base + ix] : INF;
+      id[r] = e < c ? L.gid[base + ix] : ~0ull;
+    }
+  } else {
+    if (L.fstats && lane == 0) atomicAdd(&L.hdr->bfall[1], 1ull);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = (r << 5) | lane;
+      m[r] = e < c ? L.gm[base + e] : INF;
+      t[r] = e < c ? L.gt[base + e] : INF;
+      id[r] = e < c ? L.gid[base + e] : ~0ull;
+    }
+    warp_bitonic<R>(m, t, id);
+  }
+  __syncwarp();  // every read of the bucket precedes the in-place writes
   long long carry = L.bcarry[bkt];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -2330,10 +2434,13 @@ __device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int6
     if (lane == 0) ex = INF;
     const long long v = ex < carry ? ex : carry;
     if (e < c) {
-      L.gm[base + e] = m[r];
-      L.gt[base + e] = t[r];
-      L.gid[base + e] = id[r];
-      L.gflag[base + e] = t[r] < v ? 1 : 0;
+      const bool kf = t[r] < v;
+      L.gflag[base + e] = kf;
+      if (kf) {
+        L.gm[base + e] = m[r];
+        L.gt[base + e] = t[r];
+        L.gid[base + e] = id[r];
+      }
     }
     const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
     carry = rowmin < carry ? rowmin : carry;
@@ -2343,8 +2450,11 @@ __device__ __forceinline__ void warp_bucket(const LevelDev& L, int64_t bkt, int6
 // Buckets of 2..32 candidates: the 32/S buckets of one size class
 // (S/2, S] of a 32-bucket tile are sorted together, one per S-lane group
 // (bitonic with shuffles inside the group, segmented warp scans for Alg. 1).
+// Keys as in warp_bucket (m << 5 | e; the (m, t, id) network for the whole
+// warp pass when some m needs more than B.kspan bits or a group has equal m;
+// always for pairs, where the triple network is the cheaper one).
 template <int S>
-__device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int64_t b0, int* slist) {
+__device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int64_t b0, int* slist, int kspan) {
   const int lane = threadIdx.x & 31;
   const bool mine = c > S / 2 && c <= S;
   const unsigned mask = __ballot_sync(0xffffffffu, mine);
@@ -2354,6 +2464,7 @@ __device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int6
   const int n = __popc(mask);
   constexpr int G = 32 / S;
   const int g = lane / S, e = lane & (S - 1);
+  const int sb = kspan < 58 ? kspan : 58;
   for (int p0 = 0; p0 < n; p0 += G) {
     const int q = p0 + g;
     const int src = q < n ? slist[q] : 0;
@@ -2362,6 +2473,7 @@ __device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int6
     uint64_t id = ~0ull;
     long long carry = INF;
     const int64_t bk = b0 + src;
+    const bool valid = q < n && e < cc;
     if (q < n) {
       base = L.boff[bk];
       carry = L.bcarry[bk];
@@ -2371,19 +2483,48 @@ __device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int6
         id = L.gid[base + e];
       }
     }
+    const bool fits = S > 2 && (!valid || ((uint64_t)m >> sb) == 0);
+    uint64_t key = valid ? ((uint64_t)m << 5) | (uint64_t)e : ~0ull;
 #pragma unroll
-    for (int k = 2; k <= S; k <<= 1) {
+    for (int k = 2; k <= (S > 2 ? S : 1); k <<= 1) {
 #pragma unroll
       for (int j = k >> 1; j > 0; j >>= 1) {
-        const int64_t pm = __shfl_xor_sync(0xffffffffu, m, j);
-        const int64_t pt = __shfl_xor_sync(0xffffffffu, t, j);
-        const uint64_t pi = __shfl_xor_sync(0xffffffffu, id, j);
+        const uint64_t pk = __shfl_xor_sync(0xffffffffu, key, j);
         const bool up = (e & k) == 0, lower = (e & j) == 0;
-        const bool p_lt = key_lt(pm, pt, pi, m, t, id);
-        if ((lower == up) ? p_lt : !p_lt) {
-          m = pm;
-          t = pt;
-          id = pi;
+        key = (lower == up) ? (pk < key ? pk : key) : (pk > key ? pk : key);
+      }
+    }
+    const uint64_t pv = S > 2 ? __shfl_up_sync(0xffffffffu, key, 1, S) : 0;
+    const bool tie = e > 0 && key != ~0ull && (pv >> 5) == (key >> 5);
+    if (__all_sync(0xffffffffu, fits && !tie)) {
+      const int from = (lane & ~(S - 1)) | (int)(key & (S - 1));
+      const int64_t tt = __shfl_sync(0xffffffffu, t, from);
+      const uint64_t ii = __shfl_sync(0xffffffffu, id, from);
+      if (key != ~0ull) {
+        m = (int64_t)(key >> 5);
+        t = tt;
+        id = ii;
+      } else {
+        m = INF;
+        t = INF;
+        id = ~0ull;
+      }
+    } else {
+      if (S > 2 && L.fstats && lane == 0) atomicAdd(&L.hdr->bfall[0], 1ull);
+#pragma unroll
+      for (int k = 2; k <= S; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const int64_t pm = __shfl_xor_sync(0xffffffffu, m, j);
+          const int64_t pt = __shfl_xor_sync(0xffffffffu, t, j);
+          const uint64_t pi = __shfl_xor_sync(0xffffffffu, id, j);
+          const bool up = (e & k) == 0, lower = (e & j) == 0;
+          const bool p_lt = key_lt(pm, pt, pi, m, t, id);
+          if ((lower == up) ? p_lt : !p_lt) {
+            m = pm;
+            t = pt;
+            id = pi;
+          }
         }
       }
     }
@@ -2396,11 +2537,15 @@ __device__ __forceinline__ void bucket_groups(const LevelDev& L, int64_t c, int6
     long long ex = __shfl_up_sync(0xffffffffu, inc, 1, S);
     if (e == 0) ex = INF;
     const long long v = ex < carry ? ex : carry;
+    __syncwarp();  // every read of the pass's buckets precedes the in-place writes
     if (q < n && e < cc) {
-      L.gm[base + e] = m;
-      L.gt[base + e] = t;
-      L.gid[base + e] = id;
-      L.gflag[base + e] = t < v ? 1 : 0;
+      const bool kf = t < v;
+      L.gflag[base + e] = kf;
+      if (kf) {
+        L.gm[base + e] = m;
+        L.gt[base + e] = t;
+        L.gid[base + e] = id;
+      }
     }
   }
   __syncwarp();
@@ -2434,11 +2579,11 @@ __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L
       const int64_t base = L.boff[bkt];
       L.gflag[base] = L.gt[base] < L.bcarry[bkt] ? 1 : 0;
     }
-    bucket_groups<2>(L, c, b0, slist);
-    bucket_groups<4>(L, c, b0, slist);
-    bucket_groups<8>(L, c, b0, slist);
-    bucket_groups<16>(L, c, b0, slist);
-    bucket_groups<32>(L, c, b0, slist);
+    bucket_groups<2>(L, c, b0, slist, Bt.kspan);
+    bucket_groups<4>(L, c, b0, slist, Bt.kspan);
+    bucket_groups<8>(L, c, b0, slist, Bt.kspan);
+    bucket_groups<16>(L, c, b0, slist, Bt.kspan);
+    bucket_groups<32>(L, c, b0, slist, Bt.kspan);
     unsigned big = __ballot_sync(0xffffffffu, c > 32 && c <= WARP_DIRECT);
     while (big) {
       const int src = __ffs(big) - 1;
@@ -2446,9 +2591,9 @@ __global__ void __launch_bounds__(256, 3) k_bucket_small(BatchDev Bt, LevelDev L
       const int64_t cb = __shfl_sync(0xffffffffu, c, src);
       const int64_t bk = b0 + src;
       const int64_t base = L.boff[bk];
-      if (cb <= 64) warp_bucket<2>(L, bk, cb, base);
-      else if (cb <= 128) warp_bucket<4>(L, bk, cb, base);
-      else warp_bucket<8>(L, bk, cb, base);
+      if (cb <= 64) warp_bucket<2>(L, bk, cb, base, Bt.kspan);
+      else if (cb <= 128) warp_bucket<4>(L, bk, cb, base, Bt.kspan);
+      else warp_bucket<8>(L, bk, cb, base, Bt.kspan);
     }
   }
 }
@@ -2499,10 +2644,13 @@ __device__ __forceinline__ void cta_bucket_regs(const LevelDev& L, int64_t bkt, 
     if (lane == 0) ex = INF;
     const long long v = ex < carry ? ex : carry;
     if (e < c) {
-      L.gm[base + e] = m[r];
-      L.gt[base + e] = t[r];
-      L.gid[base + e] = id[r];
-      L.gflag[base + e] = t[r] < v ? 1 : 0;
+      const bool kf = t[r] < v;
+      L.gflag[base + e] = kf;
+      if (kf) {  // k_compact reads kept elements only
+        L.gm[base + e] = m[r];
+        L.gt[base + e] = t[r];
+        L.gid[base + e] = id[r];
+      }
     }
     const long long rowmin = __shfl_sync(0xffffffffu, inc, 31);
     carry = rowmin < carry ? rowmin : carry;
@@ -2559,10 +2707,12 @@ __global__ void __launch_bounds__(DIRECT_NT, 3) k_bucket_large(LevelDev L) {
     bitonic_smem<DIRECT_NT>(sm, stt, sid, N);
     alg1_sweep_smem<DIRECT_NT>(stt, (int)c, L.bcarry[bkt], kf, sh);
     for (int i = threadIdx.x; i < c; i += DIRECT_NT) {
-      L.gm[base + i] = sm[i];
-      L.gt[base + i] = stt[i];
-      L.gid[base + i] = sid[i];
-      L.gflag[base + i] = kf[i] ? 1 : 0;
+      L.gflag[base + i] = kf[i] != 0;
+      if (kf[i]) {
+        L.gm[base + i] = sm[i];
+        L.gt[base + i] = stt[i];
+        L.gid[base + i] = sid[i];
+      }
     }
     __syncthreads();
   }
@@ -3188,7 +3338,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(gm, int64_t, cand_cap);
       GROW(gt, int64_t, cand_cap);
       GROW(gid, uint64_t, cand_cap);
-      GROW(gflag, int64_t, cand_cap + 1);
+      GROW(gflag, uint8_t, cand_cap + 1);
       GROW(large_list, int64_t, bcap);
       GROW(whint, int32_t, hcap);
       GROW(ncand, int64_t, 2);
@@ -3266,7 +3416,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         L.gm = (int64_t*)gm.p;
         L.gt = (int64_t*)gt.p;
         L.gid = (uint64_t*)gid.p;
-        L.gflag = (int64_t*)gflag.p;
+        L.gflag = (uint8_t*)gflag.p;
         L.large_list = (int64_t*)large_list.p;
         L.large_n = cur + 3;
         L.whint = (int32_t*)whint.p;
@@ -3293,7 +3443,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         mark(4);
         nl += 2;  // scan, compact (+ segment ranges)
         int64_t* gpos = (int64_t*)cgb.p;  // candidate gb is dead after scatter
-        scan_excl<int64_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
+        scan_excl<uint8_t>(L.gflag, gpos, nc, cand_cap, tmp, st);
         const int64_t cbase = (int64_t)plan_copy[l];  // direct outputs of level l stay below
         launch(k_compact, dim3(148 * 8), dim3(256), 0, st, s, L, gpos, nc, cbase);
       }
@@ -3340,10 +3490,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
           bstat_acc[0][q] += hdr_host->bstat[0][q];
           bstat_acc[1][q] += hdr_host->bstat[1][q];
         }
-        fstat_acc[0] += hdr_host->fstat[0];
-        fstat_acc[1] += hdr_host->fstat[1];
-        fstat_acc[2] += hdr_host->fstat[2];
-        fstat_acc[3] += hdr_host->fstat[3];
+        bfall_acc[0] += hdr_host->bfall[0];
+        bfall_acc[1] += hdr_host->bfall[1];
+        for (int q = 0; q < 8; ++q) fstat_acc[q] += hdr_host->fstat[q];
       }
       res->filter_tuples = res->direct_tuples = 0;
       for (int l = 0; l <= D; ++l) {

@@ -138,8 +138,9 @@ class StepRunner {
   bool filter_regs64 = false;          // k_filter64 (64 registers) instead of k_filter (80)
   int item_max = 512;                 // filter work item: max sampled run elements
   int item_div = 4;                   // ... and target items per resident thread
-  unsigned long long fstat_acc[4] = {0, 0, 0, 0};
+  unsigned long long fstat_acc[8] = {};
   unsigned long long bstat_acc[2][10] = {};
+  unsigned long long bfall_acc[2] = {};
   bool profile = false;               // events between kernel groups
   DevAlloc alloc;                     // scratch memory (set once at creation)
   std::mutex mu;                      // held by a graph for a whole wave

@@ -161,7 +161,7 @@ struct LevelDev {
   uint8_t* gflag;        // keep flags (0/1), scanned -> positions
   int64_t* large_list;
   unsigned long long* large_n;
-  int32_t* whint;        // [hcap] block of filter item 32c (k_filter warp starts)
+  int32_t* whint;        // [2 hcap] block of filter item 32c (k_filter warp starts), then its step
   int64_t hcap;
   int64_t* scratch;      // global-memory sort scratch (huge buckets)
   int64_t scratch_cap;

@@ -23,6 +23,7 @@ constexpr int kDwGenUnroll = DW_GEN_UNROLL;
 // Launches of the per-level pipeline: with programmatic stream serialisation
 // (FT_PDL_ENTRY in every kernel launched here) unless FT_PDL=0.
 static bool g_pdl = true;
+__constant__ bool g_fence = true;  // k_filter: warp-cooperative G lower bound (FT_FENCE=0: per-lane gallop)
 
 template <typename... KArgs, typename... Args>
 static inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -1992,9 +1993,10 @@ struct LoadWork {
 };
 
 // Warp-start block hints for k_filter: hint[c] = the block of filter item
-// 32c (largest beta with wo[beta] <= 32c), one thread per hint, so that a
-// k_filter warp finds its items' blocks with two loads instead of two binary
-// searches over all blocks at the head of its dependent-load chain.  (Written
+// 32c (largest beta with wo[beta] <= 32c) and hint[hcap + c] its step, one
+// thread per hint, so that a k_filter warp finds its items' blocks and steps
+// with a few loads instead of binary searches over all blocks and steps at
+// the head of its dependent-load chain.  (Written
 // first in the work-offset scan's epilogue: serial per block, ~30 us per
 // LDP level.)
 __global__ void __launch_bounds__(256) k_hints(BatchDev B, LevelDev L) {
@@ -2010,6 +2012,7 @@ __global__ void __launch_bounds__(256) k_hints(BatchDev B, LevelDev L) {
       else hi = mid;
     }
     L.whint[c] = (int32_t)lo;
+    L.whint[L.hcap + c] = find_base(B.blk_base, B.nsteps, lo);  // its step
   }
 }
 
@@ -2022,6 +2025,31 @@ __global__ void __launch_bounds__(256) k_hints(BatchDev B, LevelDev L) {
 // the first element with t < t_g (binary search on t).  Otherwise x is a
 // candidate: emitted with bucket = #G points with m <= m_x.
 constexpr int EPRE = 2;  // run elements loaded ahead in k_filter's element test (4: spills at 80 regs)
+
+// lower_bound(G[0, g), x) for every lane of a warp whose lanes share G (the
+// 32 items of a warp pass lie in one block, ~90% of passes): one coalesced
+// load of 32 fences (the last point of each of 32 slices), a 5-step search
+// over them by shuffles, then a per-lane binary search inside one slice --
+// ~log2(g / 32) dependent loads instead of a gallop over all of G.
+__device__ __forceinline__ int warp_lower_bound(const int64_t* G, int g, int64_t x) {
+  const int lane = threadIdx.x & 31;
+  const int s1 = (g + 31) >> 5;
+  const int64_t f = G[min((lane + 1) * s1, g) - 1];
+  int c = 0;  // fences below x
+#pragma unroll
+  for (int b = 16; b > 0; b >>= 1) {
+    const int64_t v = __shfl_sync(0xffffffffu, f, c + b - 1);
+    if (v < x) c += b;
+  }
+  if (__shfl_sync(0xffffffffu, f, 31) < x) return g;
+  int a0 = c * s1, a1 = min((c + 1) * s1, g) - 1;  // G[a1] >= x
+  while (a0 < a1) {
+    const int mid = (a0 + a1) >> 1;
+    if (G[mid] < x) a0 = mid + 1;
+    else a1 = mid;
+  }
+  return a0;
+}
 
 __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L) {
   namespace cg = cooperative_groups;
@@ -2044,9 +2072,16 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     // bounded binary search per lane.
     const int64_t c0 = w0 >> 5;
     int64_t blo, bhi;  // wo[blo] <= w0 + lane < wo[bhi]
+    int jlo = 0, jhi = B.nsteps;  // steps of the warp's blocks: [jlo, jhi)
     if (c0 + 1 < L.hcap) {
       blo = L.whint[c0];
-      bhi = w0 + 32 < W ? (int64_t)L.whint[c0 + 1] + 1 : nbl;
+      jlo = L.whint[L.hcap + c0];
+      if (w0 + 32 < W) {
+        bhi = (int64_t)L.whint[c0 + 1] + 1;
+        jhi = L.whint[L.hcap + c0 + 1] + 1;
+      } else {
+        bhi = nbl;
+      }
     } else {
       int64_t lo = 0;
       if (lane == 0 || lane == 31) {
@@ -2062,6 +2097,8 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       bhi = __shfl_sync(0xffffffffu, lo, 31) + 1;
     }
     const int64_t w = w0 + lane;
+    // all 32 items in one block (hence one G): cooperative first lower bound
+    const bool one = g_fence && bhi - blo <= 1 && w0 + 32 <= W;
     if (L.fstats) {  // warp passes, and those whose items all lie in one block
       const unsigned act = __ballot_sync(0xffffffffu, w < W);
       if (lane == 0) {
@@ -2078,7 +2115,12 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       else hi = mid;
     }
     const int64_t beta = lo, wl = w - L.wo[beta];
-    const int jstep = find_base(B.blk_base, B.nsteps, beta);
+    int jstep = jlo;  // largest j in [jlo, jhi) with blk_base[j] <= beta
+    for (int jh = jhi; jh - jstep > 1;) {
+      const int mid = (jstep + jh) >> 1;
+      if (__ldg(B.blk_base + mid) <= beta) jstep = mid;
+      else jh = mid;
+    }
     const StepDev& s = B.steps[jstep];
     const int64_t lb = beta - B.blk_base[jstep];
     const int64_t li0 = lb / s.nblk, k = lb - li0 * s.nblk;
@@ -2133,13 +2175,20 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     // q: #G points with m < m of the current chunk start (galloping lower bound)
     int q = 0;
     int jj = j0;
+    bool exact = false;  // q = lower_bound(mf) of the first chunk already
+    if (one && g > 0) {  // warp-uniform: every lane of the warp is here
+      q = warp_lower_bound(Gm, g, ms + __ldg(Lm + samp_idx32(j0, nL, sh)));
+      exact = true;
+    }
     unsigned c_tests = 0, c_skip = 0, c_elem = 0, c_gallop = 0;
     while (jj < j1) {
       ++c_tests;
       const int je = min(jj + CHUNK, j1);
       const int64_t mf = ms + __ldg(Lm + samp_idx32(jj, nL, sh));
       const int64_t tl = ts + __ldg(Lt + samp_idx32(je - 1, nL, sh));
-      if (q < g && Gm[q] < mf) {  // lower_bound(mf) in G, starting at q
+      const bool known = exact;
+      exact = false;
+      if (!known && q < g && Gm[q] < mf) {  // lower_bound(mf) in G, starting at q
         {  // short advances are the common case: probe q+1..q+4 with independent loads
           const int64_t v1 = q + 1 < g ? Gm[q + 1] : INF, v2 = q + 2 < g ? Gm[q + 2] : INF;
           const int64_t v3 = q + 3 < g ? Gm[q + 3] : INF, v4 = q + 4 < g ? Gm[q + 4] : INF;
@@ -3340,7 +3389,7 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
       GROW(gid, uint64_t, cand_cap);
       GROW(gflag, uint8_t, cand_cap + 1);
       GROW(large_list, int64_t, bcap);
-      GROW(whint, int32_t, hcap);
+      GROW(whint, int32_t, 2 * hcap);  // blocks, then their steps
       GROW(ncand, int64_t, 2);
     }
     // scan scratch: the largest single scan, or the bucket-count + work-item pair
@@ -3571,6 +3620,10 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
   if (const char* e = getenv("FT_PDL")) g_pdl = atoi(e) != 0;
+  if (const char* e = getenv("FT_FENCE")) {
+    const bool v = atoi(e) != 0;
+    cudaMemcpyToSymbol(g_fence, &v, sizeof(v));
+  }
   if (const char* e = getenv("FT_PACK_GRID")) pack_grid = std::max(1, atoi(e));  // tests: packs per CTA
   filter_regs64 = getenv("FT_FILTER_REGS") && atoi(getenv("FT_FILTER_REGS")) == 64;
   filter_grid = 148 * 256;

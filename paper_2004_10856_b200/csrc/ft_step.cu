@@ -2043,6 +2043,16 @@ __device__ __forceinline__ int warp_lower_bound(const int64_t* G, int g, int64_t
   }
   if (__shfl_sync(0xffffffffu, f, 31) < x) return g;
   int a0 = c * s1, a1 = min((c + 1) * s1, g) - 1;  // G[a1] >= x
+  if (a1 - a0 > 8) {  // second level: 8 sub-fences of the slice, independent loads
+    const int s2 = (a1 - a0 + 8) >> 3;
+    int c2 = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c2 += G[min(a0 + (k + 1) * s2, a1 + 1) - 1] < x;
+    // G[a0 + c2 * s2 - 1] < x (c2 > 0), G[min(a0 + (c2 + 1) * s2, a1 + 1) - 1] >= x
+    const int b0 = a0 + c2 * s2;
+    a1 = min(b0 + s2, a1 + 1) - 1;
+    a0 = b0;
+  }
   while (a0 < a1) {
     const int mid = (a0 + a1) >> 1;
     if (G[mid] < x) a0 = mid + 1;

@@ -17,7 +17,19 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]
-d = rows[2:]
+# a report with several launches prints one block per launch: summed by SASS offset
+blocks, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = []
+        blocks.append(cur)
+    elif r and r[0] != "Address" and cur is not None:
+        cur.append(r)
+d = [[None] * len(h) for _ in range(max(len(b) for b in blocks))]
+for b in blocks:
+    for i, r in enumerate(b):
+        for c in (h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")):
+            d[i][c] = str(float(d[i][c] or 0) + float(r[c] or 0))
 iss, iex = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 # offset -> source line
 tmp = tempfile.mkdtemp()

@@ -23,6 +23,7 @@ constexpr int kDwGenUnroll = DW_GEN_UNROLL;
 // Launches of the per-level pipeline: with programmatic stream serialisation
 // (FT_PDL_ENTRY in every kernel launched here) unless FT_PDL=0.
 static bool g_pdl = true;
+__constant__ bool g_bskip = true;  // k_blocks: drop blocks dominated as a whole (FT_BLOCK_SKIP=0: keep)
 __constant__ bool g_fence = true;  // k_filter: warp-cooperative G lower bound (FT_FENCE=0: per-lane gallop)
 
 template <typename... KArgs, typename... Args>
@@ -1911,9 +1912,9 @@ __device__ __forceinline__ void run_shape(const Blk& b, int st, int& lf, int& fa
 
 // Work items of the filter: L.run_item consecutive sampled indices of one run
 // (a multiple of CHUNK, chosen per level so that the grid has enough threads).
-// Per-segment bucket counts nb and per-block work-item counts wcnt, computed
-// as scan loaders (fused into the scans that consume them: bucket bases,
-// work offsets) and stored for the later kernels.
+// Per-segment bucket counts nb are computed by the bucket-base scan's loader
+// and stored for the later kernels; per-block work-item counts wcnt come from
+// k_blocks.
 struct LoadNb {
   LevelDev L;
   template <int N>
@@ -1927,68 +1928,6 @@ struct LoadNb {
 #pragma unroll
     for (int i = 0; i < N; ++i)
       if (base + i < n) L.nb[base + i] = v[i];
-  }
-};
-
-// A thread's N consecutive blocks: when they belong to one step (the common
-// case) one binary search for the step and straight-line, independent loads
-// per block (the N load chains overlap; a loop per block would serialise
-// them), stores deferred to keep().
-struct LoadWork {
-  BatchDev B;
-  LevelDev L;
-  __device__ __forceinline__ long long work(const StepDev& s, int64_t sg, int64_t k, bool filt) const {
-    const Blk b = load_blk(s, sg, k);
-    int lf, fa, fb;
-    int64_t cL, cA, cB;
-    run_shape(b, L.st, lf, fa, fb, cL, cA, cB);
-    return filt ? cA * cB * ((cL + L.run_item - 1) / L.run_item) : 0;
-  }
-  template <int N>
-  __device__ __forceinline__ void load(int64_t base, int64_t n, long long (&v)[N]) const {
-    if (base >= n) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) v[i] = 0;
-      return;
-    }
-    const int64_t last = min(base + (int64_t)N, n) - 1;
-    const int j = find_base(B.blk_base, B.nsteps, base);
-    if (last < __ldg(B.blk_base + j + 1)) {  // one step
-      const StepDev& s = B.steps[j];
-      const int64_t nblk = s.nblk, b0 = __ldg(B.blk_base + j), sb = __ldg(B.seg_base + j), slo = s.seg_lo;
-      const bool small = ((last - b0) >> 31) == 0 && (nblk >> 31) == 0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const int64_t lb = min(base + i, last) - b0;
-        int64_t li;
-        if (small) li = (unsigned)lb / (unsigned)nblk;
-        else li = lb / nblk;
-        const int64_t k = lb - li * nblk;
-        const bool filt = is_filter(L.seg_d[sb + li], L.level);
-        const long long w = work(s, slo + li, k, filt);
-        v[i] = base + i <= last ? w : 0;
-      }
-      return;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const int64_t beta = base + i;
-      if (beta > last) {
-        v[i] = 0;
-        continue;
-      }
-      const int jj = find_base(B.blk_base, B.nsteps, beta);
-      const StepDev& s = B.steps[jj];
-      const int64_t lb = beta - B.blk_base[jj];
-      const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
-      v[i] = work(s, s.seg_lo + li, k, is_filter(L.seg_d[B.seg_base[jj] + li], L.level));
-    }
-  }
-  template <int N>
-  __device__ __forceinline__ void keep(int64_t base, int64_t n, const long long (&v)[N]) const {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-      if (base + i < n) L.wcnt[base + i] = v[i];
   }
 };
 
@@ -2059,6 +1998,68 @@ __device__ __forceinline__ int warp_lower_bound(const int64_t* G, int g, int64_t
     else a1 = mid;
   }
   return a0;
+}
+
+// Per-block work-item counts of a filter level (wcnt[beta], scanned next into
+// the work offsets) with a block-level pre-filter: one thread per block, so
+// the G lower bounds of all blocks are in flight at once (as the scan's
+// loader, each thread ran 8 of them back to back); a warp whose 32 blocks
+// share one segment searches G cooperatively.
+__global__ void __launch_bounds__(256) k_blocks(BatchDev B, LevelDev L) {
+  FT_PDL_ENTRY();
+  const int64_t nbl = B.nblk;
+  const int lane = threadIdx.x & 31;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < nbl; b0 += gstride) {
+    const int64_t beta = b0 + lane;
+    const bool valid = beta < nbl;
+    const int64_t bb = valid ? beta : nbl - 1;
+    const int j = find_base(B.blk_base, B.nsteps, bb);
+    const StepDev& s = B.steps[j];
+    const int64_t lb = bb - B.blk_base[j];
+    const int64_t li = lb / s.nblk, k = lb - li * s.nblk;
+    const int64_t lseg = B.seg_base[j] + li;
+    const bool filt = valid && is_filter(L.seg_d[lseg], L.level);
+    const Blk b = load_blk(s, s.seg_lo + li, k);
+    int lf, fa, fb;
+    int64_t cL, cA, cB;
+    run_shape(b, L.st, lf, fa, fb, cL, cA, cB);
+    long long w = filt ? cA * cB * ((cL + L.run_item - 1) / L.run_item) : 0;
+    const bool need = w > 0 && g_bskip;
+    int64_t mlo = 0, tlo = 0;
+    if (need) {
+      // Block-level pre-filter: every sampled tuple of the block has m >= the
+      // sum of the factors' first m and t >= the sum of their last t (factor
+      // segments are staircases and each sample keeps indices 0 and n-1).
+      // The last G point with m below that bound has the least t among them;
+      // if it is <= the t bound it strictly dominates the whole block, which
+      // then emits no candidate -- the outcome of K1's chunk test on every
+      // item of the block, without the items (C5: 92 M items -> 30 M).
+      mlo = __ldg(s.X.m + b.o[0]) + __ldg(s.Y.m + b.o[1]) + __ldg(s.Z.m + b.o[2]);
+      tlo = __ldg(s.X.t + b.o[0] + b.n[0] - 1) + __ldg(s.Y.t + b.o[1] + b.n[1] - 1) +
+            __ldg(s.Z.t + b.o[2] + b.n[2] - 1);
+    }
+    if (g_bskip) {
+      const int64_t l0 = __shfl_sync(0xffffffffu, lseg, 0);
+      const bool same = __all_sync(0xffffffffu, valid && lseg == l0);
+      const int64_t g0 = L.in.start[lseg];
+      const int g = (int)L.in.cnt[lseg];
+      int q = 0;
+      if (same) {
+        if (g > 0 && __any_sync(0xffffffffu, need)) q = warp_lower_bound(L.in.m + g0, g, mlo);
+      } else if (need) {
+        const int64_t* Gm = L.in.m + g0;
+        int a1 = g;
+        while (q < a1) {
+          const int mid = (q + a1) >> 1;
+          if (Gm[mid] < mlo) q = mid + 1;
+          else a1 = mid;
+        }
+      }
+      if (need && q > 0 && L.in.t[g0 + q - 1] <= tlo) w = 0;
+    }
+    if (valid) L.wcnt[beta] = w;
+  }
 }
 
 __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L) {
@@ -3483,8 +3484,9 @@ cudaError_t StepRunner::run(const std::vector<StepDev>& steps, cudaStream_t st, 
         int64_t* nc = (int64_t*)ncand.p;
         int64_t* tmp = (int64_t*)scan_tmp.p;
         mark(4);  // scans (bucket bases, work offsets) count as scan/compaction time
-        nl += 2;  // scan(+nb) and scan(+work counts) in one launch, filter
-        scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadWork{s, L}, nbl, L.wo, tmp, st, NoPost());
+        nl += 3;  // block work counts, scan(+nb) and work-offset scan in one launch, filter
+        launch(k_blocks, dim3(grid_for(nbl, 256, 148 * 8)), dim3(256), 0, st, s, L);
+        scan2_excl_fn(LoadNb{L}, nloc, L.bucket_base, LoadArr<int64_t>{L.wcnt}, nbl, L.wo, tmp, st, NoPost());
         ++nl;
         launch(k_hints, dim3(148 * 4), dim3(256), 0, st, s, L);
         mark(2);  // filter_ms: k_filter alone
@@ -3630,6 +3632,10 @@ cudaError_t StepRunner::gather(const std::vector<StepDev>& steps, const StepResu
 cudaError_t StepRunner::configure() {
   fstats = getenv("FT_FILTER_STATS") != nullptr;
   if (const char* e = getenv("FT_PDL")) g_pdl = atoi(e) != 0;
+  if (const char* e = getenv("FT_BLOCK_SKIP")) {
+    const bool v = atoi(e) != 0;
+    cudaMemcpyToSymbol(g_bskip, &v, sizeof(v));
+  }
   if (const char* e = getenv("FT_FENCE")) {
     const bool v = atoi(e) != 0;
     cudaMemcpyToSymbol(g_fence, &v, sizeof(v));

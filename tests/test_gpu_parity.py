@@ -225,6 +225,44 @@ def test_partition_invariance_pack_reuse():
     assert int(tok[tok.index("BAD") + 1]) == 0, out.stdout
 
 
+_KNOBS = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+import paper_2004_10856_b200 as ft
+from synth import graphs as G
+bad = steps = 0
+for w in (G.c3(), G.c4(layers=2), G.c5(n_ops=300, K=32, B=8, Lmin=3, Lmax=8)):
+    og = oracle.load(w, 8); og.eliminate(); om, ot = og.frontier()
+    gg = ft.load(w, keep_all=True); gg.eliminate(); gm, gt = gg.frontier()
+    bad += not (np.array_equal(om, gm) and np.array_equal(ot, gt))
+    for s in range(og.num_steps()):
+        steps += 1
+        bad += not all(np.array_equal(x, y) for x, y in zip(og.step_output(s), gg.step_output(s)))
+print("BAD", bad, "STEPS", steps)
+"""
+
+
+@pytest.mark.parametrize("knobs", [{"FT_PDL": "0"}, {"FT_FENCE": "0", "FT_BLOCK_SKIP": "0"},
+                                   {"FT_FILTER_GRID": "148", "FT_PDL": "1"}])
+def test_pipeline_knobs(knobs):
+    """The per-process pipeline switches (read once per device runner, hence a
+    subprocess each): plain stream launches instead of programmatic dependent
+    launch, the per-lane G gallop instead of the warp-cooperative lower bound
+    and no block-level pre-filter, a small filter grid (grid-stride passes) --
+    every step still bit-exact against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _KNOBS.format(root=root)], env=dict(os.environ, **knobs),
+                         cwd=root, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    tok = out.stdout.split()
+    assert int(tok[tok.index("STEPS") + 1]) > 50
+    assert int(tok[tok.index("BAD") + 1]) == 0, out.stdout
+
+
 def _wide(K, edges, seed=0, hi=1 << 30):
     """Explicit graph with the given configuration counts and edges."""
     from synth.graphs import Workload

@@ -15,6 +15,7 @@
 #include <queue>
 #include <set>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <nccl.h>
@@ -49,6 +50,36 @@ struct StepRec {
   int64_t KA = 0, KB = 0, KC = 0, nseg = 0, nblk = 0;
   bool done = false;
   ft_step_stats st{};
+};
+
+// Ascending set of edge ids with the std::set<int> operations the policy
+// uses, in a contiguous vector: operator degrees are small and new edge ids
+// are the largest, so inserts append (tree nodes cost ~1 us per policy step
+// on C5).
+struct IdSet {
+  std::vector<int> v;
+  std::vector<int>::const_iterator begin() const { return v.begin(); }
+  std::vector<int>::const_iterator end() const { return v.end(); }
+  size_t size() const { return v.size(); }
+  bool empty() const { return v.empty(); }
+  void insert(int x) {
+    if (v.empty() || v.back() < x) {
+      v.push_back(x);
+      return;
+    }
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (*it != x) v.insert(it, x);
+  }
+  void erase(int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it != v.end() && *it == x) v.erase(it);
+  }
+};
+
+struct PairHash {
+  size_t operator()(const std::pair<int, int>& p) const {
+    return std::hash<uint64_t>()(((uint64_t)(uint32_t)p.first << 32) | (uint32_t)p.second);
+  }
 };
 
 struct EdgeRec {
@@ -87,7 +118,7 @@ struct ft_graph {
   std::vector<char> op_alive;
   std::vector<int> op_set;
   std::vector<EdgeRec> edges;
-  std::vector<std::set<int>> in_e, out_e;
+  std::vector<IdSet> in_e, out_e;
   // FT_AUTO policy state (R9): positions in the original topological order and
   // ordered candidate sets maintained incrementally
   std::vector<int> pos0, order0;
@@ -95,7 +126,7 @@ struct ft_graph {
   std::set<std::pair<int, int>> one_one;    // live ops with one in- and one out-edge
   std::set<std::pair<int, int>> leaf;       // live ops with exactly one edge (branch elimination)
   std::set<std::pair<int, int>> k1src;      // live K=1 sources with out-edges
-  std::map<std::pair<int, int>, std::set<int>> pair_edges;  // (src, dst) -> live edges
+  std::unordered_map<std::pair<int, int>, IdSet, PairHash> pair_edges;  // (src, dst) -> live edges
   std::set<std::pair<int, int>> multi;      // (pos0 src, pos0 dst) with >= 2 live edges
   std::vector<int> mark_stamp;
   int stamp = 0;

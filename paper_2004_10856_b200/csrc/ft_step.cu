@@ -2280,6 +2280,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       int64_t gmp = p < g ? Gm[p] : INF;
       int64_t gmq = p > 0 ? Gm[p - 1] : 0, gtq = p > 0 ? Gt[p - 1] : INF;
       unsigned surv = 0;  // bit j - jj: run element j is a candidate
+      uint64_t pdel = 0;  // 4 bits per candidate: min(p - q, 15) (its bucket, for the emission)
       for (int j4 = jj; j4 < je; j4 += EPRE) {
         int64_t em[EPRE], et[EPRE];
 #pragma unroll
@@ -2301,7 +2302,11 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
             } while (gmp <= m);
             gtq = Gt[p - 1];
           }
-          if (!(p > 0 && (gtq < t || (gtq == t && gmq < m)))) surv |= 1u << (j4 + u - jj);
+          if (!(p > 0 && (gtq < t || (gtq == t && gmq < m)))) {
+            const int x = j4 + u - jj;
+            surv |= 1u << x;
+            pdel |= (uint64_t)min(p - q, 15) << (4 * x);
+          }
         }
       }
       if (surv) {
@@ -2321,7 +2326,13 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
           const int il = samp_idx32(jj + b, nL, sh);
           const int64_t m = ms + __ldg(Lm + il);
           const int64_t t = ts + __ldg(Lt + il);
-          while (pp < g && Gm[pp] <= m) ++pp;
+          const int dp = (int)(pdel >> (4 * b)) & 15;  // p - q from the element test
+          if (dp < 15) {
+            pp = q + dp;
+          } else {  // p >= q + 15: walk on from there
+            pp = max(pp, q + 15);
+            while (pp < g && Gm[pp] <= m) ++pp;
+          }
           int64_t x, y, z;  // (x, y, z) in 64 bits for the id
           if (lf == 0) { x = il; y = ia; z = ib; }
           else if (lf == 1) { x = ia; y = il; z = ib; }

@@ -2146,6 +2146,9 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     const int64_t* const ft[3] = {s.X.t, s.Y.t, s.Z.t};
     const int64_t oL = lf == 0 ? b.o[0] : (lf == 1 ? b.o[1] : b.o[2]);
     const int nL = (int)(lf == 0 ? b.n[0] : (lf == 1 ? b.n[1] : b.n[2]));
+    // samp_idx32 over the long factor with its sample count hoisted
+    const int cL0 = (int)(((int64_t)nL + ((int64_t)1 << sh) - 1) >> sh);
+    auto sidx = [cL0](int j, int n, int shv) { return j < cL0 ? (int)((int64_t)j << shv) : n - 1; };
     const int64_t oA = fa == 0 ? b.o[0] : b.o[1];
     const int64_t nA = fa == 0 ? b.n[0] : b.n[1];
     const int64_t oB = fb == 2 ? b.o[2] : b.o[1];
@@ -2188,15 +2191,15 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
     int jj = j0;
     bool exact = false;  // q = lower_bound(mf) of the first chunk already
     if (one && g > 0) {  // warp-uniform: every lane of the warp is here
-      q = warp_lower_bound(Gm, g, ms + __ldg(Lm + samp_idx32(j0, nL, sh)));
+      q = warp_lower_bound(Gm, g, ms + __ldg(Lm + sidx(j0, nL, sh)));
       exact = true;
     }
     unsigned c_tests = 0, c_skip = 0, c_elem = 0, c_gallop = 0;
     while (jj < j1) {
       ++c_tests;
       const int je = min(jj + CHUNK, j1);
-      const int64_t mf = ms + __ldg(Lm + samp_idx32(jj, nL, sh));
-      const int64_t tl = ts + __ldg(Lt + samp_idx32(je - 1, nL, sh));
+      const int64_t mf = ms + __ldg(Lm + sidx(jj, nL, sh));
+      const int64_t tl = ts + __ldg(Lt + sidx(je - 1, nL, sh));
       const bool known = exact;
       exact = false;
       if (!known && q < g && Gm[q] < mf) {  // lower_bound(mf) in G, starting at q
@@ -2251,20 +2254,20 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
         // G[q-1] (m < mf) strictly dominates the whole chunk and every later
         // element with t >= its t: gallop along the run to the first t below it.
         const int64_t tg = Gt[q - 1];
-        if (ts + __ldg(Lt + samp_idx32(j1 - 1, nL, sh)) >= tg) {  // common: the rest of the item
+        if (ts + __ldg(Lt + sidx(j1 - 1, nL, sh)) >= tg) {  // common: the rest of the item
           c_skip += j1 - jj;
           jj = j1;
           continue;
         }
         int step = 1, last = je - 1;  // t(last) >= tg
-        while (last + step < j1 && ts + __ldg(Lt + samp_idx32(last + step, nL, sh)) >= tg) {
+        while (last + step < j1 && ts + __ldg(Lt + sidx(last + step, nL, sh)) >= tg) {
           last += step;
           step <<= 1;
         }
         int a0 = last + 1, a1 = min(last + step, j1);  // first index with t < tg in [a0, a1]
         while (a0 < a1) {
           const int mid = (a0 + a1) >> 1;
-          if (ts + __ldg(Lt + samp_idx32(mid, nL, sh)) >= tg) a0 = mid + 1;
+          if (ts + __ldg(Lt + sidx(mid, nL, sh)) >= tg) a0 = mid + 1;
           else a1 = mid;
         }
         c_skip += a0 - jj;
@@ -2277,7 +2280,8 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
       int p = q;
       // G[p] and G[p-1] kept in registers: consecutive run elements mostly
       // share p, so the walk and the dominance test reload only when p moves
-      int64_t gmp = p < g ? Gm[p] : INF;
+      // (and G[p+1] one step ahead: a one-point advance does not wait for a load)
+      int64_t gmp = p < g ? Gm[p] : INF, gmn = p + 1 < g ? Gm[p + 1] : INF;
       int64_t gmq = p > 0 ? Gm[p - 1] : 0, gtq = p > 0 ? Gt[p - 1] : INF;
       unsigned surv = 0;  // bit j - jj: run element j is a candidate
       uint64_t pdel = 0;  // 4 bits per candidate: min(p - q, 15) (its bucket, for the emission)
@@ -2285,7 +2289,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
         int64_t em[EPRE], et[EPRE];
 #pragma unroll
         for (int u = 0; u < EPRE; ++u) {
-          const int iu = samp_idx32(min(j4 + u, je - 1), nL, sh);
+          const int iu = sidx(min(j4 + u, je - 1), nL, sh);
           em[u] = __ldg(Lm + iu);
           et[u] = __ldg(Lt + iu);
         }
@@ -2298,7 +2302,8 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
             do {
               gmq = gmp;
               ++p;
-              gmp = p < g ? Gm[p] : INF;
+              gmp = gmn;
+              gmn = p + 1 < g ? Gm[p + 1] : INF;
             } while (gmp <= m);
             gtq = Gt[p - 1];
           }
@@ -2323,7 +2328,7 @@ __device__ __forceinline__ void filter_body(const BatchDev& B, const LevelDev& L
         while (surv) {
           const int b = __ffs(surv) - 1;
           surv &= surv - 1;
-          const int il = samp_idx32(jj + b, nL, sh);
+          const int il = sidx(jj + b, nL, sh);
           const int64_t m = ms + __ldg(Lm + il);
           const int64_t t = ts + __ldg(Lt + il);
           const int dp = (int)(pdel >> (4 * b)) & 15;  // p - q from the element test

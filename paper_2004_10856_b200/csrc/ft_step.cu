@@ -3658,7 +3658,7 @@ cudaError_t StepRunner::configure() {
   }
   if (const char* e = getenv("FT_PACK_GRID")) pack_grid = std::max(1, atoi(e));  // tests: packs per CTA
   filter_regs64 = getenv("FT_FILTER_REGS") && atoi(getenv("FT_FILTER_REGS")) == 64;
-  filter_grid = 148 * 256;
+  filter_grid = 148 * 128;  // A/B after the block pre-filter (C5 / C4 ms, items <= 256): 148x256 47.8 / 36.2, 148x128 46.0 / 34.4, 148x64 46.4 / 34.8
   if (const char* e = getenv("FT_FILTER_GRID")) filter_grid = std::max(148, atoi(e));
   if (const char* e = getenv("FT_ITEM_MAX")) item_max = std::max(16, atoi(e));
   if (const char* e = getenv("FT_ITEM_DIV")) item_div = std::max(1, atoi(e));

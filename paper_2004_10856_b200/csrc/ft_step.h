@@ -133,11 +133,12 @@ class StepRunner {
   int small_wave_segs = 4096;         // waves with <= this many segments: capacity cdirect_small (A/B: 4096 > 1024 > 0)
   int cdirect_small = 2048;           // direct capacity of waves of <= small_wave_segs segments
   int fstats = 0;                     // FT_FILTER_STATS: accumulate filter work counters
-  int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; finer tail balance)
+  int filter_grid = 148 * 128;         // CTAs of k_filter (grid-stride; set in configure())
   int pack_grid = 148 * 6;             // CTAs of k_node_pack (each takes a contiguous pack range; A/B: 888 > 592 > 444 > 296 on C5)
   bool filter_regs64 = false;          // k_filter64 (64 registers) instead of k_filter (80)
-  int item_max = 512;                 // filter work item: max sampled run elements
-  int item_div = 4;                   // ... and target items per resident thread
+  int item_max = 256;                 // filter work item: max sampled run elements
+  int item_div = 16;                  // ... and target items per resident thread (A/B: 256/16 best since
+                                      // the block pre-filter; was 512/4)
   unsigned long long fstat_acc[8] = {};
   unsigned long long bstat_acc[2][10] = {};
   unsigned long long bfall_acc[2] = {};

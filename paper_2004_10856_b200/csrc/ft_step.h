@@ -126,7 +126,8 @@ class StepRunner {
     fence_st = st;
   }
 
-  int slog = 4;                       // sample stride x16 per level beyond level 1
+  int slog = 3;                       // sample stride x8 per level beyond level 1 (A/B after the block
+                                      // pre-filter, C5 / C4 ms: x8 44.6 / 33.8, x16 45.4 / 34.4, x32 48.3 / 38.3)
   int slog0 = 2;                      // level-1 stride 2^slog0 = 4 (tight G for level 0)
   int cdirect = 512;                  // direct-path capacity of large waves (power of 2 <= C_DIRECT;
                                       // A/B: 512 beats 1024 on C4 by 1 ms, C5 equal)
